@@ -1,0 +1,144 @@
+/*
+ * feti_b200.h -- C-ABI of the B200-native explicit FETI local dual operator.
+ *
+ * This is the drop-in boundary for the explicit strategy of the reference's
+ * `tfeti.dualop.DualOperator` (arXiv 2502.08382 reference, pkg/src/tfeti).
+ * The reference is pure Python+numba and has no FFI of its own; the entry
+ * points below are exactly the operations its object interface performs on
+ * the hot path, so a ctypes binding can stand in for them.
+ * Plain C types only: pointers, sizes, status codes.  No torch types.
+ *
+ * Status codes: 0 = ok, otherwise one of FETI_ERR_*; feti_last_error()
+ * returns a thread-local message for the last failing call on this thread.
+ *
+ * Reference interface each entry replaces (file:line under pkg/src/tfeti/):
+ *   feti_create            DualOperator.__init__            dualop.py:124-148
+ *   feti_add_subdomain     prepare(), per subdomain: B~ permutation by the
+ *                          factor's iperm, persistent buffers
+ *                                                           dualop.py:233-248, 85-97
+ *   feti_finalize          prepare(), capacity check / layout
+ *                                                           dualop.py:250-269
+ *   feti_set_factor        numeric refill target of CholFactor.values
+ *                                                           dualop.py:313, sparse.py:287-299
+ *   feti_assemble          assemble_explicit_local (SYRK path) for every
+ *                          subdomain, inside preprocess     dualop.py:316-320, 427-501
+ *   feti_local_operator    local_operator(i)                dualop.py:399-401
+ *   feti_apply             apply(p, out)                    dualop.py:348-388
+ *   feti_apply_device      apply on device-resident vectors (multi-GPU / solver on device)
+ *   feti_destroy           close()                          dualop.py:198-208
+ */
+#ifndef FETI_B200_H
+#define FETI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FETI_B200_ABI_VERSION 1
+
+enum {
+  FETI_OK = 0,
+  FETI_ERR_ARG = 1,        /* maps to ValueError                         */
+  FETI_ERR_LIFECYCLE = 2,  /* maps to dualop.LifecycleError              */
+  FETI_ERR_CUDA = 3,       /* CUDA runtime failure (RuntimeError)        */
+  FETI_ERR_CAPACITY = 4,   /* device memory too small: PoolCapacityError */
+  FETI_ERR_SINGULAR = 5,   /* zero diagonal in the factor: SingularFactorError (sparse.py:491-492) */
+  FETI_ERR_INTERNAL = 6
+};
+
+enum { FETI_FACTOR_HOST = 0, FETI_FACTOR_DEVICE = 1 };
+
+typedef struct feti_ctx feti_ctx;
+
+typedef struct feti_stats {
+  /* device time of the last feti_assemble, per phase (CUDA events, ms) */
+  double ms_wait_upload;  /* waiting for host->device factor copies     */
+  double ms_unpack;
+  double ms_diag_inverse;
+  double ms_block_scale;
+  double ms_trsm;
+  double ms_syrk;
+  double ms_assemble;     /* sum of the above device phases             */
+  double ms_apply;        /* device time of the last apply (kernels)    */
+  /* algorithmic work and what the kernels execute */
+  double flops_trsm_alg;  /* sum_j (n - r_j)^2                          */
+  double flops_syrk_alg;  /* sum_{a<=b} 2 (n - max(r_a, r_b))           */
+  double flops_trsm_exec;
+  double flops_syrk_exec;
+  double flops_scale_exec;
+  double apply_bytes_alg; /* packed F~ + index/vector traffic per apply */
+  double apply_bytes_exec;
+  double factor_bytes;    /* host->device factor values per assemble   */
+  int64_t bytes_persistent;
+  int64_t bytes_temporary;
+  int64_t n_subdomains;
+  int64_t n_multipliers;
+  int32_t launches_assemble; /* kernel launches of the last assemble */
+  int32_t launches_apply;    /* kernel launches per apply             */
+} feti_stats;
+
+int feti_abi_version(void);
+const char* feti_last_error(void);
+
+/* Create a context on CUDA device `device`. */
+int feti_create(int device, feti_ctx** out);
+int feti_destroy(feti_ctx* ctx);
+
+/* Register one subdomain (call in the reference's gather order: ascending
+ * cluster, then ascending subdomain, dualop.py:375-379).
+ *   n, m       local DOFs and local multipliers (rows of B~_i)
+ *   first_row  length m: r_j = iperm[dof_j], the factor row of the single
+ *              nonzero of B~_i row j (decomposition.py:184-207 gives exactly
+ *              one nonzero per row)
+ *   sign       length m: the value of that nonzero (+-1)
+ *   gids       length m: global multiplier ids (multiplier_ids, ascending)
+ *   up, ui     CSR-of-U factor pattern (CholSymbolic.up/ui, sparse.py:240-241);
+ *              pass NULL for a dense pattern, i.e. values are LAPACK packed
+ *              column-major lower of L = U^T (length n(n+1)/2)
+ *   nnz        number of factor values
+ *   out_slot   the slot index used by the other calls */
+int feti_add_subdomain(feti_ctx* ctx, int64_t n, int64_t m, const int64_t* first_row, const double* sign,
+                       const int64_t* gids, const int64_t* up, const int64_t* ui, int64_t nnz,
+                       int64_t* out_slot);
+
+/* Allocate persistent and temporary device memory; n_multipliers is the
+ * global dual-vector length. */
+int feti_finalize(feti_ctx* ctx, int64_t n_multipliers);
+
+/* Hand over the numeric factor of one subdomain.
+ *   where == FETI_FACTOR_HOST:   async host->device copy (pinned memory
+ *                                recommended; keep alive until assemble returns)
+ *   where == FETI_FACTOR_DEVICE: `values` is a device pointer used in place */
+int feti_set_factor(feti_ctx* ctx, int64_t slot, const double* values, int64_t nnz, int where);
+
+/* Assemble every F~_i on the device (TRSM + SYRK); returns when done. */
+int feti_assemble(feti_ctx* ctx);
+
+/* Copy F~_i back: m x m row-major, upper triangle, strictly lower = 0. */
+int feti_local_operator(feti_ctx* ctx, int64_t slot, double* out);
+
+/* q = sum_i B~_i^T F~_i B~_i p over this context's subdomains.
+ * Host vectors of length n_multipliers; q is overwritten. */
+int feti_apply(feti_ctx* ctx, const double* p, double* q);
+
+/* Same on device vectors, enqueued on `stream` (cudaStream_t; NULL = the
+ * context stream).  Does not synchronise. */
+int feti_apply_device(feti_ctx* ctx, const double* d_p, double* d_q, void* stream);
+
+int feti_get_stats(feti_ctx* ctx, feti_stats* out);
+
+/* Diagnostics: per-kernel register / thread limits as text. */
+int feti_debug_kernel_attributes(char* buf, int len);
+
+/* Pinned host memory for factor staging. */
+int feti_host_alloc(size_t bytes, void** out);
+int feti_host_free(void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FETI_B200_H */

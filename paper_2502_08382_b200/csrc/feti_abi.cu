@@ -1,0 +1,642 @@
+// Host runtime behind the C-ABI (include/feti_b200.h).
+//
+// Owns the device memory of one operator context (persistent: packed F~ apply
+// tiles, index maps, dual vectors; temporary: factor tiles and X panels of the
+// assembly), builds the batched work lists once at finalize (the reference's
+// symbolic/prepare stage, dualop.py:212-269), and sequences the kernels of
+// preprocess (dualop.py:301-327) and apply (dualop.py:348-388).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/feti_b200.h"
+#include "feti_common.cuh"
+#include "feti_kernels.h"
+
+using namespace feti;
+
+namespace {
+
+thread_local std::string g_err;
+const bool g_debug_sync = getenv("FETI_DEBUG_SYNC") != nullptr;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define FETI_DEBUG_SYNC(st)                                                                   \
+  do {                                                                                        \
+    if (g_debug_sync) {                                                                       \
+      cudaError_t _e = cudaStreamSynchronize(st);                                             \
+      if (_e == cudaSuccess) _e = cudaGetLastError();                                         \
+      if (_e != cudaSuccess)                                                                  \
+        return fail(FETI_ERR_CUDA, "kernel failed at %s:%d: %s", __FILE__, __LINE__,          \
+                    cudaGetErrorString(_e));                                                  \
+    }                                                                                         \
+  } while (0)
+
+#define CUDA_TRY(expr)                                                                          \
+  do {                                                                                          \
+    cudaError_t _e = (expr);                                                                    \
+    if (_e != cudaSuccess) {                                                                    \
+      if (_e == cudaErrorMemoryAllocation)                                                      \
+        return fail(FETI_ERR_CAPACITY, "device memory exhausted in %s: %s", #expr,              \
+                    cudaGetErrorString(_e));                                                    \
+      return fail(FETI_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));               \
+    }                                                                                           \
+  } while (0)
+
+struct SubHost {
+  int64_t n = 0, m = 0, nnz = 0;
+  int T = 0, P = 0, T32 = 0;
+  bool dense = true;
+  std::vector<int64_t> colperm;      // sorted position -> original local row
+  std::vector<int> r_sorted;         // P*128
+  std::vector<double> s_sorted;      // P*128
+  std::vector<int> gids_sorted;      // T32*32
+  std::vector<int> panel_minrow;     // P
+  std::vector<int64_t> up, ui;       // sparse pattern (host copy until finalize)
+  // device
+  double* d_raw_own = nullptr;       // lib-owned upload buffer
+  const double* d_raw = nullptr;     // current factor values
+  int64_t* d_up = nullptr;
+  int64_t* d_ui = nullptr;
+  double* d_tiles = nullptr;
+  double* d_X = nullptr;
+  double* d_F = nullptr;
+  int* d_r = nullptr;
+  double* d_s = nullptr;
+  int* d_g = nullptr;
+  int* d_pmin = nullptr;
+  bool factor_set = false;
+  bool factor_from_host = false;
+  cudaEvent_t ev_upload = nullptr;
+  int64_t f_tiles() const { return (int64_t)T32 * (T32 + 1) / 2; }
+};
+
+struct DevBuf {
+  void* p = nullptr;
+};
+
+}  // namespace
+
+struct feti_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  std::vector<SubHost> subs;
+  int64_t n_mult = 0;
+  bool finalized = false, assembled = false;
+  std::vector<void*> allocs;
+  int64_t bytes_persistent = 0, bytes_temporary = 0;
+  // device tables
+  SubDev* d_subdev = nullptr;
+  int4 *d_w_unpack = nullptr, *d_w_diag = nullptr, *d_w_scale = nullptr, *d_w_chain = nullptr,
+       *d_w_syrk = nullptr, *d_w_apply = nullptr;
+  int n_unpack = 0, n_diag = 0, n_scale = 0, n_chain = 0, n_syrk = 0, n_apply = 0;
+  int64_t* d_part_off = nullptr;
+  double* d_part = nullptr;
+  int* d_cptr = nullptr;
+  int4* d_cent = nullptr;
+  double *d_p = nullptr, *d_q = nullptr;
+  int apply_nw = 8;
+  size_t apply_smem = 0;
+  feti_stats stats{};
+  cudaEvent_t ev[8] = {};
+  bool subdev_dirty = true;
+};
+
+namespace {
+
+int dev_alloc(feti_ctx* c, void** p, size_t bytes, bool persistent) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    return fail(FETI_ERR_CAPACITY,
+                "device pool of %zu bytes cannot hold %lld persistent bytes plus a %zu-byte request "
+                "(%zu free)",
+                tot, (long long)c->bytes_persistent, bytes, fr);
+  }
+  c->allocs.push_back(*p);
+  if (persistent)
+    c->bytes_persistent += (int64_t)bytes;
+  else
+    c->bytes_temporary += (int64_t)bytes;
+  return FETI_OK;
+}
+
+template <class T>
+int upload(feti_ctx* c, T** dst, const std::vector<T>& v, bool persistent = true) {
+  int rc = dev_alloc(c, (void**)dst, v.size() * sizeof(T), persistent);
+  if (rc) return rc;
+  if (!v.empty()) CUDA_TRY(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return FETI_OK;
+}
+
+int sync_subdev(feti_ctx* c) {
+  std::vector<SubDev> h(c->subs.size());
+  for (size_t i = 0; i < c->subs.size(); ++i) {
+    const SubHost& s = c->subs[i];
+    SubDev& d = h[i];
+    d.raw = s.d_raw;
+    d.up = s.dense ? nullptr : s.d_up;
+    d.ui = s.dense ? nullptr : s.d_ui;
+    d.tiles = s.d_tiles;
+    d.X = s.d_X;
+    d.F = s.d_F;
+    d.r_sorted = s.d_r;
+    d.s_sorted = s.d_s;
+    d.gids_sorted = s.d_g;
+    d.panel_minrow = s.d_pmin;
+    d.nnz = s.nnz;
+    d.n = (int)s.n;
+    d.m = (int)s.m;
+    d.T = s.T;
+    d.P = s.P;
+    d.T32 = s.T32;
+    d.pad_ = 0;
+  }
+  if (!h.empty())
+    CUDA_TRY(cudaMemcpyAsync(c->d_subdev, h.data(), h.size() * sizeof(SubDev), cudaMemcpyHostToDevice,
+                             c->stream));
+  c->subdev_dirty = false;
+  return FETI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int feti_abi_version(void) { return FETI_B200_ABI_VERSION; }
+
+const char* feti_last_error(void) { return g_err.c_str(); }
+
+int feti_create(int device, feti_ctx** out) {
+  if (!out) return fail(FETI_ERR_ARG, "out is NULL");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(FETI_ERR_ARG, "device %d out of range (%d devices)", device, ndev);
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(FETI_ERR_CUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+  feti_ctx* c = new feti_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+  CUDA_TRY(configure_kernels());
+  *out = c;
+  return FETI_OK;
+}
+
+int feti_destroy(feti_ctx* c) {
+  if (!c) return FETI_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  for (void* p : c->allocs) cudaFree(p);
+  for (auto& s : c->subs)
+    if (s.ev_upload) cudaEventDestroy(s.ev_upload);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  delete c;
+  return FETI_OK;
+}
+
+int feti_add_subdomain(feti_ctx* c, int64_t n, int64_t m, const int64_t* first_row, const double* sign,
+                       const int64_t* gids, const int64_t* up, const int64_t* ui, int64_t nnz,
+                       int64_t* out_slot) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (c->finalized) return fail(FETI_ERR_LIFECYCLE, "prepare was already called on this operator");
+  if (n <= 0 || m < 0) return fail(FETI_ERR_ARG, "bad subdomain size n=%lld m=%lld", (long long)n, (long long)m);
+  if (n > (1 << 28)) return fail(FETI_ERR_ARG, "subdomain too large");
+  if (m > 0 && (!first_row || !sign || !gids)) return fail(FETI_ERR_ARG, "NULL index arrays");
+  const bool dense = (up == nullptr);
+  if (dense && nnz != n * (n + 1) / 2)
+    return fail(FETI_ERR_ARG, "dense factor needs n(n+1)/2 = %lld values, got %lld", (long long)(n * (n + 1) / 2),
+                (long long)nnz);
+  SubHost s;
+  s.n = n;
+  s.m = m;
+  s.nnz = nnz;
+  s.dense = dense;
+  s.T = (int)((n + TB - 1) / TB);
+  s.P = (int)((m + TB - 1) / TB);
+  s.T32 = (int)((m + AT - 1) / AT);
+  for (int64_t j = 0; j < m; ++j) {
+    if (first_row[j] < 0 || first_row[j] >= n)
+      return fail(FETI_ERR_ARG, "constraint row %lld hits factor row %lld outside [0, %lld)", (long long)j,
+                  (long long)first_row[j], (long long)n);
+    if (j > 0 && gids[j] <= gids[j - 1]) return fail(FETI_ERR_ARG, "multiplier ids must be strictly ascending");
+  }
+  if (!dense) {
+    if (!ui) return fail(FETI_ERR_ARG, "ui is NULL");
+    if (up[0] != 0 || up[n] != nnz) return fail(FETI_ERR_ARG, "pattern pointer does not match nnz");
+    for (int64_t j = 0; j < n; ++j) {
+      if (up[j + 1] <= up[j] || ui[up[j]] != j)
+        return fail(FETI_ERR_SINGULAR, "factor row %lld has no leading diagonal entry", (long long)j);
+    }
+    s.up.assign(up, up + n + 1);
+    s.ui.assign(ui, ui + nnz);
+  }
+  // sort columns of P B~^T by their first nonzero row (stable)
+  s.colperm.resize(m);
+  std::iota(s.colperm.begin(), s.colperm.end(), 0);
+  std::stable_sort(s.colperm.begin(), s.colperm.end(),
+                   [&](int64_t a, int64_t b) { return first_row[a] < first_row[b]; });
+  s.r_sorted.assign((size_t)s.P * TB, BIG_ROW);
+  s.s_sorted.assign((size_t)s.P * TB, 0.0);
+  s.gids_sorted.assign((size_t)s.T32 * AT, -1);
+  for (int64_t a = 0; a < m; ++a) {
+    const int64_t j = s.colperm[a];
+    s.r_sorted[a] = (int)first_row[j];
+    s.s_sorted[a] = sign[j];
+    s.gids_sorted[a] = (int)gids[j];
+  }
+  s.panel_minrow.resize(s.P);
+  for (int p = 0; p < s.P; ++p) s.panel_minrow[p] = s.r_sorted[(size_t)p * TB];
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaEventCreateWithFlags(&s.ev_upload, cudaEventDisableTiming));
+  c->subs.push_back(std::move(s));
+  if (out_slot) *out_slot = (int64_t)c->subs.size() - 1;
+  return FETI_OK;
+}
+
+int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (c->finalized) return fail(FETI_ERR_LIFECYCLE, "prepare was already called on this operator");
+  if (n_multipliers < 0 || n_multipliers >= (int64_t)1 << 31) return fail(FETI_ERR_ARG, "bad n_multipliers");
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->n_mult = n_multipliers;
+  for (auto& s : c->subs)
+    for (int a = 0; a < s.m; ++a)
+      if (s.gids_sorted[a] >= n_multipliers) return fail(FETI_ERR_ARG, "multiplier id out of range");
+
+  // capacity check before allocating anything large
+  size_t need = 0;
+  int max_M = 0;
+  for (auto& s : c->subs) {
+    need += (size_t)s.T * (s.T + 1) / 2 * TILE * 8;   // tiles
+    need += (size_t)s.P * s.T * TILE * 8;             // X panels
+    need += (size_t)s.f_tiles() * ATILE * 8;          // F~
+    max_M = std::max(max_M, s.T32 * AT);
+  }
+  size_t fr = 0, tot = 0;
+  CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+  if (need > fr)
+    return fail(FETI_ERR_CAPACITY,
+                "device pool of %zu bytes (%zu free) cannot hold the %zu-byte explicit operator workspace", tot,
+                fr, need);
+
+  int rc;
+  for (auto& s : c->subs) {
+    if ((rc = dev_alloc(c, (void**)&s.d_tiles, (size_t)s.T * (s.T + 1) / 2 * TILE * 8, false))) return rc;
+    if ((rc = dev_alloc(c, (void**)&s.d_X, (size_t)std::max(s.P, 1) * s.T * TILE * 8, false))) return rc;
+    if ((rc = dev_alloc(c, (void**)&s.d_F, (size_t)std::max<int64_t>(s.f_tiles(), 1) * ATILE * 8, true)))
+      return rc;
+    if ((rc = upload(c, &s.d_r, s.r_sorted))) return rc;
+    if ((rc = upload(c, &s.d_s, s.s_sorted))) return rc;
+    if ((rc = upload(c, &s.d_g, s.gids_sorted))) return rc;
+    if ((rc = upload(c, &s.d_pmin, s.panel_minrow))) return rc;
+    if (!s.dense) {
+      if ((rc = upload(c, &s.d_up, s.up))) return rc;
+      if ((rc = upload(c, &s.d_ui, s.ui))) return rc;
+      std::vector<int64_t>().swap(s.up);
+      std::vector<int64_t>().swap(s.ui);
+    }
+  }
+  if ((rc = dev_alloc(c, (void**)&c->d_subdev, c->subs.size() * sizeof(SubDev), true))) return rc;
+
+  // ---- work lists (largest work first where it varies)
+  std::vector<int4> wu, wd, ws, wc, wy, wa;
+  double trsm_alg = 0, syrk_alg = 0, trsm_exec = 0, syrk_exec = 0, scale_exec = 0;
+  const double tb3 = 2.0 * TB * TB * TB;
+  for (int si = 0; si < (int)c->subs.size(); ++si) {
+    const SubHost& s = c->subs[si];
+    for (int K = 0; K < s.T; ++K)
+      for (int L = 0; L <= K; ++L) wu.push_back(make_int4(si, K, L, 0));
+    for (int k = 0; k < s.T; ++k) wd.push_back(make_int4(si, k, 0, 0));
+    for (int k = 1; k < s.T; ++k)
+      for (int l = 0; l < k; ++l)
+        for (int h = 0; h < 2; ++h) ws.push_back(make_int4(si, k, l, h));
+    scale_exec += (double)s.T * (s.T - 1) / 2 * 2.0 * (2.0 * 64 * 32 * 32 * (1 + 2 + 3 + 4));
+    for (int p = 0; p < s.P; ++p) {
+      wc.push_back(make_int4(si, p, 0, 0));
+      const double s0 = s.panel_minrow[p] / TB;
+      trsm_exec += tb3 * (s.T - 1 - s0) * (s.T - s0) / 2.0;
+    }
+    const int rend = (int)((s.n + KS - 1) / KS * KS);
+    for (int I = 0; I < s.P; ++I)
+      for (int J = I; J < s.P; ++J) {
+        wy.push_back(make_int4(si, I, J, 0));
+        const int rs = std::max(s.panel_minrow[I], s.panel_minrow[J]) & ~(KS - 1);
+        syrk_exec += 2.0 * TB * TB * (rend - rs);
+      }
+    for (int a = 0; a < s.m; ++a) {
+      const double d = (double)(s.n - s.r_sorted[a]);
+      trsm_alg += d * d;
+      syrk_alg += 2.0 * d * (a + 1);
+    }
+  }
+  // chains: longest first so the tail is short
+  std::sort(wc.begin(), wc.end(), [&](const int4& a, const int4& b) {
+    const SubHost& sa = c->subs[a.x];
+    const SubHost& sb = c->subs[b.x];
+    const double la = sa.T - sa.panel_minrow[a.y] / TB, lb = sb.T - sb.panel_minrow[b.y] / TB;
+    return la > lb;
+  });
+  std::sort(wy.begin(), wy.end(), [&](const int4& a, const int4& b) {
+    const SubHost& sa = c->subs[a.x];
+    const SubHost& sb = c->subs[b.x];
+    const int la = (int)sa.n - std::max(sa.panel_minrow[a.y], sa.panel_minrow[a.z]);
+    const int lb = (int)sb.n - std::max(sb.panel_minrow[b.y], sb.panel_minrow[b.z]);
+    return la > lb;
+  });
+
+  // ---- apply work: split each subdomain's tiles over CTAs, partial slots
+  int64_t total_tiles = 0;
+  for (auto& s : c->subs) total_tiles += s.f_tiles();
+  const int64_t tpc = std::max<int64_t>(16, (total_tiles + 4 * c->num_sms - 1) / (4 * c->num_sms));
+  std::vector<int64_t> part_off;
+  std::vector<int> cta_begin(c->subs.size()), cta_end(c->subs.size());
+  int64_t poff = 0;
+  double apply_alg = 16.0 * (double)c->n_mult, apply_exec = 16.0 * (double)c->n_mult;
+  for (int si = 0; si < (int)c->subs.size(); ++si) {
+    const SubHost& s = c->subs[si];
+    cta_begin[si] = (int)part_off.size();
+    const int64_t nt = s.f_tiles();
+    if (s.m > 0) {
+      const int64_t nct = std::max<int64_t>(1, (nt + tpc - 1) / tpc);
+      for (int64_t k = 0; k < nct; ++k) {
+        const int64_t t0 = nt * k / nct, t1 = nt * (k + 1) / nct;
+        wa.push_back(make_int4(si, (int)t0, (int)t1, (int)part_off.size()));
+        part_off.push_back(poff);
+        poff += s.m;
+      }
+    }
+    cta_end[si] = (int)part_off.size();
+    apply_alg += 8.0 * s.m * (s.m + 1) / 2 + s.m * (8.0 + 16.0 + 4.0);
+    apply_exec += 8.0 * ATILE * nt + s.T32 * AT * 12.0;
+  }
+  apply_exec += 16.0 * poff;
+  // contributions per global multiplier, in registration (gather) order
+  std::vector<std::vector<int4>> per_g((size_t)c->n_mult);
+  for (int si = 0; si < (int)c->subs.size(); ++si) {
+    const SubHost& s = c->subs[si];
+    for (int a = 0; a < s.m; ++a) per_g[s.gids_sorted[a]].push_back(make_int4(a, cta_begin[si], cta_end[si], 0));
+  }
+  std::vector<int> cptr((size_t)c->n_mult + 1, 0);
+  std::vector<int4> cent;
+  for (int64_t g = 0; g < c->n_mult; ++g) {
+    cptr[g] = (int)cent.size();
+    cent.insert(cent.end(), per_g[g].begin(), per_g[g].end());
+  }
+  cptr[c->n_mult] = (int)cent.size();
+
+  // per-warp accumulators in smem: (NW + 1) * M doubles
+  c->apply_nw = 8;
+  while (c->apply_nw > 1 && (size_t)(c->apply_nw + 1) * max_M * 8 > 227 * 1024) c->apply_nw >>= 1;
+  c->apply_smem = (size_t)(c->apply_nw + 1) * max_M * 8;
+  if (c->apply_smem > 227 * 1024)
+    return fail(FETI_ERR_CAPACITY, "subdomain with %d multipliers exceeds the apply kernel's shared memory", max_M);
+
+  if ((rc = upload(c, &c->d_w_unpack, wu))) return rc;
+  if ((rc = upload(c, &c->d_w_diag, wd))) return rc;
+  if ((rc = upload(c, &c->d_w_scale, ws))) return rc;
+  if ((rc = upload(c, &c->d_w_chain, wc))) return rc;
+  if ((rc = upload(c, &c->d_w_syrk, wy))) return rc;
+  if ((rc = upload(c, &c->d_w_apply, wa))) return rc;
+  if ((rc = upload(c, &c->d_part_off, part_off))) return rc;
+  if ((rc = upload(c, &c->d_cptr, cptr))) return rc;
+  if ((rc = upload(c, &c->d_cent, cent))) return rc;
+  if ((rc = dev_alloc(c, (void**)&c->d_part, (size_t)std::max<int64_t>(poff, 1) * 8, true))) return rc;
+  if ((rc = dev_alloc(c, (void**)&c->d_p, (size_t)std::max<int64_t>(c->n_mult, 1) * 8, true))) return rc;
+  if ((rc = dev_alloc(c, (void**)&c->d_q, (size_t)std::max<int64_t>(c->n_mult, 1) * 8, true))) return rc;
+  c->n_unpack = (int)wu.size();
+  c->n_diag = (int)wd.size();
+  c->n_scale = (int)ws.size();
+  c->n_chain = (int)wc.size();
+  c->n_syrk = (int)wy.size();
+  c->n_apply = (int)wa.size();
+
+  feti_stats& st = c->stats;
+  st.flops_trsm_alg = trsm_alg;
+  st.flops_syrk_alg = syrk_alg;
+  st.flops_trsm_exec = trsm_exec;
+  st.flops_syrk_exec = syrk_exec;
+  st.flops_scale_exec = scale_exec;
+  st.apply_bytes_alg = apply_alg;
+  st.apply_bytes_exec = apply_exec;
+  st.n_subdomains = (int64_t)c->subs.size();
+  st.n_multipliers = c->n_mult;
+  st.launches_apply = 2;
+  CUDA_TRY(cudaDeviceSynchronize());
+  c->finalized = true;
+  return FETI_OK;
+}
+
+int feti_set_factor(feti_ctx* c, int64_t slot, const double* values, int64_t nnz, int where) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->finalized) return fail(FETI_ERR_LIFECYCLE, "preprocess before prepare");
+  if (slot < 0 || slot >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot %lld out of range", (long long)slot);
+  SubHost& s = c->subs[slot];
+  if (nnz != s.nnz)
+    return fail(FETI_ERR_ARG, "factor value buffer has the wrong length (%lld, expected %lld)", (long long)nnz,
+                (long long)s.nnz);
+  if (!values) return fail(FETI_ERR_ARG, "values is NULL");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (where == FETI_FACTOR_DEVICE) {
+    s.d_raw = values;
+    s.factor_from_host = false;
+  } else {
+    if (!s.d_raw_own) {
+      int rc = dev_alloc(c, (void**)&s.d_raw_own, (size_t)s.nnz * 8, true);
+      if (rc) return rc;
+    }
+    CUDA_TRY(cudaMemcpyAsync(s.d_raw_own, values, (size_t)s.nnz * 8, cudaMemcpyHostToDevice, c->copy_stream));
+    CUDA_TRY(cudaEventRecord(s.ev_upload, c->copy_stream));
+    s.d_raw = s.d_raw_own;
+    s.factor_from_host = true;
+  }
+  s.factor_set = true;
+  c->subdev_dirty = true;
+  return FETI_OK;
+}
+
+int feti_assemble(feti_ctx* c) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->finalized) return fail(FETI_ERR_LIFECYCLE, "preprocess before prepare");
+  for (size_t i = 0; i < c->subs.size(); ++i)
+    if (!c->subs[i].factor_set) return fail(FETI_ERR_LIFECYCLE, "subdomain slot %zu has no factor values", i);
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  int launches = 0;
+  CUDA_TRY(cudaEventRecord(c->ev[0], st));
+  for (auto& s : c->subs)
+    if (s.factor_from_host) CUDA_TRY(cudaStreamWaitEvent(st, s.ev_upload, 0));
+  if (c->subdev_dirty) {
+    int rc = sync_subdev(c);
+    if (rc) return rc;
+  }
+  CUDA_TRY(cudaEventRecord(c->ev[1], st));
+  launch_unpack(c->d_subdev, c->d_w_unpack, c->n_unpack, st);
+  launches += c->n_unpack > 0;
+  for (int si = 0; si < (int)c->subs.size(); ++si)
+    if (!c->subs[si].dense) {
+      launch_scatter_sparse(c->d_subdev, si, (int)c->subs[si].n, st);
+      ++launches;
+    }
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  CUDA_TRY(cudaEventRecord(c->ev[2], st));
+  launch_diag_inverse(c->d_subdev, c->d_w_diag, c->n_diag, st);
+  launches += c->n_diag > 0;
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  CUDA_TRY(cudaEventRecord(c->ev[3], st));
+  launch_block_scale(c->d_subdev, c->d_w_scale, c->n_scale, st);
+  launches += c->n_scale > 0;
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  CUDA_TRY(cudaEventRecord(c->ev[4], st));
+  launch_trsm_chain(c->d_subdev, c->d_w_chain, c->n_chain, st);
+  launches += c->n_chain > 0;
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  CUDA_TRY(cudaEventRecord(c->ev[5], st));
+  launch_syrk(c->d_subdev, c->d_w_syrk, c->n_syrk, st);
+  launches += c->n_syrk > 0;
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  CUDA_TRY(cudaEventRecord(c->ev[6], st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float ms[6];
+  for (int i = 0; i < 6; ++i) CUDA_TRY(cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]));
+  feti_stats& S = c->stats;
+  S.ms_wait_upload = ms[0];
+  S.ms_unpack = ms[1];
+  S.ms_diag_inverse = ms[2];
+  S.ms_block_scale = ms[3];
+  S.ms_trsm = ms[4];
+  S.ms_syrk = ms[5];
+  S.ms_assemble = ms[1] + ms[2] + ms[3] + ms[4] + ms[5];
+  S.launches_assemble = launches;
+  double fb = 0;
+  for (auto& s : c->subs)
+    if (s.factor_from_host) fb += 8.0 * s.nnz;
+  S.factor_bytes = fb;
+  c->assembled = true;
+  return FETI_OK;
+}
+
+int feti_local_operator(feti_ctx* c, int64_t slot, double* out) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "local operator before preprocess");
+  if (slot < 0 || slot >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot out of range");
+  const SubHost& s = c->subs[slot];
+  CUDA_TRY(cudaSetDevice(c->device));
+  std::vector<double> tiles((size_t)s.f_tiles() * ATILE);
+  if (!tiles.empty())
+    CUDA_TRY(cudaMemcpy(tiles.data(), s.d_F, tiles.size() * 8, cudaMemcpyDeviceToHost));
+  const int64_t m = s.m;
+  std::vector<int64_t> pos(m);
+  for (int64_t a = 0; a < m; ++a) pos[s.colperm[a]] = a;
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < m; ++j) {
+      double v = 0.0;
+      if (j >= i) {
+        int64_t u = pos[i], w = pos[j];
+        if (u > w) std::swap(u, w);
+        v = tiles[(size_t)apply_tile_index(u / AT, w / AT, s.T32) * ATILE + (u % AT) * AT + (w % AT)];
+      }
+      out[i * m + j] = v;
+    }
+  return FETI_OK;
+}
+
+// The descriptor table was uploaded by feti_assemble on the context stream;
+// apply reads only finalize-time fields of it (F~ tiles, index maps).
+static int apply_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st, bool time_it) {
+  if (time_it) CUDA_TRY(cudaEventRecord(c->ev[0], st));
+  launch_apply(c->apply_nw, c->apply_smem, c->d_subdev, c->d_w_apply, c->n_apply, c->d_part_off, c->d_part, d_p,
+               st);
+  launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_part_off, c->d_part, d_q, st);
+  CUDA_TRY(cudaGetLastError());
+  if (time_it) CUDA_TRY(cudaEventRecord(c->ev[1], st));
+  return FETI_OK;
+}
+
+int feti_apply(feti_ctx* c, const double* p, double* q) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "apply before preprocess for the current values");
+  if (!p || !q) return fail(FETI_ERR_ARG, "NULL vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  CUDA_TRY(cudaMemcpyAsync(c->d_p, p, (size_t)c->n_mult * 8, cudaMemcpyHostToDevice, st));
+  int rc = apply_enqueue(c, c->d_p, c->d_q, st, true);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(q, c->d_q, (size_t)c->n_mult * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  c->stats.ms_apply = ms;
+  return FETI_OK;
+}
+
+int feti_apply_device(feti_ctx* c, const double* d_p, double* d_q, void* stream) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "apply before preprocess for the current values");
+  if (!d_p || !d_q) return fail(FETI_ERR_ARG, "NULL vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+  return apply_enqueue(c, d_p, d_q, st, false);
+}
+
+int feti_get_stats(feti_ctx* c, feti_stats* out) {
+  if (!c || !out) return fail(FETI_ERR_ARG, "NULL argument");
+  c->stats.bytes_persistent = c->bytes_persistent;
+  c->stats.bytes_temporary = c->bytes_temporary;
+  *out = c->stats;
+  return FETI_OK;
+}
+
+int feti_debug_kernel_attributes(char* buf, int len) {
+  if (!buf || len <= 0) return fail(FETI_ERR_ARG, "bad buffer");
+  buf[0] = 0;
+  feti::kernel_attributes(buf, len);
+  return FETI_OK;
+}
+
+int feti_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(FETI_ERR_ARG, "out is NULL");
+  CUDA_TRY(cudaHostAlloc(out, bytes ? bytes : 16, cudaHostAllocPortable));
+  return FETI_OK;
+}
+
+int feti_host_free(void* ptr) {
+  if (ptr) CUDA_TRY(cudaFreeHost(ptr));
+  return FETI_OK;
+}
+
+}  // extern "C"

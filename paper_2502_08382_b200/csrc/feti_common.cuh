@@ -1,0 +1,114 @@
+// Shared device helpers for the B200 explicit FETI dual operator.
+//
+// FP64 on sm_100a has no tcgen05 kind (ptxas rejects .kind::f64), so the dense
+// contractions run on the FP64 tensor pipe through warp-level
+// mma.sync.m8n8k4.f64 (SASS: DMMA.8x8x4).  Operand tiles are staged into
+// shared memory with the Blackwell bulk-copy engine (cp.async.bulk, SASS
+// UBLKCP) completing on mbarriers, consumed by warp-specialised DMMA warps.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace feti {
+
+// ---- tiling constants ------------------------------------------------------
+constexpr int TB = 128;            // block rows of L / columns per RHS panel
+constexpr int TILE = TB * TB;      // doubles per 128x128 tile (128 KB)
+constexpr int KS = 32;             // k-slice depth staged per pipeline stage
+constexpr int SLICE = KS * TB;     // doubles per slice (32 KB)
+constexpr int AT = 32;             // apply-side tile edge (32x32 = 8 KB)
+constexpr int ATILE = AT * AT;
+constexpr int BIG_ROW = 1 << 30;   // sentinel first-row of padding columns
+
+// Every 128-wide tile (L blocks, X panels, inverse diagonal blocks) is stored
+// as [major][minor] with the minor index XOR-swizzled by the major index:
+//     pos(major, minor) = major*128 + (minor ^ ((major & 3) << 2))
+// so that the DMMA fragment reads (4 k-values x 8 rows per 16 lanes) hit 16
+// distinct bank pairs, and a 32-major slice is one contiguous 32 KB chunk a
+// single bulk copy lands conflict-free in shared memory.
+__host__ __device__ __forceinline__ int swz(int major, int minor) {
+  return major * TB + (minor ^ ((major & 3) << 2));
+}
+
+__host__ __device__ __forceinline__ int64_t tri_index(int64_t K, int64_t Lc) {
+  return K * (K + 1) / 2 + Lc;   // lower block-triangle tile (K >= Lc)
+}
+
+// upper triangle of apply tiles, row-major over tile rows
+__host__ __device__ __forceinline__ int64_t apply_tile_index(int64_t ti, int64_t tj, int64_t T32) {
+  return ti * T32 - ti * (ti - 1) / 2 + (tj - ti);
+}
+
+// Per-subdomain device descriptor (all pointers device).
+struct SubDev {
+  const double* raw;        // factor values, reference CSR-of-U order
+  const int64_t* up;        // pattern (nullptr => dense packed col-major lower)
+  const int64_t* ui;
+  double* tiles;            // T(T+1)/2 tiles, col-major swizzled
+  double* X;                // P panels x (T*128 rows) x 128, row-major swizzled
+  double* F;                // apply tiles (upper triangle of 32x32 tiles)
+  const int* r_sorted;      // P*128 first rows, sorted ascending, BIG_ROW pads
+  const double* s_sorted;   // P*128 signs (0 for pads)
+  const int* gids_sorted;   // T32*32 global multiplier ids (-1 pads)
+  const int* panel_minrow;  // P
+  int64_t nnz;
+  int n, m, T, P, T32;
+  int pad_;
+};
+
+// ---- PTX wrappers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared (TMA engine), completes on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Make this thread's generic-proxy global writes visible to later async-proxy
+// (bulk copy) reads.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+}  // namespace feti

@@ -1,0 +1,578 @@
+// Device kernels of the explicit FETI local dual operator (sm_100a).
+//
+// Assembly of F~_i = X^T X with X = L^-1 P B~^T (
+// reference dualop.py:427-501, sparse.py:469-563, _kernels.py:168-214,299-305):
+//
+//   1. unpack   raw factor (CSR-of-U == packed col-major L)  -> 128x128 tiles
+//   2. diaginv  inv(L_kk) of every diagonal block             -> tile (k,k)
+//   3. scale    Lhat_kl = inv(L_kk) L_kl  (block-row scaling, l<k)  [DMMA]
+//   4. trsm     per (subdomain, 128-column panel) chain:            [DMMA]
+//                 X_k = inv(L_kk) Z_k - sum_{l=s..k-1} Lhat_kl X_l
+//               Z = P B~^T is never materialised: each column is one +-1 at
+//               its first row r_j, so inv(L_kk) Z_k is a signed column gather
+//               of tile (k,k); panels start at their first nonzero block row.
+//   5. syrk     F_IJ = sum_rows X_I^T X_J over rows >= max(first rows) [DMMA]
+//               written as packed upper-triangle 32x32 tiles for the apply.
+//
+// Apply q = sum_i B~_i^T F~_i B~_i p (dualop.py:348-388, _kernels.py:274-287):
+//   6. apply    gather p~ into smem, stream every stored tile once, row sums via
+//               a butterfly transpose-reduce, column sums in registers;
+//               per-warp smem accumulators combined in fixed order
+//   7. reduce   q[g] = sum over (subdomain, local) contributions in the
+//               reference's fixed gather order (dualop.py:375-379).
+#include <cstdio>
+
+#include "feti_common.cuh"
+#include "feti_kernels.h"
+
+namespace feti {
+
+// ---------------------------------------------------------------------------
+// 1. unpack
+// ---------------------------------------------------------------------------
+// work: (sub, K, Lc, -).  Dense pattern: column j of L = raw[colstart(j) ..]
+// with rows j..n-1 (reference: rows of U, diagonal first, sparse.py:9-15).
+// raw == nullptr (sparse pattern) => zero fill, then the scatter kernel.
+__global__ void __launch_bounds__(256) unpack_dense_kernel(const SubDev* __restrict__ subs,
+                                                           const int4* __restrict__ work) {
+  const int4 w = work[blockIdx.x];
+  const SubDev& S = subs[w.x];
+  const int K = w.y, Lc = w.z;
+  const int64_t n = S.n;
+  double* tile = S.tiles + tri_index(K, Lc) * TILE;
+  const bool dense = (S.up == nullptr);
+  for (int idx = threadIdx.x; idx < TILE; idx += blockDim.x) {
+    const int jl = idx >> 7;
+    const int il = (idx & 127) ^ ((jl & 3) << 2);
+    const int64_t i = (int64_t)K * TB + il, j = (int64_t)Lc * TB + jl;
+    double v = 0.0;
+    if (i < n && j < n) {
+      if (dense && i >= j) v = __ldcs(S.raw + (j * n - j * (j - 1) / 2) + (i - j));
+    } else if (i == j) {
+      v = 1.0;  // identity padding keeps the diagonal blocks invertible
+    }
+    tile[idx] = v;
+  }
+}
+
+// Sparse pattern: one CTA per factor column j (row j of U), entries up[j]..
+__global__ void __launch_bounds__(256) scatter_sparse_kernel(const SubDev* __restrict__ subs, int sub) {
+  const SubDev& S = subs[sub];
+  const int64_t j = blockIdx.x;
+  const int64_t b = S.up[j], e = S.up[j + 1];
+  const int Lc = (int)(j / TB), jl = (int)(j % TB);
+  for (int64_t p = b + threadIdx.x; p < e; p += blockDim.x) {
+    const int64_t i = S.ui[p];
+    const int K = (int)(i / TB), il = (int)(i % TB);
+    S.tiles[tri_index(K, Lc) * TILE + swz(jl, il)] = S.raw[p];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 2. inverse of each diagonal block (column forward substitution in smem)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) diag_inverse_kernel(const SubDev* __restrict__ subs,
+                                                           const int4* __restrict__ work) {
+  extern __shared__ double dsm[];
+  double* sL = dsm;             // packed row-major lower: (i,j) at i(i+1)/2+j
+  double* sY = dsm + 8256;
+  const int4 w = work[blockIdx.x];
+  const SubDev& S = subs[w.x];
+  const int k = w.y;
+  double* tile = S.tiles + tri_index(k, k) * TILE;
+  for (int idx = threadIdx.x; idx < TILE; idx += 128) {
+    const int jl = idx >> 7;
+    const int il = (idx & 127) ^ ((jl & 3) << 2);
+    if (il >= jl) sL[il * (il + 1) / 2 + jl] = tile[idx];
+  }
+  __syncthreads();
+  const int c = threadIdx.x;
+  for (int i = c; i < TB; ++i) {
+    const double* Li = sL + i * (i + 1) / 2;
+    double acc = (i == c) ? 1.0 : 0.0;
+    for (int j = c; j < i; ++j) acc -= Li[j] * sY[j * (j + 1) / 2 + c];
+    sY[i * (i + 1) / 2 + c] = acc / Li[i];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < TILE; idx += 128) {
+    const int jl = idx >> 7;
+    const int il = (idx & 127) ^ ((jl & 3) << 2);
+    tile[idx] = (il >= jl) ? sY[il * (il + 1) / 2 + jl] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3. block-row scaling  Lhat_kl = inv(L_kk) * L_kl  (in place, half tile/CTA)
+// ---------------------------------------------------------------------------
+// work: (sub, k, l, half).  A = inv(L_kk) (col-major swizzled, 4 slices),
+// B = L_kl columns [half*64, half*64+64) read as [n][k] (col-major) tiles.
+__global__ void __launch_bounds__(256, 1) block_scale_kernel(const SubDev* __restrict__ subs,
+                                                             const int4* __restrict__ work) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);   // 4 * SLICE
+  double* sB = sA + 4 * SLICE;                        // 64 x 128
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sB + 64 * TB);  // [0..3] A slices, [4] B
+  const int4 w = work[blockIdx.x];
+  const SubDev& S = subs[w.x];
+  const int k = w.y, l = w.z, half = w.w;
+  const double* inv = S.tiles + tri_index(k, k) * TILE;
+  double* Lkl = S.tiles + tri_index(k, l) * TILE;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 5; ++i) mbar_init(&bar[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&bar[4], 64 * TB * 8);
+    bulk_g2s(sB, Lkl + half * 64 * TB, 64 * TB * 8, &bar[4]);
+    for (int s = 0; s < 4; ++s) {
+      mbar_arrive_expect_tx(&bar[s], SLICE * 8);
+      bulk_g2s(sA + s * SLICE, inv + s * SLICE, SLICE * 8, &bar[s]);
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp >> 1, wn = warp & 1;     // warp tile 32 x 32 of 128 x 64
+  const int g = lane >> 2, t = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  mbar_wait(&bar[4], 0);
+  // inv(L_kk)[i][kk] == 0 for kk > i: rows wm*32.. need kk <= wm*32+31
+  const int kb_end = wm * 8 + 8;
+  for (int kb = 0; kb < kb_end; ++kb) {
+    if ((kb & 7) == 0) mbar_wait(&bar[kb >> 3], 0);
+    const int kk = kb * 4 + t;
+    double af[4], bf[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) af[mi] = sA[swz(kk, wm * 32 + mi * 8 + g)];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) bf[ni] = sB[swz(wn * 32 + ni * 8 + g, kk)];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+  }
+  // every warp must be done reading sB/sA before anyone overwrites L_kl?  The
+  // writes go to global memory (Lkl), which sB was copied from; the bulk copy
+  // has completed (waited above), so no hazard.
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int i = wm * 32 + mi * 8 + g;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int j = half * 64 + wn * 32 + ni * 8 + 2 * t;
+      Lkl[swz(j, i)] = acc[mi][ni][0];
+      Lkl[swz(j + 1, i)] = acc[mi][ni][1];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// shared consumer micro-kernel: 128x128 CTA tile, 8 warps of 64x32,
+// one 32-deep slice of A ([k][m] swizzled) and B ([k][n] swizzled).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mma_slice_128x128(const double* __restrict__ a_s,
+                                                  const double* __restrict__ b_s, double (&acc)[8][4][2],
+                                                  int wm, int wn, int g, int t) {
+#pragma unroll
+  for (int kb = 0; kb < KS / 4; ++kb) {
+    const int kr = kb * 4 + t;
+    double bf[4];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) bf[ni] = b_s[swz(kr, wn * 32 + ni * 8 + g)];
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const double af = a_s[swz(kr, wm * 64 + mi * 8 + g)];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
+    }
+  }
+}
+
+constexpr int PIPE_STAGES = 3;
+constexpr int PIPE_THREADS = 288;   // 8 DMMA warps + 1 bulk-copy producer warp
+
+// ---------------------------------------------------------------------------
+// 4. pruned forward solve, one (subdomain, panel) chain per CTA
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(PIPE_THREADS, 1) trsm_chain_kernel(const SubDev* __restrict__ subs,
+                                                                     const int4* __restrict__ work) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);
+  double* sB = sA + PIPE_STAGES * SLICE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + PIPE_STAGES * SLICE);
+  uint64_t* empty = full + PIPE_STAGES;
+  uint64_t* xready = empty + PIPE_STAGES;
+
+  const int4 w = work[blockIdx.x];
+  const SubDev& S = subs[w.x];
+  const int c = w.y;
+  const int T = S.T;
+  const int s0 = S.panel_minrow[c] / TB;
+  double* X = S.X + (size_t)c * T * TILE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PIPE_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 8);
+    }
+    mbar_init(xready, 8);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == 8) {  // ---- producer: bulk copies of Lhat_kl and X_l slices
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int k = s0 + 1; k < T; ++k) {
+        const double* Lrow = S.tiles + tri_index(k, 0) * TILE;
+        for (int l = s0; l < k; ++l) {
+          if (l == k - 1) mbar_wait(xready, (uint32_t)((k - 1 - s0) & 1));
+          const double* At = Lrow + (size_t)l * TILE;
+          const double* Bt = X + (size_t)l * TILE;
+          for (int s = 0; s < TB / KS; ++s) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], 2 * SLICE * 8);
+            bulk_g2s(sA + stage * SLICE, At + s * SLICE, SLICE * 8, &full[stage]);
+            bulk_g2s(sB + stage * SLICE, Bt + s * SLICE, SLICE * 8, &full[stage]);
+            if (++stage == PIPE_STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers
+  const int wm = warp >> 2, wn = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+  int rj[4][2];
+  double sj[4][2];
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = c * TB + wn * 32 + ni * 8 + 2 * t + e;
+      rj[ni][e] = S.r_sorted[j];
+      sj[ni][e] = S.s_sorted[j];
+    }
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int k = s0; k < T; ++k) {
+    double acc[8][4][2];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    const int nsl = (k - s0) * (TB / KS);
+    for (int sl = 0; sl < nsl; ++sl) {
+      mbar_wait(&full[stage], phase);
+      mma_slice_128x128(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == PIPE_STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    // epilogue: X_k = inv(L_kk) Z_k - acc
+    const double* inv = S.tiles + tri_index(k, k) * TILE;
+    double* Xk = X + (size_t)k * TILE;
+    const int kb0 = k * TB;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int i = wm * 64 + mi * 8 + g;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        double v[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int rr = rj[ni][e] - kb0;
+          double pv = 0.0;
+          if (rr >= 0 && rr < TB && i >= rr) pv = sj[ni][e] * inv[swz(rr, i)];
+          v[e] = pv - acc[mi][ni][e];
+        }
+        const int j0 = wn * 32 + ni * 8 + 2 * t;
+        *reinterpret_cast<double2*>(Xk + swz(i, j0)) = make_double2(v[0], v[1]);
+      }
+    }
+    fence_proxy_async_global();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(xready);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 5. SYRK  F_IJ = X_I^T X_J  (I <= J), pruned to rows >= max first row
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(PIPE_THREADS, 1) syrk_kernel(const SubDev* __restrict__ subs,
+                                                               const int4* __restrict__ work) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);
+  double* sB = sA + PIPE_STAGES * SLICE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + PIPE_STAGES * SLICE);
+  uint64_t* empty = full + PIPE_STAGES;
+
+  const int4 w = work[blockIdx.x];
+  const SubDev& S = subs[w.x];
+  const int I = w.y, J = w.z;
+  const int T = S.T;
+  const int rstart = max(S.panel_minrow[I], S.panel_minrow[J]) & ~(KS - 1);
+  const int rend = (S.n + KS - 1) & ~(KS - 1);
+  const int nsl = (rend - rstart) / KS;
+  const double* XI = S.X + (size_t)I * T * TILE;
+  const double* XJ = S.X + (size_t)J * T * TILE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PIPE_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 8);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == 8) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int sl = 0; sl < nsl; ++sl) {
+        const size_t off = (size_t)(rstart + sl * KS) * TB;
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], 2 * SLICE * 8);
+        bulk_g2s(sA + stage * SLICE, XI + off, SLICE * 8, &full[stage]);
+        bulk_g2s(sB + stage * SLICE, XJ + off, SLICE * 8, &full[stage]);
+        if (++stage == PIPE_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  const int wm = warp >> 2, wn = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int sl = 0; sl < nsl; ++sl) {
+    mbar_wait(&full[stage], phase);
+    mma_slice_128x128(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == PIPE_STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  const int T32 = S.T32;
+#pragma unroll
+  for (int mi = 0; mi < 8; ++mi) {
+    const int a = I * TB + wm * 64 + mi * 8 + g;
+    const int ti = a >> 5;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int b = J * TB + wn * 32 + ni * 8 + 2 * t;
+      const int tj = b >> 5;
+      if (ti <= tj && tj < T32) {
+        double* dst = S.F + apply_tile_index(ti, tj, T32) * ATILE + (a & 31) * AT + (b & 31);
+        *reinterpret_cast<double2*>(dst) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 6. apply: batched packed SYMV fused with the B~ gather/scatter
+// ---------------------------------------------------------------------------
+// work: (sub, tile_begin, tile_end, partial slot)
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict__ subs,
+                                                        const int4* __restrict__ work,
+                                                        const int64_t* __restrict__ part_off,
+                                                        double* __restrict__ part,
+                                                        const double* __restrict__ p) {
+  extern __shared__ double asmem[];
+  const int4 w = work[blockIdx.x];
+  const SubDev& S = subs[w.x];
+  const int T32 = S.T32;
+  const int M = T32 * AT;
+  double* sp = asmem;
+  double* sq = asmem + M;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int a = tid; a < M; a += NW * 32) {
+    const int gi = S.gids_sorted[a];
+    sp[a] = gi >= 0 ? __ldg(p + gi) : 0.0;
+  }
+  for (int a = tid; a < NW * M; a += NW * 32) sq[a] = 0.0;
+  __syncthreads();
+  double* myq = sq + warp * M;
+
+  int64_t tt = (int64_t)w.y + warp;
+  const int64_t t1 = w.z;
+  int ti = 0;
+  int64_t rowstart = 0;
+  while (ti < T32 && rowstart + (T32 - ti) <= tt) {
+    rowstart += T32 - ti;
+    ++ti;
+  }
+  int tj = ti + (int)(tt - rowstart);
+  const double* Fbase = S.F;
+  for (; tt < t1; tt += NW) {
+    const double* Ft = Fbase + tt * ATILE + lane;
+    double f[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) f[r] = __ldcs(Ft + r * AT);
+    if (ti != tj) {
+      double cs = 0.0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) cs = fma(f[r], sp[ti * AT + r], cs);
+      myq[tj * AT + lane] += cs;
+    }
+    const double pj = sp[tj * AT + lane];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) f[r] *= pj;
+    // butterfly transpose-reduce: lane r ends with sum_l F[r][l] p_J[l]
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const bool up = (lane & off) != 0;
+#pragma unroll
+      for (int i = 0; i < off; ++i) {
+        const double send = up ? f[i] : f[i + off];
+        const double keep = up ? f[i + off] : f[i];
+        f[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    myq[ti * AT + lane] += f[0];
+    int rem = (tj - ti) + NW;
+    while (ti < T32 && rem >= T32 - ti) {
+      rem -= T32 - ti;
+      ++ti;
+    }
+    tj = ti + rem;
+  }
+  __syncthreads();
+  double* out = part + part_off[w.w];
+  for (int a = tid; a < S.m; a += NW * 32) {
+    double s = 0.0;
+#pragma unroll
+    for (int wi = 0; wi < NW; ++wi) s += sq[wi * M + a];
+    out[a] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 7. ordered reduction into the global dual vector
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) reduce_kernel(int n_mult, const int* __restrict__ cptr,
+                                                     const int4* __restrict__ cent,
+                                                     const int64_t* __restrict__ part_off,
+                                                     const double* __restrict__ part, double* __restrict__ q) {
+  const int gidx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gidx >= n_mult) return;
+  double acc = 0.0;
+  for (int e = cptr[gidx]; e < cptr[gidx + 1]; ++e) {
+    const int4 c = cent[e];
+    double v = 0.0;
+    for (int s = c.y; s < c.z; ++s) v += part[part_off[s] + c.x];
+    acc += v;
+  }
+  q[gidx] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static size_t pipe_smem() { return 2 * PIPE_STAGES * SLICE * sizeof(double) + 8 * (2 * PIPE_STAGES + 1); }
+static size_t scale_smem() { return (4 * SLICE + 64 * TB) * sizeof(double) + 8 * 5; }
+
+cudaError_t configure_kernels() {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(trsm_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem())))
+    return e;
+  if ((e = cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem())))
+    return e;
+  if ((e = cudaFuncSetAttribute(block_scale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)scale_smem())))
+    return e;
+  if ((e = cudaFuncSetAttribute(diag_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                2 * 8256 * 8)))
+    return e;
+  if ((e = cudaFuncSetAttribute(apply_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
+    return e;
+  if ((e = cudaFuncSetAttribute(apply_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
+    return e;
+  if ((e = cudaFuncSetAttribute(apply_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
+    return e;
+  if ((e = cudaFuncSetAttribute(apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
+    return e;
+  return cudaSuccess;
+}
+
+void launch_unpack(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
+  if (nwork > 0) unpack_dense_kernel<<<nwork, 256, 0, st>>>(subs, work);
+}
+void launch_scatter_sparse(const SubDev* subs, int sub, int n, cudaStream_t st) {
+  if (n > 0) scatter_sparse_kernel<<<n, 256, 0, st>>>(subs, sub);
+}
+void launch_diag_inverse(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
+  if (nwork > 0) diag_inverse_kernel<<<nwork, 128, 2 * 8256 * 8, st>>>(subs, work);
+}
+void launch_block_scale(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
+  if (nwork > 0) block_scale_kernel<<<nwork, 256, scale_smem(), st>>>(subs, work);
+}
+void launch_trsm_chain(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
+  if (nwork > 0) trsm_chain_kernel<<<nwork, PIPE_THREADS, pipe_smem(), st>>>(subs, work);
+}
+void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
+  if (nwork > 0) syrk_kernel<<<nwork, PIPE_THREADS, pipe_smem(), st>>>(subs, work);
+}
+void launch_apply(int nw, size_t smem, const SubDev* subs, const int4* work, int nwork, const int64_t* part_off,
+                  double* part, const double* p, cudaStream_t st) {
+  if (nwork <= 0) return;
+  switch (nw) {
+    case 8: apply_kernel<8><<<nwork, 256, smem, st>>>(subs, work, part_off, part, p); break;
+    case 4: apply_kernel<4><<<nwork, 128, smem, st>>>(subs, work, part_off, part, p); break;
+    case 2: apply_kernel<2><<<nwork, 64, smem, st>>>(subs, work, part_off, part, p); break;
+    default: apply_kernel<1><<<nwork, 32, smem, st>>>(subs, work, part_off, part, p); break;
+  }
+}
+void launch_reduce(int n_mult, const int* cptr, const int4* cent, const int64_t* part_off, const double* part,
+                   double* q, cudaStream_t st) {
+  if (n_mult > 0) reduce_kernel<<<(n_mult + 255) / 256, 256, 0, st>>>(n_mult, cptr, cent, part_off, part, q);
+}
+
+}  // namespace feti
+
+namespace feti {
+// diagnostics: per-kernel register/thread limits (used by tests and debugging)
+int kernel_attributes(char* buf, int len) {
+  struct K { const char* name; const void* fn; } ks[] = {
+      {"unpack_dense", (const void*)unpack_dense_kernel},   {"scatter_sparse", (const void*)scatter_sparse_kernel},
+      {"diag_inverse", (const void*)diag_inverse_kernel},   {"block_scale", (const void*)block_scale_kernel},
+      {"trsm_chain", (const void*)trsm_chain_kernel},       {"syrk", (const void*)syrk_kernel},
+      {"apply8", (const void*)apply_kernel<8>},             {"reduce", (const void*)reduce_kernel}};
+  int off = 0;
+  for (auto& k : ks) {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, k.fn);
+    off += snprintf(buf + off, len - off, "%s: err=%d regs=%d maxthr=%d smem_static=%zu maxdyn=%d\n", k.name, (int)e,
+                    a.numRegs, a.maxThreadsPerBlock, a.sharedSizeBytes, a.maxDynamicSharedSizeBytes);
+    if (off >= len) break;
+  }
+  return off;
+}
+}  // namespace feti

@@ -1,0 +1,23 @@
+// Host-side launch interface of the device kernels (feti_kernels.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "feti_common.cuh"
+
+namespace feti {
+
+cudaError_t configure_kernels();
+int kernel_attributes(char* buf, int len);
+void launch_unpack(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
+void launch_scatter_sparse(const SubDev* subs, int sub, int n, cudaStream_t st);
+void launch_diag_inverse(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
+void launch_block_scale(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
+void launch_trsm_chain(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
+void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
+void launch_apply(int nw, size_t smem, const SubDev* subs, const int4* work, int nwork, const int64_t* part_off,
+                  double* part, const double* p, cudaStream_t st);
+void launch_reduce(int n_mult, const int* cptr, const int4* cent, const int64_t* part_off, const double* part,
+                   double* q, cudaStream_t st);
+
+}  // namespace feti
