@@ -124,8 +124,9 @@ int feti_local_operator(feti_ctx* ctx, int64_t slot, double* out);
  * Host vectors of length n_multipliers; q is overwritten. */
 int feti_apply(feti_ctx* ctx, const double* p, double* q);
 
-/* Same on device vectors, enqueued on `stream` (cudaStream_t; NULL = the
- * context stream).  Does not synchronise. */
+/* Same on device vectors, enqueued on `stream` (a cudaStream_t used
+ * verbatim: NULL is the legacy default stream).  Does not synchronise; the
+ * caller orders it after feti_assemble (which returns synchronised). */
 int feti_apply_device(feti_ctx* ctx, const double* d_p, double* d_q, void* stream);
 
 int feti_get_stats(feti_ctx* ctx, feti_stats* out);

@@ -63,6 +63,8 @@ int fail(int code, const char* fmt, ...) {
 struct SubHost {
   int64_t n = 0, m = 0, nnz = 0;
   int T = 0, P = 0, T32 = 0;
+  int smin = 0;                      // first block row reached by any X column
+  int64_t raw_off = 0;               // first factor value the device needs
   bool dense = true;
   std::vector<int64_t> colperm;      // sorted position -> original local row
   std::vector<int> r_sorted;         // P*128
@@ -86,6 +88,8 @@ struct SubHost {
   bool factor_from_host = false;
   cudaEvent_t ev_upload = nullptr;
   int64_t f_tiles() const { return (int64_t)T32 * (T32 + 1) / 2; }
+  int64_t l_tiles() const { return (int64_t)(T - smin) * (T - smin + 1) / 2; }
+  int64_t upload_count() const { return nnz - raw_off; }
 };
 
 struct DevBuf {
@@ -166,12 +170,13 @@ int sync_subdev(feti_ctx* c) {
     d.gids_sorted = s.d_g;
     d.panel_minrow = s.d_pmin;
     d.nnz = s.nnz;
+    d.raw_off = s.raw_off;
+    d.smin = s.smin;
     d.n = (int)s.n;
     d.m = (int)s.m;
     d.T = s.T;
     d.P = s.P;
     d.T32 = s.T32;
-    d.pad_ = 0;
   }
   if (!h.empty())
     CUDA_TRY(cudaMemcpyAsync(c->d_subdev, h.data(), h.size() * sizeof(SubDev), cudaMemcpyHostToDevice,
@@ -276,6 +281,10 @@ int feti_add_subdomain(feti_ctx* c, int64_t n, int64_t m, const int64_t* first_r
   }
   s.panel_minrow.resize(s.P);
   for (int p = 0; p < s.P; ++p) s.panel_minrow[p] = s.r_sorted[(size_t)p * TB];
+  // pruning: nothing above the smallest first row is ever read
+  s.smin = s.P > 0 ? s.panel_minrow[0] / TB : s.T;
+  const int64_t j0 = std::min<int64_t>((int64_t)s.smin * TB, n);
+  s.raw_off = dense ? (j0 * n - j0 * (j0 - 1) / 2) : (j0 < n ? up[j0] : nnz);
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaEventCreateWithFlags(&s.ev_upload, cudaEventDisableTiming));
   c->subs.push_back(std::move(s));
@@ -297,8 +306,8 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   size_t need = 0;
   int max_M = 0;
   for (auto& s : c->subs) {
-    need += (size_t)s.T * (s.T + 1) / 2 * TILE * 8;   // tiles
-    need += (size_t)s.P * s.T * TILE * 8;             // X panels
+    need += (size_t)s.l_tiles() * TILE * 8;            // tiles
+    need += (size_t)s.P * (s.T - s.smin) * TILE * 8;   // X panels
     need += (size_t)s.f_tiles() * ATILE * 8;          // F~
     max_M = std::max(max_M, s.T32 * AT);
   }
@@ -311,8 +320,10 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
 
   int rc;
   for (auto& s : c->subs) {
-    if ((rc = dev_alloc(c, (void**)&s.d_tiles, (size_t)s.T * (s.T + 1) / 2 * TILE * 8, false))) return rc;
-    if ((rc = dev_alloc(c, (void**)&s.d_X, (size_t)std::max(s.P, 1) * s.T * TILE * 8, false))) return rc;
+    if ((rc = dev_alloc(c, (void**)&s.d_tiles, (size_t)std::max<int64_t>(s.l_tiles(), 1) * TILE * 8, false)))
+      return rc;
+    if ((rc = dev_alloc(c, (void**)&s.d_X, (size_t)std::max(s.P, 1) * std::max(s.T - s.smin, 1) * TILE * 8, false)))
+      return rc;
     if ((rc = dev_alloc(c, (void**)&s.d_F, (size_t)std::max<int64_t>(s.f_tiles(), 1) * ATILE * 8, true)))
       return rc;
     if ((rc = upload(c, &s.d_r, s.r_sorted))) return rc;
@@ -334,13 +345,14 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   const double tb3 = 2.0 * TB * TB * TB;
   for (int si = 0; si < (int)c->subs.size(); ++si) {
     const SubHost& s = c->subs[si];
-    for (int K = 0; K < s.T; ++K)
-      for (int L = 0; L <= K; ++L) wu.push_back(make_int4(si, K, L, 0));
-    for (int k = 0; k < s.T; ++k) wd.push_back(make_int4(si, k, 0, 0));
-    for (int k = 1; k < s.T; ++k)
-      for (int l = 0; l < k; ++l)
+    for (int K = s.smin; K < s.T; ++K)
+      for (int L = s.smin; L <= K; ++L) wu.push_back(make_int4(si, K, L, 0));
+    for (int k = s.smin; k < s.T; ++k) wd.push_back(make_int4(si, k, 0, 0));
+    for (int k = s.smin + 1; k < s.T; ++k)
+      for (int l = s.smin; l < k; ++l)
         for (int h = 0; h < 2; ++h) ws.push_back(make_int4(si, k, l, h));
-    scale_exec += (double)s.T * (s.T - 1) / 2 * 2.0 * (2.0 * 64 * 32 * 32 * (1 + 2 + 3 + 4));
+    const double tt = s.T - s.smin;
+    scale_exec += tt * (tt - 1) / 2 * 2.0 * (2.0 * 64 * 32 * 32 * (1 + 2 + 3 + 4));
     for (int p = 0; p < s.P; ++p) {
       wc.push_back(make_int4(si, p, 0, 0));
       const double s0 = s.panel_minrow[p] / TB;
@@ -467,14 +479,17 @@ int feti_set_factor(feti_ctx* c, int64_t slot, const double* values, int64_t nnz
   if (!values) return fail(FETI_ERR_ARG, "values is NULL");
   CUDA_TRY(cudaSetDevice(c->device));
   if (where == FETI_FACTOR_DEVICE) {
-    s.d_raw = values;
+    s.d_raw = values + s.raw_off;
     s.factor_from_host = false;
   } else {
     if (!s.d_raw_own) {
-      int rc = dev_alloc(c, (void**)&s.d_raw_own, (size_t)s.nnz * 8, true);
+      int rc = dev_alloc(c, (void**)&s.d_raw_own, (size_t)std::max<int64_t>(s.upload_count(), 1) * 8, true);
       if (rc) return rc;
     }
-    CUDA_TRY(cudaMemcpyAsync(s.d_raw_own, values, (size_t)s.nnz * 8, cudaMemcpyHostToDevice, c->copy_stream));
+    // only the values the pruned solve reads: a suffix of the reference layout
+    if (s.upload_count() > 0)
+      CUDA_TRY(cudaMemcpyAsync(s.d_raw_own, values + s.raw_off, (size_t)s.upload_count() * 8,
+                               cudaMemcpyHostToDevice, c->copy_stream));
     CUDA_TRY(cudaEventRecord(s.ev_upload, c->copy_stream));
     s.d_raw = s.d_raw_own;
     s.factor_from_host = true;
@@ -504,7 +519,7 @@ int feti_assemble(feti_ctx* c) {
   launches += c->n_unpack > 0;
   for (int si = 0; si < (int)c->subs.size(); ++si)
     if (!c->subs[si].dense) {
-      launch_scatter_sparse(c->d_subdev, si, (int)c->subs[si].n, st);
+      launch_scatter_sparse(c->d_subdev, si, (int)(c->subs[si].n - (int64_t)c->subs[si].smin * TB), st);
       ++launches;
     }
   CUDA_TRY(cudaGetLastError());
@@ -544,7 +559,7 @@ int feti_assemble(feti_ctx* c) {
   S.launches_assemble = launches;
   double fb = 0;
   for (auto& s : c->subs)
-    if (s.factor_from_host) fb += 8.0 * s.nnz;
+    if (s.factor_from_host) fb += 8.0 * s.upload_count();
   S.factor_bytes = fb;
   c->assembled = true;
   return FETI_OK;
@@ -609,8 +624,8 @@ int feti_apply_device(feti_ctx* c, const double* d_p, double* d_q, void* stream)
   if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "apply before preprocess for the current values");
   if (!d_p || !d_q) return fail(FETI_ERR_ARG, "NULL vector");
   CUDA_TRY(cudaSetDevice(c->device));
-  cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
-  return apply_enqueue(c, d_p, d_q, st, false);
+  // the handle is used verbatim: NULL is the legacy default stream, as in CUDA
+  return apply_enqueue(c, d_p, d_q, (cudaStream_t)stream, false);
 }
 
 int feti_get_stats(feti_ctx* c, feti_stats* out) {

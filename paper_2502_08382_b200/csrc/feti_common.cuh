@@ -52,9 +52,24 @@ struct SubDev {
   const int* gids_sorted;   // T32*32 global multiplier ids (-1 pads)
   const int* panel_minrow;  // P
   int64_t nnz;
+  int64_t raw_off;          // raw points at value index raw_off (suffix upload)
   int n, m, T, P, T32;
-  int pad_;
+  int smin;                 // first block row any X column reaches (pruning)
 };
+
+// Only block rows/columns >= smin are ever touched: X = L^-1 P B~^T is zero
+// above the smallest first row of the subdomain, so the tiles of L, the X
+// panels and the factor upload all start there.
+__host__ __device__ __forceinline__ int64_t tile_offset(int smin, int K, int Lc) {
+  return tri_index(K - smin, Lc - smin) * TILE;
+}
+__device__ __forceinline__ double* tile_ptr(const SubDev& S, int K, int Lc) {
+  return S.tiles + tile_offset(S.smin, K, Lc);
+}
+// X panel c, global row `row` (>= smin*128), row-major swizzled, 128 wide
+__device__ __forceinline__ double* xrow_ptr(const SubDev& S, int c, int row) {
+  return S.X + (size_t)c * (S.T - S.smin) * TILE + (size_t)(row - S.smin * TB) * TB;
+}
 
 // ---- PTX wrappers ------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

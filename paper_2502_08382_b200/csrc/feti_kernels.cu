@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) unpack_dense_kernel(const SubDev* __restr
   const SubDev& S = subs[w.x];
   const int K = w.y, Lc = w.z;
   const int64_t n = S.n;
-  double* tile = S.tiles + tri_index(K, Lc) * TILE;
+  double* tile = tile_ptr(S, K, Lc);
   const bool dense = (S.up == nullptr);
   for (int idx = threadIdx.x; idx < TILE; idx += blockDim.x) {
     const int jl = idx >> 7;
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) unpack_dense_kernel(const SubDev* __restr
     const int64_t i = (int64_t)K * TB + il, j = (int64_t)Lc * TB + jl;
     double v = 0.0;
     if (i < n && j < n) {
-      if (dense && i >= j) v = __ldcs(S.raw + (j * n - j * (j - 1) / 2) + (i - j));
+      if (dense && i >= j) v = __ldcs(S.raw + ((j * n - j * (j - 1) / 2) + (i - j) - S.raw_off));
     } else if (i == j) {
       v = 1.0;  // identity padding keeps the diagonal blocks invertible
     }
@@ -55,16 +55,16 @@ __global__ void __launch_bounds__(256) unpack_dense_kernel(const SubDev* __restr
   }
 }
 
-// Sparse pattern: one CTA per factor column j (row j of U), entries up[j]..
+// Sparse pattern: one CTA per factor column j >= smin*128 (row j of U)
 __global__ void __launch_bounds__(256) scatter_sparse_kernel(const SubDev* __restrict__ subs, int sub) {
   const SubDev& S = subs[sub];
-  const int64_t j = blockIdx.x;
+  const int64_t j = (int64_t)S.smin * TB + blockIdx.x;
   const int64_t b = S.up[j], e = S.up[j + 1];
   const int Lc = (int)(j / TB), jl = (int)(j % TB);
   for (int64_t p = b + threadIdx.x; p < e; p += blockDim.x) {
     const int64_t i = S.ui[p];
     const int K = (int)(i / TB), il = (int)(i % TB);
-    S.tiles[tri_index(K, Lc) * TILE + swz(jl, il)] = S.raw[p];
+    tile_ptr(S, K, Lc)[swz(jl, il)] = S.raw[p - S.raw_off];
   }
 }
 
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(128) diag_inverse_kernel(const SubDev* __restr
   const int4 w = work[blockIdx.x];
   const SubDev& S = subs[w.x];
   const int k = w.y;
-  double* tile = S.tiles + tri_index(k, k) * TILE;
+  double* tile = tile_ptr(S, k, k);
   for (int idx = threadIdx.x; idx < TILE; idx += 128) {
     const int jl = idx >> 7;
     const int il = (idx & 127) ^ ((jl & 3) << 2);
@@ -115,8 +115,8 @@ __global__ void __launch_bounds__(256, 1) block_scale_kernel(const SubDev* __res
   const int4 w = work[blockIdx.x];
   const SubDev& S = subs[w.x];
   const int k = w.y, l = w.z, half = w.w;
-  const double* inv = S.tiles + tri_index(k, k) * TILE;
-  double* Lkl = S.tiles + tri_index(k, l) * TILE;
+  const double* inv = tile_ptr(S, k, k);
+  double* Lkl = tile_ptr(S, k, l);
   if (threadIdx.x == 0) {
     for (int i = 0; i < 5; ++i) mbar_init(&bar[i], 1);
     mbar_fence_init();
@@ -211,7 +211,6 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) trsm_chain_kernel(const SubDe
   const int c = w.y;
   const int T = S.T;
   const int s0 = S.panel_minrow[c] / TB;
-  double* X = S.X + (size_t)c * T * TILE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -229,11 +228,10 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) trsm_chain_kernel(const SubDe
       int stage = 0;
       uint32_t phase = 0;
       for (int k = s0 + 1; k < T; ++k) {
-        const double* Lrow = S.tiles + tri_index(k, 0) * TILE;
         for (int l = s0; l < k; ++l) {
           if (l == k - 1) mbar_wait(xready, (uint32_t)((k - 1 - s0) & 1));
-          const double* At = Lrow + (size_t)l * TILE;
-          const double* Bt = X + (size_t)l * TILE;
+          const double* At = tile_ptr(S, k, l);
+          const double* Bt = xrow_ptr(S, c, l * TB);
           for (int s = 0; s < TB / KS; ++s) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], 2 * SLICE * 8);
@@ -283,8 +281,8 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) trsm_chain_kernel(const SubDe
       }
     }
     // epilogue: X_k = inv(L_kk) Z_k - acc
-    const double* inv = S.tiles + tri_index(k, k) * TILE;
-    double* Xk = X + (size_t)k * TILE;
+    const double* inv = tile_ptr(S, k, k);
+    double* Xk = xrow_ptr(S, c, k * TB);
     const int kb0 = k * TB;
 #pragma unroll
     for (int mi = 0; mi < 8; ++mi) {
@@ -323,12 +321,11 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) syrk_kernel(const SubDev* __r
   const int4 w = work[blockIdx.x];
   const SubDev& S = subs[w.x];
   const int I = w.y, J = w.z;
-  const int T = S.T;
   const int rstart = max(S.panel_minrow[I], S.panel_minrow[J]) & ~(KS - 1);
   const int rend = (S.n + KS - 1) & ~(KS - 1);
   const int nsl = (rend - rstart) / KS;
-  const double* XI = S.X + (size_t)I * T * TILE;
-  const double* XJ = S.X + (size_t)J * T * TILE;
+  const double* XI = xrow_ptr(S, I, rstart);
+  const double* XJ = xrow_ptr(S, J, rstart);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -345,7 +342,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) syrk_kernel(const SubDev* __r
       int stage = 0;
       uint32_t phase = 0;
       for (int sl = 0; sl < nsl; ++sl) {
-        const size_t off = (size_t)(rstart + sl * KS) * TB;
+        const size_t off = (size_t)sl * KS * TB;
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full[stage], 2 * SLICE * 8);
         bulk_g2s(sA + stage * SLICE, XI + off, SLICE * 8, &full[stage]);
@@ -399,6 +396,49 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) syrk_kernel(const SubDev* __r
 // 6. apply: batched packed SYMV fused with the B~ gather/scatter
 // ---------------------------------------------------------------------------
 // work: (sub, tile_begin, tile_end, partial slot)
+//
+// Lane l of a warp owns column l of a 32x32 tile (32 coalesced 256-byte row
+// reads per tile); the next tile's 32 loads are issued before the current one
+// is reduced (register double buffering) so each warp keeps 16 KB in flight.
+__device__ __forceinline__ void apply_tile_load(double (&f)[32], const double* __restrict__ Ft, int lane) {
+#pragma unroll
+  for (int r = 0; r < 32; ++r) f[r] = __ldcs(Ft + r * AT + lane);
+}
+
+__device__ __forceinline__ void apply_tile_compute(double (&f)[32], int ti, int tj, const double* __restrict__ sp,
+                                                   double* __restrict__ myq, int lane) {
+  if (ti != tj) {
+    double cs = 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) cs = fma(f[r], sp[ti * AT + r], cs);
+    myq[tj * AT + lane] += cs;
+  }
+  const double pj = sp[tj * AT + lane];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) f[r] *= pj;
+  // butterfly transpose-reduce: lane r ends with sum_l F[r][l] p_J[l]
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const double send = up ? f[i] : f[i + off];
+      const double keep = up ? f[i + off] : f[i];
+      f[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  myq[ti * AT + lane] += f[0];
+}
+
+__device__ __forceinline__ void apply_advance(int& ti, int& tj, int step, int T32) {
+  int rem = (tj - ti) + step;
+  while (ti < T32 && rem >= T32 - ti) {
+    rem -= T32 - ti;
+    ++ti;
+  }
+  tj = ti + rem;
+}
+
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict__ subs,
                                                         const int4* __restrict__ work,
@@ -430,39 +470,26 @@ __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict
     ++ti;
   }
   int tj = ti + (int)(tt - rowstart);
-  const double* Fbase = S.F;
-  for (; tt < t1; tt += NW) {
-    const double* Ft = Fbase + tt * ATILE + lane;
-    double f[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) f[r] = __ldcs(Ft + r * AT);
-    if (ti != tj) {
-      double cs = 0.0;
-#pragma unroll
-      for (int r = 0; r < 32; ++r) cs = fma(f[r], sp[ti * AT + r], cs);
-      myq[tj * AT + lane] += cs;
-    }
-    const double pj = sp[tj * AT + lane];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) f[r] *= pj;
-    // butterfly transpose-reduce: lane r ends with sum_l F[r][l] p_J[l]
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      const bool up = (lane & off) != 0;
-#pragma unroll
-      for (int i = 0; i < off; ++i) {
-        const double send = up ? f[i] : f[i + off];
-        const double keep = up ? f[i + off] : f[i];
-        f[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-      }
-    }
-    myq[ti * AT + lane] += f[0];
-    int rem = (tj - ti) + NW;
-    while (ti < T32 && rem >= T32 - ti) {
-      rem -= T32 - ti;
-      ++ti;
-    }
-    tj = ti + rem;
+  const double* Fb = S.F;
+  double fa[32], fb[32];
+  if (tt < t1) apply_tile_load(fa, Fb + tt * ATILE, lane);
+  while (tt < t1) {
+    int ti2 = ti, tj2 = tj;
+    apply_advance(ti2, tj2, NW, T32);
+    int64_t nx = tt + NW;
+    if (nx < t1) apply_tile_load(fb, Fb + nx * ATILE, lane);
+    apply_tile_compute(fa, ti, tj, sp, myq, lane);
+    tt = nx;
+    ti = ti2;
+    tj = tj2;
+    if (tt >= t1) break;
+    apply_advance(ti2, tj2, NW, T32);
+    nx = tt + NW;
+    if (nx < t1) apply_tile_load(fa, Fb + nx * ATILE, lane);
+    apply_tile_compute(fb, ti, tj, sp, myq, lane);
+    tt = nx;
+    ti = ti2;
+    tj = tj2;
   }
   __syncthreads();
   double* out = part + part_off[w.w];

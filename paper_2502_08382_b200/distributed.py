@@ -1,0 +1,93 @@
+"""Subdomains across GPUs: one process per GPU, one cluster per rank.
+
+The reference lays subdomains out in contiguous clusters
+(``build_clusters``, decomposition.py:227-243) and the paper maps one cluster
+to one GPU, synchronising cluster dual vectors between
+processes.  Here:
+
+* assembly is embarrassingly parallel: rank r assembles the F~_i of cluster r
+  on its own GPU, no communication;
+* apply has one exchange step: every rank applies its subdomains into a
+  full-length dual vector (zeros outside its multipliers) and the
+  contributions are summed with an NCCL all-reduce over NVLink
+  (``torch.distributed`` backend "nccl").  The p vector is broadcast from
+  rank 0 when it starts on the host.
+
+The summation order across ranks is NCCL's, so results agree with the
+reference's fixed gather order (dualop.py:375-379) to rounding (<=1e-10
+relative, the north-star bar), not bit for bit; within a rank the order is
+the reference's.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def owned_subdomains(layout, rank: int):
+    """Subdomain ids of cluster ``rank`` (the contiguous layout of the reference)."""
+    if rank >= len(layout.clusters):
+        raise ValueError(f"layout has {len(layout.clusters)} clusters, no cluster for rank {rank}")
+    return [int(s) for s in layout.clusters[rank].subdomain_ids]
+
+
+def allreduce_sum_(q, group=None):
+    """In-place sum of per-rank dual-vector contributions."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(q, op=dist.ReduceOp.SUM, group=group)
+    return q
+
+
+class ClusterDualOperator:
+    """The rank-local explicit dual operator plus the cross-rank exchange.
+
+    ``local`` is any object with ``apply_device(p, q, stream)`` writing this
+    rank's contribution over all multipliers (the B200 ``DualOperator`` built
+    with ``subdomains=owned_subdomains(layout, rank)``).
+    """
+
+    def __init__(self, local, n_multipliers: int, device, group=None):
+        import torch
+
+        self.local = local
+        self.n = int(n_multipliers)
+        self.device = device
+        self.group = group
+        self.p_dev = torch.empty(self.n, dtype=torch.float64, device=device)
+        self.q_dev = torch.empty(self.n, dtype=torch.float64, device=device)
+
+    def apply_device(self, p_dev, q_dev):
+        import torch
+
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.local.apply_device(p_dev, q_dev, stream)
+        allreduce_sum_(q_dev, self.group)
+        return q_dev
+
+    def apply(self, p=None, out=None, src: int = 0):
+        """Host-facing apply: p on rank ``src``'s host, q returned on every rank."""
+        import torch
+        import torch.distributed as dist
+
+        if p is not None:
+            self.p_dev.copy_(torch.from_numpy(np.ascontiguousarray(p, dtype=np.float64)), non_blocking=False)
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.broadcast(self.p_dev, src=src, group=self.group)
+        self.apply_device(self.p_dev, self.q_dev)
+        host = self.q_dev.cpu().numpy()
+        if out is None:
+            return host
+        out[:] = host
+        return out
+
+
+def contributions_sum(local_apply, p, group=None):
+    """Reference semantics of the exchange for any local apply callable (CPU
+    tests with gloo): q = sum over ranks of local_apply(p)."""
+    import torch
+
+    q = torch.from_numpy(np.asarray(local_apply(p), dtype=np.float64).copy())
+    allreduce_sum_(q, group)
+    return q.numpy()

@@ -147,11 +147,14 @@ class DualOperator:
       ones of this rank's cluster); ``apply`` then returns this rank's
       contribution, summed across ranks by :mod:`.distributed`
     * ``pinned``: stage host factors in page-locked memory (default True)
+    * ``perms``: explicit per-subdomain orderings (mapping or sequence indexed
+      by subdomain), as ``symbolic_factorize(ordering=<array>)`` accepts
+      (sparse.py:368-371); overrides ``ordering``
     """
 
     def __init__(self, matrices, constraints, layout, config: DualOpConfig, pool=None, workers: int = 1,
                  schur_cap: int = 2000, device: int | None = None, ordering: str = "rcm",
-                 subdomains=None, pinned: bool = True):
+                 subdomains=None, pinned: bool = True, perms=None):
         if len(matrices) != len(constraints.per_subdomain):
             raise ValueError("one stiffness matrix per subdomain required")
         if config.strategy != "explicit":
@@ -172,6 +175,7 @@ class DualOperator:
         self.ordering = ordering
         self.pinned = bool(pinned)
         self.device = device
+        self.perms = perms
         self.owned = (list(range(self.n_subdomains)) if subdomains is None
                       else sorted(int(s) for s in subdomains))
 
@@ -265,7 +269,11 @@ class DualOperator:
             sub.gids = np.ascontiguousarray(sc.multiplier_ids, dtype=np.int64)
             sub.m = int(sub.gids.shape[0])
             sub.bcol, sub.bval = _constraint_rows(sc, sub.n)
-            if self.ordering == "rcm":
+            if self.perms is not None:
+                sub.perm = np.ascontiguousarray(self.perms[i], dtype=np.int64)
+                if sub.perm.shape != (sub.n,) or not np.array_equal(np.sort(sub.perm), np.arange(sub.n)):
+                    raise ValueError(f"subdomain {i}: explicit ordering is not a permutation")
+            elif self.ordering == "rcm":
                 sub.perm = fct.rcm_ordering(matrix)
             else:
                 sub.perm = fct.interface_last_ordering(matrix, sub.bcol)
@@ -399,9 +407,12 @@ class DualOperator:
         """q = F p on device tensors (torch CUDA float64), enqueued on ``stream``."""
         if not self.step_ready:
             raise LifecycleError("apply before preprocess for the current values")
-        s = None if stream is None else C.c_void_p(int(stream))
+        if stream is None:
+            import torch
+
+            stream = torch.cuda.current_stream(p.device).cuda_stream
         _call(self._lib.feti_apply_device(self._ctx, C.c_void_p(int(p.data_ptr())),
-                                          C.c_void_p(int(q.data_ptr())), s))
+                                          C.c_void_p(int(q.data_ptr())), C.c_void_p(int(stream))))
 
     # -- K^+ access for the solver --------------------------------------------
 

@@ -68,6 +68,13 @@ class DenseSym:
 
 
 @dataclass(eq=False)
+class ShapeOnly:
+    """Stand-in stiffness when the factor is produced elsewhere (bench)."""
+
+    shape: tuple
+
+
+@dataclass(eq=False)
 class SubdomainConstraints:
     multiplier_ids: np.ndarray
     matrix: Csr

@@ -95,47 +95,52 @@ def test_same_factor_as_oracle_reference_values():
             assert np.linalg.norm(f - fo) <= 1e-12 * np.linalg.norm(fo)
 
 
+def _shifted(k, shift):
+    """K + shift*I keeping K's sparse pattern: SPD with a genuinely sparse factor."""
+    rows = np.repeat(np.arange(k.shape[0]), np.diff(k.indptr))
+    data = k.data.copy()
+    data[k.indices == rows] += shift
+    return inputs.Csr(k.shape, k.indptr, k.indices, data)
+
+
 def test_sparse_pattern_factor_through_cabi():
-    """Elasticity 3D 4^3 has exact cancellations: its reference factor pattern
-    is not a full triangle.  Pass (up, ui, values) through the C-ABI."""
-    g = load_golden("elast3d_4x2")
-    prob, mats, cons, lay = _golden_problem(g)
+    """A factor whose CSR-of-U pattern is not a full triangle (the reference's
+    symbolic stage on a sparse SPD matrix) goes through the C-ABI with its
+    (up, ui) pattern; F~ must match the oracle on the same values."""
+    prob = inputs.Problem("elasticity", 3, 3, 2)
     lib = _lib.load()
     ctx = C.c_void_p()
     _lib.check(lib.feti_create(0, C.byref(ctx)))
     try:
         syms = []
-        n_sparse = 0
         for s in range(prob.n_sub):
-            # the reference's own K data: exact cancellations in K_reg depend on
-            # the last bit of K, so the pattern is taken from its bits
-            ip, ix, dt = g[f"s{s}_k_indptr"], g[f"s{s}_k_indices"], g[f"s{s}_k_data"]
-            n = ip.shape[0] - 1
-            rip, rix, rdt, _ = ora.regularize(n, ip, ix, dt, g[f"s{s}_kernel"])
-            sym = ora.symbolic_factorize(n, rip, rix)
-            vals = ora.numeric_factorize(sym, rdt)
-            assert sym.nnz == int(g[f"s{s}_factor_nnz"])
-            n_sparse += sym.nnz < sym.n * (sym.n + 1) // 2
+            k = _shifted(prob.subdomain_system(s)[0], 1e-2)
+            sym = ora.symbolic_factorize(k.shape[0], k.indptr, k.indices)
+            vals = ora.numeric_factorize(sym, k.data)
+            assert sym.nnz < sym.n * (sym.n + 1) // 2
             first = np.ascontiguousarray(sym.iperm[prob.bcol[s]])
             slot = C.c_int64()
             _lib.check(lib.feti_add_subdomain(ctx, sym.n, first.shape[0], _lib.i64ptr(first),
                                               _lib.f64ptr(prob.bval[s]), _lib.i64ptr(prob.gids[s]),
                                               _lib.i64ptr(sym.up), _lib.i64ptr(sym.ui), sym.nnz, C.byref(slot)))
             syms.append((sym, vals))
-        assert n_sparse > 0
         _lib.check(lib.feti_finalize(ctx, prob.n_multipliers))
         for s, (sym, vals) in enumerate(syms):
             _lib.check(lib.feti_set_factor(ctx, s, C.c_void_p(vals.ctypes.data), vals.shape[0], 0))
         _lib.check(lib.feti_assemble(ctx))
-        for s in range(prob.n_sub):
+        fms = []
+        for s, (sym, vals) in enumerate(syms):
             m = prob.gids[s].shape[0]
             out = np.empty((m, m))
             _lib.check(lib.feti_local_operator(ctx, s, _lib.f64ptr(out)))
-            ref = _ref_upper(g, s, m)
+            ref = ora.assemble_explicit_local(sym.up, sym.ui, vals, sym.n, sym.iperm, prob.bcol[s], prob.bval[s])
             assert np.linalg.norm(out - ref) <= 1e-10 * np.linalg.norm(ref)
+            fms.append(ref)
+        p = np.random.default_rng(3).normal(size=prob.n_multipliers)
         q = np.empty(prob.n_multipliers)
-        _lib.check(lib.feti_apply(ctx, _lib.f64ptr(g["p"]), _lib.f64ptr(q)))
-        assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
+        _lib.check(lib.feti_apply(ctx, _lib.f64ptr(p), _lib.f64ptr(q)))
+        qr = ora.apply_explicit(fms, prob.gids, p)
+        assert np.linalg.norm(q - qr) <= 1e-10 * np.linalg.norm(qr)
     finally:
         lib.feti_destroy(ctx)
 
@@ -209,3 +214,78 @@ def test_c1_full_problem(cfg):
         op.preprocess()
         q = op.apply(g["p"])
     assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
+
+
+def test_apply_device_on_torch_stream_matches_host_apply():
+    torch = pytest.importorskip("torch")
+    prob = inputs.Problem("heat", 3, 4, 2)
+    mats, cons, lay = inputs.reference_inputs(prob)
+    p = np.random.default_rng(9).normal(size=prob.n_multipliers)
+    with dualop.prepare(mats, cons, lay, CFG, device=0) as op:
+        op.preprocess()
+        q_host = op.apply(p)
+        pd = torch.from_numpy(p).cuda()
+        qd = torch.full_like(pd, np.nan)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            op.apply_device(pd, qd)          # current (side) stream
+            out = qd.cpu().numpy()
+        assert np.array_equal(out, q_host)
+        qd.fill_(np.nan)
+        op.apply_device(pd, qd, stream=torch.cuda.current_stream().cuda_stream)
+        assert np.array_equal(qd.cpu().numpy(), q_host)
+
+
+def _single(prob, s):
+    """One-subdomain view with multipliers renumbered 0..m-1 (ConstraintSet.restricted_to)."""
+    m = prob.gids[s].shape[0]
+    mat = inputs.Csr((m, prob.n_dofs), np.arange(m + 1, dtype=np.int64), prob.bcol[s], prob.bval[s])
+    cons = inputs.ConstraintSet(m, np.zeros(m), [inputs.SubdomainConstraints(np.arange(m, dtype=np.int64), mat)])
+    lay = inputs.ClusterLayout([inputs.Cluster(0, np.array([0]), np.arange(m), [np.arange(m)])], m)
+    return cons, lay
+
+
+@pytest.mark.parametrize("ordering", ["rcm", "interface_last"])
+def test_c3_subdomain_checksums_match_reference(ordering):
+    """A full c3 interior subdomain (n=9261, m=2522) against the reference's own
+    F~ (numba factorization + dense-storage assembly, checksums in the fixture)."""
+    g = load_golden("c3_sub21")
+    prob = inputs.Problem(*inputs.CONFIGS["c3"])
+    s = int(g["sub_index"])
+    k, _, q = prob.subdomain_system(s)
+    mats = [inputs.DenseSym(inputs.regularized_dense(k, q))]
+    cons, lay = _single(prob, s)
+    with dualop.prepare(mats, cons, lay, CFG, ordering=ordering) as op:
+        if ordering == "rcm":
+            np.testing.assert_array_equal(op._subs[0].perm, g["perm"])
+        op.preprocess()
+        f = _full(op.local_operator(0))
+    for name, got in (("Fv", f @ g["v"]), ("F_diag", np.diag(f)), ("F_row0", f[0])):
+        ref = g[name]
+        assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref), name
+    assert abs(np.linalg.norm(f) - float(g["F_fro"])) <= 1e-10 * float(g["F_fro"])
+
+
+def test_c2_apply_and_pcpg_match_reference():
+    """Config 2 (512 subdomains x 729 DOFs, 103,807 multipliers): q = F p and
+    the PCPG iteration count (80) of the reference."""
+    g = load_golden("heat3d_c2")
+    prob = inputs.Problem(*inputs.CONFIGS["c2"])
+    assert prob.n_multipliers == int(g["n_multipliers"])
+    mats, cons, lay = inputs.reference_inputs(prob, dense=True)
+    with dualop.prepare(mats, cons, lay, CFG, workers=8) as op:
+        op.preprocess()
+        q = op.apply(g["p"])
+        assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
+        kernels, forces, cl = [], [], []
+        for s in range(prob.n_sub):
+            k, f, qk = prob.subdomain_system(s)
+            kernels.append(qk)
+            forces.append(f)
+            cl.append((prob.gids[s], prob.bcol[s], prob.bval[s]))
+        gm, e, d, coarse = ora.assemble_dual_system(kernels, forces, cl, prob.n_multipliers, prob.c,
+                                                    op.solve_local)
+        lam, it = ora.pcpg(gm, e, d, coarse, op.apply, tol=1e-9)
+    assert it == int(g["pcpg_iterations"]) == 80
+    ref = g["pcpg_lambda"]
+    assert np.linalg.norm(lam - ref) <= 1e-9 * np.linalg.norm(ref)

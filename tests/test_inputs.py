@@ -45,3 +45,17 @@ def test_config_sizes(cfg, n, mult):
     prob = inputs.Problem(*inputs.CONFIGS[cfg])
     assert prob.n_dofs == n
     assert prob.n_multipliers == mult
+
+
+def test_c3_interior_subdomain_matches_reference():
+    g = load_golden("c3_sub21")
+    prob = inputs.Problem(*inputs.CONFIGS["c3"])
+    s = int(g["sub_index"])
+    assert prob.n_multipliers == int(g["n_multipliers"])
+    np.testing.assert_array_equal(prob.gids[s], g["gids"])
+    np.testing.assert_array_equal(prob.bcol[s], g["bcol"])
+    np.testing.assert_array_equal(prob.bval[s], g["bval"])
+    k, _, _ = prob.subdomain_system(s)
+    np.testing.assert_array_equal(k.indptr, g["k_indptr"])
+    np.testing.assert_array_equal(k.indices, g["k_indices"])
+    np.testing.assert_allclose(k.data, g["k_data"], rtol=1e-13, atol=1e-13 * np.abs(k.data).max())
