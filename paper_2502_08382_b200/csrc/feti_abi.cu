@@ -86,6 +86,7 @@ struct SubHost {
   int* d_pmin = nullptr;
   bool factor_set = false;
   bool factor_from_host = false;
+  const double* h_values = nullptr;  // host factor awaiting upload at assemble
   cudaEvent_t ev_upload = nullptr;
   int64_t f_tiles() const { return (int64_t)T32 * (T32 + 1) / 2; }
   int64_t l_tiles() const { return (int64_t)(T - smin) * (T - smin + 1) / 2; }
@@ -113,6 +114,7 @@ struct feti_ctx {
        *d_w_syrk = nullptr, *d_w_apply = nullptr;
   int n_unpack = 0, n_diag = 0, n_scale = 0, n_chain = 0, n_syrk = 0, n_apply = 0;
   int64_t* d_part_off = nullptr;
+  int* d_apply_seg_ptr = nullptr;
   double* d_part = nullptr;
   int* d_cptr = nullptr;
   int4* d_cent = nullptr;
@@ -122,6 +124,17 @@ struct feti_ctx {
   feti_stats stats{};
   cudaEvent_t ev[8] = {};
   bool subdev_dirty = true;
+  // upload/compute pipeline for host factors: subdomains grouped in waves
+  // (largest work first); wave w's H2D on copy_stream, its kernels on
+  // wave_streams[w % 2] once its copies landed
+  static constexpr int kWaveStreams = 2;
+  cudaStream_t wave_streams[kWaveStreams] = {};
+  cudaEvent_t wave_join[kWaveStreams] = {};
+  std::vector<std::vector<int>> waves;
+  std::vector<cudaEvent_t> wave_ev;
+  // per-wave work lists: [kind][wave] -> (offset, count) into d_wv[kind]
+  int4* d_wv[5] = {};
+  std::vector<std::pair<int, int>> wv_range[5];
 };
 
 namespace {
@@ -207,6 +220,10 @@ int feti_create(int device, feti_ctx** out) {
   c->num_sms = prop.multiProcessorCount;
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < feti_ctx::kWaveStreams; ++i) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->wave_streams[i], cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->wave_join[i], cudaEventDisableTiming));
+  }
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(configure_kernels());
   *out = c;
@@ -223,6 +240,12 @@ int feti_destroy(feti_ctx* c) {
     if (s.ev_upload) cudaEventDestroy(s.ev_upload);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->wave_ev)
+    if (e) cudaEventDestroy(e);
+  for (int i = 0; i < feti_ctx::kWaveStreams; ++i) {
+    if (c->wave_join[i]) cudaEventDestroy(c->wave_join[i]);
+    if (c->wave_streams[i]) cudaStreamDestroy(c->wave_streams[i]);
+  }
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   delete c;
@@ -345,12 +368,13 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   const double tb3 = 2.0 * TB * TB * TB;
   for (int si = 0; si < (int)c->subs.size(); ++si) {
     const SubHost& s = c->subs[si];
-    for (int K = s.smin; K < s.T; ++K)
-      for (int L = s.smin; L <= K; ++L) wu.push_back(make_int4(si, K, L, 0));
+    // dense pattern: the kernels read the packed factor directly (no unpack);
+    // sparse pattern: zero-fill + scatter into tiles first
+    if (!s.dense)
+      for (int K = s.smin; K < s.T; ++K)
+        for (int L = s.smin; L <= K; ++L) wu.push_back(make_int4(si, K, L, 0));
     for (int k = s.smin; k < s.T; ++k) wd.push_back(make_int4(si, k, 0, 0));
-    for (int k = s.smin + 1; k < s.T; ++k)
-      for (int l = s.smin; l < k; ++l)
-        for (int h = 0; h < 2; ++h) ws.push_back(make_int4(si, k, l, h));
+    for (int k = s.T - 1; k > s.smin; --k) ws.push_back(make_int4(si, k, 0, 0));
     const double tt = s.T - s.smin;
     scale_exec += tt * (tt - 1) / 2 * 2.0 * (2.0 * 64 * 32 * 32 * (1 + 2 + 3 + 4));
     for (int p = 0; p < s.P; ++p) {
@@ -372,6 +396,9 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     }
   }
   // chains: longest first so the tail is short
+  std::stable_sort(ws.begin(), ws.end(), [&](const int4& a, const int4& b) {
+    return a.y - c->subs[a.x].smin > b.y - c->subs[b.x].smin;
+  });
   std::sort(wc.begin(), wc.end(), [&](const int4& a, const int4& b) {
     const SubHost& sa = c->subs[a.x];
     const SubHost& sb = c->subs[b.x];
@@ -386,30 +413,77 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     return la > lb;
   });
 
-  // ---- apply work: split each subdomain's tiles over CTAs, partial slots
-  int64_t total_tiles = 0;
-  for (auto& s : c->subs) total_tiles += s.f_tiles();
-  const int64_t tpc = std::max<int64_t>(16, (total_tiles + 4 * c->num_sms - 1) / (4 * c->num_sms));
-  std::vector<int64_t> part_off;
-  std::vector<int> cta_begin(c->subs.size()), cta_end(c->subs.size());
-  int64_t poff = 0;
-  double apply_alg = 16.0 * (double)c->n_mult, apply_exec = 16.0 * (double)c->n_mult;
-  for (int si = 0; si < (int)c->subs.size(); ++si) {
-    const SubHost& s = c->subs[si];
-    cta_begin[si] = (int)part_off.size();
-    const int64_t nt = s.f_tiles();
-    if (s.m > 0) {
-      const int64_t nct = std::max<int64_t>(1, (nt + tpc - 1) / tpc);
-      for (int64_t k = 0; k < nct; ++k) {
-        const int64_t t0 = nt * k / nct, t1 = nt * (k + 1) / nct;
-        wa.push_back(make_int4(si, (int)t0, (int)t1, (int)part_off.size()));
-        part_off.push_back(poff);
-        poff += s.m;
+  // ---- upload/compute waves (host-factor pipeline), largest work first
+  {
+    std::vector<int> order(c->subs.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::vector<double> work(c->subs.size(), 0.0);
+    for (size_t si = 0; si < c->subs.size(); ++si) {
+      const SubHost& s = c->subs[si];
+      for (int p = 0; p < s.P; ++p) {
+        const double len = s.T - s.panel_minrow[p] / TB;
+        work[si] += len * len;
       }
     }
-    cta_end[si] = (int)part_off.size();
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
+    const int nw = (int)std::min<size_t>(c->subs.size(), 8);
+    c->waves.assign(nw, {});
+    for (size_t k = 0; k < order.size(); ++k) c->waves[k * nw / order.size()].push_back(order[k]);
+    std::vector<int> wave_of(c->subs.size());
+    for (int w = 0; w < nw; ++w)
+      for (int si : c->waves[w]) wave_of[si] = w;
+    const std::vector<int4>* lists[5] = {&wu, &wd, &ws, &wc, &wy};
+    for (int kind = 0; kind < 5; ++kind) {
+      std::vector<int4> v;
+      c->wv_range[kind].assign(nw, {0, 0});
+      for (int w = 0; w < nw; ++w) {
+        const int b = (int)v.size();
+        for (const int4& x : *lists[kind])
+          if (wave_of[x.x] == w) v.push_back(x);
+        c->wv_range[kind][w] = {b, (int)v.size() - b};
+      }
+      if ((rc = upload(c, &c->d_wv[kind], v))) return rc;
+    }
+    c->wave_ev.resize(nw);
+    for (auto& e : c->wave_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+
+  // ---- apply work: the concatenated tile list of all subdomains is cut into
+  // one contiguous, equal range per SM (persistent CTAs); each range becomes
+  // segments (sub, t0, t1, partial slot) where it crosses subdomain bounds
+  int64_t total_tiles = 0;
+  for (auto& s : c->subs) total_tiles += s.f_tiles();
+  const int64_t ncta = std::max<int64_t>(1, std::min<int64_t>(c->num_sms, (total_tiles + 63) / 64));
+  std::vector<int64_t> part_off;
+  std::vector<int> cta_begin(c->subs.size()), cta_end(c->subs.size());
+  std::vector<int> seg_ptr;
+  int64_t poff = 0;
+  double apply_alg = 16.0 * (double)c->n_mult, apply_exec = 16.0 * (double)c->n_mult;
+  {
+    std::vector<int64_t> base(c->subs.size() + 1, 0);
+    for (size_t si = 0; si < c->subs.size(); ++si) base[si + 1] = base[si] + c->subs[si].f_tiles();
+    for (size_t si = 0; si < c->subs.size(); ++si) cta_begin[si] = cta_end[si] = -1;
+    for (int64_t b = 0; b < ncta; ++b) {
+      seg_ptr.push_back((int)wa.size());
+      const int64_t g0 = total_tiles * b / ncta, g1 = total_tiles * (b + 1) / ncta;
+      for (size_t si = 0; si < c->subs.size(); ++si) {
+        const int64_t lo = std::max(g0, base[si]), hi = std::min(g1, base[si + 1]);
+        if (lo >= hi || c->subs[si].m == 0) continue;
+        if (cta_begin[si] < 0) cta_begin[si] = (int)part_off.size();
+        wa.push_back(make_int4((int)si, (int)(lo - base[si]), (int)(hi - base[si]), (int)part_off.size()));
+        part_off.push_back(poff);
+        poff += c->subs[si].m;
+        cta_end[si] = (int)part_off.size();
+      }
+    }
+    seg_ptr.push_back((int)wa.size());
+    for (size_t si = 0; si < c->subs.size(); ++si)
+      if (cta_begin[si] < 0) cta_begin[si] = cta_end[si] = 0;
+  }
+  for (int si = 0; si < (int)c->subs.size(); ++si) {
+    const SubHost& s = c->subs[si];
     apply_alg += 8.0 * s.m * (s.m + 1) / 2 + s.m * (8.0 + 16.0 + 4.0);
-    apply_exec += 8.0 * ATILE * nt + s.T32 * AT * 12.0;
+    apply_exec += 8.0 * ATILE * s.f_tiles() + s.T32 * AT * 12.0;
   }
   apply_exec += 16.0 * poff;
   // contributions per global multiplier, in registration (gather) order
@@ -439,6 +513,7 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   if ((rc = upload(c, &c->d_w_chain, wc))) return rc;
   if ((rc = upload(c, &c->d_w_syrk, wy))) return rc;
   if ((rc = upload(c, &c->d_w_apply, wa))) return rc;
+  if ((rc = upload(c, &c->d_apply_seg_ptr, seg_ptr))) return rc;
   if ((rc = upload(c, &c->d_part_off, part_off))) return rc;
   if ((rc = upload(c, &c->d_cptr, cptr))) return rc;
   if ((rc = upload(c, &c->d_cent, cent))) return rc;
@@ -450,7 +525,7 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   c->n_scale = (int)ws.size();
   c->n_chain = (int)wc.size();
   c->n_syrk = (int)wy.size();
-  c->n_apply = (int)wa.size();
+  c->n_apply = (int)ncta;
 
   feti_stats& st = c->stats;
   st.flops_trsm_alg = trsm_alg;
@@ -481,21 +556,58 @@ int feti_set_factor(feti_ctx* c, int64_t slot, const double* values, int64_t nnz
   if (where == FETI_FACTOR_DEVICE) {
     s.d_raw = values + s.raw_off;
     s.factor_from_host = false;
+    s.h_values = nullptr;
   } else {
     if (!s.d_raw_own) {
       int rc = dev_alloc(c, (void**)&s.d_raw_own, (size_t)std::max<int64_t>(s.upload_count(), 1) * 8, true);
       if (rc) return rc;
     }
-    // only the values the pruned solve reads: a suffix of the reference layout
-    if (s.upload_count() > 0)
-      CUDA_TRY(cudaMemcpyAsync(s.d_raw_own, values + s.raw_off, (size_t)s.upload_count() * 8,
-                               cudaMemcpyHostToDevice, c->copy_stream));
-    CUDA_TRY(cudaEventRecord(s.ev_upload, c->copy_stream));
+    // the copy itself is issued by feti_assemble, in wave order, so that
+    // each wave's kernels start as soon as its factors have landed
+    s.h_values = values;
+    if (s.d_raw != s.d_raw_own) c->subdev_dirty = true;
     s.d_raw = s.d_raw_own;
     s.factor_from_host = true;
   }
   s.factor_set = true;
-  c->subdev_dirty = true;
+  if (where == FETI_FACTOR_DEVICE) c->subdev_dirty = true;
+  return FETI_OK;
+}
+
+// Launch the five assembly kernels for one set of work lists on `st`.
+static int launch_assembly(feti_ctx* c, cudaStream_t st, const int4* wu, int nu, const int4* wd, int nd,
+                           const int4* ws, int ns, const int4* wc, int nc, const int4* wy, int ny,
+                           const std::vector<int>& sparse_slots, cudaEvent_t* marks, int* launches) {
+  if (marks) CUDA_TRY(cudaEventRecord(marks[0], st));
+  launch_unpack(c->d_subdev, wu, nu, st);
+  *launches += nu > 0;
+  for (int si : sparse_slots) {
+    launch_scatter_sparse(c->d_subdev, si, (int)(c->subs[si].n - (int64_t)c->subs[si].smin * TB), st);
+    ++*launches;
+  }
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  if (marks) CUDA_TRY(cudaEventRecord(marks[1], st));
+  launch_diag_inverse(c->d_subdev, wd, nd, st);
+  *launches += nd > 0;
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  if (marks) CUDA_TRY(cudaEventRecord(marks[2], st));
+  launch_block_scale(c->d_subdev, ws, ns, st);
+  *launches += ns > 0;
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  if (marks) CUDA_TRY(cudaEventRecord(marks[3], st));
+  launch_trsm_chain(c->d_subdev, wc, nc, st);
+  *launches += nc > 0;
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  if (marks) CUDA_TRY(cudaEventRecord(marks[4], st));
+  launch_syrk(c->d_subdev, wy, ny, st);
+  *launches += ny > 0;
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  if (marks) CUDA_TRY(cudaEventRecord(marks[5], st));
   return FETI_OK;
 }
 
@@ -506,61 +618,80 @@ int feti_assemble(feti_ctx* c) {
     if (!c->subs[i].factor_set) return fail(FETI_ERR_LIFECYCLE, "subdomain slot %zu has no factor values", i);
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
-  int launches = 0;
-  CUDA_TRY(cudaEventRecord(c->ev[0], st));
-  for (auto& s : c->subs)
-    if (s.factor_from_host) CUDA_TRY(cudaStreamWaitEvent(st, s.ev_upload, 0));
-  if (c->subdev_dirty) {
-    int rc = sync_subdev(c);
-    if (rc) return rc;
-  }
-  CUDA_TRY(cudaEventRecord(c->ev[1], st));
-  launch_unpack(c->d_subdev, c->d_w_unpack, c->n_unpack, st);
-  launches += c->n_unpack > 0;
-  for (int si = 0; si < (int)c->subs.size(); ++si)
-    if (!c->subs[si].dense) {
-      launch_scatter_sparse(c->d_subdev, si, (int)(c->subs[si].n - (int64_t)c->subs[si].smin * TB), st);
-      ++launches;
-    }
-  CUDA_TRY(cudaGetLastError());
-  FETI_DEBUG_SYNC(st);
-  CUDA_TRY(cudaEventRecord(c->ev[2], st));
-  launch_diag_inverse(c->d_subdev, c->d_w_diag, c->n_diag, st);
-  launches += c->n_diag > 0;
-  CUDA_TRY(cudaGetLastError());
-  FETI_DEBUG_SYNC(st);
-  CUDA_TRY(cudaEventRecord(c->ev[3], st));
-  launch_block_scale(c->d_subdev, c->d_w_scale, c->n_scale, st);
-  launches += c->n_scale > 0;
-  CUDA_TRY(cudaGetLastError());
-  FETI_DEBUG_SYNC(st);
-  CUDA_TRY(cudaEventRecord(c->ev[4], st));
-  launch_trsm_chain(c->d_subdev, c->d_w_chain, c->n_chain, st);
-  launches += c->n_chain > 0;
-  CUDA_TRY(cudaGetLastError());
-  FETI_DEBUG_SYNC(st);
-  CUDA_TRY(cudaEventRecord(c->ev[5], st));
-  launch_syrk(c->d_subdev, c->d_w_syrk, c->n_syrk, st);
-  launches += c->n_syrk > 0;
-  CUDA_TRY(cudaGetLastError());
-  FETI_DEBUG_SYNC(st);
-  CUDA_TRY(cudaEventRecord(c->ev[6], st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  float ms[6];
-  for (int i = 0; i < 6; ++i) CUDA_TRY(cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]));
-  feti_stats& S = c->stats;
-  S.ms_wait_upload = ms[0];
-  S.ms_unpack = ms[1];
-  S.ms_diag_inverse = ms[2];
-  S.ms_block_scale = ms[3];
-  S.ms_trsm = ms[4];
-  S.ms_syrk = ms[5];
-  S.ms_assemble = ms[1] + ms[2] + ms[3] + ms[4] + ms[5];
-  S.launches_assemble = launches;
+  int launches = 0, rc;
+  bool pending = false;
   double fb = 0;
   for (auto& s : c->subs)
-    if (s.factor_from_host) fb += 8.0 * s.upload_count();
-  S.factor_bytes = fb;
+    if (s.factor_from_host && s.h_values) {
+      pending = true;
+      fb += 8.0 * s.upload_count();
+    }
+  feti_stats& S = c->stats;
+  CUDA_TRY(cudaEventRecord(c->ev[0], st));
+  if (c->subdev_dirty && (rc = sync_subdev(c))) return rc;
+  if (!pending) {
+    // factors resident on the device: one batched launch per kernel over all
+    // subdomains (largest chains first)
+    std::vector<int> sparse;
+    for (int si = 0; si < (int)c->subs.size(); ++si)
+      if (!c->subs[si].dense) sparse.push_back(si);
+    if ((rc = launch_assembly(c, st, c->d_w_unpack, c->n_unpack, c->d_w_diag, c->n_diag, c->d_w_scale, c->n_scale,
+                              c->d_w_chain, c->n_chain, c->d_w_syrk, c->n_syrk, sparse, &c->ev[1], &launches)))
+      return rc;
+    CUDA_TRY(cudaStreamSynchronize(st));
+    float ms[5];
+    for (int i = 0; i < 5; ++i) CUDA_TRY(cudaEventElapsedTime(&ms[i], c->ev[i + 1], c->ev[i + 2]));
+    S.ms_wait_upload = 0.0;
+    S.ms_unpack = ms[0];
+    S.ms_diag_inverse = ms[1];
+    S.ms_block_scale = ms[2];
+    S.ms_trsm = ms[3];
+    S.ms_syrk = ms[4];
+    S.ms_assemble = ms[0] + ms[1] + ms[2] + ms[3] + ms[4];
+    S.factor_bytes = 0.0;
+  } else {
+    // host factors: H2D in wave order on the copy stream; each wave's kernels
+    // run on alternating streams as soon as its copies have landed, so the
+    // PCIe transfer of wave w+1 overlaps the DMMA work of wave w
+    CUDA_TRY(cudaEventRecord(c->ev[1], st));
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->ev[1], 0));
+    for (size_t w = 0; w < c->waves.size(); ++w) {
+      for (int si : c->waves[w]) {
+        SubHost& s = c->subs[si];
+        if (s.factor_from_host && s.h_values && s.upload_count() > 0)
+          CUDA_TRY(cudaMemcpyAsync(s.d_raw_own, s.h_values + s.raw_off, (size_t)s.upload_count() * 8,
+                                   cudaMemcpyHostToDevice, c->copy_stream));
+      }
+      CUDA_TRY(cudaEventRecord(c->wave_ev[w], c->copy_stream));
+    }
+    for (size_t w = 0; w < c->waves.size(); ++w) {
+      cudaStream_t ws = c->wave_streams[w % feti_ctx::kWaveStreams];
+      CUDA_TRY(cudaStreamWaitEvent(ws, c->wave_ev[w], 0));
+      std::vector<int> sparse;
+      for (int si : c->waves[w])
+        if (!c->subs[si].dense) sparse.push_back(si);
+      const auto& r = c->wv_range;
+      if ((rc = launch_assembly(c, ws, c->d_wv[0] + r[0][w].first, r[0][w].second, c->d_wv[1] + r[1][w].first,
+                                r[1][w].second, c->d_wv[2] + r[2][w].first, r[2][w].second,
+                                c->d_wv[3] + r[3][w].first, r[3][w].second, c->d_wv[4] + r[4][w].first,
+                                r[4][w].second, sparse, nullptr, &launches)))
+        return rc;
+    }
+    for (int i = 0; i < feti_ctx::kWaveStreams; ++i) {
+      CUDA_TRY(cudaEventRecord(c->wave_join[i], c->wave_streams[i]));
+      CUDA_TRY(cudaStreamWaitEvent(st, c->wave_join[i], 0));
+    }
+    CUDA_TRY(cudaEventRecord(c->ev[2], st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]));
+    S.ms_wait_upload = ms;  // H2D + overlapped assembly, first copy to last kernel
+    S.ms_unpack = S.ms_diag_inverse = S.ms_block_scale = S.ms_trsm = S.ms_syrk = 0.0;
+    S.ms_assemble = ms;
+    S.factor_bytes = fb;
+    for (auto& s : c->subs) s.h_values = nullptr;
+  }
+  S.launches_assemble = launches;
   c->assembled = true;
   return FETI_OK;
 }
@@ -594,8 +725,8 @@ int feti_local_operator(feti_ctx* c, int64_t slot, double* out) {
 // apply reads only finalize-time fields of it (F~ tiles, index maps).
 static int apply_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st, bool time_it) {
   if (time_it) CUDA_TRY(cudaEventRecord(c->ev[0], st));
-  launch_apply(c->apply_nw, c->apply_smem, c->d_subdev, c->d_w_apply, c->n_apply, c->d_part_off, c->d_part, d_p,
-               st);
+  launch_apply(c->apply_nw, c->apply_smem, c->d_subdev, c->d_w_apply, c->d_apply_seg_ptr, c->n_apply,
+               c->d_part_off, c->d_part, d_p, st);
   launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_part_off, c->d_part, d_q, st);
   CUDA_TRY(cudaGetLastError());
   if (time_it) CUDA_TRY(cudaEventRecord(c->ev[1], st));

@@ -120,6 +120,17 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
       : "memory");
 }
 
+// 8-byte asynchronous global->shared copy (LDGSTS) for gathers whose source
+// alignment rules out bulk copies (the reference's packed factor columns).
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+
+// Arrive on `bar` once all of this thread's prior cp.async copies landed.
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // Make this thread's generic-proxy global writes visible to later async-proxy
 // (bulk copy) reads.
 __device__ __forceinline__ void fence_proxy_async_global() {

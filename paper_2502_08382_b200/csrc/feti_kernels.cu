@@ -69,102 +69,231 @@ __global__ void __launch_bounds__(256) scatter_sparse_kernel(const SubDev* __res
 }
 
 // ---------------------------------------------------------------------------
-// 2. inverse of each diagonal block (column forward substitution in smem)
+// 2. inverse of each diagonal block, blocked 4 x 4 over 32-wide sub-blocks
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) diag_inverse_kernel(const SubDev* __restrict__ subs,
+// Phase 1: warp w inverts the 32x32 diagonal sub-block D_w; lane c carries
+// column c of inv(D_w) in registers through a lock-step forward substitution
+// (the L row is a shared-memory broadcast).  Phase 2: the off-diagonal
+// sub-blocks by distance d = 1, 2, 3:  Y_IJ = -inv(D_I) sum_{K=J}^{I-1} L_IK Y_KJ.
+// L and Y live as packed lower triangles in shared memory.
+__device__ __forceinline__ int plo(int i, int j) { return i * (i + 1) / 2 + j; }
+
+__global__ void __launch_bounds__(256) diag_inverse_kernel(const SubDev* __restrict__ subs,
                                                            const int4* __restrict__ work) {
   extern __shared__ double dsm[];
-  double* sL = dsm;             // packed row-major lower: (i,j) at i(i+1)/2+j
-  double* sY = dsm + 8256;
+  double* sL = dsm;               // 8256: packed row-major lower L_kk
+  double* sY = dsm + 8256;        // 8256: packed row-major lower inv(L_kk)
+  double* sT = dsm + 2 * 8256;    // 3 x 1024 scratch
   const int4 w = work[blockIdx.x];
   const SubDev& S = subs[w.x];
   const int k = w.y;
   double* tile = tile_ptr(S, k, k);
-  for (int idx = threadIdx.x; idx < TILE; idx += 128) {
-    const int jl = idx >> 7;
-    const int il = (idx & 127) ^ ((jl & 3) << 2);
-    if (il >= jl) sL[il * (il + 1) / 2 + jl] = tile[idx];
+  const int tid = threadIdx.x;
+  if (S.up == nullptr) {
+    // dense pattern: the diagonal block straight from the packed factor
+    const int64_t n = S.n;
+    for (int idx = tid; idx < TILE; idx += 256) {
+      const int jl = idx >> 7, il = idx & 127;
+      if (il < jl) continue;
+      const int64_t i = (int64_t)k * TB + il, j = (int64_t)k * TB + jl;
+      double v;
+      if (i < n)
+        v = S.raw[(j * n - j * (j - 1) / 2) + (i - j) - S.raw_off];
+      else
+        v = (i == j) ? 1.0 : 0.0;    // identity padding
+      sL[plo(il, jl)] = v;
+    }
+  } else {
+    for (int idx = tid; idx < TILE; idx += 256) {
+      const int jl = idx >> 7;
+      const int il = (idx & 127) ^ ((jl & 3) << 2);
+      if (il >= jl) sL[plo(il, jl)] = tile[idx];
+    }
   }
   __syncthreads();
-  const int c = threadIdx.x;
-  for (int i = c; i < TB; ++i) {
-    const double* Li = sL + i * (i + 1) / 2;
-    double acc = (i == c) ? 1.0 : 0.0;
-    for (int j = c; j < i; ++j) acc -= Li[j] * sY[j * (j + 1) / 2 + c];
-    sY[i * (i + 1) / 2 + c] = acc / Li[i];
+  const int warp = tid >> 5, lane = tid & 31;
+  if (warp < 4) {
+    const int o = warp * 32;
+    double y[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const double* Lr = sL + plo(o + r, o);
+      double acc = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = 0; j < r; ++j) acc = fma(-Lr[j], y[j], acc);
+      y[r] = acc / Lr[r];
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r >= lane) sY[plo(o + r, o + lane)] = y[r];
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < TILE; idx += 128) {
+  // thread -> (row r, 4 consecutive columns c..c+3) of a 32x32 sub-block
+  const int rr = tid >> 3, cc = (tid & 7) * 4;
+  for (int d = 1; d < 4; ++d) {
+    const int nb = 4 - d;
+    for (int bI = 0; bI < nb; ++bI) {          // T_b = sum_{K=J}^{I-1} L_IK Y_KJ
+      const int J = bI, I = bI + d;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* Lr = sL + plo(I * 32 + rr, 0);
+      for (int kk = J * 32; kk < I * 32; ++kk) {
+        const double lv = Lr[kk];
+        const double* Yk = sY + plo(kk, 0);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = J * 32 + cc + e;
+          if (kk >= col) acc[e] = fma(lv, Yk[col], acc[e]);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sT[bI * 1024 + rr * 32 + cc + e] = acc[e];
+    }
+    __syncthreads();
+    for (int bI = 0; bI < nb; ++bI) {          // Y_IJ = -inv(D_I) T_b
+      const int J = bI, I = bI + d;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* Yr = sY + plo(I * 32 + rr, I * 32);
+      for (int kk = 0; kk <= rr; ++kk) {
+        const double yv = Yr[kk];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = fma(yv, sT[bI * 1024 + kk * 32 + cc + e], acc[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sY[plo(I * 32 + rr, J * 32 + cc + e)] = -acc[e];
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < TILE; idx += 256) {
     const int jl = idx >> 7;
     const int il = (idx & 127) ^ ((jl & 3) << 2);
-    tile[idx] = (il >= jl) ? sY[il * (il + 1) / 2 + jl] : 0.0;
+    tile[idx] = (il >= jl) ? sY[plo(il, jl)] : 0.0;
   }
 }
 
 // ---------------------------------------------------------------------------
-// 3. block-row scaling  Lhat_kl = inv(L_kk) * L_kl  (in place, half tile/CTA)
+// 3. block-row scaling  Lhat_kl = inv(L_kk) * L_kl  for smin <= l < k
 // ---------------------------------------------------------------------------
-// work: (sub, k, l, half).  A = inv(L_kk) (col-major swizzled, 4 slices),
-// B = L_kl columns [half*64, half*64+64) read as [n][k] (col-major) tiles.
-__global__ void __launch_bounds__(256, 1) block_scale_kernel(const SubDev* __restrict__ subs,
-                                                             const int4* __restrict__ work) {
+// One CTA per block row (sub, k): inv(L_kk) stays resident in shared memory
+// (128 KB, bulk copy) while the row's L_kl are streamed through a 3-stage ring
+// of 32-column quarters.  Dense pattern: quarters are gathered straight from
+// the reference's packed factor with 8-byte cp.async (no unpacked copy of L
+// is ever written); sparse pattern: bulk copies of the scattered tiles.
+// The producer warp fills the ring, 8 DMMA warps compute 128x32 per quarter
+// (inv(L_kk) is lower triangular: k-steps above each warp's rows are skipped).
+constexpr int BS_STAGES = 3;
+constexpr int QCOLS = 32;
+constexpr int QSIZE = QCOLS * TB;   // 4096 doubles (32 KB)
+constexpr int BS_THREADS = 288;
+
+__global__ void __launch_bounds__(BS_THREADS, 1) block_scale_kernel(const SubDev* __restrict__ subs,
+                                                                    const int4* __restrict__ work) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* sA = reinterpret_cast<double*>(smem_raw);   // 4 * SLICE
-  double* sB = sA + 4 * SLICE;                        // 64 x 128
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sB + 64 * TB);  // [0..3] A slices, [4] B
+  double* sA = reinterpret_cast<double*>(smem_raw);      // TILE
+  double* sB = sA + TILE;                                 // BS_STAGES * QSIZE
+  uint64_t* barA = reinterpret_cast<uint64_t*>(sB + BS_STAGES * QSIZE);
+  uint64_t* full = barA + 1;
+  uint64_t* empty = full + BS_STAGES;
   const int4 w = work[blockIdx.x];
   const SubDev& S = subs[w.x];
-  const int k = w.y, l = w.z, half = w.w;
-  const double* inv = tile_ptr(S, k, k);
-  double* Lkl = tile_ptr(S, k, l);
+  const int k = w.y;
+  const int l0 = S.smin;
+  const int nq = (k - l0) * (TB / QCOLS);
+  const bool dense = (S.up == nullptr);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 5; ++i) mbar_init(&bar[i], 1);
+    mbar_init(barA, 1);
+    for (int i = 0; i < BS_STAGES; ++i) {
+      mbar_init(&full[i], dense ? 32 : 1);
+      mbar_init(&empty[i], 8);
+    }
     mbar_fence_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&bar[4], 64 * TB * 8);
-    bulk_g2s(sB, Lkl + half * 64 * TB, 64 * TB * 8, &bar[4]);
-    for (int s = 0; s < 4; ++s) {
-      mbar_arrive_expect_tx(&bar[s], SLICE * 8);
-      bulk_g2s(sA + s * SLICE, inv + s * SLICE, SLICE * 8, &bar[s]);
+  if (warp == 8) {
+    const int64_t n = S.n;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(barA, TILE * 8);
+      const double* inv = tile_ptr(S, k, k);
+      for (int s = 0; s < 4; ++s) bulk_g2s(sA + s * SLICE, inv + s * SLICE, SLICE * 8, barA);
     }
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int qi = 0; qi < nq; ++qi) {
+      const int l = l0 + qi / (TB / QCOLS), q = qi % (TB / QCOLS);
+      mbar_wait(&empty[stage], phase ^ 1);
+      double* dst = sB + stage * QSIZE;
+      if (dense) {
+        // column jg of L: rows k*128 + kk at raw[colstart(jg) + (i - jg)]
+        const int64_t i0 = (int64_t)k * TB;
+#pragma unroll 4
+        for (int jq = 0; jq < QCOLS; ++jq) {
+          const int64_t jg = (int64_t)l * TB + q * QCOLS + jq;
+          const double* col = S.raw + (jg * n - jg * (jg - 1) / 2 - jg - S.raw_off);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int kk = lane + 32 * t;
+            if (i0 + kk < n) cp_async8(dst + swz(jq, kk), col + i0 + kk);
+          }
+        }
+        cp_async_mbar_arrive(&full[stage]);
+      } else if (lane == 0) {
+        mbar_arrive_expect_tx(&full[stage], QSIZE * 8);
+        bulk_g2s(dst, tile_ptr(S, k, l) + q * QSIZE, QSIZE * 8, &full[stage]);
+      }
+      if (++stage == BS_STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    return;
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = warp >> 1, wn = warp & 1;     // warp tile 32 x 32 of 128 x 64
+  const int wm = warp >> 1, wn = warp & 1;     // warp tile 32 x 16 of 128 x 32
   const int g = lane >> 2, t = lane & 3;
-  double acc[4][4][2];
+  const int kb_end = wm * 8 + 8;               // inv(L_kk)[i][kk] = 0 for kk > i
+  const int rows_valid = S.n - k * TB;         // padding rows of the last block row
+  mbar_wait(barA, 0);
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int qi = 0; qi < nq; ++qi) {
+    const int l = l0 + qi / (TB / QCOLS), q = qi % (TB / QCOLS);
+    double acc[4][2][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  mbar_wait(&bar[4], 0);
-  // inv(L_kk)[i][kk] == 0 for kk > i: rows wm*32.. need kk <= wm*32+31
-  const int kb_end = wm * 8 + 8;
-  for (int kb = 0; kb < kb_end; ++kb) {
-    if ((kb & 7) == 0) mbar_wait(&bar[kb >> 3], 0);
-    const int kk = kb * 4 + t;
-    double af[4], bf[4];
+      for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    mbar_wait(&full[stage], phase);
+    const double* b_s = sB + stage * QSIZE;
+    for (int kb = 0; kb < kb_end; ++kb) {
+      const int kk = kb * 4 + t;
+      double bf[2];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) af[mi] = sA[swz(kk, wm * 32 + mi * 8 + g)];
+      for (int ni = 0; ni < 2; ++ni) {
+        const double v = b_s[swz(wn * 16 + ni * 8 + g, kk)];
+        bf[ni] = kk < rows_valid ? v : 0.0;
+      }
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) bf[ni] = sB[swz(wn * 32 + ni * 8 + g, kk)];
+      for (int mi = 0; mi < 4; ++mi) {
+        const double af = sA[swz(kk, wm * 32 + mi * 8 + g)];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == BS_STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+    double* Lkl = tile_ptr(S, k, l);
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
-  }
-  // every warp must be done reading sB/sA before anyone overwrites L_kl?  The
-  // writes go to global memory (Lkl), which sB was copied from; the bulk copy
-  // has completed (waited above), so no hazard.
+    for (int mi = 0; mi < 4; ++mi) {
+      const int i = wm * 32 + mi * 8 + g;
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi) {
-    const int i = wm * 32 + mi * 8 + g;
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int j = half * 64 + wn * 32 + ni * 8 + 2 * t;
-      Lkl[swz(j, i)] = acc[mi][ni][0];
-      Lkl[swz(j + 1, i)] = acc[mi][ni][1];
+      for (int ni = 0; ni < 2; ++ni) {
+        const int j = q * QCOLS + wn * 16 + ni * 8 + 2 * t;
+        Lkl[swz(j, i)] = acc[mi][ni][0];
+        Lkl[swz(j + 1, i)] = acc[mi][ni][1];
+      }
     }
   }
 }
@@ -358,6 +487,8 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) syrk_kernel(const SubDev* __r
 
   const int wm = warp >> 2, wn = warp & 3;
   const int g = lane >> 2, t = lane & 3;
+  // diagonal blocks: warps strictly below the diagonal produce nothing stored
+  const bool idle = (I == J) && (wn * 32 + 31 < wm * 64);
   double acc[8][4][2];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
@@ -367,7 +498,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) syrk_kernel(const SubDev* __r
   uint32_t phase = 0;
   for (int sl = 0; sl < nsl; ++sl) {
     mbar_wait(&full[stage], phase);
-    mma_slice_128x128(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
+    if (!idle) mma_slice_128x128(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
     if (++stage == PIPE_STAGES) {
@@ -441,63 +572,68 @@ __device__ __forceinline__ void apply_advance(int& ti, int& tj, int step, int T3
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict__ subs,
-                                                        const int4* __restrict__ work,
+                                                        const int4* __restrict__ segs,
+                                                        const int* __restrict__ seg_ptr,
                                                         const int64_t* __restrict__ part_off,
                                                         double* __restrict__ part,
                                                         const double* __restrict__ p) {
+  // persistent: CTA b walks its segments (sub, tile range, partial slot)
   extern __shared__ double asmem[];
-  const int4 w = work[blockIdx.x];
-  const SubDev& S = subs[w.x];
-  const int T32 = S.T32;
-  const int M = T32 * AT;
-  double* sp = asmem;
-  double* sq = asmem + M;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int a = tid; a < M; a += NW * 32) {
-    const int gi = S.gids_sorted[a];
-    sp[a] = gi >= 0 ? __ldg(p + gi) : 0.0;
-  }
-  for (int a = tid; a < NW * M; a += NW * 32) sq[a] = 0.0;
-  __syncthreads();
-  double* myq = sq + warp * M;
+  for (int sg = seg_ptr[blockIdx.x]; sg < seg_ptr[blockIdx.x + 1]; ++sg) {
+    const int4 w = segs[sg];
+    const SubDev& S = subs[w.x];
+    const int T32 = S.T32;
+    const int M = T32 * AT;
+    double* sp = asmem;
+    double* sq = asmem + M;
+    __syncthreads();   // previous segment's combine is done with smem
+    for (int a = tid; a < M; a += NW * 32) {
+      const int gi = S.gids_sorted[a];
+      sp[a] = gi >= 0 ? __ldg(p + gi) : 0.0;
+    }
+    for (int a = tid; a < NW * M; a += NW * 32) sq[a] = 0.0;
+    __syncthreads();
+    double* myq = sq + warp * M;
 
-  int64_t tt = (int64_t)w.y + warp;
-  const int64_t t1 = w.z;
-  int ti = 0;
-  int64_t rowstart = 0;
-  while (ti < T32 && rowstart + (T32 - ti) <= tt) {
-    rowstart += T32 - ti;
-    ++ti;
-  }
-  int tj = ti + (int)(tt - rowstart);
-  const double* Fb = S.F;
-  double fa[32], fb[32];
-  if (tt < t1) apply_tile_load(fa, Fb + tt * ATILE, lane);
-  while (tt < t1) {
-    int ti2 = ti, tj2 = tj;
-    apply_advance(ti2, tj2, NW, T32);
-    int64_t nx = tt + NW;
-    if (nx < t1) apply_tile_load(fb, Fb + nx * ATILE, lane);
-    apply_tile_compute(fa, ti, tj, sp, myq, lane);
-    tt = nx;
-    ti = ti2;
-    tj = tj2;
-    if (tt >= t1) break;
-    apply_advance(ti2, tj2, NW, T32);
-    nx = tt + NW;
-    if (nx < t1) apply_tile_load(fa, Fb + nx * ATILE, lane);
-    apply_tile_compute(fb, ti, tj, sp, myq, lane);
-    tt = nx;
-    ti = ti2;
-    tj = tj2;
-  }
-  __syncthreads();
-  double* out = part + part_off[w.w];
-  for (int a = tid; a < S.m; a += NW * 32) {
-    double s = 0.0;
+    int64_t tt = (int64_t)w.y + warp;
+    const int64_t t1 = w.z;
+    int ti = 0;
+    int64_t rowstart = 0;
+    while (ti < T32 && rowstart + (T32 - ti) <= tt) {
+      rowstart += T32 - ti;
+      ++ti;
+    }
+    int tj = ti + (int)(tt - rowstart);
+    const double* Fb = S.F;
+    double fa[32], fb[32];
+    if (tt < t1) apply_tile_load(fa, Fb + tt * ATILE, lane);
+    while (tt < t1) {
+      int ti2 = ti, tj2 = tj;
+      apply_advance(ti2, tj2, NW, T32);
+      int64_t nx = tt + NW;
+      if (nx < t1) apply_tile_load(fb, Fb + nx * ATILE, lane);
+      apply_tile_compute(fa, ti, tj, sp, myq, lane);
+      tt = nx;
+      ti = ti2;
+      tj = tj2;
+      if (tt >= t1) break;
+      apply_advance(ti2, tj2, NW, T32);
+      nx = tt + NW;
+      if (nx < t1) apply_tile_load(fa, Fb + nx * ATILE, lane);
+      apply_tile_compute(fb, ti, tj, sp, myq, lane);
+      tt = nx;
+      ti = ti2;
+      tj = tj2;
+    }
+    __syncthreads();
+    double* out = part + part_off[w.w];
+    for (int a = tid; a < S.m; a += NW * 32) {
+      double s = 0.0;
 #pragma unroll
-    for (int wi = 0; wi < NW; ++wi) s += sq[wi * M + a];
-    out[a] = s;
+      for (int wi = 0; wi < NW; ++wi) s += sq[wi * M + a];
+      out[a] = s;
+    }
   }
 }
 
@@ -524,7 +660,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(int n_mult, const int* __re
 // launchers
 // ---------------------------------------------------------------------------
 static size_t pipe_smem() { return 2 * PIPE_STAGES * SLICE * sizeof(double) + 8 * (2 * PIPE_STAGES + 1); }
-static size_t scale_smem() { return (4 * SLICE + 64 * TB) * sizeof(double) + 8 * 5; }
+static size_t scale_smem() { return (TILE + BS_STAGES * QSIZE) * sizeof(double) + 8 * (1 + 2 * BS_STAGES); }
 
 cudaError_t configure_kernels() {
   cudaError_t e;
@@ -536,7 +672,7 @@ cudaError_t configure_kernels() {
                                 (int)scale_smem())))
     return e;
   if ((e = cudaFuncSetAttribute(diag_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                2 * 8256 * 8)))
+                                (2 * 8256 + 3 * 1024) * 8)))
     return e;
   if ((e = cudaFuncSetAttribute(apply_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
     return e;
@@ -556,10 +692,10 @@ void launch_scatter_sparse(const SubDev* subs, int sub, int n, cudaStream_t st) 
   if (n > 0) scatter_sparse_kernel<<<n, 256, 0, st>>>(subs, sub);
 }
 void launch_diag_inverse(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
-  if (nwork > 0) diag_inverse_kernel<<<nwork, 128, 2 * 8256 * 8, st>>>(subs, work);
+  if (nwork > 0) diag_inverse_kernel<<<nwork, 256, (2 * 8256 + 3 * 1024) * 8, st>>>(subs, work);
 }
 void launch_block_scale(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
-  if (nwork > 0) block_scale_kernel<<<nwork, 256, scale_smem(), st>>>(subs, work);
+  if (nwork > 0) block_scale_kernel<<<nwork, BS_THREADS, scale_smem(), st>>>(subs, work);
 }
 void launch_trsm_chain(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
   if (nwork > 0) trsm_chain_kernel<<<nwork, PIPE_THREADS, pipe_smem(), st>>>(subs, work);
@@ -567,14 +703,14 @@ void launch_trsm_chain(const SubDev* subs, const int4* work, int nwork, cudaStre
 void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
   if (nwork > 0) syrk_kernel<<<nwork, PIPE_THREADS, pipe_smem(), st>>>(subs, work);
 }
-void launch_apply(int nw, size_t smem, const SubDev* subs, const int4* work, int nwork, const int64_t* part_off,
-                  double* part, const double* p, cudaStream_t st) {
-  if (nwork <= 0) return;
+void launch_apply(int nw, size_t smem, const SubDev* subs, const int4* segs, const int* seg_ptr, int nctas,
+                  const int64_t* part_off, double* part, const double* p, cudaStream_t st) {
+  if (nctas <= 0) return;
   switch (nw) {
-    case 8: apply_kernel<8><<<nwork, 256, smem, st>>>(subs, work, part_off, part, p); break;
-    case 4: apply_kernel<4><<<nwork, 128, smem, st>>>(subs, work, part_off, part, p); break;
-    case 2: apply_kernel<2><<<nwork, 64, smem, st>>>(subs, work, part_off, part, p); break;
-    default: apply_kernel<1><<<nwork, 32, smem, st>>>(subs, work, part_off, part, p); break;
+    case 8: apply_kernel<8><<<nctas, 256, smem, st>>>(subs, segs, seg_ptr, part_off, part, p); break;
+    case 4: apply_kernel<4><<<nctas, 128, smem, st>>>(subs, segs, seg_ptr, part_off, part, p); break;
+    case 2: apply_kernel<2><<<nctas, 64, smem, st>>>(subs, segs, seg_ptr, part_off, part, p); break;
+    default: apply_kernel<1><<<nctas, 32, smem, st>>>(subs, segs, seg_ptr, part_off, part, p); break;
   }
 }
 void launch_reduce(int n_mult, const int* cptr, const int4* cent, const int64_t* part_off, const double* part,
