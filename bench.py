@@ -573,6 +573,8 @@ def main():
     ap.add_argument("--ordering", default="rcm", choices=("rcm", "interface_last"))
     ap.add_argument("--applies", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
+                    help="gloo only to exercise N > 1 with several ranks sharing one GPU")
     ap.add_argument("--single-ordering", action="store_true",
                     help="skip the second (alternative ordering) measurement")
     args = ap.parse_args()
@@ -589,8 +591,12 @@ def main():
         import torch
         import torch.distributed as dist
 
+        local_rank = local_rank % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:   # gloo: exercises the N > 1 code path with several ranks on one GPU
+            dist.init_process_group("gloo")
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -183,7 +183,68 @@ __global__ void __launch_bounds__(256) diag_inverse_kernel(const SubDev* __restr
 constexpr int BS_STAGES = 3;
 constexpr int QCOLS = 32;
 constexpr int QSIZE = QCOLS * TB;   // 4096 doubles (32 KB)
-constexpr int BS_THREADS = 288;
+constexpr int BS_THREADS = 256;
+
+// Issue the copies of quarter qi of row k into `dst` (all 256 threads).
+__device__ __forceinline__ void bs_load_quarter(const SubDev& S, int k, int qi, double* dst, bool dense) {
+  const int l = S.smin + qi / (TB / QCOLS), q = qi % (TB / QCOLS);
+  if (dense) {
+    // column jg of L: rows k*128 + kk at raw[colstart(jg) + (i - jg)]; thread
+    // (jq, kk-quarter): 4 columns x 32 consecutive rows per warp -> coalesced
+    const int64_t n = S.n;
+    const int64_t i0 = (int64_t)k * TB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int c = 0; c < QCOLS / 8; ++c) {
+      const int jq = warp * (QCOLS / 8) + c;
+      const int64_t jg = (int64_t)l * TB + q * QCOLS + jq;
+      const double* col = S.raw + (jg * n - jg * (jg - 1) / 2 - jg - S.raw_off);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int kk = lane + 32 * t;
+        if (i0 + kk < n) cp_async8(dst + swz(jq, kk), col + i0 + kk);
+      }
+    }
+  } else {
+    const double* src = tile_ptr(S, k, l) + q * QSIZE;
+    for (int idx = threadIdx.x * 2; idx < QSIZE; idx += BS_THREADS * 2) cp_async16(dst + idx, src + idx);
+  }
+}
+
+// k-steps [kb0, kb1) for the row groups M0..3 of this warp (all active).
+// Even and odd k-steps accumulate into separate registers so that each warp
+// keeps twice as many independent DMMA chains in flight (the tail phases have
+// only 1-2 active row groups).
+template <int M0>
+__device__ __forceinline__ void bs_step(int kb, double (&acc)[4][2][2], const int (&rg)[4],
+                                        const double* __restrict__ sA, const double* __restrict__ b_s, int wn,
+                                        int g, int t, int rows_valid) {
+  const int kk = kb * 4 + t;
+  double bf[2], af[4];
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni) {
+    const double v = b_s[swz(wn * 16 + ni * 8 + g, kk)];
+    bf[ni] = kk < rows_valid ? v : 0.0;
+  }
+#pragma unroll
+  for (int mi = M0; mi < 4; ++mi) af[mi] = sA[swz(kk, rg[mi] * 8 + g)];
+#pragma unroll
+  for (int mi = M0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+}
+
+template <int M0>
+__device__ __forceinline__ void bs_steps(int kb0, int kb1, double (&acc)[4][2][2], double (&acc2)[4][2][2],
+                                         const int (&rg)[4], const double* __restrict__ sA,
+                                         const double* __restrict__ b_s, int wn, int g, int t, int rows_valid) {
+  int kb = kb0;
+  for (; kb + 1 < kb1; kb += 2) {
+    bs_step<M0>(kb, acc, rg, sA, b_s, wn, g, t, rows_valid);
+    bs_step<M0>(kb + 1, acc2, rg, sA, b_s, wn, g, t, rows_valid);
+  }
+  if (kb < kb1) bs_step<M0>(kb, acc, rg, sA, b_s, wn, g, t, rows_valid);
+}
 
 __global__ void __launch_bounds__(BS_THREADS, 1) block_scale_kernel(const SubDev* __restrict__ subs,
                                                                     const int4* __restrict__ work) {
@@ -191,103 +252,68 @@ __global__ void __launch_bounds__(BS_THREADS, 1) block_scale_kernel(const SubDev
   double* sA = reinterpret_cast<double*>(smem_raw);      // TILE
   double* sB = sA + TILE;                                 // BS_STAGES * QSIZE
   uint64_t* barA = reinterpret_cast<uint64_t*>(sB + BS_STAGES * QSIZE);
-  uint64_t* full = barA + 1;
-  uint64_t* empty = full + BS_STAGES;
   const int4 w = work[blockIdx.x];
   const SubDev& S = subs[w.x];
   const int k = w.y;
-  const int l0 = S.smin;
-  const int nq = (k - l0) * (TB / QCOLS);
+  const int nq = (k - S.smin) * (TB / QCOLS);
   const bool dense = (S.up == nullptr);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(barA, 1);
-    for (int i = 0; i < BS_STAGES; ++i) {
-      mbar_init(&full[i], dense ? 32 : 1);
-      mbar_init(&empty[i], 8);
-    }
     mbar_fence_init();
   }
   __syncthreads();
-  if (warp == 8) {
-    const int64_t n = S.n;
-    if (lane == 0) {
-      mbar_arrive_expect_tx(barA, TILE * 8);
-      const double* inv = tile_ptr(S, k, k);
-      for (int s = 0; s < 4; ++s) bulk_g2s(sA + s * SLICE, inv + s * SLICE, SLICE * 8, barA);
-    }
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int qi = 0; qi < nq; ++qi) {
-      const int l = l0 + qi / (TB / QCOLS), q = qi % (TB / QCOLS);
-      mbar_wait(&empty[stage], phase ^ 1);
-      double* dst = sB + stage * QSIZE;
-      if (dense) {
-        // column jg of L: rows k*128 + kk at raw[colstart(jg) + (i - jg)]
-        const int64_t i0 = (int64_t)k * TB;
-#pragma unroll 4
-        for (int jq = 0; jq < QCOLS; ++jq) {
-          const int64_t jg = (int64_t)l * TB + q * QCOLS + jq;
-          const double* col = S.raw + (jg * n - jg * (jg - 1) / 2 - jg - S.raw_off);
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int kk = lane + 32 * t;
-            if (i0 + kk < n) cp_async8(dst + swz(jq, kk), col + i0 + kk);
-          }
-        }
-        cp_async_mbar_arrive(&full[stage]);
-      } else if (lane == 0) {
-        mbar_arrive_expect_tx(&full[stage], QSIZE * 8);
-        bulk_g2s(dst, tile_ptr(S, k, l) + q * QSIZE, QSIZE * 8, &full[stage]);
-      }
-      if (++stage == BS_STAGES) {
-        stage = 0;
-        phase ^= 1;
-      }
-    }
-    return;
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(barA, TILE * 8);
+    const double* inv = tile_ptr(S, k, k);
+    for (int s = 0; s < 4; ++s) bulk_g2s(sA + s * SLICE, inv + s * SLICE, SLICE * 8, barA);
   }
-  const int wm = warp >> 1, wn = warp & 1;     // warp tile 32 x 16 of 128 x 32
+  // classic multistage cp.async ring for the L_kl quarters (every thread
+  // issues 16 of the 8-byte copies of a quarter; the sources are the
+  // reference's packed columns, whose alignment rules out bulk copies)
+#pragma unroll
+  for (int st = 0; st < BS_STAGES - 1; ++st) {
+    if (st < nq) bs_load_quarter(S, k, st, sB + st * QSIZE, dense);
+    cp_async_commit();
+  }
+  // inv(L_kk) is lower triangular: 8-row group r needs k-steps kb <= 2r+1.
+  // Each warp takes 4 row groups whose triangular costs sum to the same 68
+  // DMMA k-steps ({w, 15-w, 7-w, 8+w}), so no warp idles at the quarter end.
+  const int wm = warp >> 1, wn = warp & 1;     // 4 row groups x 16 columns of 128 x 32
   const int g = lane >> 2, t = lane & 3;
-  const int kb_end = wm * 8 + 8;               // inv(L_kk)[i][kk] = 0 for kk > i
+  const int rg[4] = {wm, 7 - wm, 8 + wm, 15 - wm};
   const int rows_valid = S.n - k * TB;         // padding rows of the last block row
   mbar_wait(barA, 0);
-  int stage = 0;
-  uint32_t phase = 0;
   for (int qi = 0; qi < nq; ++qi) {
-    const int l = l0 + qi / (TB / QCOLS), q = qi % (TB / QCOLS);
-    double acc[4][2][2];
+    cp_async_wait_group<BS_STAGES - 2>();
+    __syncthreads();                           // quarter qi landed; stage (qi-1) free
+    const int nx = qi + BS_STAGES - 1;
+    if (nx < nq) bs_load_quarter(S, k, nx, sB + (nx % BS_STAGES) * QSIZE, dense);
+    cp_async_commit();
+    const double* b_s = sB + (qi % BS_STAGES) * QSIZE;
+    double acc[4][2][2], acc2[4][2][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    mbar_wait(&full[stage], phase);
-    const double* b_s = sB + stage * QSIZE;
-    for (int kb = 0; kb < kb_end; ++kb) {
-      const int kk = kb * 4 + t;
-      double bf[2];
+      for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = acc2[a][b][0] = acc2[a][b][1] = 0.0;
+    // rg ascending (w < 7-w < 8+w < 15-w): the active row groups shrink at
+    // k-step 2w+2, 16-2w, 18+2w; each phase runs a fixed, unrolled set
+    bs_steps<0>(0, 2 * wm + 2, acc, acc2, rg, sA, b_s, wn, g, t, rows_valid);
+    bs_steps<1>(2 * wm + 2, 16 - 2 * wm, acc, acc2, rg, sA, b_s, wn, g, t, rows_valid);
+    bs_steps<2>(16 - 2 * wm, 18 + 2 * wm, acc, acc2, rg, sA, b_s, wn, g, t, rows_valid);
+    bs_steps<3>(18 + 2 * wm, 32 - 2 * wm, acc, acc2, rg, sA, b_s, wn, g, t, rows_valid);
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) {
-        const double v = b_s[swz(wn * 16 + ni * 8 + g, kk)];
-        bf[ni] = kk < rows_valid ? v : 0.0;
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        acc[a][b][0] += acc2[a][b][0];
+        acc[a][b][1] += acc2[a][b][1];
       }
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const double af = sA[swz(kk, wm * 32 + mi * 8 + g)];
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
-    if (++stage == BS_STAGES) {
-      stage = 0;
-      phase ^= 1;
-    }
+    const int l = S.smin + qi / (TB / QCOLS), q = qi % (TB / QCOLS);
     double* Lkl = tile_ptr(S, k, l);
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {
-      const int i = wm * 32 + mi * 8 + g;
+      const int i = rg[mi] * 8 + g;
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni) {
         const int j = q * QCOLS + wn * 16 + ni * 8 + 2 * t;
@@ -296,6 +322,7 @@ __global__ void __launch_bounds__(BS_THREADS, 1) block_scale_kernel(const SubDev
       }
     }
   }
+  cp_async_wait_group<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -660,7 +687,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(int n_mult, const int* __re
 // launchers
 // ---------------------------------------------------------------------------
 static size_t pipe_smem() { return 2 * PIPE_STAGES * SLICE * sizeof(double) + 8 * (2 * PIPE_STAGES + 1); }
-static size_t scale_smem() { return (TILE + BS_STAGES * QSIZE) * sizeof(double) + 8 * (1 + 2 * BS_STAGES); }
+static size_t scale_smem() { return (TILE + BS_STAGES * QSIZE) * sizeof(double) + 16; }
 
 cudaError_t configure_kernels() {
   cudaError_t e;
