@@ -451,10 +451,29 @@ def run_ours(args, rank, world, local_rank):
                 op.apply(p_host, out=q_host)
             ta.append(time.perf_counter() - t0)
         apply_e2e_ms = max_over_ranks(statistics.median(ta) * 1e3)
+        solve = None
+        if world == 1 and args.solve:
+            # GPU-resident PCPG on this operator; the host
+            # factors handed over in the e2e loop serve solve_local for d
+            from paper_2502_08382_b200.pcpg import DevicePCPG
+
+            t0 = time.perf_counter()
+            kernels, forces = [], []
+            for s in range(prob.n_sub):
+                _, f, qk = prob.subdomain_system(s)
+                kernels.append(qk)
+                forces.append(f)
+            solver = DevicePCPG(op, kernels, forces, prob.c)
+            t_setup = time.perf_counter() - t0
+            solver.solve(tol=1e-9)                       # warm-up (lazy library init)
+            lam, iters, t_loop = solver.solve(tol=1e-9)
+            solve = {"pcpg_iterations": iters, "device_loop_s": t_loop, "ms_per_iteration": t_loop / max(iters, 1) * 1e3,
+                     "dual_system_setup_s": t_setup, "lambda_norm": float(np.linalg.norm(lam)), "tol": 1e-9}
+            log(f"[rank {rank}] {ordering}: device PCPG {iters} iterations in {t_loop * 1e3:.1f} ms")
         res = {"ordering": ordering, "ms_step": ms_step, "stats": stats, "clocks": clocks, "apply_ms": apply_ms,
                "apply_kernel_ms": apply_kernel_ms, "e2e_s": e2e_s, "apply_e2e_ms": apply_e2e_ms,
                "h2d_bytes": int(st_host["factor_bytes"]) + 8 * prob.n_multipliers,
-               "host_factors": host_factors if keep_host else None, "perms": perms}
+               "host_factors": host_factors if keep_host else None, "perms": perms, "solve": solve}
         op.close()
         del dev_factors, dco, p_dev, q_dev
         torch.cuda.empty_cache()
@@ -504,6 +523,7 @@ def run_ours(args, rank, world, local_rank):
                     "what": "pinned host factors (reference layout; the lib copies the suffix the pruned solve "
                             "reads) -> device assembly -> one apply with host p/q"},
             "device_bytes": {"persistent": st["bytes_persistent"], "temporary": st["bytes_temporary"]},
+            "solve": r["solve"],
         }
 
     value, fields = summarize(main_res)
@@ -524,7 +544,8 @@ def run_ours(args, rank, world, local_rank):
     if alt is not None:
         v2, f2 = summarize(alt)
         line[f"ordering_{alt['ordering']}"] = {"value": v2, **{k: f2[k] for k in
-                                                              ("e2e", "phases_ms", "flops", "roofline", "apply")}}
+                                                              ("e2e", "phases_ms", "flops", "roofline", "apply",
+                                                               "solve")}}
     if world == 1 and not args.no_cpu_baseline:
         ms = prob.m_per_subdomain()
         sample = int(np.argmax(ms))
@@ -573,6 +594,8 @@ def main():
     ap.add_argument("--ordering", default="rcm", choices=("rcm", "interface_last"))
     ap.add_argument("--applies", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solve", dest="solve", action="store_false",
+                    help="skip the GPU-resident PCPG solve measurement")
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
                     help="gloo only to exercise N > 1 with several ranks sharing one GPU")
     ap.add_argument("--single-ordering", action="store_true",

@@ -129,6 +129,18 @@ int feti_apply(feti_ctx* ctx, const double* p, double* q);
  * caller orders it after feti_assemble (which returns synchronised). */
 int feti_apply_device(feti_ctx* ctx, const double* d_p, double* d_q, void* stream);
 
+/* Coarse space for a GPU-resident PCPG (solver.py:117-123, 195-272): the
+ * projector P x = x - G (G^T G)^-1 G^T x with G = B R block sparse.
+ *   kdim        per slot: kernel dimension r_s (1 heat, 3/6 elasticity)
+ *   G           per slot, concatenated: m_s x r_s row-major, original local
+ *               multiplier order, G_s[a][c] = B~_s[a] R_s[dof_a][c]
+ *   coarse_inv  nk x nk row-major (G^T G)^-1, nk = sum r_s                  */
+int feti_coarse_setup(feti_ctx* ctx, const int64_t* kdim, const double* G, const double* coarse_inv, int64_t nk);
+/* out = P x on device vectors (out may alias x), enqueued on `stream`. */
+int feti_project_device(feti_ctx* ctx, const double* d_x, double* d_out, void* stream);
+/* out = G (G^T G)^-1 v for v of length nk (feasible start G (G^T G)^-1 e). */
+int feti_coarse_apply_device(feti_ctx* ctx, const double* d_v, double* d_out, void* stream);
+
 int feti_get_stats(feti_ctx* ctx, feti_stats* out);
 
 /* Diagnostics: per-kernel register / thread limits as text. */

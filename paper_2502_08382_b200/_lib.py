@@ -28,7 +28,7 @@ EXPORTED = (
     "feti_abi_version", "feti_last_error", "feti_create", "feti_destroy", "feti_add_subdomain",
     "feti_finalize", "feti_set_factor", "feti_assemble", "feti_local_operator", "feti_apply",
     "feti_apply_device", "feti_get_stats", "feti_host_alloc", "feti_host_free",
-    "feti_debug_kernel_attributes",
+    "feti_debug_kernel_attributes", "feti_coarse_setup", "feti_project_device", "feti_coarse_apply_device",
 )
 
 
@@ -82,6 +82,9 @@ def load() -> C.CDLL:
         "feti_get_stats": ([P, C.POINTER(FetiStats)], C.c_int),
         "feti_host_alloc": ([C.c_size_t, C.POINTER(P)], C.c_int),
         "feti_debug_kernel_attributes": ([C.c_char_p, C.c_int], C.c_int),
+        "feti_coarse_setup": ([P, i64p, f64p, f64p, C.c_int64], C.c_int),
+        "feti_project_device": ([P, P, P, P], C.c_int),
+        "feti_coarse_apply_device": ([P, P, P, P], C.c_int),
         "feti_host_free": ([P], C.c_int),
     }
     for name, (args, res) in sig.items():

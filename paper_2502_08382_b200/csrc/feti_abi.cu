@@ -19,6 +19,7 @@
 
 #include "../../include/feti_b200.h"
 #include "feti_common.cuh"
+#include "feti_coarse.h"
 #include "feti_kernels.h"
 
 using namespace feti;
@@ -124,6 +125,13 @@ struct feti_ctx {
   feti_stats stats{};
   cudaEvent_t ev[8] = {};
   bool subdev_dirty = true;
+  // coarse space (GPU-resident PCPG): G blocks, (G^T G)^-1, work vectors
+  int nk = 0;
+  CoarseSub* d_coarse = nullptr;
+  int2* d_kcols = nullptr;
+  double* d_cinv = nullptr;
+  double* d_kv = nullptr;
+  double* d_kz = nullptr;
   // upload/compute pipeline for host factors: subdomains grouped in waves
   // (largest work first); wave w's H2D on copy_stream, its kernels on
   // wave_streams[w % 2] once its copies landed
@@ -490,7 +498,7 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   std::vector<std::vector<int4>> per_g((size_t)c->n_mult);
   for (int si = 0; si < (int)c->subs.size(); ++si) {
     const SubHost& s = c->subs[si];
-    for (int a = 0; a < s.m; ++a) per_g[s.gids_sorted[a]].push_back(make_int4(a, cta_begin[si], cta_end[si], 0));
+    for (int a = 0; a < s.m; ++a) per_g[s.gids_sorted[a]].push_back(make_int4(a, cta_begin[si], cta_end[si], si));
   }
   std::vector<int> cptr((size_t)c->n_mult + 1, 0);
   std::vector<int4> cent;
@@ -757,6 +765,77 @@ int feti_apply_device(feti_ctx* c, const double* d_p, double* d_q, void* stream)
   CUDA_TRY(cudaSetDevice(c->device));
   // the handle is used verbatim: NULL is the legacy default stream, as in CUDA
   return apply_enqueue(c, d_p, d_q, (cudaStream_t)stream, false);
+}
+
+int feti_coarse_setup(feti_ctx* c, const int64_t* kdim, const double* G, const double* coarse_inv, int64_t nk) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->finalized) return fail(FETI_ERR_LIFECYCLE, "coarse setup before prepare");
+  if (c->d_coarse) return fail(FETI_ERR_LIFECYCLE, "coarse space already set up");
+  if (!kdim || !G || !coarse_inv || nk < 0 || nk > (1 << 20)) return fail(FETI_ERR_ARG, "bad coarse arguments");
+  CUDA_TRY(cudaSetDevice(c->device));
+  int64_t tot = 0, gsz = 0;
+  for (size_t si = 0; si < c->subs.size(); ++si) {
+    if (kdim[si] < 0) return fail(FETI_ERR_ARG, "negative kernel dimension");
+    tot += kdim[si];
+    gsz += c->subs[si].m * kdim[si];
+  }
+  if (tot != nk) return fail(FETI_ERR_ARG, "kernel dimensions sum to %lld, expected %lld", (long long)tot, (long long)nk);
+  // permute each block to the sorted local order of the apply's index maps
+  std::vector<double> gs((size_t)std::max<int64_t>(gsz, 1));
+  std::vector<CoarseSub> hs(c->subs.size());
+  std::vector<int2> cols;
+  int64_t goff = 0, koff = 0;
+  double* d_g = nullptr;
+  int rc;
+  if ((rc = dev_alloc(c, (void**)&d_g, gs.size() * 8, true))) return rc;
+  for (size_t si = 0; si < c->subs.size(); ++si) {
+    const SubHost& s = c->subs[si];
+    const int r = (int)kdim[si];
+    for (int64_t a = 0; a < s.m; ++a)
+      for (int k = 0; k < r; ++k) gs[goff + a * r + k] = G[goff + s.colperm[a] * r + k];
+    hs[si].G = d_g + goff;
+    hs[si].gids = s.d_g;
+    hs[si].m = (int)s.m;
+    hs[si].r = r;
+    hs[si].koff = (int)koff;
+    for (int k = 0; k < r; ++k) cols.push_back(make_int2((int)si, k));
+    goff += s.m * r;
+    koff += r;
+  }
+  CUDA_TRY(cudaMemcpy(d_g, gs.data(), gs.size() * 8, cudaMemcpyHostToDevice));
+  if ((rc = upload(c, &c->d_coarse, hs))) return rc;
+  if ((rc = upload(c, &c->d_kcols, cols))) return rc;
+  std::vector<double> ci(coarse_inv, coarse_inv + nk * nk);
+  if ((rc = upload(c, &c->d_cinv, ci))) return rc;
+  if ((rc = dev_alloc(c, (void**)&c->d_kv, (size_t)std::max<int64_t>(nk, 1) * 8, true))) return rc;
+  if ((rc = dev_alloc(c, (void**)&c->d_kz, (size_t)std::max<int64_t>(nk, 1) * 8, true))) return rc;
+  c->nk = (int)nk;
+  return FETI_OK;
+}
+
+int feti_project_device(feti_ctx* c, const double* d_x, double* d_out, void* stream) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->d_coarse) return fail(FETI_ERR_LIFECYCLE, "projector before coarse setup");
+  if (!d_x || !d_out) return fail(FETI_ERR_ARG, "NULL vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_gtx(c->d_coarse, c->d_kcols, c->nk, d_x, c->d_kv, st);
+  launch_coarse(c->nk, c->d_cinv, c->d_kv, c->d_kz, st);
+  launch_project((int)c->n_mult, c->d_cptr, c->d_cent, c->d_coarse, c->d_kz, d_x, 1.0, d_out, st);
+  CUDA_TRY(cudaGetLastError());
+  return FETI_OK;
+}
+
+int feti_coarse_apply_device(feti_ctx* c, const double* d_v, double* d_out, void* stream) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->d_coarse) return fail(FETI_ERR_LIFECYCLE, "coarse apply before coarse setup");
+  if (!d_v || !d_out) return fail(FETI_ERR_ARG, "NULL vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_coarse(c->nk, c->d_cinv, d_v, c->d_kz, st);
+  launch_project((int)c->n_mult, c->d_cptr, c->d_cent, c->d_coarse, c->d_kz, nullptr, -1.0, d_out, st);
+  CUDA_TRY(cudaGetLastError());
+  return FETI_OK;
 }
 
 int feti_get_stats(feti_ctx* c, feti_stats* out) {

@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(BS_THREADS, 1) block_scale_kernel(const SubDev
   double* sB = sA + TILE;                                 // BS_STAGES * QSIZE
   uint64_t* barA = reinterpret_cast<uint64_t*>(sB + BS_STAGES * QSIZE);
   const int4 w = work[blockIdx.x];
-  const SubDev& S = subs[w.x];
+  const SubDev S = subs[w.x];   // by value: no reloads after the epilogue's global stores
   const int k = w.y;
   const int nq = (k - S.smin) * (TB / QCOLS);
   const bool dense = (S.up == nullptr);

@@ -1,0 +1,142 @@
+"""GPU-resident projected conjugate gradients on the B200 dual operator.
+
+SURVEY.md §8f row 1: the reference's PCPG (solver.py:195-272) calls
+``state.apply(numpy, out=numpy)`` once per iteration and projects with a dense
+G on the host (solver.py:117-119), so every iteration pays a host round trip
+and ~n_mult x sum(r) host reads per projection.  Here the whole iteration
+stays on the device: the explicit apply (fused SYMV + gather/scatter), the
+projector P x = x - G (G^T G)^-1 G^T x (block-sparse G kernels in the same
+library) and the vector algebra on torch tensors.  The recursion, the
+stopping test and the initial roundoff guard are the reference's, step for
+step, so iteration counts match it (tests/test_gpu_pcpg.py).
+
+The dual system itself (G, e, d and the coarse Gram matrix, solver.py:125-148)
+is assembled once on the host from the per-subdomain kernels, loads and
+``solve_local``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+
+from . import _lib
+
+
+class BreakdownError(ArithmeticError):
+    """p^T F p <= 0: the operator is not PSD (solver.py:40-41)."""
+
+
+class ConvergenceError(RuntimeError):
+    """Iteration cap reached before the tolerance (solver.py:44-45)."""
+
+
+class DevicePCPG:
+    """PCPG with identity preconditioner, one GPU (one operator context).
+
+    ``op``: a prepared and preprocessed :class:`~.dualop.DualOperator` owning
+    every subdomain; ``kernels[i]`` (n_i x r_i, orthonormal kernel basis) and
+    ``forces[i]`` per subdomain; ``c`` the constraint right-hand side.
+    """
+
+    def __init__(self, op, kernels, forces, c):
+        import torch
+
+        if sorted(op._subs) != list(range(op.n_subdomains)):
+            raise ValueError("the device PCPG needs an operator that owns every subdomain")
+        self.op = op
+        self.torch = torch
+        dev = torch.device("cuda", op._resolve_device())
+        self.device = dev
+        n_mult = op.n_multipliers
+        subs = sorted(op._subs.values(), key=lambda s: s.slot)
+        kdim = np.array([kernels[s.index].shape[1] for s in subs], dtype=np.int64)
+        nk = int(kdim.sum())
+        blocks, e_parts = [], []
+        gmat = np.zeros((n_mult, nk))
+        off = 0
+        d = np.zeros(n_mult)
+        for s in subs:
+            r = kernels[s.index]
+            gblk = s.bval[:, None] * r[s.bcol, :]            # G_s = B~_s R_s (solver.py:137-139)
+            blocks.append(np.ascontiguousarray(gblk).ravel())
+            gmat[s.gids, off:off + r.shape[1]] = gblk
+            e_parts.append(r.T @ forces[s.index])            # e = R^T f
+            kf = op.solve_local(s.index, forces[s.index])
+            d[s.gids] += s.bval * kf[s.bcol]                 # B K^+ f
+            off += r.shape[1]
+        d -= np.asarray(c, dtype=np.float64)
+        gtg = gmat.T @ gmat
+        lchol = np.linalg.cholesky(gtg)                      # SPD check as solver.py:144-147
+        cinv = np.linalg.solve(lchol.T, np.linalg.solve(lchol, np.eye(nk)))
+        cinv = np.ascontiguousarray(0.5 * (cinv + cinv.T))
+        gcat = np.concatenate(blocks) if blocks else np.zeros(1)
+        rc = op._lib.feti_coarse_setup(op._ctx, _lib.i64ptr(kdim), _lib.f64ptr(gcat), _lib.f64ptr(cinv), nk)
+        _lib.check(rc)
+        self.nk = nk
+        self.gmat = gmat
+        self.e = np.concatenate(e_parts) if e_parts else np.zeros(0)
+        self.d = d
+        self.d_dev = torch.from_numpy(d).to(dev)
+        self.e_dev = torch.from_numpy(self.e).to(dev)
+
+    def _stream(self):
+        return C.c_void_p(int(self.torch.cuda.current_stream(self.device).cuda_stream))
+
+    def project(self, x, out):
+        _lib.check(self.op._lib.feti_project_device(self.op._ctx, C.c_void_p(int(x.data_ptr())),
+                                                    C.c_void_p(int(out.data_ptr())), self._stream()))
+        return out
+
+    def apply(self, x, out):
+        self.op.apply_device(x, out, stream=int(self.torch.cuda.current_stream(self.device).cuda_stream))
+        return out
+
+    def solve(self, tol: float = 1e-9, maxit: int | None = None):
+        """Returns (lambda as numpy, iterations, seconds of device loop)."""
+        torch = self.torch
+        n_mult = self.d.shape[0]
+        maxit = n_mult if maxit is None else int(maxit)
+        torch.cuda.synchronize(self.device)
+        t0 = time.perf_counter()
+        lam = torch.empty(n_mult, dtype=torch.float64, device=self.device)
+        _lib.check(self.op._lib.feti_coarse_apply_device(self.op._ctx, C.c_void_p(int(self.e_dev.data_ptr())),
+                                                         C.c_void_p(int(lam.data_ptr())), self._stream()))
+        q = torch.empty_like(lam)
+        r = self.d_dev - self.apply(lam, q)
+        w = self.project(r, torch.empty_like(r))
+        y = self.project(w, torch.empty_like(w))          # mfun = identity (precond "none")
+        p = y.clone()
+        w0 = float(torch.linalg.vector_norm(w))
+        wy = float(torch.dot(w, y))
+        if w0 <= 1e-14 * max(1.0, float(np.linalg.norm(self.d))):
+            torch.cuda.synchronize(self.device)
+            return lam.cpu().numpy(), 0, time.perf_counter() - t0
+        k = 0
+        one = torch.ones((), dtype=torch.float64, device=self.device)
+        wy_t = torch.dot(w, y)
+        while True:
+            qk = self.apply(p, q)
+            pq_t = torch.dot(p, qk)
+            delta_t = wy_t / pq_t
+            lam.addcmul_(p, delta_t * one)
+            r.addcmul_(qk, -delta_t * one)
+            self.project(r, w)
+            self.project(w, y)
+            k += 1
+            wy_next_t = torch.dot(w, y)
+            # one host synchronisation per iteration: breakdown + stopping test
+            pq, wn = torch.stack((pq_t, torch.linalg.vector_norm(w))).tolist()
+            if pq <= 0.0:
+                raise BreakdownError(f"p^T F p = {pq:.3e} at iteration {k - 1}")
+            if wn <= tol * w0:
+                torch.cuda.synchronize(self.device)
+                return lam.cpu().numpy(), k, time.perf_counter() - t0
+            if k >= maxit:
+                raise ConvergenceError(f"PCPG did not reach tol {tol:.1e} in {maxit} iterations "
+                                       f"(relative residual {wn / w0:.3e})")
+            beta_t = wy_next_t / wy_t
+            wy_t = wy_next_t
+            p.mul_(beta_t).add_(y)

@@ -24,3 +24,15 @@ def load_golden(name):
 
 
 SMALL_CASES = ["heat2d_3x2", "heat2d_c1", "heat3d_4x2", "elast2d_4x2", "elast3d_4x2"]
+
+
+# PCPG iteration counts that are robust to 1e-14 rounding differences are
+# asserted exactly; elasticity 3D 4^3 sits at 9.83e-10 vs tol 1e-9 and flips
+# between 93 and 94 under such perturbations (tests/test_oracle.py::
+# test_pcpg_iteration_count_sensitivity), so one extra iteration is accepted.
+ROUNDING_SENSITIVE = {"elast3d_4x2"}
+
+
+def expected_iterations(case, g):
+    it = int(g["pcpg_iterations"])
+    return {it, it + 1} if case in ROUNDING_SENSITIVE else {it}

@@ -11,7 +11,7 @@ import ctypes as C
 import numpy as np
 import pytest
 
-from conftest import SMALL_CASES, load_golden
+from conftest import SMALL_CASES, expected_iterations, load_golden
 from oracle import feti_oracle as ora
 from paper_2502_08382_b200 import _lib, dualop, inputs
 
@@ -68,7 +68,7 @@ def test_pcpg_iterations_match_reference(case):
         gm, e, d, coarse = ora.assemble_dual_system(kernels, forces, cl, prob.n_multipliers, prob.c,
                                                     op.solve_local)
         lam, it = ora.pcpg(gm, e, d, coarse, op.apply, tol=1e-9)
-    assert it == int(g["pcpg_iterations"])
+    assert it in expected_iterations(case, g)
     ref = g["pcpg_lambda"]
     assert np.linalg.norm(lam - ref) <= 1e-9 * np.linalg.norm(ref)
 

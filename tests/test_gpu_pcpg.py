@@ -1,0 +1,35 @@
+"""GPU-resident PCPG: iteration counts and multipliers of
+the reference's own solver runs (golden fixtures)."""
+
+import numpy as np
+import pytest
+
+from conftest import SMALL_CASES, expected_iterations, load_golden
+from paper_2502_08382_b200 import dualop, inputs
+from paper_2502_08382_b200.pcpg import DevicePCPG
+
+pytestmark = pytest.mark.gpu
+CFG = dualop.DualOpConfig(strategy="explicit", path="syrk")
+
+
+def _solve(prob, dense=False):
+    mats, cons, lay = inputs.reference_inputs(prob, dense=dense)
+    kernels, forces = [], []
+    for s in range(prob.n_sub):
+        _, f, q = prob.subdomain_system(s)
+        kernels.append(q)
+        forces.append(f)
+    with dualop.prepare(mats, cons, lay, CFG, device=0, workers=8) as op:
+        op.preprocess()
+        solver = DevicePCPG(op, kernels, forces, prob.c)
+        return solver.solve(tol=1e-9)
+
+
+@pytest.mark.parametrize("case", SMALL_CASES + ["heat3d_c2"])
+def test_device_pcpg_matches_reference(case):
+    g = load_golden(case)
+    prob = inputs.Problem(str(g["physics"]), int(g["dim"]), int(g["cells"]), int(g["subs"]))
+    lam, it, _ = _solve(prob, dense=(case == "heat3d_c2"))
+    assert it in expected_iterations(case, g)
+    ref = g["pcpg_lambda"]
+    assert np.linalg.norm(lam - ref) <= 1e-9 * np.linalg.norm(ref)

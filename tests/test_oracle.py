@@ -86,3 +86,36 @@ def test_known_answers():
     x = np.array([2.0, 3.0])
     ora.lib().ora_utsolve_rows(2, 1, up.ctypes.data, ui.ctypes.data, ux.ctypes.data, x.ctypes.data)
     np.testing.assert_allclose(x, [1.0, 1.0], atol=1e-15)
+
+
+def test_pcpg_iteration_count_sensitivity():
+    """Which golden cases have a rounding-robust PCPG iteration count.
+
+    Perturbing every F~_i by random relative 1e-14 (the size of the difference
+    between any two correct implementations: different summation orders)
+    never changes the count for heat 2D/3D, config 1 or elasticity 2D, so the
+    device tests assert equality there.  Elasticity 3D 4^3 stops at relative
+    residual 9.83e-10 against tol 1e-9 after 93 iterations (the reference's
+    own run); such perturbations flip it to 94 in a fraction of trials, so
+    the device tests accept 93 or 94 there (lambda still within 1e-9)."""
+    rng = np.random.default_rng(0)
+    for case, robust in (("heat3d_4x2", True), ("elast3d_4x2", False)):
+        g = load_golden(case)
+        n_sub = int(g["n_sub"])
+        facs, cons = _case_factors(g, n_sub)
+        kernels = [g[f"s{s}_kernel"] for s in range(n_sub)]
+        forces = [g[f"s{s}_force"] for s in range(n_sub)]
+        op = ora.OracleOperator(facs, cons)
+        op.preprocess()
+        gm, e, d, coarse = ora.assemble_dual_system(kernels, forces, cons, int(g["n_multipliers"]), g["c"],
+                                                    op.solve_local)
+        counts = set()
+        for _ in range(8):
+            op2 = ora.OracleOperator(facs, cons)
+            op2.fmats = [f * (1 + 1e-14 * np.triu(rng.standard_normal(f.shape))) for f in op.fmats]
+            counts.add(ora.pcpg(gm, e, d, coarse, op2.apply, tol=1e-9)[1])
+        ref_it = int(g["pcpg_iterations"])
+        if robust:
+            assert counts == {ref_it}
+        else:
+            assert counts <= {ref_it, ref_it + 1} and len(counts) == 2
