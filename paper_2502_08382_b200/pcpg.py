@@ -94,14 +94,21 @@ class DevicePCPG:
         self.op.apply_device(x, out, stream=int(self.torch.cuda.current_stream(self.device).cuda_stream))
         return out
 
-    def solve(self, tol: float = 1e-9, maxit: int | None = None):
-        """Returns (lambda as numpy, iterations, seconds of device loop)."""
+    def solve(self, tol: float = 1e-9, maxit: int | None = None, graph: bool = False):
+        """Returns (lambda as numpy, iterations, seconds of the device loop).
+
+        With ``graph`` the iteration body (apply, two projections, the vector
+        updates and reductions) is captured once as a CUDA graph and replayed;
+        the host reads two scalars per iteration for the breakdown and
+        stopping tests, exactly where the reference tests them.
+        """
         torch = self.torch
         n_mult = self.d.shape[0]
         maxit = n_mult if maxit is None else int(maxit)
-        torch.cuda.synchronize(self.device)
+        dev = self.device
+        torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        lam = torch.empty(n_mult, dtype=torch.float64, device=self.device)
+        lam = torch.empty(n_mult, dtype=torch.float64, device=dev)
         _lib.check(self.op._lib.feti_coarse_apply_device(self.op._ctx, C.c_void_p(int(self.e_dev.data_ptr())),
                                                          C.c_void_p(int(lam.data_ptr())), self._stream()))
         q = torch.empty_like(lam)
@@ -110,33 +117,50 @@ class DevicePCPG:
         y = self.project(w, torch.empty_like(w))          # mfun = identity (precond "none")
         p = y.clone()
         w0 = float(torch.linalg.vector_norm(w))
-        wy = float(torch.dot(w, y))
         if w0 <= 1e-14 * max(1.0, float(np.linalg.norm(self.d))):
-            torch.cuda.synchronize(self.device)
+            torch.cuda.synchronize(dev)
             return lam.cpu().numpy(), 0, time.perf_counter() - t0
-        k = 0
-        one = torch.ones((), dtype=torch.float64, device=self.device)
-        wy_t = torch.dot(w, y)
-        while True:
+        wy_t = torch.sum(w * y).reshape(1)
+        pq_t = torch.empty(1, dtype=torch.float64, device=dev)
+        wn_t = torch.empty(1, dtype=torch.float64, device=dev)
+
+        def body():
+            # one PCPG iteration (solver.py:244-272) with device scalars
             qk = self.apply(p, q)
-            pq_t = torch.dot(p, qk)
-            delta_t = wy_t / pq_t
-            lam.addcmul_(p, delta_t * one)
-            r.addcmul_(qk, -delta_t * one)
+            pq_t.copy_(torch.sum(p * qk).reshape(1))
+            delta = wy_t / pq_t
+            lam.addcmul_(p, delta)
+            r.addcmul_(qk, -delta)
             self.project(r, w)
             self.project(w, y)
+            wy_next = torch.sum(w * y).reshape(1)
+            wn_t.copy_(torch.linalg.vector_norm(w).reshape(1))
+            beta = wy_next / wy_t
+            wy_t.copy_(wy_next)
+            p.mul_(beta).add_(y)
+
+        step = body
+        if graph:
+            g = torch.cuda.CUDAGraph()
+            # capture on a side stream; the captured body is replayed per
+            # iteration (capturing does not execute it)
+            s = torch.cuda.Stream(device=dev)
+            s.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    body()
+            torch.cuda.current_stream(dev).wait_stream(s)
+            step = g.replay
+        k = 0
+        while True:
+            step()
             k += 1
-            wy_next_t = torch.dot(w, y)
-            # one host synchronisation per iteration: breakdown + stopping test
-            pq, wn = torch.stack((pq_t, torch.linalg.vector_norm(w))).tolist()
+            pq, wn = torch.cat((pq_t, wn_t)).tolist()
             if pq <= 0.0:
                 raise BreakdownError(f"p^T F p = {pq:.3e} at iteration {k - 1}")
             if wn <= tol * w0:
-                torch.cuda.synchronize(self.device)
+                torch.cuda.synchronize(dev)
                 return lam.cpu().numpy(), k, time.perf_counter() - t0
             if k >= maxit:
                 raise ConvergenceError(f"PCPG did not reach tol {tol:.1e} in {maxit} iterations "
                                        f"(relative residual {wn / w0:.3e})")
-            beta_t = wy_next_t / wy_t
-            wy_t = wy_next_t
-            p.mul_(beta_t).add_(y)

@@ -33,3 +33,23 @@ def test_device_pcpg_matches_reference(case):
     assert it in expected_iterations(case, g)
     ref = g["pcpg_lambda"]
     assert np.linalg.norm(lam - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_graph_and_eager_iterations_agree(graph):
+    g = load_golden("heat2d_c1")
+    prob = inputs.Problem(*inputs.CONFIGS["c1"])
+    mats, cons, lay = inputs.reference_inputs(prob)
+    kernels, forces = [], []
+    for s in range(prob.n_sub):
+        _, f, q = prob.subdomain_system(s)
+        kernels.append(q)
+        forces.append(f)
+    with dualop.prepare(mats, cons, lay, CFG, device=0) as op:
+        op.preprocess()
+        solver = DevicePCPG(op, kernels, forces, prob.c)
+        lam, it, _ = solver.solve(tol=1e-9, graph=graph)
+        lam2, it2, _ = solver.solve(tol=1e-9, graph=graph)
+    assert it == it2 == int(g["pcpg_iterations"]) == 63
+    assert np.array_equal(lam, lam2)          # deterministic
+    assert np.linalg.norm(lam - g["pcpg_lambda"]) <= 1e-9 * np.linalg.norm(g["pcpg_lambda"])
