@@ -429,6 +429,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) trsm_chain_kernel(const SubDe
     for (int sl = 0; sl < nsl; ++sl) {
       mbar_wait(&full[stage], phase);
       mma_slice_128x128(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
+      fence_proxy_async_shared();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == PIPE_STAGES) {
@@ -526,6 +527,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) syrk_kernel(const SubDev* __r
   for (int sl = 0; sl < nsl; ++sl) {
     mbar_wait(&full[stage], phase);
     if (!idle) mma_slice_128x128(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
+    fence_proxy_async_shared();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
     if (++stage == PIPE_STAGES) {

@@ -1,0 +1,35 @@
+"""Small end-to-end exercise of every kernel for compute-sanitizer runs:
+assembly (dense + sparse pattern), apply (host + device), coarse projector."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+
+from paper_2502_08382_b200 import dualop, inputs  # noqa: E402
+from paper_2502_08382_b200.pcpg import DevicePCPG  # noqa: E402
+
+CFG = dualop.DualOpConfig(strategy="explicit", path="syrk")
+for phys, dim, cells, subs in (("heat", 3, 4, 2), ("elasticity", 2, 6, 2)):
+    prob = inputs.Problem(phys, dim, cells, subs)
+    mats, cons, lay = inputs.reference_inputs(prob)
+    for ordering in ("rcm", "interface_last"):
+        with dualop.prepare(mats, cons, lay, CFG, device=0, ordering=ordering) as op:
+            op.preprocess()
+            p = np.random.default_rng(0).normal(size=prob.n_multipliers)
+            q = op.apply(p)
+            kernels, forces = [], []
+            for s in range(prob.n_sub):
+                _, f, qk = prob.subdomain_system(s)
+                kernels.append(qk)
+                forces.append(f)
+            lam, it, _ = DevicePCPG(op, kernels, forces, prob.c).solve(tol=1e-9)
+            print(phys, dim, ordering, "apply norm", np.linalg.norm(q), "pcpg it", it)
+# sparse CSR-of-U pattern through the C-ABI
+import test_gpu_parity as t  # noqa: E402
+
+t.test_sparse_pattern_factor_through_cabi()
+print("sparse pattern ok")
