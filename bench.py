@@ -422,6 +422,15 @@ def run_ours(args, rank, world, local_rank):
         e1.record()
         e1.synchronize()
         apply_kernel_ms = e0.elapsed_time(e1) / args.applies
+        # implicit strategy on the device through the same factor tiles
+        n_impl = max(3, args.applies // 20)
+        op.apply_implicit_device(p_dev, q_dev, stream)
+        e0.record()
+        for _ in range(n_impl):
+            op.apply_implicit_device(p_dev, q_dev, stream)
+        e1.record()
+        e1.synchronize()
+        implicit_ms = e0.elapsed_time(e1) / n_impl
         # e2e: pinned host factors -> H2D -> device assembly -> one host apply
         p_host = np.random.default_rng(1).normal(size=prob.n_multipliers)
         q_host = np.zeros(prob.n_multipliers)
@@ -471,6 +480,7 @@ def run_ours(args, rank, world, local_rank):
                      "dual_system_setup_s": t_setup, "lambda_norm": float(np.linalg.norm(lam)), "tol": 1e-9}
             log(f"[rank {rank}] {ordering}: device PCPG {iters} iterations in {t_loop * 1e3:.1f} ms")
         res = {"ordering": ordering, "ms_step": ms_step, "stats": stats, "clocks": clocks, "apply_ms": apply_ms,
+               "implicit_ms": implicit_ms,
                "apply_kernel_ms": apply_kernel_ms, "e2e_s": e2e_s, "apply_e2e_ms": apply_e2e_ms,
                "h2d_bytes": int(st_host["factor_bytes"]) + 8 * prob.n_multipliers,
                "host_factors": host_factors if keep_host else None, "perms": perms, "solve": solve}
@@ -517,7 +527,10 @@ def run_ours(args, rank, world, local_rank):
                       "assembly_alg_tflops": (alg_trsm + alg_syrk) / value / 1e12,
                       "assembly_alg_frac_of_dgemm": (alg_trsm + alg_syrk) / value / 1e12 / peak_f64},
             "apply": {"ms_per_iter": r["apply_ms"], "kernel_ms_per_iter": r["apply_kernel_ms"],
-                      "e2e_ms_per_iter": r["apply_e2e_ms"], "roofline": roof_apply},
+                      "e2e_ms_per_iter": r["apply_e2e_ms"], "roofline": roof_apply,
+                      "gpu_implicit_ms_per_iter": r["implicit_ms"],
+                      "amortization_vs_gpu_implicit": amortization_point(
+                          (0.0, r["implicit_ms"] / 1e3), (value, r["apply_kernel_ms"] / 1e3))},
             "e2e": {"value": r["e2e_s"], "unit": UNIT, "h2d_bytes_per_step": r["h2d_bytes"],
                     "d2h_bytes_per_step": int(8 * prob.n_multipliers),
                     "what": "pinned host factors (reference layout; the lib copies the suffix the pruned solve "

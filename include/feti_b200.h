@@ -141,6 +141,13 @@ int feti_project_device(feti_ctx* ctx, const double* d_x, double* d_out, void* s
 /* out = G (G^T G)^-1 v for v of length nk (feasible start G (G^T G)^-1 e). */
 int feti_coarse_apply_device(feti_ctx* ctx, const double* d_v, double* d_out, void* stream);
 
+/* Implicit strategy on the device (apply_implicit_local, dualop.py:504-521):
+ * q = sum_i B~_i^T K_reg,i^-1 B~_i p through two block triangular sweeps over
+ * the scaled factor the last feti_assemble left in HBM (same result as
+ * feti_apply to rounding; reads the factor tiles instead of F~). */
+int feti_apply_implicit(feti_ctx* ctx, const double* p, double* q);
+int feti_apply_implicit_device(feti_ctx* ctx, const double* d_p, double* d_q, void* stream);
+
 int feti_get_stats(feti_ctx* ctx, feti_stats* out);
 
 /* Diagnostics: per-kernel register / thread limits as text. */

@@ -29,6 +29,7 @@ EXPORTED = (
     "feti_finalize", "feti_set_factor", "feti_assemble", "feti_local_operator", "feti_apply",
     "feti_apply_device", "feti_get_stats", "feti_host_alloc", "feti_host_free",
     "feti_debug_kernel_attributes", "feti_coarse_setup", "feti_project_device", "feti_coarse_apply_device",
+    "feti_apply_implicit", "feti_apply_implicit_device",
 )
 
 
@@ -85,6 +86,8 @@ def load() -> C.CDLL:
         "feti_coarse_setup": ([P, i64p, f64p, f64p, C.c_int64], C.c_int),
         "feti_project_device": ([P, P, P, P], C.c_int),
         "feti_coarse_apply_device": ([P, P, P, P], C.c_int),
+        "feti_apply_implicit": ([P, f64p, f64p], C.c_int),
+        "feti_apply_implicit_device": ([P, P, P, P], C.c_int),
         "feti_host_free": ([P], C.c_int),
     }
     for name, (args, res) in sig.items():

@@ -20,6 +20,7 @@
 #include "../../include/feti_b200.h"
 #include "feti_common.cuh"
 #include "feti_coarse.h"
+#include "feti_implicit.h"
 #include "feti_kernels.h"
 
 using namespace feti;
@@ -125,6 +126,10 @@ struct feti_ctx {
   feti_stats stats{};
   cudaEvent_t ev[8] = {};
   bool subdev_dirty = true;
+  // implicit apply: per-slot offsets into a partial buffer of sum(m) values
+  int64_t* d_impl_off = nullptr;
+  double* d_impl_part = nullptr;
+  int impl_max_blocks = 0;
   // coarse space (GPU-resident PCPG): G blocks, (G^T G)^-1, work vectors
   int nk = 0;
   CoarseSub* d_coarse = nullptr;
@@ -526,6 +531,21 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   if ((rc = upload(c, &c->d_cptr, cptr))) return rc;
   if ((rc = upload(c, &c->d_cent, cent))) return rc;
   if ((rc = dev_alloc(c, (void**)&c->d_part, (size_t)std::max<int64_t>(poff, 1) * 8, true))) return rc;
+  {
+    std::vector<int64_t> ioff(c->subs.size());
+    int64_t tot = 0;
+    for (size_t si = 0; si < c->subs.size(); ++si) {
+      ioff[si] = tot;
+      tot += c->subs[si].m;
+      c->impl_max_blocks = std::max(c->impl_max_blocks, c->subs[si].T - c->subs[si].smin);
+    }
+    if ((rc = upload(c, &c->d_impl_off, ioff))) return rc;
+    if ((rc = dev_alloc(c, (void**)&c->d_impl_part, (size_t)std::max<int64_t>(tot, 1) * 8, true))) return rc;
+    if (implicit_smem(c->impl_max_blocks) > 227 * 1024)
+      c->impl_max_blocks = -1;   // implicit apply unavailable for this size
+    else
+      CUDA_TRY(configure_implicit(c->impl_max_blocks));
+  }
   if ((rc = dev_alloc(c, (void**)&c->d_p, (size_t)std::max<int64_t>(c->n_mult, 1) * 8, true))) return rc;
   if ((rc = dev_alloc(c, (void**)&c->d_q, (size_t)std::max<int64_t>(c->n_mult, 1) * 8, true))) return rc;
   c->n_unpack = (int)wu.size();
@@ -765,6 +785,42 @@ int feti_apply_device(feti_ctx* c, const double* d_p, double* d_q, void* stream)
   CUDA_TRY(cudaSetDevice(c->device));
   // the handle is used verbatim: NULL is the legacy default stream, as in CUDA
   return apply_enqueue(c, d_p, d_q, (cudaStream_t)stream, false);
+}
+
+static int implicit_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st) {
+  if (c->impl_max_blocks < 0)
+    return fail(FETI_ERR_CAPACITY, "implicit apply: subdomain too large for the single-CTA sweep");
+  launch_implicit_apply(c->d_subdev, (int)c->subs.size(), c->impl_max_blocks, c->d_impl_off, d_p, c->d_impl_part,
+                        (int)c->n_mult, c->d_cptr, c->d_cent, d_q, st);
+  CUDA_TRY(cudaGetLastError());
+  return FETI_OK;
+}
+
+int feti_apply_implicit(feti_ctx* c, const double* p, double* q) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "apply before preprocess for the current values");
+  if (!p || !q) return fail(FETI_ERR_ARG, "NULL vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  CUDA_TRY(cudaMemcpyAsync(c->d_p, p, (size_t)c->n_mult * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaEventRecord(c->ev[0], st));
+  int rc = implicit_enqueue(c, c->d_p, c->d_q, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(c->ev[1], st));
+  CUDA_TRY(cudaMemcpyAsync(q, c->d_q, (size_t)c->n_mult * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  c->stats.ms_apply = ms;
+  return FETI_OK;
+}
+
+int feti_apply_implicit_device(feti_ctx* c, const double* d_p, double* d_q, void* stream) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "apply before preprocess for the current values");
+  if (!d_p || !d_q) return fail(FETI_ERR_ARG, "NULL vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  return implicit_enqueue(c, d_p, d_q, (cudaStream_t)stream);
 }
 
 int feti_coarse_setup(feti_ctx* c, const int64_t* kdim, const double* G, const double* coarse_inv, int64_t nk) {

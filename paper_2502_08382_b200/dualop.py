@@ -403,6 +403,29 @@ class DualOperator:
             out[:] = tmp
         return out
 
+    def apply_implicit(self, p, out=None):
+        """Implicit strategy on the device: q = sum B~ K_reg^-1 B~^T p through
+        the factor tiles of the last assembly (dualop.py:504-521 semantics)."""
+        if not self.step_ready:
+            raise LifecycleError("apply before preprocess for the current values")
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        if p.shape != (self.n_multipliers,):
+            raise ValueError("dual vector has the wrong length")
+        if out is None:
+            out = np.zeros(self.n_multipliers)
+        _call(self._lib.feti_apply_implicit(self._ctx, _lib.f64ptr(p), _lib.f64ptr(out)))
+        return out
+
+    def apply_implicit_device(self, p, q, stream=None) -> None:
+        if not self.step_ready:
+            raise LifecycleError("apply before preprocess for the current values")
+        if stream is None:
+            import torch
+
+            stream = torch.cuda.current_stream(p.device).cuda_stream
+        _call(self._lib.feti_apply_implicit_device(self._ctx, C.c_void_p(int(p.data_ptr())),
+                                                   C.c_void_p(int(q.data_ptr())), C.c_void_p(int(stream))))
+
     def apply_device(self, p, q, stream=None) -> None:
         """q = F p on device tensors (torch CUDA float64), enqueued on ``stream``."""
         if not self.step_ready:

@@ -309,3 +309,21 @@ def test_c4_interior_subdomain_matches_oracle():
                                          storage="dense")
     assert f.shape == (3873, 3873)
     assert np.linalg.norm(f - fo) <= 1e-10 * np.linalg.norm(fo)
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+@pytest.mark.parametrize("ordering", ["rcm", "interface_last"])
+def test_implicit_device_apply_matches_reference(case, ordering):
+    """Implicit strategy on the device (two block sweeps over the assembly's
+    scaled factor) vs the reference's implicit apply (dualop.py:504-521) and
+    vs the explicit apply (test_dualop.py:215-224 bar: 1e-11)."""
+    g = load_golden(case)
+    prob, mats, cons, lay = _golden_problem(g)
+    with dualop.prepare(mats, cons, lay, CFG, ordering=ordering) as op:
+        op.preprocess()
+        qi = op.apply_implicit(g["p"])
+        qe = op.apply(g["p"])
+        qi2 = op.apply_implicit(g["p"])
+    assert np.array_equal(qi, qi2)
+    assert np.linalg.norm(qi - g["q_implicit"]) <= 1e-11 * np.linalg.norm(g["q_implicit"])
+    assert np.linalg.norm(qi - qe) <= 1e-11 * np.linalg.norm(qe)
