@@ -46,7 +46,8 @@ enum {
   FETI_ERR_CUDA = 3,       /* CUDA runtime failure (RuntimeError)        */
   FETI_ERR_CAPACITY = 4,   /* device memory too small: PoolCapacityError */
   FETI_ERR_SINGULAR = 5,   /* zero diagonal in the factor: SingularFactorError (sparse.py:491-492) */
-  FETI_ERR_INTERNAL = 6
+  FETI_ERR_INTERNAL = 6,
+  FETI_ERR_NOT_SPD = 7     /* non-positive pivot in the device factorization: SpdError (sparse.py:297-298) */
 };
 
 enum { FETI_FACTOR_HOST = 0, FETI_FACTOR_DEVICE = 1 };
@@ -78,6 +79,7 @@ typedef struct feti_stats {
   int64_t n_multipliers;
   int32_t launches_assemble; /* kernel launches of the last assemble */
   int32_t launches_apply;    /* kernel launches per apply             */
+  double ms_factorize;       /* device time of the last feti_factorize  */
 } feti_stats;
 
 int feti_abi_version(void);
@@ -147,6 +149,23 @@ int feti_coarse_apply_device(feti_ctx* ctx, const double* d_v, double* d_out, vo
  * feti_apply to rounding; reads the factor tiles instead of F~). */
 int feti_apply_implicit(feti_ctx* ctx, const double* p, double* q);
 int feti_apply_implicit_device(feti_ctx* ctx, const double* d_p, double* d_q, void* stream);
+
+/* Device numeric factorization (replaces the host numeric stage,
+ * sparse.py:418-424 + regularize sparse.py:427-454): call
+ * feti_enable_device_factorization before feti_finalize, then per step
+ * feti_set_stiffness for every slot (the UNregularized sparse K as CSR, the
+ * orthonormal kernel basis Q (n x r row-major), rho = trace(K)/n and the
+ * symbolic ordering perm), feti_factorize, feti_assemble.  K_reg = P (K +
+ * rho Q Q^T) P^T is formed and factored on the device; feti_set_factor is not
+ * used.  All subdomains must have the same size. */
+int feti_enable_device_factorization(feti_ctx* ctx);
+int feti_set_stiffness(feti_ctx* ctx, int64_t slot, int64_t n, const int64_t* indptr, const int64_t* indices,
+                       const double* data, int64_t nnz, const double* Q, int64_t r, double rho,
+                       const int64_t* perm);
+int feti_factorize(feti_ctx* ctx);
+/* x = K_reg^-1 b for the listed slots (host vectors concatenated in list
+ * order), through the device factor (CholFactor.solve, sparse.py:324-337). */
+int feti_solve_many(feti_ctx* ctx, int64_t nslots, const int64_t* slots, const double* b, double* x);
 
 int feti_get_stats(feti_ctx* ctx, feti_stats* out);
 

@@ -21,6 +21,7 @@ FETI_ERR_CUDA = 3
 FETI_ERR_CAPACITY = 4
 FETI_ERR_SINGULAR = 5
 FETI_ERR_INTERNAL = 6
+FETI_ERR_NOT_SPD = 7
 FETI_FACTOR_HOST = 0
 FETI_FACTOR_DEVICE = 1
 
@@ -29,7 +30,8 @@ EXPORTED = (
     "feti_finalize", "feti_set_factor", "feti_assemble", "feti_local_operator", "feti_apply",
     "feti_apply_device", "feti_get_stats", "feti_host_alloc", "feti_host_free",
     "feti_debug_kernel_attributes", "feti_coarse_setup", "feti_project_device", "feti_coarse_apply_device",
-    "feti_apply_implicit", "feti_apply_implicit_device",
+    "feti_apply_implicit", "feti_apply_implicit_device", "feti_enable_device_factorization", "feti_set_stiffness",
+    "feti_factorize", "feti_solve_many",
 )
 
 
@@ -45,6 +47,7 @@ class FetiStats(C.Structure):
         ("bytes_persistent", C.c_int64), ("bytes_temporary", C.c_int64),
         ("n_subdomains", C.c_int64), ("n_multipliers", C.c_int64),
         ("launches_assemble", C.c_int32), ("launches_apply", C.c_int32),
+        ("ms_factorize", C.c_double),
     ]
 
     def as_dict(self):
@@ -88,6 +91,11 @@ def load() -> C.CDLL:
         "feti_coarse_apply_device": ([P, P, P, P], C.c_int),
         "feti_apply_implicit": ([P, f64p, f64p], C.c_int),
         "feti_apply_implicit_device": ([P, P, P, P], C.c_int),
+        "feti_enable_device_factorization": ([P], C.c_int),
+        "feti_set_stiffness": ([P, C.c_int64, C.c_int64, i64p, i64p, f64p, C.c_int64, f64p, C.c_int64, C.c_double,
+                                i64p], C.c_int),
+        "feti_factorize": ([P], C.c_int),
+        "feti_solve_many": ([P, C.c_int64, i64p, f64p, f64p], C.c_int),
         "feti_host_free": ([P], C.c_int),
     }
     for name, (args, res) in sig.items():

@@ -20,6 +20,7 @@
 #include "../../include/feti_b200.h"
 #include "feti_common.cuh"
 #include "feti_coarse.h"
+#include "feti_factor.h"
 #include "feti_implicit.h"
 #include "feti_kernels.h"
 
@@ -89,9 +90,19 @@ struct SubHost {
   bool factor_set = false;
   bool factor_from_host = false;
   const double* h_values = nullptr;  // host factor awaiting upload at assemble
+  int tbase = 0;                     // first stored tile block
+  int src = SRC_RAW_DENSE;
+  // device factorization inputs (feti_set_stiffness)
+  bool stiff_set = false;
+  int64_t k_nnz = 0;
+  int kr = 0;
+  double rho = 0.0;
+  double* d_Q = nullptr;
+  int64_t *d_perm = nullptr, *d_iperm = nullptr, *d_kptr = nullptr, *d_kind = nullptr;
+  double* d_kdata = nullptr;
   cudaEvent_t ev_upload = nullptr;
   int64_t f_tiles() const { return (int64_t)T32 * (T32 + 1) / 2; }
-  int64_t l_tiles() const { return (int64_t)(T - smin) * (T - smin + 1) / 2; }
+  int64_t l_tiles() const { return (int64_t)(T - tbase) * (T - tbase + 1) / 2; }
   int64_t upload_count() const { return nnz - raw_off; }
 };
 
@@ -126,6 +137,16 @@ struct feti_ctx {
   feti_stats stats{};
   cudaEvent_t ev[8] = {};
   bool subdev_dirty = true;
+  // device factorization (feti_enable_device_factorization before finalize)
+  bool device_factor = false;
+  bool tiles_fresh = false;          // tiles hold L (not yet block-scaled)
+  int uniform_T = 0;
+  FactorSub* d_fsub = nullptr;
+  double* d_dinv = nullptr;
+  int* d_bad = nullptr;
+  int64_t* d_vec_off = nullptr;
+  double *d_sb = nullptr, *d_sx = nullptr;
+  int* d_slots = nullptr;
   // implicit apply: per-slot offsets into a partial buffer of sum(m) values
   int64_t* d_impl_off = nullptr;
   double* d_impl_part = nullptr;
@@ -198,6 +219,8 @@ int sync_subdev(feti_ctx* c) {
     d.nnz = s.nnz;
     d.raw_off = s.raw_off;
     d.smin = s.smin;
+    d.tbase = s.tbase;
+    d.src = s.src;
     d.n = (int)s.n;
     d.m = (int)s.m;
     d.T = s.T;
@@ -282,6 +305,7 @@ int feti_add_subdomain(feti_ctx* c, int64_t n, int64_t m, const int64_t* first_r
   s.m = m;
   s.nnz = nnz;
   s.dense = dense;
+  s.src = dense ? SRC_RAW_DENSE : SRC_RAW_SPARSE;
   s.T = (int)((n + TB - 1) / TB);
   s.P = (int)((m + TB - 1) / TB);
   s.T32 = (int)((m + AT - 1) / AT);
@@ -342,7 +366,8 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   size_t need = 0;
   int max_M = 0;
   for (auto& s : c->subs) {
-    need += (size_t)s.l_tiles() * TILE * 8;            // tiles
+    const int64_t tb = c->device_factor ? 0 : s.smin;
+    need += (size_t)(s.T - tb) * (s.T - tb + 1) / 2 * TILE * 8;   // tiles
     need += (size_t)s.P * (s.T - s.smin) * TILE * 8;   // X panels
     need += (size_t)s.f_tiles() * ATILE * 8;          // F~
     max_M = std::max(max_M, s.T32 * AT);
@@ -355,6 +380,19 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
                 fr, need);
 
   int rc;
+  if (c->device_factor) {
+    // the factorization and full solves need every tile; every slot must
+    // share the block count (one batched launch per factorization step)
+    for (auto& s : c->subs) {
+      s.tbase = 0;
+      if (c->uniform_T == 0) c->uniform_T = s.T;
+      if (s.T != c->uniform_T)
+        return fail(FETI_ERR_ARG, "device factorization needs equally sized subdomains (%d vs %d blocks)", s.T,
+                    c->uniform_T);
+    }
+  } else {
+    for (auto& s : c->subs) s.tbase = s.smin;
+  }
   for (auto& s : c->subs) {
     if ((rc = dev_alloc(c, (void**)&s.d_tiles, (size_t)std::max<int64_t>(s.l_tiles(), 1) * TILE * 8, false)))
       return rc;
@@ -386,9 +424,11 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     if (!s.dense)
       for (int K = s.smin; K < s.T; ++K)
         for (int L = s.smin; L <= K; ++L) wu.push_back(make_int4(si, K, L, 0));
-    for (int k = s.smin; k < s.T; ++k) wd.push_back(make_int4(si, k, 0, 0));
-    for (int k = s.T - 1; k > s.smin; --k) ws.push_back(make_int4(si, k, 0, 0));
-    const double tt = s.T - s.smin;
+    // device factorization: every block row is scaled (full solves need it)
+    const int k0 = c->device_factor ? 0 : s.smin;
+    for (int k = k0; k < s.T; ++k) wd.push_back(make_int4(si, k, 0, 0));
+    for (int k = s.T - 1; k > k0; --k) ws.push_back(make_int4(si, k, 0, 0));
+    const double tt = s.T - k0;
     scale_exec += tt * (tt - 1) / 2 * 2.0 * (2.0 * 64 * 32 * 32 * (1 + 2 + 3 + 4));
     for (int p = 0; p < s.P; ++p) {
       wc.push_back(make_int4(si, p, 0, 0));
@@ -410,7 +450,7 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   }
   // chains: longest first so the tail is short
   std::stable_sort(ws.begin(), ws.end(), [&](const int4& a, const int4& b) {
-    return a.y - c->subs[a.x].smin > b.y - c->subs[b.x].smin;
+    return a.y - c->subs[a.x].tbase > b.y - c->subs[b.x].tbase;
   });
   std::sort(wc.begin(), wc.end(), [&](const int4& a, const int4& b) {
     const SubHost& sa = c->subs[a.x];
@@ -566,6 +606,23 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   st.n_subdomains = (int64_t)c->subs.size();
   st.n_multipliers = c->n_mult;
   st.launches_apply = 2;
+  if (c->device_factor) {
+    const size_t ns = c->subs.size();
+    if ((rc = dev_alloc(c, (void**)&c->d_fsub, ns * sizeof(FactorSub), true))) return rc;
+    if ((rc = dev_alloc(c, (void**)&c->d_dinv, ns * TILE * 8, false))) return rc;
+    if ((rc = dev_alloc(c, (void**)&c->d_bad, ns * sizeof(int), false))) return rc;
+    std::vector<int64_t> voff(ns + 1, 0);
+    std::vector<int> slots(ns);
+    for (size_t si = 0; si < ns; ++si) {
+      voff[si + 1] = voff[si] + c->subs[si].n;
+      slots[si] = (int)si;
+    }
+    if ((rc = upload(c, &c->d_vec_off, voff))) return rc;
+    if ((rc = upload(c, &c->d_slots, slots))) return rc;
+    if ((rc = dev_alloc(c, (void**)&c->d_sb, (size_t)std::max<int64_t>(voff[ns], 1) * 8, true))) return rc;
+    if ((rc = dev_alloc(c, (void**)&c->d_sx, (size_t)std::max<int64_t>(voff[ns], 1) * 8, true))) return rc;
+    CUDA_TRY(configure_factor(c->uniform_T));
+  }
   CUDA_TRY(cudaDeviceSynchronize());
   c->finalized = true;
   return FETI_OK;
@@ -644,6 +701,9 @@ int feti_assemble(feti_ctx* c) {
   if (!c->finalized) return fail(FETI_ERR_LIFECYCLE, "preprocess before prepare");
   for (size_t i = 0; i < c->subs.size(); ++i)
     if (!c->subs[i].factor_set) return fail(FETI_ERR_LIFECYCLE, "subdomain slot %zu has no factor values", i);
+  if (c->device_factor && !c->tiles_fresh)
+    return fail(FETI_ERR_LIFECYCLE, "assemble needs a new feti_factorize (the tiles were already scaled)");
+  c->tiles_fresh = false;
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   int launches = 0, rc;
@@ -785,6 +845,123 @@ int feti_apply_device(feti_ctx* c, const double* d_p, double* d_q, void* stream)
   CUDA_TRY(cudaSetDevice(c->device));
   // the handle is used verbatim: NULL is the legacy default stream, as in CUDA
   return apply_enqueue(c, d_p, d_q, (cudaStream_t)stream, false);
+}
+
+int feti_enable_device_factorization(feti_ctx* c) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (c->finalized) return fail(FETI_ERR_LIFECYCLE, "device factorization must be chosen before finalize");
+  c->device_factor = true;
+  return FETI_OK;
+}
+
+int feti_set_stiffness(feti_ctx* c, int64_t slot, int64_t n, const int64_t* indptr, const int64_t* indices,
+                       const double* data, int64_t nnz, const double* Q, int64_t r, double rho, const int64_t* perm) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->finalized || !c->device_factor)
+    return fail(FETI_ERR_LIFECYCLE, "set_stiffness needs a finalized context with device factorization");
+  if (slot < 0 || slot >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot out of range");
+  SubHost& s = c->subs[slot];
+  if (n != s.n) return fail(FETI_ERR_ARG, "stiffness size %lld does not match the subdomain (%lld)", (long long)n,
+                            (long long)s.n);
+  if (!indptr || !indices || !data || (r > 0 && !Q) || !perm || r < 0 || r > 64 || nnz != indptr[n])
+    return fail(FETI_ERR_ARG, "bad stiffness arguments");
+  CUDA_TRY(cudaSetDevice(c->device));
+  int rc;
+  if (!s.stiff_set) {
+    std::vector<int64_t> pv(perm, perm + n), ip(n, -1);
+    for (int64_t i = 0; i < n; ++i) {
+      if (pv[i] < 0 || pv[i] >= n || ip[pv[i]] >= 0) return fail(FETI_ERR_ARG, "ordering is not a permutation");
+      ip[pv[i]] = i;
+    }
+    std::vector<int64_t> kp(indptr, indptr + n + 1), ki(indices, indices + nnz);
+    if ((rc = upload(c, &s.d_perm, pv))) return rc;
+    if ((rc = upload(c, &s.d_iperm, ip))) return rc;
+    if ((rc = upload(c, &s.d_kptr, kp))) return rc;
+    if ((rc = upload(c, &s.d_kind, ki))) return rc;
+    if ((rc = dev_alloc(c, (void**)&s.d_kdata, (size_t)std::max<int64_t>(nnz, 1) * 8, true))) return rc;
+    if ((rc = dev_alloc(c, (void**)&s.d_Q, (size_t)std::max<int64_t>(n * r, 1) * 8, true))) return rc;
+    s.k_nnz = nnz;
+    s.kr = (int)r;
+    s.stiff_set = true;
+  } else if (nnz != s.k_nnz || (int)r != s.kr) {
+    return fail(FETI_ERR_ARG, "stiffness pattern changed after the first call");
+  }
+  CUDA_TRY(cudaMemcpy(s.d_kdata, data, (size_t)nnz * 8, cudaMemcpyHostToDevice));
+  if (r > 0) CUDA_TRY(cudaMemcpy(s.d_Q, Q, (size_t)(n * r) * 8, cudaMemcpyHostToDevice));
+  s.rho = rho;
+  return FETI_OK;
+}
+
+int feti_factorize(feti_ctx* c) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->finalized || !c->device_factor)
+    return fail(FETI_ERR_LIFECYCLE, "factorize needs a finalized context with device factorization");
+  for (size_t i = 0; i < c->subs.size(); ++i)
+    if (!c->subs[i].stiff_set) return fail(FETI_ERR_LIFECYCLE, "subdomain slot %zu has no stiffness", i);
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  const int ns = (int)c->subs.size();
+  std::vector<FactorSub> fs(ns);
+  for (int si = 0; si < ns; ++si) {
+    SubHost& s = c->subs[si];
+    fs[si] = FactorSub{s.d_Q, s.d_perm, s.d_iperm, s.d_kptr, s.d_kind, s.d_kdata, s.rho, s.kr, 0};
+    s.src = SRC_TILES;
+    c->subdev_dirty = true;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->d_fsub, fs.data(), ns * sizeof(FactorSub), cudaMemcpyHostToDevice, st));
+  int rc;
+  if ((rc = sync_subdev(c))) return rc;
+  std::vector<int> big(ns, 1 << 30);
+  CUDA_TRY(cudaMemcpyAsync(c->d_bad, big.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaEventRecord(c->ev[0], st));
+  const int T = c->uniform_T;
+  launch_kreg_build(c->d_subdev, c->d_fsub, ns, T, (int)c->subs[0].n, st);
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  for (int k = 0; k < T; ++k) {
+    launch_factor_step(c->d_subdev, c->d_dinv, c->d_bad, ns, k, T, st);
+    CUDA_TRY(cudaGetLastError());
+    FETI_DEBUG_SYNC(st);
+  }
+  CUDA_TRY(cudaEventRecord(c->ev[1], st));
+  CUDA_TRY(cudaMemcpyAsync(big.data(), c->d_bad, ns * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  c->stats.ms_factorize = ms;
+  for (int si = 0; si < ns; ++si)
+    if (big[si] < (1 << 30))
+      return fail(FETI_ERR_NOT_SPD, "slot %d: non-positive pivot at permuted row %d: matrix is not SPD", si,
+                  big[si]);
+  for (auto& s : c->subs) s.factor_set = true;
+  c->tiles_fresh = true;
+  return FETI_OK;
+}
+
+int feti_solve_many(feti_ctx* c, int64_t nslots, const int64_t* slots, const double* b, double* x) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->device_factor || !c->assembled)
+    return fail(FETI_ERR_LIFECYCLE, "solve needs an assembled context with device factorization");
+  if (nslots <= 0 || nslots > (int64_t)c->subs.size() || !slots || !b || !x) return fail(FETI_ERR_ARG, "bad solve arguments");
+  if (solve_smem(c->uniform_T) > 227 * 1024) return fail(FETI_ERR_CAPACITY, "subdomain too large for the solve sweep");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  std::vector<int64_t> off(nslots + 1, 0);
+  std::vector<int> sl(nslots);
+  for (int64_t q = 0; q < nslots; ++q) {
+    if (slots[q] < 0 || slots[q] >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot out of range");
+    sl[q] = (int)slots[q];
+    off[q + 1] = off[q] + c->subs[sl[q]].n;
+  }
+  // scratch: per-call offsets/slots at the front of the lib's buffers
+  CUDA_TRY(cudaMemcpyAsync(c->d_slots, sl.data(), nslots * sizeof(int), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->d_vec_off, off.data(), (nslots + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->d_sb, b, (size_t)off[nslots] * 8, cudaMemcpyHostToDevice, st));
+  launch_solve(c->d_subdev, c->d_fsub, c->d_slots, (int)nslots, c->uniform_T, c->d_vec_off, c->d_sb, c->d_sx, st);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(x, c->d_sx, (size_t)off[nslots] * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return FETI_OK;
 }
 
 static int implicit_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st) {

@@ -55,16 +55,22 @@ struct SubDev {
   int64_t raw_off;          // raw points at value index raw_off (suffix upload)
   int n, m, T, P, T32;
   int smin;                 // first block row any X column reaches (pruning)
+  int tbase;                // first block row/column stored in `tiles`
+  int src;                  // factor source: SRC_RAW_DENSE / SRC_RAW_SPARSE / SRC_TILES
 };
 
-// Only block rows/columns >= smin are ever touched: X = L^-1 P B~^T is zero
-// above the smallest first row of the subdomain, so the tiles of L, the X
-// panels and the factor upload all start there.
-__host__ __device__ __forceinline__ int64_t tile_offset(int smin, int K, int Lc) {
-  return tri_index(K - smin, Lc - smin) * TILE;
+enum { SRC_RAW_DENSE = 0, SRC_RAW_SPARSE = 1, SRC_TILES = 2 };
+
+// Only block rows/columns >= smin are ever touched by the assembly: X = L^-1
+// P B~^T is zero above the smallest first row of the subdomain, so the X
+// panels and the factor upload start there and, for host factors, so do the
+// stored tiles (tbase = smin).  A factor computed on the device keeps every
+// tile (tbase = 0): the factorization and full solves need them.
+__host__ __device__ __forceinline__ int64_t tile_offset(int tbase, int K, int Lc) {
+  return tri_index(K - tbase, Lc - tbase) * TILE;
 }
 __device__ __forceinline__ double* tile_ptr(const SubDev& S, int K, int Lc) {
-  return S.tiles + tile_offset(S.smin, K, Lc);
+  return S.tiles + tile_offset(S.tbase, K, Lc);
 }
 // X panel c, global row `row` (>= smin*128), row-major swizzled, 128 wide
 __device__ __forceinline__ double* xrow_ptr(const SubDev& S, int c, int row) {

@@ -1,0 +1,74 @@
+// 128x128 dense lower-triangular helpers shared by the assembly's diagonal
+// inverse and the device factorization (256 threads, shared memory).
+#pragma once
+#include "feti_common.cuh"
+
+namespace feti {
+
+__device__ __forceinline__ int plo(int i, int j) { return i * (i + 1) / 2 + j; }
+
+// sY (packed lower) = inv(sL) for a 128x128 lower-triangular sL (packed
+// lower), blocked 4 x 4 over 32-wide sub-blocks.  Phase 1: warp w inverts
+// the diagonal sub-block D_w, lane c carrying column c in registers through a
+// lock-step forward substitution (the L row is a shared-memory broadcast).
+// Phase 2: off-diagonal sub-blocks by distance d = 1, 2, 3:
+//   Y_IJ = -inv(D_I) sum_{K=J}^{I-1} L_IK Y_KJ .
+// sT: 3 x 1024 scratch.  Must be called by all 256 threads; ends synchronised.
+__device__ __forceinline__ void invert_lower_128(const double* __restrict__ sL, double* __restrict__ sY,
+                                                 double* __restrict__ sT) {
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (warp < 4) {
+    const int o = warp * 32;
+    double y[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const double* Lr = sL + plo(o + r, o);
+      double acc = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = 0; j < r; ++j) acc = fma(-Lr[j], y[j], acc);
+      y[r] = acc / Lr[r];
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r >= lane) sY[plo(o + r, o + lane)] = y[r];
+  }
+  __syncthreads();
+  // thread -> (row r, 4 consecutive columns c..c+3) of a 32x32 sub-block
+  const int rr = tid >> 3, cc = (tid & 7) * 4;
+  for (int d = 1; d < 4; ++d) {
+    const int nb = 4 - d;
+    for (int bI = 0; bI < nb; ++bI) {          // T_b = sum_{K=J}^{I-1} L_IK Y_KJ
+      const int J = bI, I = bI + d;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* Lr = sL + plo(I * 32 + rr, 0);
+      for (int kk = J * 32; kk < I * 32; ++kk) {
+        const double lv = Lr[kk];
+        const double* Yk = sY + plo(kk, 0);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = J * 32 + cc + e;
+          if (kk >= col) acc[e] = fma(lv, Yk[col], acc[e]);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sT[bI * 1024 + rr * 32 + cc + e] = acc[e];
+    }
+    __syncthreads();
+    for (int bI = 0; bI < nb; ++bI) {          // Y_IJ = -inv(D_I) T_b
+      const int J = bI, I = bI + d;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* Yr = sY + plo(I * 32 + rr, I * 32);
+      for (int kk = 0; kk <= rr; ++kk) {
+        const double yv = Yr[kk];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = fma(yv, sT[bI * 1024 + kk * 32 + cc + e], acc[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sY[plo(I * 32 + rr, J * 32 + cc + e)] = -acc[e];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace feti

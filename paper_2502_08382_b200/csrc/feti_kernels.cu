@@ -23,6 +23,7 @@
 #include <cstdio>
 
 #include "feti_common.cuh"
+#include "feti_dense128.cuh"
 #include "feti_kernels.h"
 
 namespace feti {
@@ -40,7 +41,7 @@ __global__ void __launch_bounds__(256) unpack_dense_kernel(const SubDev* __restr
   const int K = w.y, Lc = w.z;
   const int64_t n = S.n;
   double* tile = tile_ptr(S, K, Lc);
-  const bool dense = (S.up == nullptr);
+  const bool dense = (S.src == SRC_RAW_DENSE);
   for (int idx = threadIdx.x; idx < TILE; idx += blockDim.x) {
     const int jl = idx >> 7;
     const int il = (idx & 127) ^ ((jl & 3) << 2);
@@ -76,8 +77,6 @@ __global__ void __launch_bounds__(256) scatter_sparse_kernel(const SubDev* __res
 // (the L row is a shared-memory broadcast).  Phase 2: the off-diagonal
 // sub-blocks by distance d = 1, 2, 3:  Y_IJ = -inv(D_I) sum_{K=J}^{I-1} L_IK Y_KJ.
 // L and Y live as packed lower triangles in shared memory.
-__device__ __forceinline__ int plo(int i, int j) { return i * (i + 1) / 2 + j; }
-
 __global__ void __launch_bounds__(256) diag_inverse_kernel(const SubDev* __restrict__ subs,
                                                            const int4* __restrict__ work) {
   extern __shared__ double dsm[];
@@ -89,7 +88,7 @@ __global__ void __launch_bounds__(256) diag_inverse_kernel(const SubDev* __restr
   const int k = w.y;
   double* tile = tile_ptr(S, k, k);
   const int tid = threadIdx.x;
-  if (S.up == nullptr) {
+  if (S.src == SRC_RAW_DENSE) {
     // dense pattern: the diagonal block straight from the packed factor
     const int64_t n = S.n;
     for (int idx = tid; idx < TILE; idx += 256) {
@@ -111,58 +110,7 @@ __global__ void __launch_bounds__(256) diag_inverse_kernel(const SubDev* __restr
     }
   }
   __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31;
-  if (warp < 4) {
-    const int o = warp * 32;
-    double y[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const double* Lr = sL + plo(o + r, o);
-      double acc = (r == lane) ? 1.0 : 0.0;
-#pragma unroll
-      for (int j = 0; j < r; ++j) acc = fma(-Lr[j], y[j], acc);
-      y[r] = acc / Lr[r];
-    }
-#pragma unroll
-    for (int r = 0; r < 32; ++r)
-      if (r >= lane) sY[plo(o + r, o + lane)] = y[r];
-  }
-  __syncthreads();
-  // thread -> (row r, 4 consecutive columns c..c+3) of a 32x32 sub-block
-  const int rr = tid >> 3, cc = (tid & 7) * 4;
-  for (int d = 1; d < 4; ++d) {
-    const int nb = 4 - d;
-    for (int bI = 0; bI < nb; ++bI) {          // T_b = sum_{K=J}^{I-1} L_IK Y_KJ
-      const int J = bI, I = bI + d;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const double* Lr = sL + plo(I * 32 + rr, 0);
-      for (int kk = J * 32; kk < I * 32; ++kk) {
-        const double lv = Lr[kk];
-        const double* Yk = sY + plo(kk, 0);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int col = J * 32 + cc + e;
-          if (kk >= col) acc[e] = fma(lv, Yk[col], acc[e]);
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) sT[bI * 1024 + rr * 32 + cc + e] = acc[e];
-    }
-    __syncthreads();
-    for (int bI = 0; bI < nb; ++bI) {          // Y_IJ = -inv(D_I) T_b
-      const int J = bI, I = bI + d;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const double* Yr = sY + plo(I * 32 + rr, I * 32);
-      for (int kk = 0; kk <= rr; ++kk) {
-        const double yv = Yr[kk];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[e] = fma(yv, sT[bI * 1024 + kk * 32 + cc + e], acc[e]);
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) sY[plo(I * 32 + rr, J * 32 + cc + e)] = -acc[e];
-    }
-    __syncthreads();
-  }
+  invert_lower_128(sL, sY, sT);
   for (int idx = tid; idx < TILE; idx += 256) {
     const int jl = idx >> 7;
     const int il = (idx & 127) ^ ((jl & 3) << 2);
@@ -187,7 +135,7 @@ constexpr int BS_THREADS = 256;
 
 // Issue the copies of quarter qi of row k into `dst` (all 256 threads).
 __device__ __forceinline__ void bs_load_quarter(const SubDev& S, int k, int qi, double* dst, bool dense) {
-  const int l = S.smin + qi / (TB / QCOLS), q = qi % (TB / QCOLS);
+  const int l = S.tbase + qi / (TB / QCOLS), q = qi % (TB / QCOLS);
   if (dense) {
     // column jg of L: rows k*128 + kk at raw[colstart(jg) + (i - jg)]; thread
     // (jq, kk-quarter): 4 columns x 32 consecutive rows per warp -> coalesced
@@ -255,8 +203,8 @@ __global__ void __launch_bounds__(BS_THREADS, 1) block_scale_kernel(const SubDev
   const int4 w = work[blockIdx.x];
   const SubDev S = subs[w.x];   // by value: no reloads after the epilogue's global stores
   const int k = w.y;
-  const int nq = (k - S.smin) * (TB / QCOLS);
-  const bool dense = (S.up == nullptr);
+  const int nq = (k - S.tbase) * (TB / QCOLS);
+  const bool dense = (S.src == SRC_RAW_DENSE);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(barA, 1);
@@ -309,7 +257,7 @@ __global__ void __launch_bounds__(BS_THREADS, 1) block_scale_kernel(const SubDev
         acc[a][b][0] += acc2[a][b][0];
         acc[a][b][1] += acc2[a][b][1];
       }
-    const int l = S.smin + qi / (TB / QCOLS), q = qi % (TB / QCOLS);
+    const int l = S.tbase + qi / (TB / QCOLS), q = qi % (TB / QCOLS);
     double* Lkl = tile_ptr(S, k, l);
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi) {

@@ -150,11 +150,18 @@ class DualOperator:
     * ``perms``: explicit per-subdomain orderings (mapping or sequence indexed
       by subdomain), as ``symbolic_factorize(ordering=<array>)`` accepts
       (sparse.py:368-371); overrides ``ordering``
+    * ``factorization``: ``"host"`` (LAPACK on the host, the factor is
+      uploaded) or ``"device"``: K_reg = K + rho Q Q^T is formed from the
+      unregularized sparse ``stiffness[i]`` and the kernel basis
+      ``kernels[i]`` and factored on the GPU (DMMA blocked Cholesky); the
+      factor never crosses PCIe.  With the reference's dense K_reg the RCM
+      ordering is the reversed natural order, which device mode uses.
     """
 
     def __init__(self, matrices, constraints, layout, config: DualOpConfig, pool=None, workers: int = 1,
                  schur_cap: int = 2000, device: int | None = None, ordering: str = "rcm",
-                 subdomains=None, pinned: bool = True, perms=None):
+                 subdomains=None, pinned: bool = True, perms=None, factorization: str = "host",
+                 stiffness=None, kernels=None):
         if len(matrices) != len(constraints.per_subdomain):
             raise ValueError("one stiffness matrix per subdomain required")
         if config.strategy != "explicit":
@@ -176,6 +183,13 @@ class DualOperator:
         self.pinned = bool(pinned)
         self.device = device
         self.perms = perms
+        if factorization not in ("host", "device"):
+            raise ValueError("factorization must be 'host' or 'device'")
+        self.factorization = factorization
+        self.stiffness = None if stiffness is None else list(stiffness)
+        self.kernels = None if kernels is None else list(kernels)
+        if factorization == "device" and (self.stiffness is None or self.kernels is None):
+            raise ValueError("device factorization needs stiffness= and kernels= per subdomain")
         self.owned = (list(range(self.n_subdomains)) if subdomains is None
                       else sorted(int(s) for s in subdomains))
 
@@ -273,6 +287,14 @@ class DualOperator:
                 sub.perm = np.ascontiguousarray(self.perms[i], dtype=np.int64)
                 if sub.perm.shape != (sub.n,) or not np.array_equal(np.sort(sub.perm), np.arange(sub.n)):
                     raise ValueError(f"subdomain {i}: explicit ordering is not a permutation")
+            elif self.factorization == "device":
+                base = np.arange(sub.n - 1, -1, -1, dtype=np.int64)   # RCM of the dense K_reg
+                if self.ordering == "rcm":
+                    sub.perm = base
+                else:
+                    mark = np.zeros(sub.n, bool)
+                    mark[sub.bcol] = True
+                    sub.perm = np.concatenate([base[~mark[base]], np.sort(np.flatnonzero(mark))])
             elif self.ordering == "rcm":
                 sub.perm = fct.rcm_ordering(matrix)
             else:
@@ -299,6 +321,8 @@ class DualOperator:
             if need > int(self.pool.capacity):
                 raise PoolCapacityError(
                     f"pool of {self.pool.capacity} bytes cannot hold the {need}-byte device operator")
+        if self.factorization == "device":
+            _call(self._lib.feti_enable_device_factorization(ctx))
         _call(self._lib.feti_finalize(ctx, self.n_multipliers))
         st = self.stats()
         self.persistent_bytes = int(st["bytes_persistent"])
@@ -325,8 +349,8 @@ class DualOperator:
                 sub.values = np.empty(n)
         return sub.values
 
-    def preprocess(self, matrices=None) -> None:
-        """Host numeric factorization, then device assembly of every F~_i."""
+    def preprocess(self, matrices=None, stiffness=None, kernels=None) -> None:
+        """Numeric factorization (host, or device), then device assembly of every F~_i."""
         import time
 
         if not self.prepared:
@@ -335,6 +359,13 @@ class DualOperator:
             if len(matrices) != self.n_subdomains:
                 raise ValueError("one stiffness matrix per subdomain required")
             self.matrices = list(matrices)
+        if self.factorization == "device":
+            if stiffness is not None:
+                self.stiffness = list(stiffness)
+            if kernels is not None:
+                self.kernels = list(kernels)
+            self._preprocess_device()
+            return
 
         t0 = time.perf_counter()
 
@@ -353,6 +384,39 @@ class DualOperator:
         t2 = time.perf_counter()
         self.timings = {"host_factorization_s": t1 - t0, "upload_and_assembly_s": t2 - t1}
         self.numeric_count += len(done)
+
+    def _preprocess_device(self) -> None:
+        import time
+
+        t0 = time.perf_counter()
+        for sub in self._subs.values():
+            n, ip, ix, dt = fct.csr_arrays(self.stiffness[sub.index])
+            if n != sub.n:
+                raise ValueError("stiffness size does not match the subdomain")
+            q, _ = np.linalg.qr(np.asarray(self.kernels[sub.index], dtype=np.float64).reshape(n, -1))
+            q = np.ascontiguousarray(q)
+            rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ip))
+            rho = float(dt[rows == ix].sum()) / n                     # trace(K)/n (sparse.py:450)
+            ip, ix, dt = (np.ascontiguousarray(ip, np.int64), np.ascontiguousarray(ix, np.int64),
+                          np.ascontiguousarray(dt, np.float64))
+            _call(self._lib.feti_set_stiffness(self._ctx, sub.slot, n, _lib.i64ptr(ip), _lib.i64ptr(ix),
+                                               _lib.f64ptr(dt), ip[-1], _lib.f64ptr(q), q.shape[1], rho,
+                                               _lib.i64ptr(sub.perm)))
+        t1 = time.perf_counter()
+        try:
+            _lib.check(self._lib.feti_factorize(self._ctx))
+        except _lib.FetiError as err:
+            if err.code == _lib.FETI_ERR_NOT_SPD:
+                slot = int(str(err).split()[1].rstrip(":"))
+                index = next(s.index for s in self._subs.values() if s.slot == slot)
+                msg = str(err).split(":", 1)[1].strip()
+                raise SpdError(f"subdomain {index}: {msg}") from None
+            _raise_from(err)
+        self.assemble()
+        t2 = time.perf_counter()
+        self.timings = {"stiffness_upload_s": t1 - t0, "device_factorization_and_assembly_s": t2 - t1,
+                        "device_factorization_ms": self.stats()["ms_factorize"]}
+        self.numeric_count += len(self._subs)
 
     # -- lower-level entry points (used by preprocess, bench and tests) -------
 
@@ -440,11 +504,35 @@ class DualOperator:
     # -- K^+ access for the solver --------------------------------------------
 
     def solve_local(self, index: int, rhs, out=None):
-        """x = K_reg^-1 rhs for one subdomain through its host factor."""
+        """x = K_reg^-1 rhs for one subdomain through its factor."""
         if not self.step_ready:
             raise LifecycleError("solve_local before preprocess")
         sub = self._subs[int(index)]
+        if self.factorization == "device":
+            x = self.solve_local_many([index], [rhs])[0]
+            if out is not None:
+                out[:] = x
+                return out
+            return x
         return fct.solve_packed(sub.values, sub.perm, rhs, out=out)
+
+    def solve_local_many(self, indices, rhs_list):
+        """Batched solve_local (one device launch in device-factorization mode)."""
+        if not self.step_ready:
+            raise LifecycleError("solve_local before preprocess")
+        subs = [self._subs[int(i)] for i in indices]
+        if self.factorization != "device":
+            return [fct.solve_packed(s.values, s.perm, r) for s, r in zip(subs, rhs_list)]
+        slots = np.array([s.slot for s in subs], dtype=np.int64)
+        b = np.ascontiguousarray(np.concatenate([np.asarray(r, dtype=np.float64) for r in rhs_list]))
+        x = np.empty_like(b)
+        _call(self._lib.feti_solve_many(self._ctx, slots.shape[0], _lib.i64ptr(slots), _lib.f64ptr(b),
+                                        _lib.f64ptr(x)))
+        out, off = [], 0
+        for s in subs:
+            out.append(x[off:off + s.n].copy())
+            off += s.n
+        return out
 
     def local_operator(self, index: int) -> np.ndarray:
         """Host copy of F~_i: m x m, upper triangle, strictly lower = 0."""

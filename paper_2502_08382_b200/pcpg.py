@@ -58,13 +58,13 @@ class DevicePCPG:
         gmat = np.zeros((n_mult, nk))
         off = 0
         d = np.zeros(n_mult)
-        for s in subs:
+        kfs = op.solve_local_many([s.index for s in subs], [forces[s.index] for s in subs])
+        for s, kf in zip(subs, kfs):
             r = kernels[s.index]
             gblk = s.bval[:, None] * r[s.bcol, :]            # G_s = B~_s R_s (solver.py:137-139)
             blocks.append(np.ascontiguousarray(gblk).ravel())
             gmat[s.gids, off:off + r.shape[1]] = gblk
             e_parts.append(r.T @ forces[s.index])            # e = R^T f
-            kf = op.solve_local(s.index, forces[s.index])
             d[s.gids] += s.bval * kf[s.bcol]                 # B K^+ f
             off += r.shape[1]
         d -= np.asarray(c, dtype=np.float64)

@@ -1,0 +1,93 @@
+"""Device numeric factorization: K_reg = K + rho Q Q^T formed and
+factored on the GPU from the sparse K; everything downstream must match the
+reference exactly as with the host factor."""
+
+import numpy as np
+import pytest
+
+from conftest import SMALL_CASES, expected_iterations, load_golden
+from paper_2502_08382_b200 import dualop, inputs
+from paper_2502_08382_b200.pcpg import DevicePCPG
+
+pytestmark = pytest.mark.gpu
+CFG = dualop.DualOpConfig(strategy="explicit", path="syrk")
+
+
+def _device_op(prob, ordering="rcm", subs=None):
+    ks, qs, fs = [], [], []
+    for s in range(prob.n_sub):
+        k, f, q = prob.subdomain_system(s)
+        ks.append(k)
+        qs.append(q)
+        fs.append(f)
+    mats = [inputs.ShapeOnly((prob.n_dofs, prob.n_dofs)) for _ in range(prob.n_sub)]
+    op = dualop.prepare(mats, prob.constraints(), prob.layout, CFG, device=0, ordering=ordering,
+                        factorization="device", stiffness=ks, kernels=qs)
+    return op, ks, qs, fs
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+@pytest.mark.parametrize("ordering", ["rcm", "interface_last"])
+def test_device_factor_matches_reference(case, ordering):
+    g = load_golden(case)
+    prob = inputs.Problem(str(g["physics"]), int(g["dim"]), int(g["cells"]), int(g["subs"]))
+    op, ks, qs, fs = _device_op(prob, ordering)
+    with op:
+        op.preprocess()
+        for s in range(prob.n_sub):
+            m = prob.gids[s].shape[0]
+            ref = np.zeros((m, m))
+            ref[np.triu_indices(m)] = g[f"s{s}_F_upper"]
+            f = op.local_operator(s)
+            assert np.linalg.norm(f - ref) <= 1e-10 * np.linalg.norm(ref), (case, s)
+        q = op.apply(g["p"])
+        assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
+        qi = op.apply_implicit(g["p"])
+        assert np.linalg.norm(qi - g["q_implicit"]) <= 1e-11 * np.linalg.norm(g["q_implicit"])
+        lam, it, _ = DevicePCPG(op, qs, fs, prob.c).solve(tol=1e-9)
+    assert it in expected_iterations(case, g)
+    assert np.linalg.norm(lam - g["pcpg_lambda"]) <= 1e-9 * np.linalg.norm(g["pcpg_lambda"])
+
+
+def test_device_solve_local_matches_dense_solve():
+    prob = inputs.Problem("elasticity", 3, 3, 2)
+    op, ks, qs, fs = _device_op(prob)
+    with op:
+        op.preprocess()
+        rng = np.random.default_rng(0)
+        for s in (0, 5):
+            kreg = inputs.regularized_dense(ks[s], qs[s])
+            b = rng.normal(size=prob.n_dofs)
+            x = op.solve_local(s, b)
+            ref = np.linalg.solve(kreg, b)
+            assert np.linalg.norm(x - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+def test_device_factor_spd_violation_reports_subdomain():
+    prob = inputs.Problem("heat", 2, 3, 2)
+    op, ks, qs, fs = _device_op(prob)
+    bad = list(ks)
+    k1 = ks[1]
+    bad[1] = inputs.Csr(k1.shape, k1.indptr, k1.indices, -k1.data)
+    with op:
+        with pytest.raises(dualop.SpdError, match="subdomain 1"):
+            op.preprocess(stiffness=bad)
+
+
+def test_device_factor_c3_subdomain_checksums():
+    g = load_golden("c3_sub21")
+    prob = inputs.Problem(*inputs.CONFIGS["c3"])
+    s = int(g["sub_index"])
+    k, f, q = prob.subdomain_system(s)
+    m = prob.gids[s].shape[0]
+    mat = inputs.Csr((m, prob.n_dofs), np.arange(m + 1, dtype=np.int64), prob.bcol[s], prob.bval[s])
+    cons = inputs.ConstraintSet(m, np.zeros(m), [inputs.SubdomainConstraints(np.arange(m, dtype=np.int64), mat)])
+    lay = inputs.ClusterLayout([inputs.Cluster(0, np.array([0]), np.arange(m), [np.arange(m)])], m)
+    with dualop.prepare([inputs.ShapeOnly((prob.n_dofs, prob.n_dofs))], cons, lay, CFG, device=0,
+                        factorization="device", stiffness=[k], kernels=[q]) as op:
+        op.preprocess()
+        fu = op.local_operator(0)
+    full = fu + np.triu(fu, 1).T
+    for name, got in (("Fv", full @ g["v"]), ("F_diag", np.diag(full)), ("F_row0", full[0])):
+        ref = g[name]
+        assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref), name
