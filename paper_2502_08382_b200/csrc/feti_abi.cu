@@ -918,8 +918,8 @@ int feti_factorize(feti_ctx* c) {
   launch_kreg_build(c->d_subdev, c->d_fsub, ns, T, (int)c->subs[0].n, st);
   CUDA_TRY(cudaGetLastError());
   FETI_DEBUG_SYNC(st);
-  for (int k = 0; k < T; ++k) {
-    launch_factor_step(c->d_subdev, c->d_dinv, c->d_bad, ns, k, T, st);
+  for (int k = 0; k < T;) {
+    k = launch_factor_step(c->d_subdev, c->d_dinv, c->d_bad, ns, k, T, st);
     CUDA_TRY(cudaGetLastError());
     FETI_DEBUG_SYNC(st);
   }

@@ -162,53 +162,73 @@ __device__ __forceinline__ void fg_mma_slice(const double* __restrict__ a_s, con
   }
 }
 
-template <bool PANEL>
+// Blocked right-looking Cholesky with a look-ahead group of FG_GROUP block
+// columns: inside a group the columns are brought up to date left-looking
+// (MODE_ACC) and factored one by one (potrf_diag + MODE_PANEL); the rest of
+// the matrix then receives one FG_GROUP*128-deep update (MODE_TRAIL), so every
+// trailing tile is read-modified-written once per group.
+//   MODE_PANEL (sub, i), i in (c, T):      tile(i,c)  = tile(i,c) dinv_c^T
+//   MODE_ACC   (sub, i), i in [c, T):      tile(i,c) -= sum_{kc=k0}^{c-1} tile(i,kc) tile(c,kc)^T
+//   MODE_TRAIL (sub, i>=j>=j0):            tile(i,j) -= sum_{kc=k0}^{k0+nk-1} tile(i,kc) tile(j,kc)^T
+enum { MODE_PANEL = 0, MODE_ACC = 1, MODE_TRAIL = 2 };
+constexpr int FG_GROUP = 16;
+
+template <int MODE>
 __global__ void __launch_bounds__(FG_THREADS, 1) factor_gemm_kernel(const SubDev* __restrict__ subs,
-                                                                    const double* __restrict__ dinv, int k, int T) {
+                                                                    const double* __restrict__ dinv, int c,
+                                                                    int k0, int nk, int T) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sA = reinterpret_cast<double*>(smem_raw);
   double* sB = sA + FG_STAGES * SLICE;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + FG_STAGES * SLICE);
   uint64_t* empty = full + FG_STAGES;
-  const int M = T - k - 1;
   int sub, i, j;
-  if (PANEL) {
+  if (MODE == MODE_PANEL) {
+    const int M = T - c - 1;
     sub = blockIdx.x / M;
-    i = k + 1 + blockIdx.x % M;
-    j = k;
+    i = c + 1 + blockIdx.x % M;
+    j = c;
+  } else if (MODE == MODE_ACC) {
+    const int M = T - c;
+    sub = blockIdx.x / M;
+    i = c + blockIdx.x % M;
+    j = c;
   } else {
+    const int M = T - c;                     // c = j0
     const int N = M * (M + 1) / 2;
     sub = blockIdx.x / N;
     const int tt = blockIdx.x % N;
     int ii = (int)((sqrt(8.0 * tt + 1.0) - 1.0) * 0.5);
     while ((ii + 1) * (ii + 2) / 2 <= tt) ++ii;
     while (ii * (ii + 1) / 2 > tt) --ii;
-    i = k + 1 + ii;
-    j = k + 1 + (tt - ii * (ii + 1) / 2);
+    i = c + ii;
+    j = c + (tt - ii * (ii + 1) / 2);
   }
   const SubDev& S = subs[sub];
-  const double* At = tile_ptr(S, i, k);
-  const double* Bt = PANEL ? dinv + (size_t)sub * TILE : tile_ptr(S, j, k);
-  double* Ct = PANEL ? tile_ptr(S, i, k) : tile_ptr(S, i, j);
+  double* Ct = tile_ptr(S, i, j);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < FG_STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 8);
+    for (int st = 0; st < FG_STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 8);
     }
     mbar_fence_init();
   }
   __syncthreads();
-  constexpr int NSL = TB / KS;
+  const int nsl = (MODE == MODE_PANEL ? 1 : nk) * (TB / KS);
   if (warp == 8) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int sl = 0; sl < NSL; ++sl) {
+      for (int sl = 0; sl < nsl; ++sl) {
+        const int kc = k0 + sl / (TB / KS);              // contraction column block
+        const double* At = (MODE == MODE_PANEL) ? tile_ptr(S, i, c) : tile_ptr(S, i, kc);
+        const double* Bt = (MODE == MODE_PANEL) ? dinv + (size_t)sub * TILE : tile_ptr(S, j, kc);
+        const int so = (sl % (TB / KS)) * SLICE;
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full[stage], 2 * SLICE * 8);
-        bulk_g2s(sA + stage * SLICE, At + sl * SLICE, SLICE * 8, &full[stage]);
-        bulk_g2s(sB + stage * SLICE, Bt + sl * SLICE, SLICE * 8, &full[stage]);
+        bulk_g2s(sA + stage * SLICE, At + so, SLICE * 8, &full[stage]);
+        bulk_g2s(sB + stage * SLICE, Bt + so, SLICE * 8, &full[stage]);
         if (++stage == FG_STAGES) {
           stage = 0;
           phase ^= 1;
@@ -226,7 +246,7 @@ __global__ void __launch_bounds__(FG_THREADS, 1) factor_gemm_kernel(const SubDev
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   int stage = 0;
   uint32_t phase = 0;
-  for (int sl = 0; sl < NSL; ++sl) {
+  for (int sl = 0; sl < nsl; ++sl) {
     mbar_wait(&full[stage], phase);
     fg_mma_slice(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
     fence_proxy_async_shared();
@@ -237,7 +257,7 @@ __global__ void __launch_bounds__(FG_THREADS, 1) factor_gemm_kernel(const SubDev
       phase ^= 1;
     }
   }
-  // all four slices of A were consumed above, so the in-place panel write is safe
+  // all slices of A were consumed above, so the in-place panel write is safe
 #pragma unroll
   for (int mi = 0; mi < 8; ++mi) {
     const int m = wm * 64 + mi * 8 + g;
@@ -246,11 +266,11 @@ __global__ void __launch_bounds__(FG_THREADS, 1) factor_gemm_kernel(const SubDev
       const int nn = wn * 32 + ni * 8 + 2 * t;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        double* c = Ct + swz(nn + e, m);
-        if (PANEL)
-          *c = acc[mi][ni][e];
+        double* cp = Ct + swz(nn + e, m);
+        if (MODE == MODE_PANEL)
+          *cp = acc[mi][ni][e];
         else
-          *c -= acc[mi][ni][e];
+          *cp -= acc[mi][ni][e];
       }
     }
   }
@@ -355,9 +375,13 @@ size_t solve_smem(int T) { return ((size_t)2 * T * TB + SV_GROUPS * TB) * sizeof
 
 cudaError_t configure_factor(int max_T) {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(factor_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fg_smem())))
+  if ((e = cudaFuncSetAttribute(factor_gemm_kernel<MODE_PANEL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fg_smem())))
     return e;
-  if ((e = cudaFuncSetAttribute(factor_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if ((e = cudaFuncSetAttribute(factor_gemm_kernel<MODE_ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fg_smem())))
+    return e;
+  if ((e = cudaFuncSetAttribute(factor_gemm_kernel<MODE_TRAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)fg_smem())))
     return e;
   if ((e = cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)potrf_smem())))
@@ -375,13 +399,23 @@ void launch_kreg_build(const SubDev* subs, const FactorSub* fs, int nsub, int T,
   kreg_scatter_kernel<<<nsub * n, 128, 0, st>>>(subs, fs, n);
 }
 
-void launch_factor_step(const SubDev* subs, double* dinv, int* bad, int nsub, int k, int T, cudaStream_t st) {
-  potrf_diag_kernel<<<nsub, 256, potrf_smem(), st>>>(subs, dinv, bad, k);
-  const int M = T - k - 1;
-  if (M > 0) {
-    factor_gemm_kernel<true><<<nsub * M, FG_THREADS, fg_smem(), st>>>(subs, dinv, k, T);
-    factor_gemm_kernel<false><<<nsub * (M * (M + 1) / 2), FG_THREADS, fg_smem(), st>>>(subs, dinv, k, T);
+// One look-ahead group starting at block column k0 (FG_GROUP columns):
+// returns the next group's first column.
+int launch_factor_step(const SubDev* subs, double* dinv, int* bad, int nsub, int k0, int T, cudaStream_t st) {
+  const int k1 = k0 + FG_GROUP < T ? k0 + FG_GROUP : T;
+  for (int c = k0; c < k1; ++c) {
+    if (c > k0)
+      factor_gemm_kernel<MODE_ACC><<<nsub * (T - c), FG_THREADS, fg_smem(), st>>>(subs, dinv, c, k0, c - k0, T);
+    potrf_diag_kernel<<<nsub, 256, potrf_smem(), st>>>(subs, dinv, bad, c);
+    if (T - c - 1 > 0)
+      factor_gemm_kernel<MODE_PANEL><<<nsub * (T - c - 1), FG_THREADS, fg_smem(), st>>>(subs, dinv, c, c, 1, T);
   }
+  if (k1 < T) {
+    const int M = T - k1;
+    factor_gemm_kernel<MODE_TRAIL><<<nsub * (M * (M + 1) / 2), FG_THREADS, fg_smem(), st>>>(subs, dinv, k1, k0,
+                                                                                             k1 - k0, T);
+  }
+  return k1;
 }
 
 void launch_solve(const SubDev* subs, const FactorSub* fs, const int* slots, int nslots, int max_T,

@@ -23,7 +23,7 @@ struct FactorSub {
 cudaError_t configure_factor(int max_T);
 size_t solve_smem(int T);
 void launch_kreg_build(const SubDev* subs, const FactorSub* fs, int nsub, int T, int n, cudaStream_t st);
-void launch_factor_step(const SubDev* subs, double* dinv, int* bad, int nsub, int k, int T, cudaStream_t st);
+int launch_factor_step(const SubDev* subs, double* dinv, int* bad, int nsub, int k, int T, cudaStream_t st);
 void launch_solve(const SubDev* subs, const FactorSub* fs, const int* slots, int nslots, int max_T,
                   const int64_t* vec_off, const double* b, double* x, cudaStream_t st);
 
