@@ -80,6 +80,10 @@ typedef struct feti_stats {
   int32_t launches_assemble; /* kernel launches of the last assemble */
   int32_t launches_apply;    /* kernel launches per apply             */
   double ms_factorize;       /* device time of the last feti_factorize  */
+  double ms_correct;         /* sparse-factor route: rank-2r update of F~ */
+  double flops_factor_exec;  /* sparse-factor route: tile flops executed by feti_factorize */
+  int32_t launches_factorize;
+  int32_t pad_;
 } feti_stats;
 
 int feti_abi_version(void);
@@ -163,6 +167,24 @@ int feti_set_stiffness(feti_ctx* ctx, int64_t slot, int64_t n, const int64_t* in
                        const double* data, int64_t nnz, const double* Q, int64_t r, double rho,
                        const int64_t* perm);
 int feti_factorize(feti_ctx* ctx);
+
+/* Sparse-factor route (SURVEY.md §7 hard part 4): the reference's dense
+ * K_reg is never formed.  K_s = K + rho E E^T (E = r fixing DOFs, E^T Q
+ * nonsingular) keeps K's pattern and is factored on the device into a
+ * block-sparse pool of 128x128 tiles; F~_i is recovered exactly by the
+ * rank-2r correction F~ = B K_s^-1 B^T - U1 U2^T - U2 U1^T + U1 (Q^T W + I/rho)
+ * U1^T (W = K_s^-1 Q, U1 = B~ Q, U2 = B~ W), which feti_assemble applies.
+ * Replaces regularize (sparse.py:427-454) + symbolic_factorize
+ * (sparse.py:340-415) + numeric_factorize (sparse.py:418-424) for
+ * assemble_explicit_local (dualop.py:427-501).
+ * Call feti_enable_sparse_factorization and, per slot, feti_set_sparse_pattern
+ * (K's CSR pattern, the ordering -- constrained DOFs last -- and the fixing
+ * DOFs) before feti_finalize; then per step feti_set_stiffness (values, Q,
+ * rho = trace(K)/n, same ordering), feti_factorize, feti_assemble.
+ * feti_solve_many and the implicit apply are not available in this mode. */
+int feti_enable_sparse_factorization(feti_ctx* ctx);
+int feti_set_sparse_pattern(feti_ctx* ctx, int64_t slot, int64_t n, const int64_t* indptr, const int64_t* indices,
+                            const int64_t* perm, int64_t r, const int64_t* fix_dofs);
 /* x = K_reg^-1 b for the listed slots (host vectors concatenated in list
  * order), through the device factor (CholFactor.solve, sparse.py:324-337). */
 int feti_solve_many(feti_ctx* ctx, int64_t nslots, const int64_t* slots, const double* b, double* x);

@@ -404,3 +404,56 @@ def pcpg(gmat, e, d, coarse, fapply, tol=1e-9, maxit=None):
         beta = wy_next / wy
         wy = wy_next
         p = y + beta * p
+
+
+# ---------------------------------------------------------------------------
+# config 5 and the sparse-factor route: K_reg^-1 without the dense K_reg
+# ---------------------------------------------------------------------------
+
+
+class WoodburyKregSolver:
+    """x = K_reg^-1 b for the reference's K_reg = K + rho Q Q^T (regularize,
+    sparse.py:427-454, rho = trace(K)/n at :450) without forming it.
+
+    Independent of the product's route on purpose: K_reg = K_s' + U D U^T with
+    K_s' = K + rho E' E'^T (E' = the r DOFs a pivoted QR picks from Q^T with the
+    DOF order reversed -- a different set from the product's), U = [Q, E'],
+    D = diag(rho I, -rho I); Sherman-Morrison-Woodbury on a SuperLU factor of
+    K_s'.  Used as the parity checker where the reference's own dense path is
+    infeasible (config 5: 4.4 GB factor per subdomain)."""
+
+    def __init__(self, n, indptr, indices, data, kernel):
+        import scipy.linalg
+        from scipy.sparse.linalg import splu
+
+        ip = np.asarray(indptr, np.int64)
+        ix = np.asarray(indices, np.int64)
+        dt = np.asarray(data, np.float64)
+        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ip))
+        self.rho = float(dt[rows == ix].sum()) / n
+        q, _ = np.linalg.qr(np.asarray(kernel, dtype=np.float64).reshape(n, -1))
+        r = q.shape[1]
+        _, _, piv = scipy.linalg.qr(q[::-1].T, mode="economic", pivoting=True)
+        fix = (n - 1 - piv[:r]).astype(np.int64)
+        shift = csr_matrix((np.full(r, self.rho), (fix, fix)), shape=(n, n))
+        self.lu = splu((csr_matrix((dt, ix, ip), shape=(n, n)) + shift).tocsc())
+        e = np.zeros((n, r))
+        e[fix, np.arange(r)] = 1.0
+        self.u = np.hstack([q, e])
+        self.kinv_u = self.lu.solve(self.u)
+        dinv = np.concatenate([np.full(r, 1.0 / self.rho), np.full(r, -1.0 / self.rho)])
+        self.cap = np.diag(dinv) + self.u.T @ self.kinv_u
+
+    def solve(self, b):
+        b = np.asarray(b, dtype=np.float64)
+        y = self.lu.solve(b)
+        return y - self.kinv_u @ np.linalg.solve(self.cap, self.u.T @ y)
+
+
+def fmatrix_via_solver(solver, n, bcol, bval):
+    """F~ = B~ K_reg^-1 B~^T (full symmetric m x m) through a solver."""
+    m = bcol.shape[0]
+    z = np.zeros((n, m))
+    z[bcol, np.arange(m)] = bval
+    x = solver.solve(z)
+    return bval[:, None] * x[bcol, :]

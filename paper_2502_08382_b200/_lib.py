@@ -31,7 +31,7 @@ EXPORTED = (
     "feti_apply_device", "feti_get_stats", "feti_host_alloc", "feti_host_free",
     "feti_debug_kernel_attributes", "feti_coarse_setup", "feti_project_device", "feti_coarse_apply_device",
     "feti_apply_implicit", "feti_apply_implicit_device", "feti_enable_device_factorization", "feti_set_stiffness",
-    "feti_factorize", "feti_solve_many",
+    "feti_factorize", "feti_solve_many", "feti_enable_sparse_factorization", "feti_set_sparse_pattern",
 )
 
 
@@ -47,7 +47,8 @@ class FetiStats(C.Structure):
         ("bytes_persistent", C.c_int64), ("bytes_temporary", C.c_int64),
         ("n_subdomains", C.c_int64), ("n_multipliers", C.c_int64),
         ("launches_assemble", C.c_int32), ("launches_apply", C.c_int32),
-        ("ms_factorize", C.c_double),
+        ("ms_factorize", C.c_double), ("ms_correct", C.c_double), ("flops_factor_exec", C.c_double),
+        ("launches_factorize", C.c_int32), ("pad_", C.c_int32),
     ]
 
     def as_dict(self):
@@ -97,6 +98,8 @@ def load() -> C.CDLL:
         "feti_factorize": ([P], C.c_int),
         "feti_solve_many": ([P, C.c_int64, i64p, f64p, f64p], C.c_int),
         "feti_host_free": ([P], C.c_int),
+        "feti_enable_sparse_factorization": ([P], C.c_int),
+        "feti_set_sparse_pattern": ([P, C.c_int64, C.c_int64, i64p, i64p, i64p, C.c_int64, i64p], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -23,6 +23,7 @@
 #include "feti_factor.h"
 #include "feti_implicit.h"
 #include "feti_kernels.h"
+#include "feti_sparse.h"
 
 using namespace feti;
 
@@ -101,6 +102,17 @@ struct SubHost {
   int64_t *d_perm = nullptr, *d_iperm = nullptr, *d_kptr = nullptr, *d_kind = nullptr;
   double* d_kdata = nullptr;
   cudaEvent_t ev_upload = nullptr;
+  // sparse-factor route (feti_set_sparse_pattern): K_s = K + rho E E^T in a
+  // block-sparse tile pool, rank-2r correction after the assembly
+  bool sp_pattern = false;
+  int sp_r = 0;
+  std::vector<int64_t> sp_perm, sp_iperm, sp_kptr, sp_kind, sp_fix;
+  SpPlan sp;
+  double* d_pool = nullptr;
+  int* d_tmap = nullptr;
+  int64_t* d_fix = nullptr;
+  double* d_U1 = nullptr;
+  double* d_U2W = nullptr;
   int64_t f_tiles() const { return (int64_t)T32 * (T32 + 1) / 2; }
   int64_t l_tiles() const { return (int64_t)(T - tbase) * (T - tbase + 1) / 2; }
   int64_t upload_count() const { return nnz - raw_off; }
@@ -169,6 +181,17 @@ struct feti_ctx {
   // per-wave work lists: [kind][wave] -> (offset, count) into d_wv[kind]
   int4* d_wv[5] = {};
   std::vector<std::pair<int, int>> wv_range[5];
+  // sparse-factor route: per block column task ranges into the device lists
+  bool sparse_factor = false;
+  SpSub* d_spsub = nullptr;
+  SpInit* d_sp_init = nullptr;
+  SpTask* d_sp_tasks = nullptr;
+  SpPair* d_sp_pairs = nullptr;
+  SpDiag* d_sp_diag = nullptr;
+  int2* d_sp_panels = nullptr;
+  int n_sp_init = 0, n_sp_panels = 0, sp_max_T32 = 0, sp_max_n = 0;
+  std::vector<std::pair<int, int>> sp_acc_rng, sp_panel_rng, sp_diag_rng;
+  double sp_flops = 0.0;
 };
 
 namespace {
@@ -231,6 +254,136 @@ int sync_subdev(feti_ctx* c) {
     CUDA_TRY(cudaMemcpyAsync(c->d_subdev, h.data(), h.size() * sizeof(SubDev), cudaMemcpyHostToDevice,
                              c->stream));
   c->subdev_dirty = false;
+  return FETI_OK;
+}
+
+// Device task lists of the block-sparse factorization, ordered by block
+// column: [acc(j) | potrf(j) | panel(j)] with every subdomain batched in each
+// launch (deepest accumulations first).
+int build_sparse_tasks(feti_ctx* c) {
+  const int ns = (int)c->subs.size();
+  int rc;
+  if ((rc = dev_alloc(c, (void**)&c->d_dinv, (size_t)ns * TILE * 8, false))) return rc;
+  if ((rc = dev_alloc(c, (void**)&c->d_bad, (size_t)ns * sizeof(int), false))) return rc;
+  if ((rc = dev_alloc(c, (void**)&c->d_spsub, (size_t)ns * sizeof(SpSub), true))) return rc;
+  int maxTq = 0;
+  std::vector<SpInit> init;
+  std::vector<int2> panels;
+  for (int si = 0; si < ns; ++si) {
+    SubHost& s = c->subs[si];
+    const SpPlan& P = s.sp;
+    maxTq = std::max(maxTq, P.Tq);
+    c->sp_max_T32 = std::max(c->sp_max_T32, s.T32);
+    c->sp_max_n = std::max<int>(c->sp_max_n, (int)s.n);
+    for (int K = 0; K < P.Tq; ++K)
+      for (int L = 0; L <= K; ++L) {
+        const int slot = P.tmap[(size_t)K * P.Tq + L];
+        if (slot >= 0) init.push_back(SpInit{s.d_pool + (size_t)slot * TILE, K, L, si, 0});
+      }
+    if (s.sp_r > 0)
+      for (int p = 0; p < s.P; ++p) panels.push_back(make_int2(si, p));
+    c->sp_flops += P.flops_exec;
+  }
+  std::vector<SpTask> tasks;
+  std::vector<SpPair> pairs;
+  std::vector<SpDiag> diag;
+  c->sp_acc_rng.assign(maxTq, {0, 0});
+  c->sp_panel_rng.assign(maxTq, {0, 0});
+  c->sp_diag_rng.assign(maxTq, {0, 0});
+  for (int j = 0; j < maxTq; ++j) {
+    int b = (int)tasks.size();
+    for (int si = 0; si < ns; ++si) {
+      const SubHost& s = c->subs[si];
+      if (j >= s.sp.Tq) continue;
+      for (const auto& t : s.sp.acc[j]) {
+        tasks.push_back(SpTask{s.d_pool + (size_t)t.first * TILE, (int64_t)pairs.size(), (int)t.second.size(), 0});
+        for (const auto& pr : t.second)
+          pairs.push_back(SpPair{s.d_pool + (size_t)pr.first * TILE, s.d_pool + (size_t)pr.second * TILE});
+      }
+    }
+    std::stable_sort(tasks.begin() + b, tasks.end(),
+                     [](const SpTask& x, const SpTask& y) { return x.npairs > y.npairs; });
+    c->sp_acc_rng[j] = {b, (int)tasks.size() - b};
+    const int db = (int)diag.size();
+    for (int si = 0; si < ns; ++si) {
+      const SubHost& s = c->subs[si];
+      if (j >= s.sp.T) continue;
+      diag.push_back(SpDiag{s.d_pool + (size_t)s.sp.tmap[(size_t)j * s.sp.Tq + j] * TILE,
+                            c->d_dinv + (size_t)si * TILE, si, j * TB});
+    }
+    c->sp_diag_rng[j] = {db, (int)diag.size() - db};
+    b = (int)tasks.size();
+    for (int si = 0; si < ns; ++si) {
+      const SubHost& s = c->subs[si];
+      if (j >= s.sp.T) continue;
+      for (int slot : s.sp.panel[j]) {
+        double* C = s.d_pool + (size_t)slot * TILE;
+        tasks.push_back(SpTask{C, (int64_t)pairs.size(), 1, 1});
+        pairs.push_back(SpPair{C, c->d_dinv + (size_t)si * TILE});
+      }
+    }
+    c->sp_panel_rng[j] = {b, (int)tasks.size() - b};
+  }
+  if ((rc = upload(c, &c->d_sp_init, init))) return rc;
+  if ((rc = upload(c, &c->d_sp_tasks, tasks))) return rc;
+  if ((rc = upload(c, &c->d_sp_pairs, pairs))) return rc;
+  if ((rc = upload(c, &c->d_sp_diag, diag))) return rc;
+  if ((rc = upload(c, &c->d_sp_panels, panels))) return rc;
+  c->n_sp_init = (int)init.size();
+  c->n_sp_panels = (int)panels.size();
+  for (auto& s : c->subs) {   // the plan's task lists live on the device now
+    decltype(s.sp.acc)().swap(s.sp.acc);
+    decltype(s.sp.panel)().swap(s.sp.panel);
+  }
+  CUDA_TRY(configure_sparse());
+  return FETI_OK;
+}
+
+int factorize_sparse(feti_ctx* c) {
+  cudaStream_t st = c->stream;
+  const int ns = (int)c->subs.size();
+  std::vector<SpSub> ss(ns);
+  for (int si = 0; si < ns; ++si) {
+    SubHost& s = c->subs[si];
+    ss[si] = SpSub{s.d_pool, s.d_tmap, s.d_perm, s.d_iperm, s.d_kptr, s.d_kind, s.d_kdata, s.d_Q,
+                   s.d_fix, s.d_U1, s.d_U2W, s.rho, s.sp.T, s.sp.Tq, (int)s.n, s.sp_r, s.sp_r, 0};
+    s.src = SRC_TILES;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->d_spsub, ss.data(), ns * sizeof(SpSub), cudaMemcpyHostToDevice, st));
+  int rc;
+  c->subdev_dirty = true;
+  if ((rc = sync_subdev(c))) return rc;
+  std::vector<int> big(ns, 1 << 30);
+  CUDA_TRY(cudaMemcpyAsync(c->d_bad, big.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaEventRecord(c->ev[0], st));
+  launch_sp_init(c->d_sp_init, c->n_sp_init, c->d_spsub, st);
+  launch_sp_scatter(c->d_spsub, ns, c->sp_max_n, st);
+  CUDA_TRY(cudaGetLastError());
+  FETI_DEBUG_SYNC(st);
+  int launches = 2;
+  for (size_t j = 0; j < c->sp_acc_rng.size(); ++j) {
+    const auto a = c->sp_acc_rng[j], d = c->sp_diag_rng[j], p = c->sp_panel_rng[j];
+    launch_sp_gemm(c->d_sp_tasks + a.first, a.second, c->d_sp_pairs, st);
+    launch_sp_potrf(c->d_sp_diag + d.first, d.second, c->d_bad, st);
+    launch_sp_gemm(c->d_sp_tasks + p.first, p.second, c->d_sp_pairs, st);
+    launches += (a.second > 0) + (d.second > 0) + (p.second > 0);
+    CUDA_TRY(cudaGetLastError());
+    FETI_DEBUG_SYNC(st);
+  }
+  CUDA_TRY(cudaEventRecord(c->ev[1], st));
+  CUDA_TRY(cudaMemcpyAsync(big.data(), c->d_bad, ns * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  c->stats.ms_factorize = ms;
+  c->stats.flops_factor_exec = c->sp_flops;
+  c->stats.launches_factorize = launches;
+  for (int si = 0; si < ns; ++si)
+    if (big[si] < (1 << 30))
+      return fail(FETI_ERR_NOT_SPD, "slot %d: non-positive pivot at permuted row %d: matrix is not SPD", si,
+                  big[si]);
+  for (auto& s : c->subs) s.factor_set = true;
+  c->tiles_fresh = true;
   return FETI_OK;
 }
 
@@ -365,9 +518,16 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   // capacity check before allocating anything large
   size_t need = 0;
   int max_M = 0;
+  if (c->sparse_factor)
+    for (size_t i = 0; i < c->subs.size(); ++i) {
+      SubHost& s = c->subs[i];
+      if (!s.sp_pattern) return fail(FETI_ERR_LIFECYCLE, "slot %zu has no sparse pattern", i);
+      sp_symbolic(s.n, s.sp_kptr.data(), s.sp_kind.data(), s.sp_iperm.data(), s.sp_r, s.smin, &s.sp);
+      need += (size_t)s.sp.ntiles * TILE * 8;
+    }
   for (auto& s : c->subs) {
     const int64_t tb = c->device_factor ? 0 : s.smin;
-    need += (size_t)(s.T - tb) * (s.T - tb + 1) / 2 * TILE * 8;   // tiles
+    if (!c->sparse_factor) need += (size_t)(s.T - tb) * (s.T - tb + 1) / 2 * TILE * 8;   // tiles
     need += (size_t)s.P * (s.T - s.smin) * TILE * 8;   // X panels
     need += (size_t)s.f_tiles() * ATILE * 8;          // F~
     max_M = std::max(max_M, s.T32 * AT);
@@ -394,8 +554,15 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     for (auto& s : c->subs) s.tbase = s.smin;
   }
   for (auto& s : c->subs) {
-    if ((rc = dev_alloc(c, (void**)&s.d_tiles, (size_t)std::max<int64_t>(s.l_tiles(), 1) * TILE * 8, false)))
+    if (c->sparse_factor) {
+      if ((rc = dev_alloc(c, (void**)&s.d_pool, (size_t)std::max<int64_t>(s.sp.ntiles, 1) * TILE * 8, false)))
+        return rc;
+      s.d_tiles = s.d_pool + (size_t)s.sp.trail_base * TILE;
+      if ((rc = upload(c, &s.d_tmap, s.sp.tmap))) return rc;
+      if ((rc = upload(c, &s.d_fix, s.sp_fix))) return rc;
+    } else if ((rc = dev_alloc(c, (void**)&s.d_tiles, (size_t)std::max<int64_t>(s.l_tiles(), 1) * TILE * 8, false))) {
       return rc;
+    }
     if ((rc = dev_alloc(c, (void**)&s.d_X, (size_t)std::max(s.P, 1) * std::max(s.T - s.smin, 1) * TILE * 8, false)))
       return rc;
     if ((rc = dev_alloc(c, (void**)&s.d_F, (size_t)std::max<int64_t>(s.f_tiles(), 1) * ATILE * 8, true)))
@@ -623,6 +790,7 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     if ((rc = dev_alloc(c, (void**)&c->d_sx, (size_t)std::max<int64_t>(voff[ns], 1) * 8, true))) return rc;
     CUDA_TRY(configure_factor(c->uniform_T));
   }
+  if (c->sparse_factor && (rc = build_sparse_tasks(c))) return rc;
   CUDA_TRY(cudaDeviceSynchronize());
   c->finalized = true;
   return FETI_OK;
@@ -726,16 +894,27 @@ int feti_assemble(feti_ctx* c) {
     if ((rc = launch_assembly(c, st, c->d_w_unpack, c->n_unpack, c->d_w_diag, c->n_diag, c->d_w_scale, c->n_scale,
                               c->d_w_chain, c->n_chain, c->d_w_syrk, c->n_syrk, sparse, &c->ev[1], &launches)))
       return rc;
+    if (c->sparse_factor) {
+      launch_sp_correct(c->d_subdev, c->d_spsub, c->d_sp_panels, c->n_sp_panels, (int)c->subs.size(),
+                        c->sp_max_T32, st);
+      launches += 2;
+      CUDA_TRY(cudaGetLastError());
+      FETI_DEBUG_SYNC(st);
+    }
+    CUDA_TRY(cudaEventRecord(c->ev[7], st));
     CUDA_TRY(cudaStreamSynchronize(st));
     float ms[5];
     for (int i = 0; i < 5; ++i) CUDA_TRY(cudaEventElapsedTime(&ms[i], c->ev[i + 1], c->ev[i + 2]));
+    float msc = 0;
+    CUDA_TRY(cudaEventElapsedTime(&msc, c->ev[6], c->ev[7]));
+    S.ms_correct = msc;
     S.ms_wait_upload = 0.0;
     S.ms_unpack = ms[0];
     S.ms_diag_inverse = ms[1];
     S.ms_block_scale = ms[2];
     S.ms_trsm = ms[3];
     S.ms_syrk = ms[4];
-    S.ms_assemble = ms[0] + ms[1] + ms[2] + ms[3] + ms[4];
+    S.ms_assemble = ms[0] + ms[1] + ms[2] + ms[3] + ms[4] + msc;
     S.factor_bytes = 0.0;
   } else {
     // host factors: H2D in wave order on the copy stream; each wave's kernels
@@ -854,10 +1033,57 @@ int feti_enable_device_factorization(feti_ctx* c) {
   return FETI_OK;
 }
 
+int feti_enable_sparse_factorization(feti_ctx* c) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (c->finalized) return fail(FETI_ERR_LIFECYCLE, "sparse factorization must be chosen before finalize");
+  if (c->device_factor) return fail(FETI_ERR_ARG, "dense device factorization is already enabled");
+  c->sparse_factor = true;
+  return FETI_OK;
+}
+
+int feti_set_sparse_pattern(feti_ctx* c, int64_t slot, int64_t n, const int64_t* indptr, const int64_t* indices,
+                            const int64_t* perm, int64_t r, const int64_t* fix) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (c->finalized) return fail(FETI_ERR_LIFECYCLE, "the sparse pattern must be set before finalize");
+  if (!c->sparse_factor) return fail(FETI_ERR_LIFECYCLE, "sparse factorization is not enabled");
+  if (slot < 0 || slot >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot out of range");
+  SubHost& s = c->subs[slot];
+  if (n != s.n) return fail(FETI_ERR_ARG, "pattern size %lld does not match the subdomain (%lld)", (long long)n,
+                            (long long)s.n);
+  if (!indptr || !indices || !perm || r < 0 || r > 8 || (r > 0 && !fix))
+    return fail(FETI_ERR_ARG, "bad sparse pattern arguments (kernel dimension must be <= 8)");
+  if (indptr[0] != 0) return fail(FETI_ERR_ARG, "pattern pointer must start at 0");
+  std::vector<int64_t> pv(perm, perm + n), ip(n, -1);
+  for (int64_t i = 0; i < n; ++i) {
+    if (pv[i] < 0 || pv[i] >= n || ip[pv[i]] >= 0) return fail(FETI_ERR_ARG, "ordering is not a permutation");
+    ip[pv[i]] = i;
+  }
+  const int64_t nnz = indptr[n];
+  for (int64_t a = 0; a < n; ++a) {
+    if (indptr[a + 1] < indptr[a]) return fail(FETI_ERR_ARG, "pattern pointer is not monotone");
+    bool diag = false;
+    for (int64_t p = indptr[a]; p < indptr[a + 1]; ++p) {
+      if (indices[p] < 0 || indices[p] >= n) return fail(FETI_ERR_ARG, "pattern column out of range");
+      diag |= indices[p] == a;
+    }
+    if (!diag) return fail(FETI_ERR_ARG, "stiffness row %lld has no diagonal entry", (long long)a);
+  }
+  for (int64_t q = 0; q < r; ++q)
+    if (fix[q] < 0 || fix[q] >= n) return fail(FETI_ERR_ARG, "fixing DOF out of range");
+  s.sp_perm = std::move(pv);
+  s.sp_iperm = std::move(ip);
+  s.sp_kptr.assign(indptr, indptr + n + 1);
+  s.sp_kind.assign(indices, indices + nnz);
+  s.sp_fix.assign(fix, fix + r);
+  s.sp_r = (int)r;
+  s.sp_pattern = true;
+  return FETI_OK;
+}
+
 int feti_set_stiffness(feti_ctx* c, int64_t slot, int64_t n, const int64_t* indptr, const int64_t* indices,
                        const double* data, int64_t nnz, const double* Q, int64_t r, double rho, const int64_t* perm) {
   if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
-  if (!c->finalized || !c->device_factor)
+  if (!c->finalized || !(c->device_factor || c->sparse_factor))
     return fail(FETI_ERR_LIFECYCLE, "set_stiffness needs a finalized context with device factorization");
   if (slot < 0 || slot >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot out of range");
   SubHost& s = c->subs[slot];
@@ -865,6 +1091,12 @@ int feti_set_stiffness(feti_ctx* c, int64_t slot, int64_t n, const int64_t* indp
                             (long long)s.n);
   if (!indptr || !indices || !data || (r > 0 && !Q) || !perm || r < 0 || r > 64 || nnz != indptr[n])
     return fail(FETI_ERR_ARG, "bad stiffness arguments");
+  if (c->sparse_factor) {
+    if ((int)r != s.sp_r) return fail(FETI_ERR_ARG, "kernel dimension differs from the sparse pattern's");
+    if (nnz != s.sp_kptr[n] || !std::equal(perm, perm + n, s.sp_perm.begin()) ||
+        !std::equal(indptr, indptr + n + 1, s.sp_kptr.begin()))
+      return fail(FETI_ERR_ARG, "stiffness pattern or ordering differs from the sparse pattern");
+  }
   CUDA_TRY(cudaSetDevice(c->device));
   int rc;
   if (!s.stiff_set) {
@@ -889,16 +1121,31 @@ int feti_set_stiffness(feti_ctx* c, int64_t slot, int64_t n, const int64_t* indp
   CUDA_TRY(cudaMemcpy(s.d_kdata, data, (size_t)nnz * 8, cudaMemcpyHostToDevice));
   if (r > 0) CUDA_TRY(cudaMemcpy(s.d_Q, Q, (size_t)(n * r) * 8, cudaMemcpyHostToDevice));
   s.rho = rho;
+  if (c->sparse_factor && r > 0) {
+    // U1 = B~ Q in sorted column order: row a = sign_a Q[dof_a]
+    const size_t rows = (size_t)s.P * TB;
+    std::vector<double> u1(rows * r, 0.0);
+    for (int64_t a = 0; a < s.m; ++a) {
+      const int64_t dof = s.sp_perm[s.r_sorted[a]];
+      for (int64_t q = 0; q < r; ++q) u1[a * r + q] = s.s_sorted[a] * Q[dof * r + q];
+    }
+    if (!s.d_U1) {
+      if ((rc = dev_alloc(c, (void**)&s.d_U1, rows * r * 8, true))) return rc;
+      if ((rc = dev_alloc(c, (void**)&s.d_U2W, rows * 2 * r * 8, true))) return rc;
+    }
+    CUDA_TRY(cudaMemcpy(s.d_U1, u1.data(), rows * r * 8, cudaMemcpyHostToDevice));
+  }
   return FETI_OK;
 }
 
 int feti_factorize(feti_ctx* c) {
   if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
-  if (!c->finalized || !c->device_factor)
+  if (!c->finalized || !(c->device_factor || c->sparse_factor))
     return fail(FETI_ERR_LIFECYCLE, "factorize needs a finalized context with device factorization");
   for (size_t i = 0; i < c->subs.size(); ++i)
     if (!c->subs[i].stiff_set) return fail(FETI_ERR_LIFECYCLE, "subdomain slot %zu has no stiffness", i);
   CUDA_TRY(cudaSetDevice(c->device));
+  if (c->sparse_factor) return factorize_sparse(c);
   cudaStream_t st = c->stream;
   const int ns = (int)c->subs.size();
   std::vector<FactorSub> fs(ns);
@@ -941,7 +1188,7 @@ int feti_factorize(feti_ctx* c) {
 int feti_solve_many(feti_ctx* c, int64_t nslots, const int64_t* slots, const double* b, double* x) {
   if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
   if (!c->device_factor || !c->assembled)
-    return fail(FETI_ERR_LIFECYCLE, "solve needs an assembled context with device factorization");
+    return fail(FETI_ERR_LIFECYCLE, "solve needs an assembled context with dense device factorization");
   if (nslots <= 0 || nslots > (int64_t)c->subs.size() || !slots || !b || !x) return fail(FETI_ERR_ARG, "bad solve arguments");
   if (solve_smem(c->uniform_T) > 227 * 1024) return fail(FETI_ERR_CAPACITY, "subdomain too large for the solve sweep");
   CUDA_TRY(cudaSetDevice(c->device));
@@ -965,6 +1212,8 @@ int feti_solve_many(feti_ctx* c, int64_t nslots, const int64_t* slots, const dou
 }
 
 static int implicit_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st) {
+  if (c->sparse_factor)
+    return fail(FETI_ERR_ARG, "implicit apply is not available with the sparse-factor route");
   if (c->impl_max_blocks < 0)
     return fail(FETI_ERR_CAPACITY, "implicit apply: subdomain too large for the single-CTA sweep");
   launch_implicit_apply(c->d_subdev, (int)c->subs.size(), c->impl_max_blocks, c->d_impl_off, d_p, c->d_impl_part,

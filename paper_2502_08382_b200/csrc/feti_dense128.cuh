@@ -71,4 +71,60 @@ __device__ __forceinline__ void invert_lower_128(const double* __restrict__ sL, 
   }
 }
 
+
+// In-place Cholesky of the 128x128 tile (col-major swizzled, lower part read)
+// and its inverse: tile <- L (upper part zeroed), D <- inv(L) (same layout).
+// A non-positive pivot is reported as atomicMin(bad, rowbase + j) and
+// replaced by 1 so the sweep completes.  smem: (2 * 8256 + 3 * 1024) doubles.
+// Must be called by all 256 threads of the CTA.
+__device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, double* __restrict__ D,
+                                                 int* __restrict__ bad, int rowbase, double* __restrict__ smem) {
+  double* sL = smem;              // 8256 packed lower
+  double* sY = smem + 8256;       // 8256 packed lower
+  double* sT = smem + 2 * 8256;   // 3072 scratch
+  __shared__ double piv;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < TILE; idx += 256) {
+    const int jl = idx >> 7;
+    const int il = (idx & 127) ^ ((jl & 3) << 2);
+    if (il >= jl) sL[plo(il, jl)] = tile[idx];
+  }
+  __syncthreads();
+  for (int j = 0; j < TB; ++j) {
+    if (tid == 0) {
+      double d = sL[plo(j, j)];
+      if (!(d > 0.0)) {
+        atomicMin(bad, rowbase + j);   // first non-positive pivot (permuted row)
+        d = 1.0;
+      }
+      piv = sqrt(d);
+      sL[plo(j, j)] = piv;
+    }
+    __syncthreads();
+    const double dj = piv;
+    for (int i = j + 1 + tid; i < TB; i += 256) sL[plo(i, j)] /= dj;
+    __syncthreads();
+    const int w = TB - 1 - j;                 // trailing size
+    for (int q = tid; q < w * w; q += 256) {
+      const int ii = q / w, ll = q % w;
+      if (ll <= ii) {
+        const int i = j + 1 + ii, l = j + 1 + ll;
+        sL[plo(i, l)] = fma(-sL[plo(i, j)], sL[plo(l, j)], sL[plo(i, l)]);
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < TILE; idx += 256) {
+    const int jl = idx >> 7;
+    const int il = (idx & 127) ^ ((jl & 3) << 2);
+    tile[idx] = (il >= jl) ? sL[plo(il, jl)] : 0.0;
+  }
+  invert_lower_128(sL, sY, sT);
+  for (int idx = tid; idx < TILE; idx += 256) {
+    const int jl = idx >> 7;
+    const int il = (idx & 127) ^ ((jl & 3) << 2);
+    D[idx] = (il >= jl) ? sY[plo(il, jl)] : 0.0;
+  }
+}
+
 }  // namespace feti

@@ -83,56 +83,8 @@ __global__ void __launch_bounds__(128) kreg_scatter_kernel(const SubDev* __restr
 __global__ void __launch_bounds__(256) potrf_diag_kernel(const SubDev* __restrict__ subs, double* __restrict__ dinv,
                                                          int* __restrict__ bad, int k) {
   extern __shared__ double fsm[];
-  double* sL = fsm;              // 8256 packed lower
-  double* sY = fsm + 8256;       // 8256 packed lower
-  double* sT = fsm + 2 * 8256;   // 3072 scratch
-  __shared__ double piv;
   const int sub = blockIdx.x;
-  const SubDev& S = subs[sub];
-  double* tile = tile_ptr(S, k, k);
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < TILE; idx += 256) {
-    const int jl = idx >> 7;
-    const int il = (idx & 127) ^ ((jl & 3) << 2);
-    if (il >= jl) sL[plo(il, jl)] = tile[idx];
-  }
-  __syncthreads();
-  for (int j = 0; j < TB; ++j) {
-    if (tid == 0) {
-      double d = sL[plo(j, j)];
-      if (!(d > 0.0)) {
-        atomicMin(bad + sub, k * TB + j);   // first non-positive pivot (permuted row)
-        d = 1.0;
-      }
-      piv = sqrt(d);
-      sL[plo(j, j)] = piv;
-    }
-    __syncthreads();
-    const double dj = piv;
-    for (int i = j + 1 + tid; i < TB; i += 256) sL[plo(i, j)] /= dj;
-    __syncthreads();
-    const int w = TB - 1 - j;                 // trailing size
-    for (int q = tid; q < w * w; q += 256) {
-      const int ii = q / w, ll = q % w;
-      if (ll <= ii) {
-        const int i = j + 1 + ii, l = j + 1 + ll;
-        sL[plo(i, l)] = fma(-sL[plo(i, j)], sL[plo(l, j)], sL[plo(i, l)]);
-      }
-    }
-    __syncthreads();
-  }
-  for (int idx = tid; idx < TILE; idx += 256) {
-    const int jl = idx >> 7;
-    const int il = (idx & 127) ^ ((jl & 3) << 2);
-    tile[idx] = (il >= jl) ? sL[plo(il, jl)] : 0.0;
-  }
-  invert_lower_128(sL, sY, sT);
-  double* D = dinv + (size_t)sub * TILE;
-  for (int idx = tid; idx < TILE; idx += 256) {
-    const int jl = idx >> 7;
-    const int il = (idx & 127) ^ ((jl & 3) << 2);
-    D[idx] = (il >= jl) ? sY[plo(il, jl)] : 0.0;
-  }
+  potrf_invert_128(tile_ptr(subs[sub], k, k), dinv + (size_t)sub * TILE, bad + sub, k * TB, fsm);
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,395 @@
+// Sparse-factor route on the device (SURVEY.md §7 hard part 4, §8f row 2;
+// host side: paper_2502_08382_b200/sparse_route.py).
+//
+// The reference's K_reg = K + rho Q Q^T (regularize, sparse.py:427-454) is
+// dense, so its factor is a full triangle (4.4 GB per config-5 subdomain).
+// Here the factor is of K_s = K + rho E E^T (E = fixing DOFs): it keeps K's
+// sparsity, and is stored as a pool of 128x128 tiles (the assembly's
+// col-major swizzled format) covering the block pattern of L after block
+// fill.  With every constrained DOF ordered last, the pool's trailing
+// triangle [smin, T) x [smin, T) is dense and laid out exactly as the
+// assembly expects, so the unchanged TRSM/SYRK kernels compute
+// F_s = B K_s^-1 B^T from it.
+//
+// Factorization (left-looking, one block column j at a time, all subdomains
+// batched in each launch):
+//   acc:    L_ij -= sum_k L_ik L_jk^T   over k in rows(i) ∩ rows(j), k < j
+//   potrf:  L_jj = chol(A_jj), D = inv(L_jj)
+//   panel:  L_ij = A_ij D^T              i in struct(j)
+// An extra block row holding (P Q)^T is factored along: its tiles become
+// y^T = (L^-1 P Q)^T, and a final accumulation leaves -y^T y in tile (T, T).
+//
+// Correction (after the assembly):  with U1 = B Q, U2 = B K_s^-1 Q = X^T y_b
+// (X = L^-1 P B^T lives in the interface rows only) and C = y^T y + I/rho,
+//   F~ = F_s - U1 U2^T - U2 U1^T + U1 C U1^T = F_s + U1 W^T - U2 U1^T,
+//   W = U1 C - U2,
+// applied in place to the packed 32x32 apply tiles.
+#include <algorithm>
+
+#include "feti_common.cuh"
+#include "feti_dense128.cuh"
+#include "feti_sparse.h"
+
+namespace feti {
+
+// ---------------------------------------------------------------------------
+// pool initialisation: zero tiles, identity on padded diagonal entries, and
+// the (P Q)^T block row
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) sp_init_kernel(const SpInit* __restrict__ work, const SpSub* __restrict__ ss) {
+  const SpInit w = work[blockIdx.x];
+  const SpSub& S = ss[w.sub];
+  double* tile = w.tile;
+  const int n = S.n, r = S.r;
+  const bool qrow = (w.K == S.T);
+  for (int idx = threadIdx.x; idx < TILE; idx += 256) {
+    const int jl = idx >> 7;
+    const int il = (idx & 127) ^ ((jl & 3) << 2);
+    const int j = w.L * TB + jl;
+    double v = 0.0;
+    if (qrow) {
+      if (w.L < S.T && il < r && j < n) v = S.Q[S.perm[j] * r + il];
+    } else if (w.K == w.L && il == jl && j >= n) {
+      v = 1.0;   // identity padding keeps the last diagonal block SPD
+    }
+    tile[idx] = v;
+  }
+}
+
+// K_s entries into the lower block triangle of P K_s P^T: one warp per
+// original row a; the fixing shift rho lands on the diagonal entry.
+__global__ void __launch_bounds__(256) sp_scatter_kernel(const SpSub* __restrict__ ss) {
+  const SpSub& S = ss[blockIdx.y];
+  const int a = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (a >= S.n) return;
+  const int lane = threadIdx.x & 31;
+  bool fixed = false;
+  for (int f = 0; f < S.nfix; ++f) fixed |= (S.fix[f] == a);
+  const int64_t pa = S.iperm[a];
+  for (int64_t p = S.kptr[a] + lane; p < S.kptr[a + 1]; p += 32) {
+    const int64_t b = S.kind[p];
+    const int64_t pb = S.iperm[b];
+    if (pa < pb) continue;
+    double v = S.kdata[p];
+    if (fixed && b == a) v += S.rho;
+    const int slot = S.tmap[(pa / TB) * S.Tq + pb / TB];
+    double* tile = S.pool + (size_t)slot * TILE;
+    tile[swz((int)(pb % TB), (int)(pa % TB))] += v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tile GEMM tasks on the DMMA pipe (8 consumer warps, 1 bulk-copy producer)
+// ---------------------------------------------------------------------------
+constexpr int SG_STAGES = 3;
+constexpr int SG_THREADS = 288;
+
+__device__ __forceinline__ void sg_mma_slice(const double* __restrict__ a_s, const double* __restrict__ b_s,
+                                             double (&acc)[8][4][2], int wm, int wn, int g, int t) {
+#pragma unroll
+  for (int kb = 0; kb < KS / 4; ++kb) {
+    const int kr = kb * 4 + t;
+    double bf[4];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) bf[ni] = b_s[swz(kr, wn * 32 + ni * 8 + g)];
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const double af = a_s[swz(kr, wm * 64 + mi * 8 + g)];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(SG_THREADS, 1) sp_gemm_kernel(const SpTask* __restrict__ tasks,
+                                                                const SpPair* __restrict__ pairs) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);
+  double* sB = sA + SG_STAGES * SLICE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + SG_STAGES * SLICE);
+  uint64_t* empty = full + SG_STAGES;
+  const SpTask tk = tasks[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < SG_STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 8);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int nsl = tk.npairs * (TB / KS);
+  if (warp == 8) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int sl = 0; sl < nsl; ++sl) {
+        const SpPair pr = pairs[tk.pair0 + sl / (TB / KS)];
+        const int so = (sl % (TB / KS)) * SLICE;
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], 2 * SLICE * 8);
+        bulk_g2s(sA + stage * SLICE, pr.A + so, SLICE * 8, &full[stage]);
+        bulk_g2s(sB + stage * SLICE, pr.B + so, SLICE * 8, &full[stage]);
+        if (++stage == SG_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  const int wm = warp >> 2, wn = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int sl = 0; sl < nsl; ++sl) {
+    mbar_wait(&full[stage], phase);
+    sg_mma_slice(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
+    fence_proxy_async_shared();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == SG_STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  // every slice of a panel task's A (= C) was consumed above: in-place is safe
+  double* Ct = tk.C;
+  const bool panel = tk.flags & 1;
+#pragma unroll
+  for (int mi = 0; mi < 8; ++mi) {
+    const int m = wm * 64 + mi * 8 + g;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int nn = wn * 32 + ni * 8 + 2 * t;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double* cp = Ct + swz(nn + e, m);
+        if (panel)
+          *cp = acc[mi][ni][e];
+        else
+          *cp -= acc[mi][ni][e];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) sp_potrf_kernel(const SpDiag* __restrict__ d, int* __restrict__ bad) {
+  extern __shared__ double psm[];
+  const SpDiag w = d[blockIdx.x];
+  potrf_invert_128(w.C, w.D, bad + w.sub, w.rowbase, psm);
+}
+
+// ---------------------------------------------------------------------------
+// correction
+// ---------------------------------------------------------------------------
+constexpr int MAXR = 8;
+
+// one CTA per (sub, panel c): U2[a] = sum_rows X[row][a] y[row], then
+// W[a] = C U1[a] - U2[a] with C = y^T y + I/rho = -tile(T,T) + I/rho
+__global__ void __launch_bounds__(TB) sp_u2_kernel(const SubDev* __restrict__ subs, const SpSub* __restrict__ ss,
+                                                   const int2* __restrict__ panels) {
+  const int2 pc = panels[blockIdx.x];
+  const SubDev& S = subs[pc.x];
+  const SpSub& Q = ss[pc.x];
+  const int c = pc.y, col = threadIdx.x, r = Q.r;
+  const int a = c * TB + col;
+  const int T = Q.T;
+  __shared__ double Cm[MAXR * MAXR];
+  const double* cq = Q.pool + (size_t)Q.tmap[T * Q.Tq + T] * TILE;
+  if (col < r * r) {
+    const int q = col / r, q2 = col % r;
+    Cm[col] = -cq[swz(q2, q)] + (q == q2 ? 1.0 / Q.rho : 0.0);
+  }
+  __syncthreads();
+  double acc[MAXR];
+#pragma unroll
+  for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
+  const int r0 = (S.panel_minrow[c] / TB) * TB;
+  for (int kb = r0 / TB; kb < T; ++kb) {
+    const double* yt = Q.pool + (size_t)Q.tmap[T * Q.Tq + kb] * TILE;
+    for (int il = 0; il < TB; ++il) {
+      const int row = kb * TB + il;
+      const double x = xrow_ptr(S, c, row)[col ^ ((row & 3) << 2)];
+#pragma unroll
+      for (int q = 0; q < MAXR; ++q)
+        if (q < r) acc[q] = fma(x, yt[swz(il, q)], acc[q]);
+    }
+  }
+  if (a >= S.m) {
+#pragma unroll
+    for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
+  }
+  double* out = Q.U2W + (size_t)a * 2 * r;
+  const double* u1 = Q.U1 + (size_t)a * r;
+  for (int q = 0; q < r; ++q) {
+    double w = -acc[q];
+    for (int q2 = 0; q2 < r; ++q2) w = fma(Cm[q * r + q2], u1[q2], w);
+    out[q] = acc[q];
+    out[r + q] = (a < S.m) ? w : 0.0;
+  }
+}
+
+// F[a][b] += U1[a] . W[b] - U2[a] . U1[b] over every stored apply tile
+// (grid: tile row ti x subdomain; diagonal tiles are stored full)
+__global__ void __launch_bounds__(256) sp_correct_kernel(const SubDev* __restrict__ subs,
+                                                         const SpSub* __restrict__ ss) {
+  const SubDev& S = subs[blockIdx.y];
+  const SpSub& Q = ss[blockIdx.y];
+  const int ti = blockIdx.x, T32 = S.T32, r = Q.r;
+  if (ti >= T32 || r == 0) return;
+  __shared__ double u1a[AT * MAXR], u2a[AT * MAXR];
+  for (int e = threadIdx.x; e < AT * r; e += 256) {
+    const int a = ti * AT + e / r, q = e % r;
+    u1a[e] = Q.U1[(size_t)a * r + q];
+    u2a[e] = Q.U2W[(size_t)a * 2 * r + q];
+  }
+  __syncthreads();
+  for (int tj = ti; tj < T32; ++tj) {
+    double* F = S.F + apply_tile_index(ti, tj, T32) * ATILE;
+    for (int e = threadIdx.x; e < ATILE; e += 256) {
+      const int al = e / AT, b = tj * AT + e % AT;
+      const double* u1b = Q.U1 + (size_t)b * r;
+      const double* wb = Q.U2W + (size_t)b * 2 * r + r;
+      double v = F[e];
+      for (int q = 0; q < r; ++q) v += u1a[al * r + q] * wb[q] - u2a[al * r + q] * u1b[q];
+      F[e] = v;
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// host: block symbolic factorization and task lists
+// ---------------------------------------------------------------------------
+void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* iperm, int r, int smin,
+                 SpPlan* out) {
+  SpPlan& P = *out;
+  const int T = (int)((n + TB - 1) / TB);
+  const int Tq = T + (r > 0 ? 1 : 0);
+  P.T = T;
+  P.Tq = Tq;
+  P.smin = smin = std::min(std::max(smin, 0), T);
+  // cs[j][i] = 1: block (i, j), i > j, of L is structurally nonzero
+  std::vector<std::vector<char>> cs(T, std::vector<char>(Tq, 0));
+  for (int64_t a = 0; a < n; ++a)
+    for (int64_t p = indptr[a]; p < indptr[a + 1]; ++p) {
+      int I = (int)(iperm[a] / TB), J = (int)(iperm[indices[p]] / TB);
+      if (I < J) std::swap(I, J);
+      if (I > J) cs[J][I] = 1;
+    }
+  for (int J = smin; J < T; ++J)
+    for (int I = J + 1; I < T; ++I) cs[J][I] = 1;     // dense interface block
+  if (r > 0)
+    for (int J = 0; J < T; ++J) cs[J][T] = 1;         // (P Q)^T row: y is dense
+  // block fill along the elimination tree: struct(parent) >= struct(k) \ {parent}
+  for (int k = 0; k < T; ++k) {
+    int par = -1;
+    for (int I = k + 1; I < Tq; ++I)
+      if (cs[k][I]) {
+        par = I;
+        break;
+      }
+    if (par < 0 || par >= T) continue;
+    for (int I = par + 1; I < Tq; ++I)
+      if (cs[k][I]) cs[par][I] = 1;
+  }
+  // slots: everything outside the trailing triangle first, then the trailing
+  // triangle in the assembly's tri_index order
+  P.tmap.assign((size_t)Tq * Tq, -1);
+  auto stored = [&](int I, int J) { return (I == J && J < T) || (J < T && I > J && cs[J][I]) || (I == T && J == T && r > 0); };
+  auto trailing = [&](int I, int J) { return I < T && J >= smin; };
+  int64_t ns = 0;
+  for (int J = 0; J < Tq; ++J)
+    for (int I = J; I < Tq; ++I)
+      if (stored(I, J) && !trailing(I, J)) P.tmap[(size_t)I * Tq + J] = (int)ns++;
+  P.trail_base = ns;
+  for (int I = smin; I < T; ++I)
+    for (int J = smin; J <= I; ++J) P.tmap[(size_t)I * Tq + J] = (int)(ns + tri_index(I - smin, J - smin));
+  ns += (int64_t)(T - smin) * (T - smin + 1) / 2;
+  P.ntiles = ns;
+  // row structures (ascending)
+  std::vector<std::vector<int>> rows(Tq);
+  for (int J = 0; J < T; ++J)
+    for (int I = J + 1; I < Tq; ++I)
+      if (cs[J][I]) rows[I].push_back(J);
+  const double tf = 2.0 * TB * TB * TB;
+  P.acc.assign(Tq, {});
+  P.panel.assign(Tq, {});
+  for (int j = 0; j < Tq; ++j) {
+    std::vector<int> targets;
+    targets.push_back(j);
+    if (j < T)
+      for (int I = j + 1; I < Tq; ++I)
+        if (cs[j][I]) targets.push_back(I);
+    for (int i : targets) {
+      std::vector<std::pair<int, int>> pr;
+      const std::vector<int>& ri = rows[i];
+      const std::vector<int>& rj = rows[j];
+      size_t u = 0, v = 0;
+      while (u < ri.size() && v < rj.size()) {
+        if (ri[u] < rj[v]) {
+          ++u;
+        } else if (rj[v] < ri[u]) {
+          ++v;
+        } else {
+          const int k = ri[u];
+          pr.emplace_back(P.tmap[(size_t)i * Tq + k], P.tmap[(size_t)j * Tq + k]);
+          ++u;
+          ++v;
+        }
+      }
+      if (!pr.empty()) {
+        P.flops_exec += tf * pr.size();
+        P.acc[j].emplace_back(P.tmap[(size_t)i * Tq + j], std::move(pr));
+      }
+      if (i != j) {
+        P.panel[j].push_back(P.tmap[(size_t)i * Tq + j]);
+        P.flops_exec += tf;
+      }
+    }
+    if (j < T) P.flops_exec += (double)TB * TB * TB / 3.0 + (double)TB * TB * TB / 3.0;  // potrf + inverse
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static size_t sg_smem() { return 2 * SG_STAGES * SLICE * sizeof(double) + 8 * 2 * SG_STAGES; }
+static size_t sp_potrf_smem() { return (2 * 8256 + 3 * 1024) * sizeof(double); }
+
+cudaError_t configure_sparse() {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(sp_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem())))
+    return e;
+  return cudaFuncSetAttribute(sp_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_potrf_smem());
+}
+
+void launch_sp_init(const SpInit* w, int nw, const SpSub* ss, cudaStream_t st) {
+  if (nw > 0) sp_init_kernel<<<nw, 256, 0, st>>>(w, ss);
+}
+
+void launch_sp_scatter(const SpSub* ss, int nsub, int max_n, cudaStream_t st) {
+  if (nsub > 0 && max_n > 0) sp_scatter_kernel<<<dim3((max_n + 7) / 8, nsub), 256, 0, st>>>(ss);
+}
+
+void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st) {
+  if (ntasks > 0) sp_gemm_kernel<<<ntasks, SG_THREADS, sg_smem(), st>>>(tasks, pairs);
+}
+
+void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st) {
+  if (nd > 0) sp_potrf_kernel<<<nd, 256, sp_potrf_smem(), st>>>(d, bad);
+}
+
+void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int nsub, int max_T32,
+                       cudaStream_t st) {
+  if (npanels > 0) sp_u2_kernel<<<npanels, TB, 0, st>>>(subs, ss, panels);
+  if (nsub > 0 && max_T32 > 0) sp_correct_kernel<<<dim3(max_T32, nsub), 256, 0, st>>>(subs, ss);
+}
+
+}  // namespace feti

@@ -1,0 +1,86 @@
+// Sparse-factor route: block-sparse device Cholesky of K_s = K + rho E E^T
+// plus the rank-2r correction that recovers the reference's F~ (see
+// feti_sparse.cu and paper_2502_08382_b200/sparse_route.py).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include <utility>
+#include <vector>
+
+#include "feti_common.cuh"
+
+namespace feti {
+
+// Per-subdomain data of the block-sparse factor (device pointers).
+struct SpSub {
+  double* pool;             // every stored 128x128 tile of the subdomain
+  const int* tmap;          // Tq x Tq: tile (K, L) -> slot in pool, -1 if structurally zero
+  const int64_t* perm;      // permuted position -> original DOF
+  const int64_t* iperm;     // original DOF -> permuted position
+  const int64_t* kptr;      // K (unregularized) CSR, original numbering
+  const int64_t* kind;
+  const double* kdata;
+  const double* Q;          // n x r kernel basis, row-major
+  const int64_t* fix;       // fixing DOFs (original numbering), nfix = r
+  const double* U1;         // P*128 x r: sign_a * Q[dof_a], sorted column order
+  double* U2W;              // P*128 x 2r: U2 = X^T y_b, then W = C U1 - U2
+  double rho;
+  int T;                    // block rows of K_s (the Q block row is T when r > 0)
+  int Tq;                   // T + (r > 0)
+  int n, r, nfix, pad_;
+};
+
+// One tile of the left-looking factorization:
+//   accumulate (flags 0):  C -= sum_p A_p B_p^T
+//   panel      (flags 1):  C  = C B^T  (B = inv(L_jj), one pair (C, B))
+struct SpPair {
+  const double* A;
+  const double* B;
+};
+struct SpTask {
+  double* C;
+  int64_t pair0;
+  int npairs;
+  int flags;
+};
+struct SpDiag {
+  double* C;       // tile (j, j): A_jj in, L_jj out
+  double* D;       // inv(L_jj) scratch
+  int sub;
+  int rowbase;     // j * 128 (for the pivot report)
+};
+struct SpInit {
+  double* tile;
+  int K, L, sub, pad_;
+};
+
+// Host-side block symbolic factorization of one subdomain (the sparse
+// analogue of symbolic_factorize, sparse.py:340-415, at 128-row tiles).
+struct SpPlan {
+  int T = 0, Tq = 0, smin = 0;
+  int64_t ntiles = 0;                 // tiles in the pool
+  int64_t trail_base = 0;             // slot of tile (smin, smin); the
+                                      // trailing triangle follows in tri_index order
+  std::vector<int> tmap;              // Tq x Tq -> slot or -1
+  // per block column j in [0, Tq): accumulation targets (C slot, (A, B) slot pairs)
+  std::vector<std::vector<std::pair<int, std::vector<std::pair<int, int>>>>> acc;
+  std::vector<std::vector<int>> panel;  // per column j < T: slots of L_ij, i in struct(j)
+  double flops_exec = 0.0;            // tile flops the factorization executes
+};
+// indptr/indices: symmetric pattern of K (original numbering); iperm: DOF ->
+// position; r: kernel dimension (adds the (P Q)^T block row T when > 0);
+// smin: first block row of the dense trailing triangle.
+void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* iperm, int r, int smin,
+                 SpPlan* out);
+
+cudaError_t configure_sparse();
+void launch_sp_init(const SpInit* w, int nw, const SpSub* ss, cudaStream_t st);
+void launch_sp_scatter(const SpSub* ss, int nsub, int max_n, cudaStream_t st);
+void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st);
+void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st);
+// after the assembly: U2/W per (sub, panel), then the rank-2r update of F~
+void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int nsub, int max_T32,
+                       cudaStream_t st);
+
+}  // namespace feti

@@ -32,6 +32,7 @@ import numpy as np
 
 from . import _lib
 from . import factor as fct
+from . import sparse_route as spr
 
 STRATEGIES = ("implicit", "explicit", "schur_oracle")
 PATHS = ("trsm", "syrk")
@@ -131,7 +132,7 @@ def _constraint_rows(sc, n):
 
 class _Sub:
     __slots__ = ("index", "n", "m", "gids", "bcol", "bval", "perm", "iperm", "slot", "values", "pinned",
-                 "cluster")
+                 "cluster", "fix", "solver")
 
 
 class DualOperator:
@@ -156,6 +157,11 @@ class DualOperator:
       ``kernels[i]`` and factored on the GPU (DMMA blocked Cholesky); the
       factor never crosses PCIe.  With the reference's dense K_reg the RCM
       ordering is the reversed natural order, which device mode uses.
+      ``"sparse"``: the sparse-factor route (sparse_route.py): K_s = K +
+      rho E E^T with fixing DOFs E is factored on the GPU into block-sparse
+      tiles (constrained DOFs last, interior onion-ordered) and the exact
+      rank-2r correction recovers the reference's F~_i; the dense K_reg is
+      never formed, so ``matrices`` may be shape-only stand-ins.
     """
 
     def __init__(self, matrices, constraints, layout, config: DualOpConfig, pool=None, workers: int = 1,
@@ -183,13 +189,13 @@ class DualOperator:
         self.pinned = bool(pinned)
         self.device = device
         self.perms = perms
-        if factorization not in ("host", "device"):
-            raise ValueError("factorization must be 'host' or 'device'")
+        if factorization not in ("host", "device", "sparse"):
+            raise ValueError("factorization must be 'host', 'device' or 'sparse'")
         self.factorization = factorization
         self.stiffness = None if stiffness is None else list(stiffness)
         self.kernels = None if kernels is None else list(kernels)
-        if factorization == "device" and (self.stiffness is None or self.kernels is None):
-            raise ValueError("device factorization needs stiffness= and kernels= per subdomain")
+        if factorization in ("device", "sparse") and (self.stiffness is None or self.kernels is None):
+            raise ValueError(f"{factorization} factorization needs stiffness= and kernels= per subdomain")
         self.owned = (list(range(self.n_subdomains)) if subdomains is None
                       else sorted(int(s) for s in subdomains))
 
@@ -287,6 +293,11 @@ class DualOperator:
                 sub.perm = np.ascontiguousarray(self.perms[i], dtype=np.int64)
                 if sub.perm.shape != (sub.n,) or not np.array_equal(np.sort(sub.perm), np.arange(sub.n)):
                     raise ValueError(f"subdomain {i}: explicit ordering is not a permutation")
+            elif self.factorization == "sparse":
+                n, ip, ix, _ = fct.csr_arrays(self.stiffness[i])
+                if n != sub.n:
+                    raise ValueError("stiffness size does not match the subdomain")
+                sub.perm = spr.onion_interface_last(n, ip, ix, sub.bcol)
             elif self.factorization == "device":
                 base = np.arange(sub.n - 1, -1, -1, dtype=np.int64)   # RCM of the dense K_reg
                 if self.ordering == "rcm":
@@ -302,6 +313,10 @@ class DualOperator:
             sub.iperm = fct.inverse_permutation(sub.perm)
             sub.values = None
             sub.pinned = None
+            sub.solver = None
+            sub.fix = None
+            if self.factorization == "sparse":
+                sub.fix = spr.fixing_dofs(self._kernel_basis(i, sub.n))
             return sub
 
         subs = self._map(symbolic, order)
@@ -323,6 +338,15 @@ class DualOperator:
                     f"pool of {self.pool.capacity} bytes cannot hold the {need}-byte device operator")
         if self.factorization == "device":
             _call(self._lib.feti_enable_device_factorization(ctx))
+        if self.factorization == "sparse":
+            _call(self._lib.feti_enable_sparse_factorization(ctx))
+            for sub in subs:
+                n, ip, ix, _ = fct.csr_arrays(self.stiffness[sub.index])
+                ip = np.ascontiguousarray(ip, np.int64)
+                ix = np.ascontiguousarray(ix, np.int64)
+                fix = np.ascontiguousarray(sub.fix, np.int64)
+                _call(self._lib.feti_set_sparse_pattern(ctx, sub.slot, n, _lib.i64ptr(ip), _lib.i64ptr(ix),
+                                                        _lib.i64ptr(sub.perm), fix.shape[0], _lib.i64ptr(fix)))
         _call(self._lib.feti_finalize(ctx, self.n_multipliers))
         st = self.stats()
         self.persistent_bytes = int(st["bytes_persistent"])
@@ -359,7 +383,7 @@ class DualOperator:
             if len(matrices) != self.n_subdomains:
                 raise ValueError("one stiffness matrix per subdomain required")
             self.matrices = list(matrices)
-        if self.factorization == "device":
+        if self.factorization in ("device", "sparse"):
             if stiffness is not None:
                 self.stiffness = list(stiffness)
             if kernels is not None:
@@ -385,6 +409,14 @@ class DualOperator:
         self.timings = {"host_factorization_s": t1 - t0, "upload_and_assembly_s": t2 - t1}
         self.numeric_count += len(done)
 
+    def _kernel_basis(self, index: int, n: int) -> np.ndarray:
+        """Orthonormal kernel basis as regularize takes it (np.linalg.qr, sparse.py:445-449)."""
+        kern = np.asarray(self.kernels[index], dtype=np.float64).reshape(n, -1)
+        if kern.shape[1] == 0:
+            return np.zeros((n, 0))
+        q, _ = np.linalg.qr(kern)
+        return np.ascontiguousarray(q)
+
     def _preprocess_device(self) -> None:
         import time
 
@@ -393,8 +425,8 @@ class DualOperator:
             n, ip, ix, dt = fct.csr_arrays(self.stiffness[sub.index])
             if n != sub.n:
                 raise ValueError("stiffness size does not match the subdomain")
-            q, _ = np.linalg.qr(np.asarray(self.kernels[sub.index], dtype=np.float64).reshape(n, -1))
-            q = np.ascontiguousarray(q)
+            q = self._kernel_basis(sub.index, n)
+            sub.solver = None
             rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ip))
             rho = float(dt[rows == ix].sum()) / n                     # trace(K)/n (sparse.py:450)
             ip, ix, dt = (np.ascontiguousarray(ip, np.int64), np.ascontiguousarray(ix, np.int64),
@@ -508,6 +540,12 @@ class DualOperator:
         if not self.step_ready:
             raise LifecycleError("solve_local before preprocess")
         sub = self._subs[int(index)]
+        if self.factorization == "sparse":
+            x = self._sparse_solver(sub).solve(rhs)
+            if out is not None:
+                out[:] = x
+                return out
+            return x
         if self.factorization == "device":
             x = self.solve_local_many([index], [rhs])[0]
             if out is not None:
@@ -521,6 +559,8 @@ class DualOperator:
         if not self.step_ready:
             raise LifecycleError("solve_local before preprocess")
         subs = [self._subs[int(i)] for i in indices]
+        if self.factorization == "sparse":
+            return [self._sparse_solver(s).solve(r) for s, r in zip(subs, rhs_list)]
         if self.factorization != "device":
             return [fct.solve_packed(s.values, s.perm, r) for s, r in zip(subs, rhs_list)]
         slots = np.array([s.slot for s in subs], dtype=np.int64)
@@ -533,6 +573,14 @@ class DualOperator:
             out.append(x[off:off + s.n].copy())
             off += s.n
         return out
+
+    def _sparse_solver(self, sub):
+        """Host K_reg^-1 through a sparse LU of K_s (solve_local is off the
+        explicit hot path; assemble_dual_system/recover_solution call it)."""
+        if sub.solver is None:
+            sub.solver = spr.HostSparseSolver(self.stiffness[sub.index], self._kernel_basis(sub.index, sub.n),
+                                              sub.fix)
+        return sub.solver
 
     def local_operator(self, index: int) -> np.ndarray:
         """Host copy of F~_i: m x m, upper triangle, strictly lower = 0."""

@@ -115,3 +115,36 @@ def test_spd_violation_reported():
     a = inputs.DenseSym(-np.eye(4))
     with pytest.raises(fct.SpdError, match="permuted row 0"):
         fct.numeric_factorize_dense(a, np.arange(4))
+
+
+@pytest.mark.parametrize("case", ["elast2d_4x2", "heat3d_4x2", "elast3d_4x2"])
+def test_sparse_route_host_pieces(case):
+    """Ordering (constrained DOFs last), fixing DOFs (K_s SPD) and the host
+    solve_local of the sparse-factor route against the reference's F~_i."""
+    from conftest import load_golden
+    from oracle import feti_oracle as ora
+    from paper_2502_08382_b200 import inputs
+    from paper_2502_08382_b200 import sparse_route as spr
+
+    g = load_golden(case)
+    for s in range(int(g["n_sub"])):
+        ip, ix, dt = g[f"s{s}_k_indptr"], g[f"s{s}_k_indices"], g[f"s{s}_k_data"]
+        n = ip.shape[0] - 1
+        bcol, bval = g[f"s{s}_bcol"], g[f"s{s}_bval"]
+        perm = spr.onion_interface_last(n, ip, ix, bcol)
+        assert np.array_equal(np.sort(perm), np.arange(n))
+        iface = np.unique(bcol)
+        assert np.array_equal(perm[n - iface.size:], iface)
+        q, _ = np.linalg.qr(g[f"s{s}_kernel"])
+        fix = spr.fixing_dofs(q)
+        assert fix.shape == (q.shape[1],)
+        assert np.linalg.matrix_rank(q[fix]) == q.shape[1]
+        k = inputs.Csr((n, n), ip, ix, dt)
+        dense = k.to_dense()
+        dense[fix, fix] += spr.regularization_shift(ip, ix, dt, n)
+        assert np.linalg.eigvalsh(dense).min() > 0.0
+        f = ora.fmatrix_via_solver(spr.HostSparseSolver(k, q, fix), n, bcol, bval)
+        m = f.shape[0]
+        ref = np.zeros((m, m))
+        ref[np.triu_indices(m)] = g[f"s{s}_F_upper"]
+        assert np.linalg.norm(np.triu(f) - ref) <= 1e-12 * np.linalg.norm(ref)

@@ -119,3 +119,18 @@ def test_pcpg_iteration_count_sensitivity():
             assert counts == {ref_it}
         else:
             assert counts <= {ref_it, ref_it + 1} and len(counts) == 2
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+def test_woodbury_oracle_matches_reference(case):
+    """The config-5 checker (no dense K_reg) reproduces the reference's F~_i."""
+    g = load_golden(case)
+    for s in range(int(g["n_sub"])):
+        ip, ix, dt = g[f"s{s}_k_indptr"], g[f"s{s}_k_indices"], g[f"s{s}_k_data"]
+        n = ip.shape[0] - 1
+        sol = ora.WoodburyKregSolver(n, ip, ix, dt, g[f"s{s}_kernel"])
+        f = ora.fmatrix_via_solver(sol, n, g[f"s{s}_bcol"], g[f"s{s}_bval"])
+        m = f.shape[0]
+        ref = np.zeros((m, m))
+        ref[np.triu_indices(m)] = g[f"s{s}_F_upper"]
+        assert np.linalg.norm(np.triu(f) - ref) <= 1e-12 * np.linalg.norm(ref), (case, s)
