@@ -190,7 +190,14 @@ struct feti_ctx {
   SpDiag* d_sp_diag = nullptr;
   int2* d_sp_panels = nullptr;
   int n_sp_init = 0, n_sp_panels = 0, sp_max_T32 = 0, sp_max_n = 0;
+  // subdomains are split into sp_groups groups, each factored on its own
+  // stream: one group's latency-bound diagonal factorizations overlap the
+  // DMMA tile work of the others.  Ranges are indexed [g * sp_maxTq + j].
   std::vector<std::pair<int, int>> sp_acc_rng, sp_panel_rng, sp_diag_rng;
+  int sp_groups = 1, sp_maxTq = 0;
+  static constexpr int kSpStreams = 4;
+  cudaStream_t sp_streams[kSpStreams] = {};
+  cudaEvent_t sp_join[kSpStreams] = {};
   double sp_flops = 0.0;
 };
 
@@ -287,42 +294,68 @@ int build_sparse_tasks(feti_ctx* c) {
   std::vector<SpTask> tasks;
   std::vector<SpPair> pairs;
   std::vector<SpDiag> diag;
-  c->sp_acc_rng.assign(maxTq, {0, 0});
-  c->sp_panel_rng.assign(maxTq, {0, 0});
-  c->sp_diag_rng.assign(maxTq, {0, 0});
+  const char* genv = getenv("FETI_SP_GROUPS");
+  int G = genv ? atoi(genv) : feti_ctx::kSpStreams;
+  G = std::max(1, std::min(std::min(G, (int)feti_ctx::kSpStreams), std::max(ns, 1)));
+  c->sp_groups = G;
+  c->sp_maxTq = maxTq;
+  c->sp_acc_rng.assign((size_t)G * maxTq, {0, 0});
+  c->sp_panel_rng.assign((size_t)G * maxTq, {0, 0});
+  c->sp_diag_rng.assign((size_t)G * maxTq, {0, 0});
+  for (int g = 0; g < G; ++g) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->sp_streams[g], cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->sp_join[g], cudaEventDisableTiming));
+  }
+  // contiguous groups of subdomains
+  auto group_of = [&](int si) { return (int)((int64_t)si * G / std::max(ns, 1)); };
+  // slots of the (P Q)^T block row: their tasks run "thin" (rows < 8 only)
+  std::vector<std::vector<char>> qrow(ns);
+  for (int si = 0; si < ns; ++si) {
+    const SpPlan& P = c->subs[si].sp;
+    qrow[si].assign((size_t)P.ntiles, 0);
+    if (P.Tq > P.T)
+      for (int L = 0; L <= P.T; ++L) {
+        const int slot = P.tmap[(size_t)P.T * P.Tq + L];
+        if (slot >= 0) qrow[si][slot] = 1;
+      }
+  }
+  for (int g = 0; g < G; ++g)
   for (int j = 0; j < maxTq; ++j) {
+    const size_t gj = (size_t)g * maxTq + j;
     int b = (int)tasks.size();
     for (int si = 0; si < ns; ++si) {
       const SubHost& s = c->subs[si];
-      if (j >= s.sp.Tq) continue;
+      if (j >= s.sp.Tq || group_of(si) != g) continue;
       for (const auto& t : s.sp.acc[j]) {
-        tasks.push_back(SpTask{s.d_pool + (size_t)t.first * TILE, (int64_t)pairs.size(), (int)t.second.size(), 0});
+        tasks.push_back(SpTask{s.d_pool + (size_t)t.first * TILE, (int64_t)pairs.size(), (int)t.second.size(),
+                               qrow[si][t.first] ? 2 : 0});
         for (const auto& pr : t.second)
           pairs.push_back(SpPair{s.d_pool + (size_t)pr.first * TILE, s.d_pool + (size_t)pr.second * TILE});
       }
     }
-    std::stable_sort(tasks.begin() + b, tasks.end(),
-                     [](const SpTask& x, const SpTask& y) { return x.npairs > y.npairs; });
-    c->sp_acc_rng[j] = {b, (int)tasks.size() - b};
+    std::stable_sort(tasks.begin() + b, tasks.end(), [](const SpTask& x, const SpTask& y) {
+      return x.npairs * ((x.flags & 2) ? 1 : 4) > y.npairs * ((y.flags & 2) ? 1 : 4);
+    });
+    c->sp_acc_rng[gj] = {b, (int)tasks.size() - b};
     const int db = (int)diag.size();
     for (int si = 0; si < ns; ++si) {
       const SubHost& s = c->subs[si];
-      if (j >= s.sp.T) continue;
+      if (j >= s.sp.T || group_of(si) != g) continue;
       diag.push_back(SpDiag{s.d_pool + (size_t)s.sp.tmap[(size_t)j * s.sp.Tq + j] * TILE,
                             c->d_dinv + (size_t)si * TILE, si, j * TB});
     }
-    c->sp_diag_rng[j] = {db, (int)diag.size() - db};
+    c->sp_diag_rng[gj] = {db, (int)diag.size() - db};
     b = (int)tasks.size();
     for (int si = 0; si < ns; ++si) {
       const SubHost& s = c->subs[si];
-      if (j >= s.sp.T) continue;
+      if (j >= s.sp.T || group_of(si) != g) continue;
       for (int slot : s.sp.panel[j]) {
         double* C = s.d_pool + (size_t)slot * TILE;
-        tasks.push_back(SpTask{C, (int64_t)pairs.size(), 1, 1});
+        tasks.push_back(SpTask{C, (int64_t)pairs.size(), 1, qrow[si][slot] ? 3 : 1});
         pairs.push_back(SpPair{C, c->d_dinv + (size_t)si * TILE});
       }
     }
-    c->sp_panel_rng[j] = {b, (int)tasks.size() - b};
+    c->sp_panel_rng[gj] = {b, (int)tasks.size() - b};
   }
   if ((rc = upload(c, &c->d_sp_init, init))) return rc;
   if ((rc = upload(c, &c->d_sp_tasks, tasks))) return rc;
@@ -361,14 +394,27 @@ int factorize_sparse(feti_ctx* c) {
   CUDA_TRY(cudaGetLastError());
   FETI_DEBUG_SYNC(st);
   int launches = 2;
-  for (size_t j = 0; j < c->sp_acc_rng.size(); ++j) {
-    const auto a = c->sp_acc_rng[j], d = c->sp_diag_rng[j], p = c->sp_panel_rng[j];
-    launch_sp_gemm(c->d_sp_tasks + a.first, a.second, c->d_sp_pairs, st);
-    launch_sp_potrf(c->d_sp_diag + d.first, d.second, c->d_bad, st);
-    launch_sp_gemm(c->d_sp_tasks + p.first, p.second, c->d_sp_pairs, st);
-    launches += (a.second > 0) + (d.second > 0) + (p.second > 0);
-    CUDA_TRY(cudaGetLastError());
-    FETI_DEBUG_SYNC(st);
+  // the groups' column sequences are independent: issue them round-robin on
+  // their own streams so the GPU interleaves one group's diagonal blocks with
+  // another's tile GEMMs
+  const int G = c->sp_groups;
+  CUDA_TRY(cudaEventRecord(c->ev[2], st));
+  for (int g = 0; g < G; ++g) CUDA_TRY(cudaStreamWaitEvent(c->sp_streams[g], c->ev[2], 0));
+  for (int j = 0; j < c->sp_maxTq; ++j)
+    for (int g = 0; g < G; ++g) {
+      const size_t gj = (size_t)g * c->sp_maxTq + j;
+      cudaStream_t gs = c->sp_streams[g];
+      const auto a = c->sp_acc_rng[gj], d = c->sp_diag_rng[gj], p = c->sp_panel_rng[gj];
+      launch_sp_gemm(c->d_sp_tasks + a.first, a.second, c->d_sp_pairs, gs);
+      launch_sp_potrf(c->d_sp_diag + d.first, d.second, c->d_bad, gs);
+      launch_sp_gemm(c->d_sp_tasks + p.first, p.second, c->d_sp_pairs, gs);
+      launches += (a.second > 0) + (d.second > 0) + (p.second > 0);
+      CUDA_TRY(cudaGetLastError());
+      FETI_DEBUG_SYNC(gs);
+    }
+  for (int g = 0; g < G; ++g) {
+    CUDA_TRY(cudaEventRecord(c->sp_join[g], c->sp_streams[g]));
+    CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
   }
   CUDA_TRY(cudaEventRecord(c->ev[1], st));
   CUDA_TRY(cudaMemcpyAsync(big.data(), c->d_bad, ns * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -434,6 +480,10 @@ int feti_destroy(feti_ctx* c) {
   for (int i = 0; i < feti_ctx::kWaveStreams; ++i) {
     if (c->wave_join[i]) cudaEventDestroy(c->wave_join[i]);
     if (c->wave_streams[i]) cudaStreamDestroy(c->wave_streams[i]);
+  }
+  for (int g = 0; g < feti_ctx::kSpStreams; ++g) {
+    if (c->sp_join[g]) cudaEventDestroy(c->sp_join[g]);
+    if (c->sp_streams[g]) cudaStreamDestroy(c->sp_streams[g]);
   }
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);

@@ -82,7 +82,6 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
   double* sL = smem;              // 8256 packed lower
   double* sY = smem + 8256;       // 8256 packed lower
   double* sT = smem + 2 * 8256;   // 3072 scratch
-  __shared__ double piv;
   const int tid = threadIdx.x;
   for (int idx = tid; idx < TILE; idx += 256) {
     const int jl = idx >> 7;
@@ -90,27 +89,109 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
     if (il >= jl) sL[plo(il, jl)] = tile[idx];
   }
   __syncthreads();
-  for (int j = 0; j < TB; ++j) {
-    if (tid == 0) {
-      double d = sL[plo(j, j)];
-      if (!(d > 0.0)) {
-        atomicMin(bad, rowbase + j);   // first non-positive pivot (permuted row)
-        d = 1.0;
+  // blocked right-looking factorization over four 32-wide block columns
+  const int lane = tid & 31;
+  for (int bb = 0; bb < 4; ++bb) {
+    const int o = bb * 32;
+    if (tid < 32) {
+      // (1) diagonal block, one warp, lane = row
+      double lik = 0.0;
+      for (int k = 0; k < 32; ++k) {
+        __syncwarp();
+        double d = sL[plo(o + k, o + k)];
+        if (!(d > 0.0)) {
+          if (lane == 0) atomicMin(bad, rowbase + o + k);   // first non-positive pivot (permuted row)
+          d = 1.0;
+        }
+        const double pv = sqrt(d);
+        __syncwarp();
+        if (lane == k) sL[plo(o + k, o + k)] = pv;
+        if (lane > k) {
+          lik = sL[plo(o + lane, o + k)] / pv;
+          sL[plo(o + lane, o + k)] = lik;
+        }
+        __syncwarp();
+        if (lane > k)
+          for (int l = k + 1; l <= lane; ++l) sL[plo(o + lane, o + l)] -= lik * sL[plo(o + l, o + k)];
       }
-      piv = sqrt(d);
-      sL[plo(j, j)] = piv;
+      __syncwarp();
+      // (2) inverse of the diagonal block into sY, lane = column
+      double y[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const double* Lr = sL + plo(o + r, o);
+        double acc = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int j = 0; j < r; ++j) acc = fma(-Lr[j], y[j], acc);
+        y[r] = acc / Lr[r];
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (r >= lane) sY[plo(o + r, o + lane)] = y[r];
     }
     __syncthreads();
-    const double dj = piv;
-    for (int i = j + 1 + tid; i < TB; i += 256) sL[plo(i, j)] /= dj;
-    __syncthreads();
-    const int w = TB - 1 - j;                 // trailing size
-    for (int q = tid; q < w * w; q += 256) {
-      const int ii = q / w, ll = q % w;
-      if (ll <= ii) {
-        const int i = j + 1 + ii, l = j + 1 + ll;
-        sL[plo(i, l)] = fma(-sL[plo(i, j)], sL[plo(l, j)], sL[plo(i, l)]);
+    const int R = TB - o - 32;                 // rows below the block
+    if (R == 0) break;
+    // (3) panel L_ib = A_ib inv(L_bb)^T: item = (row, 4 columns), <= 3 per thread
+    double pout[3][4];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int it = tid + u * 256;
+      if (it < R * 8) {
+        const int i = o + 32 + it / 8, c0 = (it % 8) * 4;
+        const double* Ar = sL + plo(i, o);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = c0 + e;
+          const double* Yc = sY + plo(o + c, o);
+          double acc = 0.0;
+          for (int l = 0; l <= c; ++l) acc = fma(Ar[l], Yc[l], acc);
+          pout[u][e] = acc;
+        }
       }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int it = tid + u * 256;
+      if (it < R * 8) {
+        const int i = o + 32 + it / 8, c0 = (it % 8) * 4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sL[plo(i, o + c0 + e)] = pout[u][e];
+      }
+    }
+    __syncthreads();
+    // (4) trailing update A_ij -= sum_c L_ic L_jc over 4x4 register blocks
+    const int NB = R / 4;
+    const int npairs = NB * (NB + 1) / 2;
+    for (int pidx = tid; pidx < npairs; pidx += 256) {
+      int I = (int)((sqrt(8.0 * pidx + 1.0) - 1.0) * 0.5);
+      while ((I + 1) * (I + 2) / 2 <= pidx) ++I;
+      while (I * (I + 1) / 2 > pidx) --I;
+      const int J = pidx - I * (I + 1) / 2;
+      const int i0 = o + 32 + 4 * I, j0 = o + 32 + 4 * J;
+      double acc[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+      for (int c = 0; c < 32; ++c) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          av[u] = sL[plo(i0 + u, o + c)];
+          bv[u] = sL[plo(j0 + u, o + c)];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (i0 + u >= j0 + v) sL[plo(i0 + u, j0 + v)] -= acc[u][v];
     }
     __syncthreads();
   }

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(128) kreg_scatter_kernel(const SubDev* __restr
 // ---------------------------------------------------------------------------
 // diagonal block: L_kk = chol(A_kk) in place, inv(L_kk) -> dinv scratch
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) potrf_diag_kernel(const SubDev* __restrict__ subs, double* __restrict__ dinv,
+__global__ void __launch_bounds__(256, 1) potrf_diag_kernel(const SubDev* __restrict__ subs, double* __restrict__ dinv,
                                                          int* __restrict__ bad, int k) {
   extern __shared__ double fsm[];
   const int sub = blockIdx.x;

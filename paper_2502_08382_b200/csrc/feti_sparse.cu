@@ -84,8 +84,11 @@ __global__ void __launch_bounds__(256) sp_scatter_kernel(const SpSub* __restrict
 constexpr int SG_STAGES = 3;
 constexpr int SG_THREADS = 288;
 
+// MI = 8: full 128-row tile; MI = 1: "thin" tile of the (P Q)^T block row,
+// whose rows >= r <= 8 are zero (only warp row-group 0, first 8 rows)
+template <int MI>
 __device__ __forceinline__ void sg_mma_slice(const double* __restrict__ a_s, const double* __restrict__ b_s,
-                                             double (&acc)[8][4][2], int wm, int wn, int g, int t) {
+                                             double (&acc)[MI][4][2], int wm, int wn, int g, int t) {
 #pragma unroll
   for (int kb = 0; kb < KS / 4; ++kb) {
     const int kr = kb * 4 + t;
@@ -93,10 +96,56 @@ __device__ __forceinline__ void sg_mma_slice(const double* __restrict__ a_s, con
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) bf[ni] = b_s[swz(kr, wn * 32 + ni * 8 + g)];
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi) {
+    for (int mi = 0; mi < MI; ++mi) {
       const double af = a_s[swz(kr, wm * 64 + mi * 8 + g)];
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
+    }
+  }
+}
+
+// Consumer side of sp_gemm_kernel: MI = 8 full tile, MI = 1 thin tile
+// (only warp row-group 0 computes, only rows < 8 are written).
+template <int MI>
+__device__ __forceinline__ void sg_consume(const double* __restrict__ sA, const double* __restrict__ sB,
+                                           uint64_t* full, uint64_t* empty, int nsl, double* Ct, bool panel,
+                                           int wm, int wn, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const bool active = (MI == 8) || wm == 0;
+  double acc[MI][4][2];
+#pragma unroll
+  for (int a = 0; a < MI; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int sl = 0; sl < nsl; ++sl) {
+    mbar_wait(&full[stage], phase);
+    if (active) sg_mma_slice<MI>(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
+    fence_proxy_async_shared();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == SG_STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  if (!active) return;
+  // every slice of a panel task's A (= C) was consumed above: in-place is safe
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    const int m = wm * 64 + mi * 8 + g;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int nn = wn * 32 + ni * 8 + 2 * t;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double* cp = Ct + swz(nn + e, m);
+        if (panel)
+          *cp = acc[mi][ni][e];
+        else
+          *cp -= acc[mi][ni][e];
+      }
     }
   }
 }
@@ -139,47 +188,13 @@ __global__ void __launch_bounds__(SG_THREADS, 1) sp_gemm_kernel(const SpTask* __
     return;
   }
   const int wm = warp >> 2, wn = warp & 3;
-  const int g = lane >> 2, t = lane & 3;
-  double acc[8][4][2];
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  int stage = 0;
-  uint32_t phase = 0;
-  for (int sl = 0; sl < nsl; ++sl) {
-    mbar_wait(&full[stage], phase);
-    sg_mma_slice(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
-    fence_proxy_async_shared();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
-    if (++stage == SG_STAGES) {
-      stage = 0;
-      phase ^= 1;
-    }
-  }
-  // every slice of a panel task's A (= C) was consumed above: in-place is safe
-  double* Ct = tk.C;
-  const bool panel = tk.flags & 1;
-#pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
-    const int m = wm * 64 + mi * 8 + g;
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int nn = wn * 32 + ni * 8 + 2 * t;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        double* cp = Ct + swz(nn + e, m);
-        if (panel)
-          *cp = acc[mi][ni][e];
-        else
-          *cp -= acc[mi][ni][e];
-      }
-    }
-  }
+  if (!(tk.flags & 2))
+    sg_consume<8>(sA, sB, full, empty, nsl, tk.C, tk.flags & 1, wm, wn, lane);
+  else
+    sg_consume<1>(sA, sB, full, empty, nsl, tk.C, tk.flags & 1, wm, wn, lane);
 }
 
-__global__ void __launch_bounds__(256) sp_potrf_kernel(const SpDiag* __restrict__ d, int* __restrict__ bad) {
+__global__ void __launch_bounds__(256, 1) sp_potrf_kernel(const SpDiag* __restrict__ d, int* __restrict__ bad) {
   extern __shared__ double psm[];
   const SpDiag w = d[blockIdx.x];
   potrf_invert_128(w.C, w.D, bad + w.sub, w.rowbase, psm);
@@ -344,13 +359,14 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
           ++v;
         }
       }
+      const double tfi = (i == T && r > 0) ? tf / 16.0 : tf;   // thin (P Q)^T row tiles
       if (!pr.empty()) {
-        P.flops_exec += tf * pr.size();
+        P.flops_exec += tfi * pr.size();
         P.acc[j].emplace_back(P.tmap[(size_t)i * Tq + j], std::move(pr));
       }
       if (i != j) {
         P.panel[j].push_back(P.tmap[(size_t)i * Tq + j]);
-        P.flops_exec += tf;
+        P.flops_exec += tfi;
       }
     }
     if (j < T) P.flops_exec += (double)TB * TB * TB / 3.0 + (double)TB * TB * TB / 3.0;  // potrf + inverse

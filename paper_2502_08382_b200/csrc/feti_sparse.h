@@ -34,6 +34,7 @@ struct SpSub {
 // One tile of the left-looking factorization:
 //   accumulate (flags 0):  C -= sum_p A_p B_p^T
 //   panel      (flags 1):  C  = C B^T  (B = inv(L_jj), one pair (C, B))
+//   flags & 2: C is a tile of the (P Q)^T block row (rows >= 8 are zero)
 struct SpPair {
   const double* A;
   const double* B;
