@@ -116,3 +116,52 @@ def test_sparse_route_config5_against_oracle():
             f = op.local_operator(s)
             err = np.linalg.norm(f - ref) / np.linalg.norm(ref)
             assert err <= 1e-10, (s, err)
+
+
+def test_sparse_route_c3_subdomain_checksums():
+    """Config 3 interior subdomain (n = 9261, m = 2522): F~ checksums of the
+    reference's own run (its 6-minute numba factorization of the dense K_reg)."""
+    g = load_golden("c3_sub21")
+    prob = inputs.Problem(*inputs.CONFIGS["c3"])
+    s = int(g["sub_index"])
+    op, ks, qs, fs = _sparse_op(prob, [s])
+    with op:
+        op.preprocess()
+        fu = op.local_operator(s)
+    full = fu + np.triu(fu, 1).T
+    for name, got in (("Fv", full @ g["v"]), ("F_diag", np.diag(full)), ("F_row0", full[0])):
+        ref = g[name]
+        assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref), name
+    assert abs(np.linalg.norm(full) - float(g["F_fro"])) <= 1e-10 * float(g["F_fro"])
+
+
+def test_sparse_route_c2_apply_and_pcpg():
+    """Config 2 (512 x 729 DOFs): q = F p and the reference's 80 PCPG iterations."""
+    g = load_golden("heat3d_c2")
+    prob = inputs.Problem(*inputs.CONFIGS["c2"])
+    op, ks, qs, fs = _sparse_op(prob)
+    with op:
+        op.preprocess()
+        q = op.apply(g["p"])
+        assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
+        qk, fk = [qs[s] for s in range(prob.n_sub)], [fs[s] for s in range(prob.n_sub)]
+        cons = [(prob.gids[s], prob.bcol[s], prob.bval[s]) for s in range(prob.n_sub)]
+        gm, e, d, coarse = ora.assemble_dual_system(qk, fk, cons, prob.n_multipliers, prob.c, op.solve_local)
+        lam, it = ora.pcpg(gm, e, d, coarse, op.apply, tol=1e-9)
+    assert it == int(g["pcpg_iterations"]) == 80
+    assert np.linalg.norm(lam - g["pcpg_lambda"]) <= 1e-9 * np.linalg.norm(g["pcpg_lambda"])
+
+
+def test_sparse_route_c4_subdomain_against_oracle():
+    """Config 4 (3D elasticity, n = 10125) largest-m subdomain: F~ against the
+    oracle's Woodbury restatement of the reference's K_reg^-1."""
+    prob = inputs.Problem(*inputs.CONFIGS["c4"])
+    s = int(np.argmax(prob.m_per_subdomain()))
+    op, ks, qs, fs = _sparse_op(prob, [s])
+    with op:
+        op.preprocess()
+        f = op.local_operator(s)
+    k = ks[s]
+    sol = ora.WoodburyKregSolver(prob.n_dofs, k.indptr, k.indices, k.data, qs[s])
+    ref = np.triu(ora.fmatrix_via_solver(sol, prob.n_dofs, prob.bcol[s], prob.bval[s]))
+    assert np.linalg.norm(f - ref) <= 1e-10 * np.linalg.norm(ref)
