@@ -132,7 +132,7 @@ def _constraint_rows(sc, n):
 
 class _Sub:
     __slots__ = ("index", "n", "m", "gids", "bcol", "bval", "perm", "iperm", "slot", "values", "pinned",
-                 "cluster", "fix", "solver")
+                 "cluster", "fix", "solver", "diagpos", "kcache")
 
 
 class DualOperator:
@@ -315,6 +315,8 @@ class DualOperator:
             sub.pinned = None
             sub.solver = None
             sub.fix = None
+            sub.diagpos = None
+            sub.kcache = None
             if self.factorization == "sparse":
                 sub.fix = spr.fixing_dofs(self._kernel_basis(i, sub.n))
             return sub
@@ -410,12 +412,22 @@ class DualOperator:
         self.numeric_count += len(done)
 
     def _kernel_basis(self, index: int, n: int) -> np.ndarray:
-        """Orthonormal kernel basis as regularize takes it (np.linalg.qr, sparse.py:445-449)."""
+        """Orthonormal kernel basis as regularize takes it (np.linalg.qr, sparse.py:445-449).
+
+        Cached per subdomain while the caller hands over an unchanged basis
+        (the kernel depends on the mesh only; run_steps rebuilds equal arrays)."""
         kern = np.asarray(self.kernels[index], dtype=np.float64).reshape(n, -1)
+        sub = self._subs.get(index)
+        if sub is not None and sub.kcache is not None and sub.kcache[0].shape == kern.shape \
+                and np.array_equal(sub.kcache[0], kern):
+            return sub.kcache[1]
         if kern.shape[1] == 0:
-            return np.zeros((n, 0))
-        q, _ = np.linalg.qr(kern)
-        return np.ascontiguousarray(q)
+            q = np.zeros((n, 0))
+        else:
+            q = np.ascontiguousarray(np.linalg.qr(kern)[0])
+        if sub is not None:
+            sub.kcache = (kern.copy(), q)
+        return q
 
     def _preprocess_device(self) -> None:
         import time
@@ -427,8 +439,13 @@ class DualOperator:
                 raise ValueError("stiffness size does not match the subdomain")
             q = self._kernel_basis(sub.index, n)
             sub.solver = None
-            rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ip))
-            rho = float(dt[rows == ix].sum()) / n                     # trace(K)/n (sparse.py:450)
+            # diagonal positions: the pattern is frozen after the first step
+            # (symbolic once, dualop.py:212-269); equality checks are O(nnz)
+            if sub.diagpos is None or not (sub.diagpos[0].shape == ip.shape and np.array_equal(sub.diagpos[0], ip)
+                                           and np.array_equal(sub.diagpos[1], ix)):
+                rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ip))
+                sub.diagpos = (np.array(ip), np.array(ix), np.flatnonzero(rows == ix))
+            rho = float(dt[sub.diagpos[2]].sum()) / n                 # trace(K)/n (sparse.py:450)
             ip, ix, dt = (np.ascontiguousarray(ip, np.int64), np.ascontiguousarray(ix, np.int64),
                           np.ascontiguousarray(dt, np.float64))
             _call(self._lib.feti_set_stiffness(self._ctx, sub.slot, n, _lib.i64ptr(ip), _lib.i64ptr(ix),
