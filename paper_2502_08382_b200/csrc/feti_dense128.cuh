@@ -75,78 +75,109 @@ __device__ __forceinline__ void invert_lower_128(const double* __restrict__ sL, 
 // In-place Cholesky of the 128x128 tile (col-major swizzled, lower part read)
 // and its inverse: tile <- L (upper part zeroed), D <- inv(L) (same layout).
 // A non-positive pivot is reported as atomicMin(bad, rowbase + j) and
-// replaced by 1 so the sweep completes.  smem: (2 * 8256 + 3 * 1024) doubles.
-// Must be called by all 256 threads of the CTA.
+// replaced by 1 so the sweep completes.  Must be called by all 256 threads.
+//
+// Shared memory: one 128 x 129 row-major array (odd stride: row and column
+// walks are bank-conflict free) holding L in its lower triangle and
+// Y = inv(L) transposed in its strict upper triangle (Y(i, j), i > j, at
+// [j][i]), the diagonal of Y apart, plus a 3 x 32 x 32 scratch.  Blocked
+// over four 32-wide block columns: one warp factors and inverts the 32x32
+// diagonal block in registers (shuffle broadcasts), all warps apply it to
+// the panel below and update the trailing matrix; the off-diagonal blocks of
+// Y follow by distance, Y_IJ = -Y_II sum_{K=J}^{I-1} L_IK Y_KJ.
+constexpr int PO_LD = TB + 1;
+constexpr int POTRF_SMEM_DOUBLES = TB * PO_LD + TB + 3 * 1024;
+
 __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, double* __restrict__ D,
                                                  int* __restrict__ bad, int rowbase, double* __restrict__ smem) {
-  double* sL = smem;              // 8256 packed lower
-  double* sY = smem + 8256;       // 8256 packed lower
-  double* sT = smem + 2 * 8256;   // 3072 scratch
+  double* sA = smem;                    // [i][j] at i * PO_LD + j
+  double* sYd = smem + TB * PO_LD;      // diagonal of Y
+  double* sT = sYd + TB;                // 3 x 1024 scratch
   const int tid = threadIdx.x;
+  const int lane = tid & 31;
   for (int idx = tid; idx < TILE; idx += 256) {
     const int jl = idx >> 7;
     const int il = (idx & 127) ^ ((jl & 3) << 2);
-    if (il >= jl) sL[plo(il, jl)] = tile[idx];
+    if (il >= jl) sA[il * PO_LD + jl] = tile[idx];
   }
   __syncthreads();
-  // blocked right-looking factorization over four 32-wide block columns
-  const int lane = tid & 31;
+  // Y(r, c) for r >= c (lower triangle of inv(L))
+  auto yat = [&](int r, int c) -> double { return r == c ? sYd[r] : sA[c * PO_LD + r]; };
   for (int bb = 0; bb < 4; ++bb) {
     const int o = bb * 32;
+#ifndef PO_SKIP_DIAG
     if (tid < 32) {
-      // (1) diagonal block, one warp, lane = row
-      double lik = 0.0;
+      // diagonal block: lane = row, row[j] = A(o+lane, o+j), j <= lane
+      double row[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) row[j] = (j <= lane) ? sA[(o + lane) * PO_LD + o + j] : 0.0;
+      double rdiag = 1.0;                      // 1 / L(o+lane, o+lane)
+#pragma unroll
       for (int k = 0; k < 32; ++k) {
-        __syncwarp();
-        double d = sL[plo(o + k, o + k)];
+        double d = __shfl_sync(0xffffffffu, row[k], k);
         if (!(d > 0.0)) {
           if (lane == 0) atomicMin(bad, rowbase + o + k);   // first non-positive pivot (permuted row)
           d = 1.0;
         }
         const double pv = sqrt(d);
-        __syncwarp();
-        if (lane == k) sL[plo(o + k, o + k)] = pv;
-        if (lane > k) {
-          lik = sL[plo(o + lane, o + k)] / pv;
-          sL[plo(o + lane, o + k)] = lik;
+        const double rp = 1.0 / pv;
+        if (lane == k) rdiag = rp;
+        const double lik = (lane == k) ? pv : (lane > k ? row[k] * rp : 0.0);
+        row[k] = lik;
+#pragma unroll
+        for (int j = k + 1; j < 32; ++j) {
+          const double ljk = __shfl_sync(0xffffffffu, lik, j);
+          row[j] = fma(-lik, ljk, row[j]);
         }
-        __syncwarp();
-        if (lane > k)
-          for (int l = k + 1; l <= lane; ++l) sL[plo(o + lane, o + l)] -= lik * sL[plo(o + l, o + k)];
       }
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j <= lane) sA[(o + lane) * PO_LD + o + j] = row[j];
       __syncwarp();
-      // (2) inverse of the diagonal block into sY, lane = column
+      // inverse of the diagonal block, lane = column c: y[r] = Y(o+r, o+c);
+      // row r of L comes from lane r's registers, 1/L_rr from its rdiag
       double y[32];
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
-        const double* Lr = sL + plo(o + r, o);
-        double acc = (r == lane) ? 1.0 : 0.0;
+        double a0 = (r == lane) ? 1.0 : 0.0, a1 = 0.0;
 #pragma unroll
-        for (int j = 0; j < r; ++j) acc = fma(-Lr[j], y[j], acc);
-        y[r] = acc / Lr[r];
+        for (int j = 0; j < r; ++j) {
+          const double lrj = __shfl_sync(0xffffffffu, row[j], r);
+          if (j & 1)
+            a1 = fma(-lrj, y[j], a1);
+          else
+            a0 = fma(-lrj, y[j], a0);
+        }
+        y[r] = (a0 + a1) * __shfl_sync(0xffffffffu, rdiag, r);
       }
 #pragma unroll
-      for (int r = 0; r < 32; ++r)
-        if (r >= lane) sY[plo(o + r, o + lane)] = y[r];
+      for (int r = 0; r < 32; ++r) {
+        if (r == lane) sYd[o + r] = y[r];
+        else if (r > lane) sA[(o + lane) * PO_LD + o + r] = y[r];
+      }
     }
+#endif
     __syncthreads();
     const int R = TB - o - 32;                 // rows below the block
     if (R == 0) break;
-    // (3) panel L_ib = A_ib inv(L_bb)^T: item = (row, 4 columns), <= 3 per thread
+#ifndef PO_SKIP_PANEL
+    // panel L_ic = sum_{l <= c} A_il Y(c, l): item = (row, 4 columns), <= 3 per thread
     double pout[3][4];
 #pragma unroll
     for (int u = 0; u < 3; ++u) {
       const int it = tid + u * 256;
       if (it < R * 8) {
         const int i = o + 32 + it / 8, c0 = (it % 8) * 4;
-        const double* Ar = sL + plo(i, o);
+        const double* Ar = sA + i * PO_LD + o;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int c = c0 + e;
-          const double* Yc = sY + plo(o + c, o);
-          double acc = 0.0;
-          for (int l = 0; l <= c; ++l) acc = fma(Ar[l], Yc[l], acc);
-          pout[u][e] = acc;
+        for (int e = 0; e < 4; ++e) pout[u][e] = 0.0;
+        for (int l = 0; l < c0 + 4; ++l) {
+          const double a = Ar[l];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = c0 + e;
+            if (l <= c) pout[u][e] = fma(a, yat(o + c, o + l), pout[u][e]);
+          }
         }
       }
     }
@@ -157,11 +188,13 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
       if (it < R * 8) {
         const int i = o + 32 + it / 8, c0 = (it % 8) * 4;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) sL[plo(i, o + c0 + e)] = pout[u][e];
+        for (int e = 0; e < 4; ++e) sA[i * PO_LD + o + c0 + e] = pout[u][e];
       }
     }
     __syncthreads();
-    // (4) trailing update A_ij -= sum_c L_ic L_jc over 4x4 register blocks
+#endif
+#ifndef PO_SKIP_TRAIL
+    // trailing update A_ij -= sum_c L_ic L_jc over 4x4 register blocks
     const int NB = R / 4;
     const int npairs = NB * (NB + 1) / 2;
     for (int pidx = tid; pidx < npairs; pidx += 256) {
@@ -175,12 +208,13 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
       for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+#pragma unroll 4
       for (int c = 0; c < 32; ++c) {
         double av[4], bv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          av[u] = sL[plo(i0 + u, o + c)];
-          bv[u] = sL[plo(j0 + u, o + c)];
+          av[u] = sA[(i0 + u) * PO_LD + o + c];
+          bv[u] = sA[(j0 + u) * PO_LD + o + c];
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -191,20 +225,56 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
       for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v)
-          if (i0 + u >= j0 + v) sL[plo(i0 + u, j0 + v)] -= acc[u][v];
+          if (i0 + u >= j0 + v) sA[(i0 + u) * PO_LD + j0 + v] -= acc[u][v];
+    }
+    __syncthreads();
+#endif
+  }
+#ifndef PO_SKIP_INV
+  // off-diagonal blocks of Y by distance d: T = sum_K L_IK Y_KJ, Y_IJ = -Y_II T
+  const int rr = tid >> 3, cc = (tid & 7) * 4;
+  for (int d = 1; d < 4; ++d) {
+    const int nb = 4 - d;
+    for (int bI = 0; bI < nb; ++bI) {
+      const int J = bI, I = bI + d;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const double* Lr = sA + (I * 32 + rr) * PO_LD;
+      for (int kk = J * 32; kk < I * 32; ++kk) {
+        const double lv = Lr[kk];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = J * 32 + cc + e;
+          if (kk >= col) acc[e] = fma(lv, yat(kk, col), acc[e]);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sT[bI * 1024 + rr * 32 + cc + e] = acc[e];
+    }
+    __syncthreads();
+    for (int bI = 0; bI < nb; ++bI) {
+      const int J = bI, I = bI + d;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int kk = 0; kk <= rr; ++kk) {
+        const double yv = yat(I * 32 + rr, I * 32 + kk);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = fma(yv, sT[bI * 1024 + kk * 32 + cc + e], acc[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sA[(J * 32 + cc + e) * PO_LD + I * 32 + rr] = -acc[e];
     }
     __syncthreads();
   }
+#endif
   for (int idx = tid; idx < TILE; idx += 256) {
     const int jl = idx >> 7;
     const int il = (idx & 127) ^ ((jl & 3) << 2);
-    tile[idx] = (il >= jl) ? sL[plo(il, jl)] : 0.0;
-  }
-  invert_lower_128(sL, sY, sT);
-  for (int idx = tid; idx < TILE; idx += 256) {
-    const int jl = idx >> 7;
-    const int il = (idx & 127) ^ ((jl & 3) << 2);
-    D[idx] = (il >= jl) ? sY[plo(il, jl)] : 0.0;
+    double lv = 0.0, yv = 0.0;
+    if (il >= jl) {
+      lv = sA[il * PO_LD + jl];
+      yv = yat(il, jl);
+    }
+    tile[idx] = lv;
+    D[idx] = yv;
   }
 }
 

@@ -322,7 +322,7 @@ __global__ void __cluster_dims__(SV_CLUSTER, 1, 1) __launch_bounds__(SV_THREADS,
 // launchers
 // ---------------------------------------------------------------------------
 static size_t fg_smem() { return 2 * FG_STAGES * SLICE * sizeof(double) + 8 * 2 * FG_STAGES; }
-static size_t potrf_smem() { return (2 * 8256 + 3 * 1024) * sizeof(double); }
+static size_t potrf_smem() { return POTRF_SMEM_DOUBLES * sizeof(double); }
 size_t solve_smem(int T) { return ((size_t)2 * T * TB + SV_GROUPS * TB) * sizeof(double); }
 
 cudaError_t configure_factor(int max_T) {

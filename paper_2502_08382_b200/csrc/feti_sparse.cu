@@ -377,7 +377,7 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
 // launchers
 // ---------------------------------------------------------------------------
 static size_t sg_smem() { return 2 * SG_STAGES * SLICE * sizeof(double) + 8 * 2 * SG_STAGES; }
-static size_t sp_potrf_smem() { return (2 * 8256 + 3 * 1024) * sizeof(double); }
+static size_t sp_potrf_smem() { return POTRF_SMEM_DOUBLES * sizeof(double); }
 
 cudaError_t configure_sparse() {
   cudaError_t e;
