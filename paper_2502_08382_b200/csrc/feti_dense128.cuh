@@ -86,6 +86,10 @@ __device__ __forceinline__ void invert_lower_128(const double* __restrict__ sL, 
 // the panel below and update the trailing matrix; the off-diagonal blocks of
 // Y follow by distance, Y_IJ = -Y_II sum_{K=J}^{I-1} L_IK Y_KJ.
 constexpr int PO_LD = TB + 1;
+
+// Barrier over the 256 threads (warps 0-7) that run potrf_invert_128: a named
+// barrier, so a persistent CTA with extra warps can call it.
+__device__ __forceinline__ void po_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 constexpr int POTRF_SMEM_DOUBLES = TB * PO_LD + TB + 3 * 1024;
 
 __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, double* __restrict__ D,
@@ -100,7 +104,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
     const int il = (idx & 127) ^ ((jl & 3) << 2);
     if (il >= jl) sA[il * PO_LD + jl] = tile[idx];
   }
-  __syncthreads();
+  po_sync();
   // Y(r, c) for r >= c (lower triangle of inv(L))
   auto yat = [&](int r, int c) -> double { return r == c ? sYd[r] : sA[c * PO_LD + r]; };
   for (int bb = 0; bb < 4; ++bb) {
@@ -157,7 +161,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
       }
     }
 #endif
-    __syncthreads();
+    po_sync();
     const int R = TB - o - 32;                 // rows below the block
     if (R == 0) break;
 #ifndef PO_SKIP_PANEL
@@ -181,7 +185,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
         }
       }
     }
-    __syncthreads();
+    po_sync();
 #pragma unroll
     for (int u = 0; u < 3; ++u) {
       const int it = tid + u * 256;
@@ -191,7 +195,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
         for (int e = 0; e < 4; ++e) sA[i * PO_LD + o + c0 + e] = pout[u][e];
       }
     }
-    __syncthreads();
+    po_sync();
 #endif
 #ifndef PO_SKIP_TRAIL
     // trailing update A_ij -= sum_c L_ic L_jc over 4x4 register blocks
@@ -227,7 +231,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
         for (int v = 0; v < 4; ++v)
           if (i0 + u >= j0 + v) sA[(i0 + u) * PO_LD + j0 + v] -= acc[u][v];
     }
-    __syncthreads();
+    po_sync();
 #endif
   }
 #ifndef PO_SKIP_INV
@@ -250,7 +254,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
 #pragma unroll
       for (int e = 0; e < 4; ++e) sT[bI * 1024 + rr * 32 + cc + e] = acc[e];
     }
-    __syncthreads();
+    po_sync();
     for (int bI = 0; bI < nb; ++bI) {
       const int J = bI, I = bI + d;
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -262,7 +266,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
 #pragma unroll
       for (int e = 0; e < 4; ++e) sA[(J * 32 + cc + e) * PO_LD + I * 32 + rr] = -acc[e];
     }
-    __syncthreads();
+    po_sync();
   }
 #endif
   for (int idx = tid; idx < TILE; idx += 256) {

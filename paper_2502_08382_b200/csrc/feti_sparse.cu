@@ -150,6 +150,50 @@ __device__ __forceinline__ void sg_consume(const double* __restrict__ sA, const 
   }
 }
 
+// sg_consume starting at ring position (stage0, phase0) of a persistent CTA
+template <int MI>
+__device__ __forceinline__ void sg_consume_at(const double* __restrict__ sA, const double* __restrict__ sB,
+                                              uint64_t* full, uint64_t* empty, int nsl, double* Ct, bool panel,
+                                              int wm, int wn, int lane, int stage0, uint32_t phase0) {
+  const int g = lane >> 2, t = lane & 3;
+  const bool active = (MI == 8) || wm == 0;
+  double acc[MI][4][2];
+#pragma unroll
+  for (int a = 0; a < MI; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  int stage = stage0;
+  uint32_t phase = phase0;
+  for (int sl = 0; sl < nsl; ++sl) {
+    mbar_wait(&full[stage], phase);
+    if (active) sg_mma_slice<MI>(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
+    fence_proxy_async_shared();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == SG_STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    const int m = wm * 64 + mi * 8 + g;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int nn = wn * 32 + ni * 8 + 2 * t;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double* cp = Ct + swz(nn + e, m);
+        if (panel)
+          *cp = acc[mi][ni][e];
+        else
+          *cp -= acc[mi][ni][e];
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(SG_THREADS, 1) sp_gemm_kernel(const SpTask* __restrict__ tasks,
                                                                 const SpPair* __restrict__ pairs) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -198,6 +242,187 @@ __global__ void __launch_bounds__(256, 1) sp_potrf_kernel(const SpDiag* __restri
   extern __shared__ double psm[];
   const SpDiag w = d[blockIdx.x];
   potrf_invert_128(w.C, w.D, bad + w.sub, w.rowbase, psm);
+}
+
+// ---------------------------------------------------------------------------
+// persistent dependency-driven factorization
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// (thread 0 only) make entries [first, first + n) of `kind` ready
+__device__ void dag_push(const SpDag& g, int kind, int first, int n) {
+  if (n <= 0) return;
+  const int base = atomicAdd(g.tail, n);
+  for (int t = 0; t < n; ++t) st_release(g.queue + base + t, (kind << 30) | (first + t));
+}
+
+__device__ void dag_start_column(const SpDag& g, int c);
+
+__device__ void dag_acc_done(const SpDag& g, int c) {
+  const SpCol col = g.cols[c];
+  if (col.diag >= 0) {
+    dag_push(g, SPQ_DIAG, col.diag, 1);
+  } else if (col.next >= 0) {   // (P Q)^T column: nothing to factor
+    dag_start_column(g, col.next);
+  }
+}
+
+__device__ void dag_start_column(const SpDag& g, int c) {
+  const SpCol col = g.cols[c];
+  if (col.nacc > 0)
+    dag_push(g, SPQ_TASK, col.acc0, col.nacc);
+  else
+    dag_acc_done(g, c);
+}
+
+__device__ void dag_column_done(const SpDag& g, int c) {
+  const int nx = g.cols[c].next;
+  if (nx >= 0) dag_start_column(g, nx);
+}
+
+__device__ void dag_complete(const SpDag& g, int kind, int idx) {
+  if (kind == SPQ_DIAG) {
+    const int c = g.diag_col[idx];
+    const SpCol col = g.cols[c];
+    if (col.npan > 0)
+      dag_push(g, SPQ_TASK, col.pan0, col.npan);
+    else
+      dag_column_done(g, c);
+    return;
+  }
+  const int c = g.task_col[idx];
+  if (g.tasks[idx].flags & 1) {
+    if (atomicSub(g.pan_left + c, 1) == 1) dag_column_done(g, c);
+  } else {
+    if (atomicSub(g.acc_left + c, 1) == 1) dag_acc_done(g, c);
+  }
+}
+
+// 8 warps, no dedicated producer warp: lane 0 of warp 0 issues the bulk
+// copies PREF slices ahead (after every warp released the stage), so the CTA
+// has 255 registers per thread for both the DMMA tiles and potrf_invert_128.
+constexpr int DAG_THREADS = 256;
+constexpr int DAG_PREF = SG_STAGES - 1;
+
+__device__ __forceinline__ void dag_issue(const SpPair* __restrict__ pairs, int64_t pair0, int sl, uint32_t pos,
+                                          double* sA, double* sB, uint64_t* full, uint64_t* empty) {
+  const int st = (int)(pos % SG_STAGES);
+  const uint32_t ph = (pos / SG_STAGES) & 1;
+  const SpPair pr = pairs[pair0 + sl / (TB / KS)];
+  const int so = (sl % (TB / KS)) * SLICE;
+  mbar_wait(&empty[st], ph ^ 1);
+  mbar_arrive_expect_tx(&full[st], 2 * SLICE * 8);
+  bulk_g2s(sA + st * SLICE, pr.A + so, SLICE * 8, &full[st]);
+  bulk_g2s(sB + st * SLICE, pr.B + so, SLICE * 8, &full[st]);
+}
+
+template <int MI>
+__device__ __forceinline__ void dag_gemm(const SpDag& g, const SpTask& tk, double* sA, double* sB, uint64_t* full,
+                                         uint64_t* empty, uint32_t pos0, int warp, int lane) {
+  const int nsl = tk.npairs * (TB / KS);
+  const int wm = warp >> 2, wn = warp & 3;
+  const int gq = lane >> 2, t = lane & 3;
+  const bool issuer = (threadIdx.x == 0);
+  const bool active = (MI == 8) || wm == 0;
+  if (issuer) {
+    fence_proxy_async_global();
+    fence_proxy_async_shared();
+    for (int sl = 0; sl < DAG_PREF && sl < nsl; ++sl) dag_issue(g.pairs, tk.pair0, sl, pos0 + sl, sA, sB, full, empty);
+  }
+  double acc[MI][4][2];
+#pragma unroll
+  for (int a = 0; a < MI; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int sl = 0; sl < nsl; ++sl) {
+    const uint32_t pos = pos0 + sl;
+    if (issuer && sl + DAG_PREF < nsl)
+      dag_issue(g.pairs, tk.pair0, sl + DAG_PREF, pos + DAG_PREF, sA, sB, full, empty);
+    const int st = (int)(pos % SG_STAGES);
+    mbar_wait(&full[st], (pos / SG_STAGES) & 1);
+    if (active) sg_mma_slice<MI>(sA + st * SLICE, sB + st * SLICE, acc, wm, wn, gq, t);
+    fence_proxy_async_shared();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  if (!active) return;
+  double* Ct = tk.C;
+  const bool panel = tk.flags & 1;
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    const int m = wm * 64 + mi * 8 + gq;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int nn = wn * 32 + ni * 8 + 2 * t;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double* cp = Ct + swz(nn + e, m);
+        if (panel)
+          *cp = acc[mi][ni][e];
+        else
+          *cp -= acc[mi][ni][e];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(DAG_THREADS, 1) sp_dag_kernel(const SpDag g) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);
+  double* sB = sA + SG_STAGES * SLICE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + SG_STAGES * SLICE);
+  uint64_t* empty = full + SG_STAGES;
+  __shared__ int s_entry;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < SG_STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 8);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  uint32_t pos = 0;   // ring position (slices this CTA consumed so far)
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const int slot = atomicAdd(g.head, 1);
+      int e = -2;
+      if (slot < g.total) {
+        while ((e = ld_acquire(g.queue + slot)) < 0) __nanosleep(32);
+      }
+      s_entry = e;
+    }
+    __syncthreads();
+    const int e = s_entry;
+    if (e == -2) break;
+    const int kind = e >> 30, idx = e & ((1 << 30) - 1);
+    if (kind == SPQ_TASK) {
+      const SpTask tk = g.tasks[idx];
+      if (!(tk.flags & 2))
+        dag_gemm<8>(g, tk, sA, sB, full, empty, pos, warp, lane);
+      else
+        dag_gemm<1>(g, tk, sA, sB, full, empty, pos, warp, lane);
+      pos += (uint32_t)(tk.npairs * (TB / KS));
+      fence_proxy_async_global();   // C is read by later bulk copies
+    } else {
+      const SpDiag d = g.diag[idx];
+      potrf_invert_128(d.C, d.D, g.bad + d.sub, d.rowbase, reinterpret_cast<double*>(smem_raw));
+      fence_proxy_async_shared();   // the ring reuses this shared memory via bulk copies
+      fence_proxy_async_global();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      dag_complete(g, kind, idx);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -379,8 +604,13 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
 static size_t sg_smem() { return 2 * SG_STAGES * SLICE * sizeof(double) + 8 * 2 * SG_STAGES; }
 static size_t sp_potrf_smem() { return POTRF_SMEM_DOUBLES * sizeof(double); }
 
+static size_t dag_smem() { return sg_smem(); }
+
 cudaError_t configure_sparse() {
   cudaError_t e;
+  static_assert(POTRF_SMEM_DOUBLES * 8 <= 2 * SG_STAGES * SLICE * 8, "potrf scratch must fit the GEMM ring");
+  if ((e = cudaFuncSetAttribute(sp_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dag_smem())))
+    return e;
   if ((e = cudaFuncSetAttribute(sp_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem())))
     return e;
   return cudaFuncSetAttribute(sp_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_potrf_smem());
@@ -396,6 +626,10 @@ void launch_sp_scatter(const SpSub* ss, int nsub, int max_n, cudaStream_t st) {
 
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st) {
   if (ntasks > 0) sp_gemm_kernel<<<ntasks, SG_THREADS, sg_smem(), st>>>(tasks, pairs);
+}
+
+void launch_sp_dag(const SpDag& g, int nctas, cudaStream_t st) {
+  if (g.total > 0 && nctas > 0) sp_dag_kernel<<<nctas, DAG_THREADS, dag_smem(), st>>>(g);
 }
 
 void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st) {

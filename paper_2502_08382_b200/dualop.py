@@ -441,10 +441,11 @@ class DualOperator:
             sub.solver = None
             # diagonal positions: the pattern is frozen after the first step
             # (symbolic once, dualop.py:212-269); equality checks are O(nnz)
-            if sub.diagpos is None or not (sub.diagpos[0].shape == ip.shape and np.array_equal(sub.diagpos[0], ip)
-                                           and np.array_equal(sub.diagpos[1], ix)):
+            # (the reference refills values into a frozen pattern without
+            # re-checking it either; the library verifies indptr)
+            if sub.diagpos is None or not (sub.diagpos[0].shape == ip.shape and np.array_equal(sub.diagpos[0], ip)):
                 rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ip))
-                sub.diagpos = (np.array(ip), np.array(ix), np.flatnonzero(rows == ix))
+                sub.diagpos = (np.array(ip), None, np.flatnonzero(rows == ix))
             rho = float(dt[sub.diagpos[2]].sum()) / n                 # trace(K)/n (sparse.py:450)
             ip, ix, dt = (np.ascontiguousarray(ip, np.int64), np.ascontiguousarray(ix, np.int64),
                           np.ascontiguousarray(dt, np.float64))

@@ -165,3 +165,21 @@ def test_sparse_route_c4_subdomain_against_oracle():
     sol = ora.WoodburyKregSolver(prob.n_dofs, k.indptr, k.indices, k.data, qs[s])
     ref = np.triu(ora.fmatrix_via_solver(sol, prob.n_dofs, prob.bcol[s], prob.bval[s]))
     assert np.linalg.norm(f - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_sparse_route_persistent_kernel_bit_identical(monkeypatch):
+    """The opt-in persistent, dependency-driven factorization (FETI_SP_DAG=1)
+    runs the same tile tasks in another order: identical bits."""
+    prob = inputs.Problem("elasticity", 2, 16, 2)
+    op, ks, qs, fs = _sparse_op(prob)
+    with op:
+        op.preprocess()
+        ref = [op.local_operator(s) for s in range(prob.n_sub)]
+    monkeypatch.setenv("FETI_SP_DAG", "1")
+    op2, _, _, _ = _sparse_op(prob)
+    with op2:
+        op2.preprocess()
+        got = [op2.local_operator(s) for s in range(prob.n_sub)]
+        assert op2.stats()["launches_factorize"] == 3
+    for a, b in zip(ref, got):
+        assert np.array_equal(a, b)
