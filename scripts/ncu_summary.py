@@ -49,7 +49,9 @@ def launches(path):
             data.append(dict(zip(hdr, r)))
     agg = collections.OrderedDict()
     for d in data:
-        if "feti::" not in d["Kernel Name"]:
+        # the capture's -k filter keeps our kernels only (names may or may not
+        # carry the feti:: namespace depending on the ncu version)
+        if "Kernel Name" not in d:
             continue
         agg.setdefault(short(d["Kernel Name"]), []).append(float(d["Metric Value"]) / 1e6)
     return agg
