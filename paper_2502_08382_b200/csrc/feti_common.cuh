@@ -126,6 +126,11 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
       : "memory");
 }
 
+// Bulk prefetch of a global range into L2 (TMA engine, no completion).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(gsrc), "r"(bytes) : "memory");
+}
+
 // 8-byte asynchronous global->shared copy (LDGSTS) for gathers whose source
 // alignment rules out bulk copies (the reference's packed factor columns).
 __device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {

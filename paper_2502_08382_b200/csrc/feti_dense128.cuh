@@ -98,7 +98,8 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
   double* sYd = smem + TB * PO_LD;      // diagonal of Y
   double* sT = sYd + TB;                // 3 x 1024 scratch
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g8 = lane >> 2, t4 = lane & 3;      // DMMA fragment coordinates
   for (int idx = tid; idx < TILE; idx += 256) {
     const int jl = idx >> 7;
     const int il = (idx & 127) ^ ((jl & 3) << 2);
@@ -110,8 +111,9 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
   for (int bb = 0; bb < 4; ++bb) {
     const int o = bb * 32;
 #ifndef PO_SKIP_DIAG
-    if (tid < 32) {
-      // diagonal block: lane = row, row[j] = A(o+lane, o+j), j <= lane
+    if (warp == 0) {
+      // diagonal block by warp 0 in registers; lane = row,
+      // row[j] = A(o+lane, o+j), j <= lane
       double row[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) row[j] = (j <= lane) ? sA[(o + lane) * PO_LD + o + j] : 0.0;
@@ -120,7 +122,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
       for (int k = 0; k < 32; ++k) {
         double d = __shfl_sync(0xffffffffu, row[k], k);
         if (!(d > 0.0)) {
-          if (lane == 0) atomicMin(bad, rowbase + o + k);   // first non-positive pivot (permuted row)
+          if (tid == 0) atomicMin(bad, rowbase + o + k);    // first non-positive pivot (permuted row)
           d = 1.0;
         }
         const double pv = sqrt(d);
@@ -137,13 +139,12 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
 #pragma unroll
       for (int j = 0; j < 32; ++j)
         if (j <= lane) sA[(o + lane) * PO_LD + o + j] = row[j];
-      __syncwarp();
       // inverse of the diagonal block, lane = column c: y[r] = Y(o+r, o+c);
       // row r of L comes from lane r's registers, 1/L_rr from its rdiag
       double y[32];
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
-        double a0 = (r == lane) ? 1.0 : 0.0, a1 = 0.0;
+        double a0 = (r == lane) ? 1.0 : 0.0, a1 = 0.0;   // (rows of L from registers: no smem dependency)
 #pragma unroll
         for (int j = 0; j < r; ++j) {
           const double lrj = __shfl_sync(0xffffffffu, row[j], r);
@@ -165,106 +166,97 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
     const int R = TB - o - 32;                 // rows below the block
     if (R == 0) break;
 #ifndef PO_SKIP_PANEL
-    // panel L_ic = sum_{l <= c} A_il Y(c, l): item = (row, 4 columns), <= 3 per thread
-    double pout[3][4];
+    // panel L_ib = A_ib Y_bb^T on the FP64 tensor pipe: 8x8 output tiles,
+    // (R/8) x 4 of them round-robin over the 8 warps (<= 6 each), DMMA 8x8x4
+    {
+      const int nt = (R / 8) * 4;
+      double pout[6][2];
 #pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      const int it = tid + u * 256;
-      if (it < R * 8) {
-        const int i = o + 32 + it / 8, c0 = (it % 8) * 4;
-        const double* Ar = sA + i * PO_LD + o;
+      for (int u = 0; u < 6; ++u) {
+        const int tl = warp + u * 8;
+        pout[u][0] = pout[u][1] = 0.0;
+        if (tl < nt) {
+          const int i0 = o + 32 + (tl >> 2) * 8, c0 = (tl & 3) * 8;
+          const double* Ar = sA + (i0 + g8) * PO_LD + o;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) pout[u][e] = 0.0;
-        for (int l = 0; l < c0 + 4; ++l) {
-          const double a = Ar[l];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = c0 + e;
-            if (l <= c) pout[u][e] = fma(a, yat(o + c, o + l), pout[u][e]);
+          for (int k0 = 0; k0 < 32; k0 += 4) {
+            if (k0 > c0 + 7) break;                        // Y_bb^T is upper: k <= n
+            const int k = k0 + t4, nn = c0 + g8;
+            const double bv = (k <= nn) ? yat(o + nn, o + k) : 0.0;
+            dmma(pout[u][0], pout[u][1], Ar[k], bv);
           }
         }
       }
-    }
-    po_sync();
+      po_sync();
 #pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      const int it = tid + u * 256;
-      if (it < R * 8) {
-        const int i = o + 32 + it / 8, c0 = (it % 8) * 4;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) sA[i * PO_LD + o + c0 + e] = pout[u][e];
+      for (int u = 0; u < 6; ++u) {
+        const int tl = warp + u * 8;
+        if (tl < nt) {
+          const int i0 = o + 32 + (tl >> 2) * 8, c0 = (tl & 3) * 8;
+          sA[(i0 + g8) * PO_LD + o + c0 + 2 * t4] = pout[u][0];
+          sA[(i0 + g8) * PO_LD + o + c0 + 2 * t4 + 1] = pout[u][1];
+        }
       }
+      po_sync();
     }
-    po_sync();
 #endif
 #ifndef PO_SKIP_TRAIL
-    // trailing update A_ij -= sum_c L_ic L_jc over 4x4 register blocks
-    const int NB = R / 4;
-    const int npairs = NB * (NB + 1) / 2;
-    for (int pidx = tid; pidx < npairs; pidx += 256) {
-      int I = (int)((sqrt(8.0 * pidx + 1.0) - 1.0) * 0.5);
-      while ((I + 1) * (I + 2) / 2 <= pidx) ++I;
-      while (I * (I + 1) / 2 > pidx) --I;
-      const int J = pidx - I * (I + 1) / 2;
-      const int i0 = o + 32 + 4 * I, j0 = o + 32 + 4 * J;
-      double acc[4][4];
+    // trailing update A_ij -= L_ib L_jb^T over the lower 8x8 tiles (DMMA)
+    {
+      const int nb = R / 8;
+      const int ntl = nb * (nb + 1) / 2;
+      for (int pidx = warp; pidx < ntl; pidx += 8) {
+        int I = (int)((sqrt(8.0 * pidx + 1.0) - 1.0) * 0.5);
+        while ((I + 1) * (I + 2) / 2 <= pidx) ++I;
+        while (I * (I + 1) / 2 > pidx) --I;
+        const int J = pidx - I * (I + 1) / 2;
+        const int i0 = o + 32 + 8 * I, j0 = o + 32 + 8 * J;
+        const double* Ar = sA + (i0 + g8) * PO_LD + o;
+        const double* Br = sA + (j0 + g8) * PO_LD + o;
+        double c0v = 0.0, c1v = 0.0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-#pragma unroll 4
-      for (int c = 0; c < 32; ++c) {
-        double av[4], bv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          av[u] = sA[(i0 + u) * PO_LD + o + c];
-          bv[u] = sA[(j0 + u) * PO_LD + o + c];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+        for (int k0 = 0; k0 < 32; k0 += 4) dmma(c0v, c1v, Ar[k0 + t4], Br[k0 + t4]);
+        const int row = i0 + g8, col = j0 + 2 * t4;
+        if (I > J || row >= col) sA[row * PO_LD + col] -= c0v;
+        if (I > J || row >= col + 1) sA[row * PO_LD + col + 1] -= c1v;
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-          if (i0 + u >= j0 + v) sA[(i0 + u) * PO_LD + j0 + v] -= acc[u][v];
+      po_sync();
     }
-    po_sync();
 #endif
   }
 #ifndef PO_SKIP_INV
-  // off-diagonal blocks of Y by distance d: T = sum_K L_IK Y_KJ, Y_IJ = -Y_II T
-  const int rr = tid >> 3, cc = (tid & 7) * 4;
+  // off-diagonal blocks of Y by distance d on the tensor pipe:
+  // T = sum_{K=J}^{I-1} L_IK Y_KJ, then Y_IJ = -Y_II T
+  auto ylo = [&](int r, int c) -> double { return r > c ? sA[c * PO_LD + r] : (r == c ? sYd[r] : 0.0); };
   for (int d = 1; d < 4; ++d) {
     const int nb = 4 - d;
-    for (int bI = 0; bI < nb; ++bI) {
+    for (int tl = warp; tl < nb * 16; tl += 8) {
+      const int bI = tl >> 4, tm = (tl >> 2) & 3, tn = tl & 3;
       const int J = bI, I = bI + d;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const double* Lr = sA + (I * 32 + rr) * PO_LD;
-      for (int kk = J * 32; kk < I * 32; ++kk) {
-        const double lv = Lr[kk];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int col = J * 32 + cc + e;
-          if (kk >= col) acc[e] = fma(lv, yat(kk, col), acc[e]);
-        }
+      const double* Lr = sA + (I * 32 + tm * 8 + g8) * PO_LD;
+      const int cn = J * 32 + tn * 8 + g8;
+      double c0v = 0.0, c1v = 0.0;
+      for (int k0 = J * 32 + tn * 8; k0 < I * 32; k0 += 4) {
+        const int k = k0 + t4;
+        dmma(c0v, c1v, Lr[k], ylo(k, cn));
       }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) sT[bI * 1024 + rr * 32 + cc + e] = acc[e];
+      double* Tb = sT + bI * 1024 + (tm * 8 + g8) * 32 + tn * 8 + 2 * t4;
+      Tb[0] = c0v;
+      Tb[1] = c1v;
     }
     po_sync();
-    for (int bI = 0; bI < nb; ++bI) {
+    for (int tl = warp; tl < nb * 16; tl += 8) {
+      const int bI = tl >> 4, tm = (tl >> 2) & 3, tn = tl & 3;
       const int J = bI, I = bI + d;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int kk = 0; kk <= rr; ++kk) {
-        const double yv = yat(I * 32 + rr, I * 32 + kk);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[e] = fma(yv, sT[bI * 1024 + kk * 32 + cc + e], acc[e]);
+      const int rm = I * 32 + tm * 8 + g8;
+      double c0v = 0.0, c1v = 0.0;
+      for (int k0 = 0; k0 < tm * 8 + 8; k0 += 4) {
+        const int k = k0 + t4;
+        dmma(c0v, c1v, ylo(rm, I * 32 + k), sT[bI * 1024 + k * 32 + tn * 8 + g8]);
       }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) sA[(J * 32 + cc + e) * PO_LD + I * 32 + rr] = -acc[e];
+      const int m = I * 32 + tm * 8 + g8, n = J * 32 + tn * 8 + 2 * t4;
+      sA[n * PO_LD + m] = -c0v;
+      sA[(n + 1) * PO_LD + m] = -c1v;
     }
     po_sync();
   }

@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) sp_gemm_kernel(const SpTask* __
   const int nsl = tk.npairs * (TB / KS);
   if (warp == 8) {
     if (lane == 0) {
+      // the epilogue read-modify-writes C: have it in L2 by then
+      if (!(tk.flags & 1)) bulk_prefetch_l2(tk.C, TILE * 8);
       int stage = 0;
       uint32_t phase = 0;
       for (int sl = 0; sl < nsl; ++sl) {
