@@ -25,6 +25,7 @@
 //   W = U1 C - U2,
 // applied in place to the packed 32x32 apply tiles.
 #include <algorithm>
+#include <cstdlib>
 
 #include "feti_common.cuh"
 #include "feti_dense128.cuh"
@@ -326,8 +327,8 @@ __device__ __forceinline__ void dag_issue(const SpPair* __restrict__ pairs, int6
 }
 
 template <int MI>
-__device__ __forceinline__ void dag_gemm(const SpDag& g, const SpTask& tk, double* sA, double* sB, uint64_t* full,
-                                         uint64_t* empty, uint32_t pos0, int warp, int lane) {
+__device__ __forceinline__ void dag_gemm(const SpPair* __restrict__ pairs, const SpTask& tk, double* sA, double* sB,
+                                         uint64_t* full, uint64_t* empty, uint32_t pos0, int warp, int lane) {
   const int nsl = tk.npairs * (TB / KS);
   const int wm = warp >> 2, wn = warp & 3;
   const int gq = lane >> 2, t = lane & 3;
@@ -336,7 +337,8 @@ __device__ __forceinline__ void dag_gemm(const SpDag& g, const SpTask& tk, doubl
   if (issuer) {
     fence_proxy_async_global();
     fence_proxy_async_shared();
-    for (int sl = 0; sl < DAG_PREF && sl < nsl; ++sl) dag_issue(g.pairs, tk.pair0, sl, pos0 + sl, sA, sB, full, empty);
+    if (!(tk.flags & 1)) bulk_prefetch_l2(tk.C, TILE * 8);
+    for (int sl = 0; sl < DAG_PREF && sl < nsl; ++sl) dag_issue(pairs, tk.pair0, sl, pos0 + sl, sA, sB, full, empty);
   }
   double acc[MI][4][2];
 #pragma unroll
@@ -346,7 +348,7 @@ __device__ __forceinline__ void dag_gemm(const SpDag& g, const SpTask& tk, doubl
   for (int sl = 0; sl < nsl; ++sl) {
     const uint32_t pos = pos0 + sl;
     if (issuer && sl + DAG_PREF < nsl)
-      dag_issue(g.pairs, tk.pair0, sl + DAG_PREF, pos + DAG_PREF, sA, sB, full, empty);
+      dag_issue(pairs, tk.pair0, sl + DAG_PREF, pos + DAG_PREF, sA, sB, full, empty);
     const int st = (int)(pos % SG_STAGES);
     mbar_wait(&full[st], (pos / SG_STAGES) & 1);
     if (active) sg_mma_slice<MI>(sA + st * SLICE, sB + st * SLICE, acc, wm, wn, gq, t);
@@ -373,6 +375,31 @@ __device__ __forceinline__ void dag_gemm(const SpDag& g, const SpTask& tk, doubl
       }
     }
   }
+}
+
+// one task per CTA, 8 warps (255 registers, no spills): the column-launch
+// scheduler's tile kernel
+__global__ void __launch_bounds__(DAG_THREADS, 1) sp_gemm8_kernel(const SpTask* __restrict__ tasks,
+                                                                  const SpPair* __restrict__ pairs) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);
+  double* sB = sA + SG_STAGES * SLICE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + SG_STAGES * SLICE);
+  uint64_t* empty = full + SG_STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < SG_STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 8);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const SpTask tk = tasks[blockIdx.x];
+  if (!(tk.flags & 2))
+    dag_gemm<8>(pairs, tk, sA, sB, full, empty, 0, warp, lane);
+  else
+    dag_gemm<1>(pairs, tk, sA, sB, full, empty, 0, warp, lane);
 }
 
 __global__ void __launch_bounds__(DAG_THREADS, 1) sp_dag_kernel(const SpDag g) {
@@ -408,9 +435,9 @@ __global__ void __launch_bounds__(DAG_THREADS, 1) sp_dag_kernel(const SpDag g) {
     if (kind == SPQ_TASK) {
       const SpTask tk = g.tasks[idx];
       if (!(tk.flags & 2))
-        dag_gemm<8>(g, tk, sA, sB, full, empty, pos, warp, lane);
+        dag_gemm<8>(g.pairs, tk, sA, sB, full, empty, pos, warp, lane);
       else
-        dag_gemm<1>(g, tk, sA, sB, full, empty, pos, warp, lane);
+        dag_gemm<1>(g.pairs, tk, sA, sB, full, empty, pos, warp, lane);
       pos += (uint32_t)(tk.npairs * (TB / KS));
       fence_proxy_async_global();   // C is read by later bulk copies
     } else {
@@ -613,6 +640,8 @@ cudaError_t configure_sparse() {
   static_assert(POTRF_SMEM_DOUBLES * 8 <= 2 * SG_STAGES * SLICE * 8, "potrf scratch must fit the GEMM ring");
   if ((e = cudaFuncSetAttribute(sp_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dag_smem())))
     return e;
+  if ((e = cudaFuncSetAttribute(sp_gemm8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem())))
+    return e;
   if ((e = cudaFuncSetAttribute(sp_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem())))
     return e;
   return cudaFuncSetAttribute(sp_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_potrf_smem());
@@ -626,8 +655,14 @@ void launch_sp_scatter(const SpSub* ss, int nsub, int max_n, cudaStream_t st) {
   if (nsub > 0 && max_n > 0) sp_scatter_kernel<<<dim3((max_n + 7) / 8, nsub), 256, 0, st>>>(ss);
 }
 
+static const bool g_gemm8 = getenv("FETI_SP_GEMM9") == nullptr;
+
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st) {
-  if (ntasks > 0) sp_gemm_kernel<<<ntasks, SG_THREADS, sg_smem(), st>>>(tasks, pairs);
+  if (ntasks <= 0) return;
+  if (g_gemm8)
+    sp_gemm8_kernel<<<ntasks, DAG_THREADS, sg_smem(), st>>>(tasks, pairs);
+  else
+    sp_gemm_kernel<<<ntasks, SG_THREADS, sg_smem(), st>>>(tasks, pairs);
 }
 
 void launch_sp_dag(const SpDag& g, int nctas, cudaStream_t st) {
