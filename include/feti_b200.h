@@ -84,6 +84,7 @@ typedef struct feti_stats {
   double flops_factor_exec;  /* sparse-factor route: tile flops executed by feti_factorize */
   int32_t launches_factorize;
   int32_t pad_;
+  double ms_preprocess;      /* sparse-factor route: factorize start -> assemble end (device) */
 } feti_stats;
 
 int feti_abi_version(void);

@@ -205,6 +205,10 @@ struct feti_ctx {
   int *d_dag_tcol = nullptr, *d_dag_dcol = nullptr, *d_dag_acc = nullptr, *d_dag_pan = nullptr;
   int *d_dag_queue = nullptr, *d_dag_ht = nullptr;
   static constexpr int kSpStreams = 4;
+  std::vector<std::pair<int, int>> sp_corr_rng, sp_sub_rng;   // per group: panels, subdomains
+  cudaEvent_t sp_ev[3] = {};   // factorize start, factorize end, assemble end
+  std::vector<int> sp_bad_init;
+  bool sp_pending_check = false;   // pivots of the last factorize not yet checked
   cudaStream_t sp_streams[kSpStreams] = {};
   cudaEvent_t sp_join[kSpStreams] = {};
   double sp_flops = 0.0;
@@ -296,25 +300,41 @@ int build_sparse_tasks(feti_ctx* c) {
         const int slot = P.tmap[(size_t)K * P.Tq + L];
         if (slot >= 0) init.push_back(SpInit{s.d_pool + (size_t)slot * TILE, K, L, si, 0});
       }
-    if (s.sp_r > 0)
-      for (int p = 0; p < s.P; ++p) panels.push_back(make_int2(si, p));
     c->sp_flops += P.flops_exec;
+  }
+  // correction work per group (contiguous subdomain ranges, as the waves)
+  c->sp_corr_rng.assign(c->sp_groups, {0, 0});
+  c->sp_sub_rng.assign(c->sp_groups, {0, 0});
+  for (int g = 0; g < c->sp_groups; ++g) {
+    const std::vector<int>& wv = c->waves[g];
+    const int b = (int)panels.size();
+    for (int si : wv)
+      if (c->subs[si].sp_r > 0)
+        for (int p = 0; p < c->subs[si].P; ++p) panels.push_back(make_int2(si, p));
+    c->sp_corr_rng[g] = {b, (int)panels.size() - b};
+    c->sp_sub_rng[g] = {wv.empty() ? 0 : wv.front(), (int)wv.size()};
   }
   std::vector<SpTask> tasks;
   std::vector<SpPair> pairs;
   std::vector<SpDiag> diag;
-  const char* genv = getenv("FETI_SP_GROUPS");
-  int G = genv ? atoi(genv) : feti_ctx::kSpStreams;
-  G = std::max(1, std::min(std::min(G, (int)feti_ctx::kSpStreams), std::max(ns, 1)));
-  c->sp_groups = G;
+  const int G = c->sp_groups;
   c->sp_maxTq = maxTq;
   c->sp_acc_rng.assign((size_t)G * maxTq, {0, 0});
   c->sp_panel_rng.assign((size_t)G * maxTq, {0, 0});
   c->sp_diag_rng.assign((size_t)G * maxTq, {0, 0});
+  // equal priorities by default.  FETI_SP_STAGGER=1 ranks the groups (group 0
+  // first) so early groups' assembly overlaps later factorization: the tail
+  // shrinks (c3 15 -> 6 ms) but the factorization loses more concurrency
+  // than that (61 -> 78 ms), so it is off
+  int prio_lo = 0, prio_hi = 0;
+  CUDA_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  const bool stagger = getenv("FETI_SP_STAGGER") != nullptr;
   for (int g = 0; g < G; ++g) {
-    CUDA_TRY(cudaStreamCreateWithFlags(&c->sp_streams[g], cudaStreamNonBlocking));
+    const int prio = stagger ? std::min(prio_lo, prio_hi + g) : prio_lo;   // numerically lower = higher priority
+    CUDA_TRY(cudaStreamCreateWithPriority(&c->sp_streams[g], cudaStreamNonBlocking, prio));
     CUDA_TRY(cudaEventCreateWithFlags(&c->sp_join[g], cudaEventDisableTiming));
   }
+  for (auto& e : c->sp_ev) CUDA_TRY(cudaEventCreate(&e));
   // contiguous groups of subdomains
   auto group_of = [&](int si) { return (int)((int64_t)si * G / std::max(ns, 1)); };
   // slots of the (P Q)^T block row: their tasks run "thin" (rows < 8 only)
@@ -480,9 +500,9 @@ int factorize_sparse(feti_ctx* c) {
   int rc;
   c->subdev_dirty = true;
   if ((rc = sync_subdev(c))) return rc;
-  std::vector<int> big(ns, 1 << 30);
-  CUDA_TRY(cudaMemcpyAsync(c->d_bad, big.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaEventRecord(c->ev[0], st));
+  c->sp_bad_init.assign(ns, 1 << 30);
+  CUDA_TRY(cudaMemcpyAsync(c->d_bad, c->sp_bad_init.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaEventRecord(c->sp_ev[0], st));
   launch_sp_init(c->d_sp_init, c->n_sp_init, c->d_spsub, st);
   launch_sp_scatter(c->d_spsub, ns, c->sp_max_n, st);
   CUDA_TRY(cudaGetLastError());
@@ -530,20 +550,15 @@ int factorize_sparse(feti_ctx* c) {
     CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
   }
   }
-  CUDA_TRY(cudaEventRecord(c->ev[1], st));
-  CUDA_TRY(cudaMemcpyAsync(big.data(), c->d_bad, ns * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  float ms = 0;
-  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
-  c->stats.ms_factorize = ms;
+  // the factorization end on the context stream (timing only); no host sync:
+  // feti_assemble runs each group's assembly right behind its factorization
+  // on the group's stream and checks the pivots once everything finished
+  CUDA_TRY(cudaEventRecord(c->sp_ev[1], st));
   c->stats.flops_factor_exec = c->sp_flops;
   c->stats.launches_factorize = launches;
-  for (int si = 0; si < ns; ++si)
-    if (big[si] < (1 << 30))
-      return fail(FETI_ERR_NOT_SPD, "slot %d: non-positive pivot at permuted row %d: matrix is not SPD", si,
-                  big[si]);
   for (auto& s : c->subs) s.factor_set = true;
   c->tiles_fresh = true;
+  c->sp_pending_check = true;
   return FETI_OK;
 }
 
@@ -595,6 +610,8 @@ int feti_destroy(feti_ctx* c) {
     if (c->wave_join[i]) cudaEventDestroy(c->wave_join[i]);
     if (c->wave_streams[i]) cudaStreamDestroy(c->wave_streams[i]);
   }
+  for (auto& e : c->sp_ev)
+    if (e) cudaEventDestroy(e);
   for (int g = 0; g < feti_ctx::kSpStreams; ++g) {
     if (c->sp_join[g]) cudaEventDestroy(c->sp_join[g]);
     if (c->sp_streams[g]) cudaStreamDestroy(c->sp_streams[g]);
@@ -810,9 +827,23 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
       }
     }
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
-    const int nw = (int)std::min<size_t>(c->subs.size(), 8);
-    c->waves.assign(nw, {});
-    for (size_t k = 0; k < order.size(); ++k) c->waves[k * nw / order.size()].push_back(order[k]);
+    int nw = (int)std::min<size_t>(c->subs.size(), 8);
+    if (c->sparse_factor) {
+      // sparse route: the waves are the factorization groups (contiguous
+      // subdomain ranges), so each group's assembly follows its own
+      // factorization on its stream
+      const char* genv = getenv("FETI_SP_GROUPS");
+      const int ns = (int)c->subs.size();
+      int G = genv ? atoi(genv) : feti_ctx::kSpStreams;
+      G = std::max(1, std::min(std::min(G, (int)feti_ctx::kSpStreams), std::max(ns, 1)));
+      c->sp_groups = G;
+      nw = G;
+      c->waves.assign(nw, {});
+      for (int si = 0; si < ns; ++si) c->waves[(int)((int64_t)si * G / ns)].push_back(si);
+    } else {
+      c->waves.assign(nw, {});
+      for (size_t k = 0; k < order.size(); ++k) c->waves[k * nw / order.size()].push_back(order[k]);
+    }
     std::vector<int> wave_of(c->subs.size());
     for (int w = 0; w < nw; ++w)
       for (int si : c->waves[w]) wave_of[si] = w;
@@ -1033,7 +1064,7 @@ int feti_assemble(feti_ctx* c) {
   if (!c->finalized) return fail(FETI_ERR_LIFECYCLE, "preprocess before prepare");
   for (size_t i = 0; i < c->subs.size(); ++i)
     if (!c->subs[i].factor_set) return fail(FETI_ERR_LIFECYCLE, "subdomain slot %zu has no factor values", i);
-  if (c->device_factor && !c->tiles_fresh)
+  if ((c->device_factor || c->sparse_factor) && !c->tiles_fresh)
     return fail(FETI_ERR_LIFECYCLE, "assemble needs a new feti_factorize (the tiles were already scaled)");
   c->tiles_fresh = false;
   CUDA_TRY(cudaSetDevice(c->device));
@@ -1049,6 +1080,52 @@ int feti_assemble(feti_ctx* c) {
   feti_stats& S = c->stats;
   CUDA_TRY(cudaEventRecord(c->ev[0], st));
   if (c->subdev_dirty && (rc = sync_subdev(c))) return rc;
+  if (c->sparse_factor) {
+    // sparse route: each group's assembly + correction on the group's stream,
+    // right behind its factorization (the persistent scheduler ran on the
+    // context stream: the groups wait for it)
+    const int G = c->sp_groups;
+    CUDA_TRY(cudaEventRecord(c->ev[2], st));
+    const auto& r = c->wv_range;
+    for (int g = 0; g < G; ++g) {
+      cudaStream_t gs = c->sp_streams[g];
+      if (c->sp_use_dag) CUDA_TRY(cudaStreamWaitEvent(gs, c->ev[2], 0));
+      std::vector<int> none;
+      if ((rc = launch_assembly(c, gs, c->d_wv[0] + r[0][g].first, r[0][g].second, c->d_wv[1] + r[1][g].first,
+                                r[1][g].second, c->d_wv[2] + r[2][g].first, r[2][g].second,
+                                c->d_wv[3] + r[3][g].first, r[3][g].second, c->d_wv[4] + r[4][g].first,
+                                r[4][g].second, none, nullptr, &launches)))
+        return rc;
+      launch_sp_correct(c->d_subdev, c->d_spsub, c->d_sp_panels + c->sp_corr_rng[g].first, c->sp_corr_rng[g].second,
+                        c->sp_sub_rng[g].first, c->sp_sub_rng[g].second, c->sp_max_T32, gs);
+      launches += 2;
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaEventRecord(c->sp_join[g], gs));
+      CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
+    }
+    CUDA_TRY(cudaEventRecord(c->sp_ev[2], st));
+    std::vector<int> bad(c->subs.size(), 1 << 30);
+    if (!c->subs.empty())
+      CUDA_TRY(cudaMemcpyAsync(bad.data(), c->d_bad, bad.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    float mf = 0, mp = 0;
+    CUDA_TRY(cudaEventElapsedTime(&mf, c->sp_ev[0], c->sp_ev[1]));
+    CUDA_TRY(cudaEventElapsedTime(&mp, c->sp_ev[0], c->sp_ev[2]));
+    S.ms_factorize = mf;
+    S.ms_preprocess = mp;
+    S.ms_wait_upload = 0.0;
+    S.ms_unpack = S.ms_diag_inverse = S.ms_block_scale = S.ms_trsm = S.ms_syrk = S.ms_correct = 0.0;
+    S.ms_assemble = mp - mf;   // past the last group's factorization
+    S.factor_bytes = 0.0;
+    S.launches_assemble = launches;
+    c->sp_pending_check = false;
+    for (size_t si = 0; si < bad.size(); ++si)
+      if (bad[si] < (1 << 30))
+        return fail(FETI_ERR_NOT_SPD, "slot %d: non-positive pivot at permuted row %d: matrix is not SPD", (int)si,
+                    bad[si]);
+    c->assembled = true;
+    return FETI_OK;
+  }
   if (!pending) {
     // factors resident on the device: one batched launch per kernel over all
     // subdomains (largest chains first)
@@ -1058,13 +1135,6 @@ int feti_assemble(feti_ctx* c) {
     if ((rc = launch_assembly(c, st, c->d_w_unpack, c->n_unpack, c->d_w_diag, c->n_diag, c->d_w_scale, c->n_scale,
                               c->d_w_chain, c->n_chain, c->d_w_syrk, c->n_syrk, sparse, &c->ev[1], &launches)))
       return rc;
-    if (c->sparse_factor) {
-      launch_sp_correct(c->d_subdev, c->d_spsub, c->d_sp_panels, c->n_sp_panels, (int)c->subs.size(),
-                        c->sp_max_T32, st);
-      launches += 2;
-      CUDA_TRY(cudaGetLastError());
-      FETI_DEBUG_SYNC(st);
-    }
     CUDA_TRY(cudaEventRecord(c->ev[7], st));
     CUDA_TRY(cudaStreamSynchronize(st));
     float ms[5];

@@ -507,9 +507,9 @@ __global__ void __launch_bounds__(TB) sp_u2_kernel(const SubDev* __restrict__ su
 // F[a][b] += U1[a] . W[b] - U2[a] . U1[b] over every stored apply tile
 // (grid: tile row ti x subdomain; diagonal tiles are stored full)
 __global__ void __launch_bounds__(256) sp_correct_kernel(const SubDev* __restrict__ subs,
-                                                         const SpSub* __restrict__ ss) {
-  const SubDev& S = subs[blockIdx.y];
-  const SpSub& Q = ss[blockIdx.y];
+                                                         const SpSub* __restrict__ ss, int sub0) {
+  const SubDev& S = subs[sub0 + blockIdx.y];
+  const SpSub& Q = ss[sub0 + blockIdx.y];
   const int ti = blockIdx.x, T32 = S.T32, r = Q.r;
   if (ti >= T32 || r == 0) return;
   __shared__ double u1a[AT * MAXR], u2a[AT * MAXR];
@@ -673,10 +673,10 @@ void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st) {
   if (nd > 0) sp_potrf_kernel<<<nd, 256, sp_potrf_smem(), st>>>(d, bad);
 }
 
-void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int nsub, int max_T32,
-                       cudaStream_t st) {
+void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int sub0, int nsub,
+                       int max_T32, cudaStream_t st) {
   if (npanels > 0) sp_u2_kernel<<<npanels, TB, 0, st>>>(subs, ss, panels);
-  if (nsub > 0 && max_T32 > 0) sp_correct_kernel<<<dim3(max_T32, nsub), 256, 0, st>>>(subs, ss);
+  if (nsub > 0 && max_T32 > 0) sp_correct_kernel<<<dim3(max_T32, nsub), 256, 0, st>>>(subs, ss, sub0);
 }
 
 }  // namespace feti

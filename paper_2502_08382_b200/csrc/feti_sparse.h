@@ -108,7 +108,8 @@ void launch_sp_scatter(const SpSub* ss, int nsub, int max_n, cudaStream_t st);
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st);
 void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st);
 // after the assembly: U2/W per (sub, panel), then the rank-2r update of F~
-void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int nsub, int max_T32,
+void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int sub0, int nsub,
+                       int max_T32,
                        cudaStream_t st);
 
 }  // namespace feti

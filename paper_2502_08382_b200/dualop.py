@@ -453,16 +453,20 @@ class DualOperator:
                                                _lib.f64ptr(dt), ip[-1], _lib.f64ptr(q), q.shape[1], rho,
                                                _lib.i64ptr(sub.perm)))
         t1 = time.perf_counter()
-        try:
-            _lib.check(self._lib.feti_factorize(self._ctx))
-        except _lib.FetiError as err:
-            if err.code == _lib.FETI_ERR_NOT_SPD:
-                slot = int(str(err).split()[1].rstrip(":"))
-                index = next(s.index for s in self._subs.values() if s.slot == slot)
-                msg = str(err).split(":", 1)[1].strip()
-                raise SpdError(f"subdomain {index}: {msg}") from None
-            _raise_from(err)
-        self.assemble()
+        # the sparse route reports a non-SPD pivot from feti_assemble (it
+        # checks the pivots once the overlapped factorization/assembly ended)
+        for fn in (self._lib.feti_factorize, self._lib.feti_assemble):
+            try:
+                _lib.check(fn(self._ctx))
+            except _lib.FetiError as err:
+                self.step_ready = False
+                if err.code == _lib.FETI_ERR_NOT_SPD:
+                    slot = int(str(err).split()[1].rstrip(":"))
+                    index = next(s.index for s in self._subs.values() if s.slot == slot)
+                    msg = str(err).split(":", 1)[1].strip()
+                    raise SpdError(f"subdomain {index}: {msg}") from None
+                _raise_from(err)
+        self.step_ready = True
         t2 = time.perf_counter()
         self.timings = {"stiffness_upload_s": t1 - t0, "device_factorization_and_assembly_s": t2 - t1,
                         "device_factorization_ms": self.stats()["ms_factorize"]}
