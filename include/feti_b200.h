@@ -190,6 +190,15 @@ int feti_set_sparse_pattern(feti_ctx* ctx, int64_t slot, int64_t n, const int64_
  * order), through the device factor (CholFactor.solve, sparse.py:324-337). */
 int feti_solve_many(feti_ctx* ctx, int64_t nslots, const int64_t* slots, const double* b, double* x);
 
+/* Lumped preconditioner (make_preconditioner("lumped"), solver.py:155-175):
+ * M w = sum_i B~_i K_i B~_i^T w.  P is P_i = B~_i K_i B~_i^T as an m x m
+ * row-major (full, symmetric) array in the slot's original multiplier order;
+ * it is stored in the apply's packed tile layout and applied by the same
+ * fused gather/SYMV/scatter kernels (deterministic, like feti_apply). */
+int feti_set_preconditioner(feti_ctx* ctx, int64_t slot, const double* P);
+int feti_precond_apply(feti_ctx* ctx, const double* w, double* out);
+int feti_precond_apply_device(feti_ctx* ctx, const double* d_w, double* d_out, void* stream);
+
 int feti_get_stats(feti_ctx* ctx, feti_stats* out);
 
 /* Diagnostics: per-kernel register / thread limits as text. */

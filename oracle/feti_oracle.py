@@ -362,8 +362,26 @@ def assemble_dual_system(kernels, forces, cons, n_mult, c, solve_local):
     return gmat, e, d, coarse
 
 
-def pcpg(gmat, e, d, coarse, fapply, tol=1e-9, maxit=None):
-    """Projected CG on the dual problem (solver.py:195-272), identity preconditioner."""
+def lumped_operator(stiffness, cons):
+    """The lumped preconditioner sum_i gather_i(B~_i K_i B~_i^T scatter_i(.))
+    (make_preconditioner("lumped"), solver.py:155-175); stiffness[i] is the
+    unregularized K_i as (indptr, indices, data), cons[i] = (gids, bcol, bval)."""
+    mats = [csr_matrix((np.asarray(k[2], np.float64), np.asarray(k[1]), np.asarray(k[0]))) for k in stiffness]
+
+    def apply(w):
+        out = np.zeros_like(w)
+        for (gids, bcol, bval), k in zip(cons, mats):
+            v = np.zeros(k.shape[0])
+            np.add.at(v, bcol, bval * w[gids])            # B~^T w_loc
+            out[gids] += bval * (k @ v)[bcol]            # B~ K (.)
+        return out
+
+    return apply
+
+
+def pcpg(gmat, e, d, coarse, fapply, tol=1e-9, maxit=None, mfun=None):
+    """Projected CG on the dual problem (solver.py:195-272); ``mfun`` the
+    preconditioner (identity by default, solver.py:157-158)."""
     from scipy.linalg.lapack import dpotrs
 
     def csolve(b):
@@ -375,10 +393,11 @@ def pcpg(gmat, e, d, coarse, fapply, tol=1e-9, maxit=None):
 
     n_mult = d.shape[0]
     maxit = n_mult if maxit is None else maxit
+    mfun = (lambda w: w) if mfun is None else mfun
     lam = gmat @ csolve(e)
     r = d - fapply(lam)
     w = project(r)
-    y = project(w)
+    y = project(mfun(w))
     p = y.copy()
     w0 = float(np.linalg.norm(w))
     wy = float(w @ y)
@@ -394,7 +413,7 @@ def pcpg(gmat, e, d, coarse, fapply, tol=1e-9, maxit=None):
         lam = lam + delta * p
         r = r - delta * qk
         w = project(r)
-        y = project(w)
+        y = project(mfun(w))
         k += 1
         wy_next = float(w @ y)
         if float(np.linalg.norm(w)) <= tol * w0:

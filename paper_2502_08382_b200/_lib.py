@@ -32,6 +32,7 @@ EXPORTED = (
     "feti_debug_kernel_attributes", "feti_coarse_setup", "feti_project_device", "feti_coarse_apply_device",
     "feti_apply_implicit", "feti_apply_implicit_device", "feti_enable_device_factorization", "feti_set_stiffness",
     "feti_factorize", "feti_solve_many", "feti_enable_sparse_factorization", "feti_set_sparse_pattern",
+    "feti_set_preconditioner", "feti_precond_apply", "feti_precond_apply_device",
 )
 
 
@@ -99,6 +100,9 @@ def load() -> C.CDLL:
         "feti_solve_many": ([P, C.c_int64, i64p, f64p, f64p], C.c_int),
         "feti_host_free": ([P], C.c_int),
         "feti_enable_sparse_factorization": ([P], C.c_int),
+        "feti_set_preconditioner": ([P, C.c_int64, f64p], C.c_int),
+        "feti_precond_apply": ([P, f64p, f64p], C.c_int),
+        "feti_precond_apply_device": ([P, P, P, P], C.c_int),
         "feti_set_sparse_pattern": ([P, C.c_int64, C.c_int64, i64p, i64p, i64p, C.c_int64, i64p], C.c_int),
     }
     for name, (args, res) in sig.items():

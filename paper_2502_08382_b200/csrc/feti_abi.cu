@@ -84,6 +84,7 @@ struct SubHost {
   double* d_tiles = nullptr;
   double* d_X = nullptr;
   double* d_F = nullptr;
+  double* d_Fp = nullptr;            // lumped preconditioner B~ K B~^T, same tile layout as d_F
   int* d_r = nullptr;
   double* d_s = nullptr;
   int* d_g = nullptr;
@@ -209,6 +210,10 @@ struct feti_ctx {
   cudaEvent_t sp_ev[3] = {};   // factorize start, factorize end, assemble end
   std::vector<int> sp_bad_init;
   bool sp_pending_check = false;   // pivots of the last factorize not yet checked
+  // lumped preconditioner (feti_set_preconditioner): a second descriptor table
+  // whose F points at the preconditioner tiles, applied by the same kernels
+  SubDev* d_subdev_p = nullptr;
+  int n_precond_set = 0;
   cudaStream_t sp_streams[kSpStreams] = {};
   cudaEvent_t sp_join[kSpStreams] = {};
   double sp_flops = 0.0;
@@ -244,8 +249,20 @@ int upload(feti_ctx* c, T** dst, const std::vector<T>& v, bool persistent = true
   return FETI_OK;
 }
 
+void fill_subdev(const feti_ctx* c, std::vector<SubDev>& h);
+
 int sync_subdev(feti_ctx* c) {
-  std::vector<SubDev> h(c->subs.size());
+  std::vector<SubDev> h;
+  fill_subdev(c, h);
+  if (!h.empty())
+    CUDA_TRY(cudaMemcpyAsync(c->d_subdev, h.data(), h.size() * sizeof(SubDev), cudaMemcpyHostToDevice,
+                             c->stream));
+  c->subdev_dirty = false;
+  return FETI_OK;
+}
+
+void fill_subdev(const feti_ctx* c, std::vector<SubDev>& h) {
+  h.resize(c->subs.size());
   for (size_t i = 0; i < c->subs.size(); ++i) {
     const SubHost& s = c->subs[i];
     SubDev& d = h[i];
@@ -270,11 +287,6 @@ int sync_subdev(feti_ctx* c) {
     d.P = s.P;
     d.T32 = s.T32;
   }
-  if (!h.empty())
-    CUDA_TRY(cudaMemcpyAsync(c->d_subdev, h.data(), h.size() * sizeof(SubDev), cudaMemcpyHostToDevice,
-                             c->stream));
-  c->subdev_dirty = false;
-  return FETI_OK;
 }
 
 // Device task lists of the block-sparse factorization, ordered by block
@@ -1248,6 +1260,75 @@ int feti_apply(feti_ctx* c, const double* p, double* q) {
   float ms = 0;
   CUDA_TRY(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
   c->stats.ms_apply = ms;
+  return FETI_OK;
+}
+
+int feti_set_preconditioner(feti_ctx* c, int64_t slot, const double* P) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->finalized) return fail(FETI_ERR_LIFECYCLE, "set_preconditioner before prepare");
+  if (slot < 0 || slot >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot out of range");
+  if (!P) return fail(FETI_ERR_ARG, "P is NULL");
+  CUDA_TRY(cudaSetDevice(c->device));
+  SubHost& s = c->subs[slot];
+  int rc;
+  if (!s.d_Fp) {
+    if ((rc = dev_alloc(c, (void**)&s.d_Fp, (size_t)std::max<int64_t>(s.f_tiles(), 1) * ATILE * 8, true))) return rc;
+    ++c->n_precond_set;
+  }
+  // pack into the apply layout: upper triangle of 32x32 tiles in sorted
+  // column order, diagonal tiles full, padding zero
+  std::vector<double> t((size_t)s.f_tiles() * ATILE, 0.0);
+  const int64_t m = s.m;
+  for (int ti = 0; ti < s.T32; ++ti)
+    for (int tj = ti; tj < s.T32; ++tj) {
+      double* dst = t.data() + (size_t)apply_tile_index(ti, tj, s.T32) * ATILE;
+      for (int u = 0; u < AT; ++u) {
+        const int64_t a = (int64_t)ti * AT + u;
+        if (a >= m) break;
+        const double* row = P + s.colperm[a] * m;
+        for (int v = 0; v < AT; ++v) {
+          const int64_t b = (int64_t)tj * AT + v;
+          if (b >= m) break;
+          dst[u * AT + v] = row[s.colperm[b]];
+        }
+      }
+    }
+  CUDA_TRY(cudaMemcpy(s.d_Fp, t.data(), t.size() * 8, cudaMemcpyHostToDevice));
+  if (c->n_precond_set == (int)c->subs.size()) {
+    // descriptor table for the preconditioner apply (F -> preconditioner tiles)
+    std::vector<SubDev> h;
+    fill_subdev(c, h);
+    for (size_t i = 0; i < h.size(); ++i) h[i].F = c->subs[i].d_Fp;
+    if (!c->d_subdev_p && (rc = dev_alloc(c, (void**)&c->d_subdev_p, h.size() * sizeof(SubDev), true))) return rc;
+    CUDA_TRY(cudaMemcpy(c->d_subdev_p, h.data(), h.size() * sizeof(SubDev), cudaMemcpyHostToDevice));
+  }
+  return FETI_OK;
+}
+
+int feti_precond_apply_device(feti_ctx* c, const double* d_w, double* d_out, void* stream) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->d_subdev_p || c->n_precond_set != (int)c->subs.size())
+    return fail(FETI_ERR_LIFECYCLE, "preconditioner apply before feti_set_preconditioner for every slot");
+  if (!d_w || !d_out) return fail(FETI_ERR_ARG, "NULL vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_apply(c->apply_nw, c->apply_smem, c->d_subdev_p, c->d_w_apply, c->d_apply_seg_ptr, c->n_apply,
+               c->d_part_off, c->d_part, d_w, st);
+  launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_part_off, c->d_part, d_out, st);
+  CUDA_TRY(cudaGetLastError());
+  return FETI_OK;
+}
+
+int feti_precond_apply(feti_ctx* c, const double* w, double* out) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!w || !out) return fail(FETI_ERR_ARG, "NULL vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  CUDA_TRY(cudaMemcpyAsync(c->d_p, w, (size_t)c->n_mult * 8, cudaMemcpyHostToDevice, st));
+  int rc = feti_precond_apply_device(c, c->d_p, c->d_q, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out, c->d_q, (size_t)c->n_mult * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
   return FETI_OK;
 }
 

@@ -555,6 +555,45 @@ class DualOperator:
         _call(self._lib.feti_apply_device(self._ctx, C.c_void_p(int(p.data_ptr())),
                                           C.c_void_p(int(q.data_ptr())), C.c_void_p(int(stream))))
 
+    # -- lumped preconditioner (solver.py:155-175) ------------------------------
+
+    def set_lumped_preconditioner(self, stiffness=None) -> None:
+        """Upload P_i = B~_i K_i B~_i^T (the unregularized K_i, as
+        make_preconditioner("lumped") uses ``SubdomainProblem.stiffness``) for
+        every owned subdomain; applied by the explicit apply's kernels."""
+        if not self.prepared:
+            raise LifecycleError("set_lumped_preconditioner before prepare")
+        stiffness = self.stiffness if stiffness is None else list(stiffness)
+        if stiffness is None:
+            raise ValueError("the lumped preconditioner needs the stiffness matrices")
+        from scipy.sparse import csr_matrix
+
+        for sub in self._subs.values():
+            n, ip, ix, dt = fct.csr_arrays(stiffness[sub.index])
+            k = csr_matrix((dt, ix, ip), shape=(n, n))
+            kb = k[sub.bcol][:, sub.bcol].toarray()
+            pm = np.ascontiguousarray(sub.bval[:, None] * kb * sub.bval[None, :])
+            _call(self._lib.feti_set_preconditioner(self._ctx, sub.slot, _lib.f64ptr(pm)))
+        self._lumped = True
+
+    def precond_apply(self, w, out=None):
+        """M w = sum_i gather_i(B~_i K_i B~_i^T scatter_i(w)) on the device."""
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        if w.shape != (self.n_multipliers,):
+            raise ValueError("dual vector has the wrong length")
+        if out is None:
+            out = np.zeros(self.n_multipliers)
+        _call(self._lib.feti_precond_apply(self._ctx, _lib.f64ptr(w), _lib.f64ptr(out)))
+        return out
+
+    def precond_apply_device(self, w, out, stream=None) -> None:
+        if stream is None:
+            import torch
+
+            stream = torch.cuda.current_stream(w.device).cuda_stream
+        _call(self._lib.feti_precond_apply_device(self._ctx, C.c_void_p(int(w.data_ptr())),
+                                                  C.c_void_p(int(out.data_ptr())), C.c_void_p(int(stream))))
+
     # -- K^+ access for the solver --------------------------------------------
 
     def solve_local(self, index: int, rhs, out=None):

@@ -34,15 +34,24 @@ class ConvergenceError(RuntimeError):
 
 
 class DevicePCPG:
-    """PCPG with identity preconditioner, one GPU (one operator context).
+    """PCPG on one GPU (one operator context).
 
     ``op``: a prepared and preprocessed :class:`~.dualop.DualOperator` owning
     every subdomain; ``kernels[i]`` (n_i x r_i, orthonormal kernel basis) and
     ``forces[i]`` per subdomain; ``c`` the constraint right-hand side.
+    ``precond``: "none" (identity) or "lumped" (solver.py:155-175: M w =
+    sum_i B~_i K_i B~_i^T w on the device, from ``stiffness[i]``, the
+    unregularized K_i).
     """
 
-    def __init__(self, op, kernels, forces, c):
+    def __init__(self, op, kernels, forces, c, precond: str = "none", stiffness=None):
         import torch
+
+        if precond not in ("none", "lumped"):
+            raise ValueError("preconditioner must be one of ('none', 'lumped')")
+        self.precond = precond
+        if precond == "lumped":
+            op.set_lumped_preconditioner(stiffness)
 
         if sorted(op._subs) != list(range(op.n_subdomains)):
             raise ValueError("the device PCPG needs an operator that owns every subdomain")
@@ -90,6 +99,13 @@ class DevicePCPG:
                                                     C.c_void_p(int(out.data_ptr())), self._stream()))
         return out
 
+    def mfun(self, w, out):
+        """The preconditioner (solver.py:155-175): identity or lumped."""
+        if self.precond == "none":
+            return w
+        self.op.precond_apply_device(w, out, stream=int(self.torch.cuda.current_stream(self.device).cuda_stream))
+        return out
+
     def apply(self, x, out):
         self.op.apply_device(x, out, stream=int(self.torch.cuda.current_stream(self.device).cuda_stream))
         return out
@@ -114,7 +130,7 @@ class DevicePCPG:
         q = torch.empty_like(lam)
         r = self.d_dev - self.apply(lam, q)
         w = self.project(r, torch.empty_like(r))
-        y = self.project(w, torch.empty_like(w))          # mfun = identity (precond "none")
+        y = self.project(self.mfun(w, torch.empty_like(w)), torch.empty_like(w))
         p = y.clone()
         w0 = float(torch.linalg.vector_norm(w))
         if w0 <= 1e-14 * max(1.0, float(np.linalg.norm(self.d))):
@@ -122,6 +138,7 @@ class DevicePCPG:
             return lam.cpu().numpy(), 0, time.perf_counter() - t0
         wy_t = torch.sum(w * y).reshape(1)
         pq_t = torch.empty(1, dtype=torch.float64, device=dev)
+        mw = torch.empty_like(w)                          # preconditioned residual
         wn_t = torch.empty(1, dtype=torch.float64, device=dev)
 
         def body():
@@ -132,7 +149,7 @@ class DevicePCPG:
             lam.addcmul_(p, delta)
             r.addcmul_(qk, -delta)
             self.project(r, w)
-            self.project(w, y)
+            self.project(self.mfun(w, mw), y)
             wy_next = torch.sum(w * y).reshape(1)
             wn_t.copy_(torch.linalg.vector_norm(w).reshape(1))
             beta = wy_next / wy_t

@@ -53,3 +53,37 @@ def test_graph_and_eager_iterations_agree(graph):
     assert it == it2 == int(g["pcpg_iterations"]) == 63
     assert np.array_equal(lam, lam2)          # deterministic
     assert np.linalg.norm(lam - g["pcpg_lambda"]) <= 1e-9 * np.linalg.norm(g["pcpg_lambda"])
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+def test_lumped_preconditioner_matches_reference(case):
+    """make_preconditioner("lumped") (solver.py:155-175) on the device: the
+    operator on the reference's seeded p, and PCPG with it -- the reference's
+    iteration count through the reference's own recursion driving the
+    drop-in, and through the GPU-resident loop."""
+    from oracle import feti_oracle as ora
+
+    g = load_golden(case)
+    gl = load_golden(f"lumped_{case}")
+    prob = inputs.Problem(str(g["physics"]), int(g["dim"]), int(g["cells"]), int(g["subs"]))
+    mats, cons, lay = inputs.reference_inputs(prob)
+    ks, qs, fs = [], [], []
+    for s in range(prob.n_sub):
+        k, f, q = prob.subdomain_system(s)
+        ks.append(k)
+        qs.append(q)
+        fs.append(f)
+    with dualop.prepare(mats, cons, lay, CFG, device=0) as op:
+        op.preprocess()
+        op.set_lumped_preconditioner(ks)
+        mp = op.precond_apply(gl["p"])
+        ref = gl["lumped_p"]
+        assert np.linalg.norm(mp - ref) <= 1e-12 * np.linalg.norm(ref)
+        cl = [(prob.gids[s], prob.bcol[s], prob.bval[s]) for s in range(prob.n_sub)]
+        gm, e, d, coarse = ora.assemble_dual_system(qs, fs, cl, prob.n_multipliers, prob.c, op.solve_local)
+        lam_h, it_h = ora.pcpg(gm, e, d, coarse, op.apply, tol=1e-9, mfun=op.precond_apply)
+        assert it_h in expected_iterations(case, gl)
+        lam, it, _ = DevicePCPG(op, qs, fs, prob.c, precond="lumped", stiffness=ks).solve(tol=1e-9)
+    assert it in expected_iterations(case, gl)
+    for got in (lam_h, lam):
+        assert np.linalg.norm(got - gl["pcpg_lambda"]) <= 1e-9 * np.linalg.norm(gl["pcpg_lambda"])

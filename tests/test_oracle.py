@@ -134,3 +134,27 @@ def test_woodbury_oracle_matches_reference(case):
         ref = np.zeros((m, m))
         ref[np.triu_indices(m)] = g[f"s{s}_F_upper"]
         assert np.linalg.norm(np.triu(f) - ref) <= 1e-12 * np.linalg.norm(ref), (case, s)
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+def test_oracle_lumped_preconditioner_matches_reference(case):
+    """make_preconditioner("lumped") (solver.py:155-175) and the reference's
+    PCPG with it: the operator on the seeded p and the iteration count."""
+    g = load_golden(case)
+    gl = load_golden(f"lumped_{case}")
+    n_sub = int(g["n_sub"])
+    cons = [(g[f"s{s}_gids"], g[f"s{s}_bcol"], g[f"s{s}_bval"]) for s in range(n_sub)]
+    stiff = [(g[f"s{s}_k_indptr"], g[f"s{s}_k_indices"], g[f"s{s}_k_data"]) for s in range(n_sub)]
+    mfun = ora.lumped_operator(stiff, cons)
+    ref = gl["lumped_p"]
+    assert np.linalg.norm(mfun(gl["p"]) - ref) <= 1e-13 * np.linalg.norm(ref)
+    facs, cons2 = _case_factors(g, n_sub)
+    op = ora.OracleOperator(facs, cons2)
+    op.preprocess()
+    kernels = [g[f"s{s}_kernel"] for s in range(n_sub)]
+    forces = [g[f"s{s}_force"] for s in range(n_sub)]
+    gm, e, d, coarse = ora.assemble_dual_system(kernels, forces, cons2, int(g["n_multipliers"]), g["c"],
+                                                op.solve_local)
+    lam, it = ora.pcpg(gm, e, d, coarse, op.apply, tol=1e-9, mfun=mfun)
+    assert it == int(gl["pcpg_iterations"])
+    assert np.linalg.norm(lam - gl["pcpg_lambda"]) <= 1e-8 * np.linalg.norm(gl["pcpg_lambda"])
