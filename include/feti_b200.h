@@ -199,6 +199,23 @@ int feti_set_preconditioner(feti_ctx* ctx, int64_t slot, const double* P);
 int feti_precond_apply(feti_ctx* ctx, const double* w, double* out);
 int feti_precond_apply_device(feti_ctx* ctx, const double* d_w, double* d_out, void* stream);
 
+/* Multi-GPU apply with the exchange fused into the reduction (one process
+ * per GPU, this context = this rank's cluster, decomposition.py:227-243).
+ * The reduction kernel stores its per-multiplier sums straight into every
+ * rank's receive slab over NVLink (CUDA IPC peer memory) and publishes an
+ * epoch flag; a second kernel waits for all ranks and sums the slabs in rank
+ * order, so q is identical on every rank and deterministic.  Replaces the
+ * apply + all-reduce pair.  Setup: feti_exchange_setup returns this rank's
+ * IPC handle (FETI_IPC_HANDLE_BYTES), the caller all-gathers the handles
+ * (rank order) and passes them to feti_exchange_connect.  Every rank must
+ * issue the same number of exchange applies; a rank that waits ~2 s for a
+ * peer gives up and feti_exchange_status reports it. */
+#define FETI_IPC_HANDLE_BYTES 64
+int feti_exchange_setup(feti_ctx* ctx, int rank, int world, char* handle_out);
+int feti_exchange_connect(feti_ctx* ctx, const char* handles);
+int feti_apply_exchange_device(feti_ctx* ctx, const double* d_p, double* d_q, void* stream);
+int feti_exchange_status(feti_ctx* ctx);
+
 int feti_get_stats(feti_ctx* ctx, feti_stats* out);
 
 /* Diagnostics: per-kernel register / thread limits as text. */

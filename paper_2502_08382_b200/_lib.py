@@ -33,7 +33,9 @@ EXPORTED = (
     "feti_apply_implicit", "feti_apply_implicit_device", "feti_enable_device_factorization", "feti_set_stiffness",
     "feti_factorize", "feti_solve_many", "feti_enable_sparse_factorization", "feti_set_sparse_pattern",
     "feti_set_preconditioner", "feti_precond_apply", "feti_precond_apply_device",
+    "feti_exchange_setup", "feti_exchange_connect", "feti_apply_exchange_device", "feti_exchange_status",
 )
+FETI_IPC_HANDLE_BYTES = 64
 
 
 class FetiStats(C.Structure):
@@ -101,6 +103,10 @@ def load() -> C.CDLL:
         "feti_host_free": ([P], C.c_int),
         "feti_enable_sparse_factorization": ([P], C.c_int),
         "feti_set_preconditioner": ([P, C.c_int64, f64p], C.c_int),
+        "feti_exchange_setup": ([P, C.c_int, C.c_int, C.c_char_p], C.c_int),
+        "feti_exchange_connect": ([P, C.c_char_p], C.c_int),
+        "feti_apply_exchange_device": ([P, P, P, P], C.c_int),
+        "feti_exchange_status": ([P], C.c_int),
         "feti_precond_apply": ([P, f64p, f64p], C.c_int),
         "feti_precond_apply_device": ([P, P, P, P], C.c_int),
         "feti_set_sparse_pattern": ([P, C.c_int64, C.c_int64, i64p, i64p, i64p, C.c_int64, i64p], C.c_int),

@@ -20,6 +20,7 @@
 #include "../../include/feti_b200.h"
 #include "feti_common.cuh"
 #include "feti_coarse.h"
+#include "feti_exchange.h"
 #include "feti_factor.h"
 #include "feti_implicit.h"
 #include "feti_kernels.h"
@@ -214,6 +215,18 @@ struct feti_ctx {
   // whose F points at the preconditioner tiles, applied by the same kernels
   SubDev* d_subdev_p = nullptr;
   int n_precond_set = 0;
+  // fused cross-rank exchange (feti_exchange_setup/connect)
+  int x_rank = 0, x_world = 1;
+  double* x_slab = nullptr;          // own slab (IPC-exported)
+  std::vector<double*> x_open;       // peer slabs opened through IPC (to close)
+  double** d_x_peers = nullptr;
+  int* d_x_touched = nullptr;
+  int x_n_touched = 0;
+  unsigned* d_x_done = nullptr;
+  int* d_x_error = nullptr;
+  int64_t x_epoch = 0;
+  bool x_ready = false;
+  std::vector<int> h_cptr;           // host copy of the contribution CSR pointer
   cudaStream_t sp_streams[kSpStreams] = {};
   cudaEvent_t sp_join[kSpStreams] = {};
   double sp_flops = 0.0;
@@ -628,6 +641,7 @@ int feti_destroy(feti_ctx* c) {
     if (c->sp_join[g]) cudaEventDestroy(c->sp_join[g]);
     if (c->sp_streams[g]) cudaStreamDestroy(c->sp_streams[g]);
   }
+  for (double* pp : c->x_open) cudaIpcCloseMemHandle(pp);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   delete c;
@@ -942,6 +956,7 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   if ((rc = upload(c, &c->d_w_apply, wa))) return rc;
   if ((rc = upload(c, &c->d_apply_seg_ptr, seg_ptr))) return rc;
   if ((rc = upload(c, &c->d_part_off, part_off))) return rc;
+  c->h_cptr = cptr;
   if ((rc = upload(c, &c->d_cptr, cptr))) return rc;
   if ((rc = upload(c, &c->d_cent, cent))) return rc;
   if ((rc = dev_alloc(c, (void**)&c->d_part, (size_t)std::max<int64_t>(poff, 1) * 8, true))) return rc;
@@ -1329,6 +1344,88 @@ int feti_precond_apply(feti_ctx* c, const double* w, double* out) {
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(out, c->d_q, (size_t)c->n_mult * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return FETI_OK;
+}
+
+int feti_exchange_setup(feti_ctx* c, int rank, int world, char* handle_out) {
+  if (!c || !handle_out) return fail(FETI_ERR_ARG, "NULL argument");
+  if (!c->finalized) return fail(FETI_ERR_LIFECYCLE, "exchange setup before prepare");
+  if (world < 1 || rank < 0 || rank >= world) return fail(FETI_ERR_ARG, "bad rank %d of %d", rank, world);
+  if (c->x_slab) return fail(FETI_ERR_LIFECYCLE, "exchange already set up");
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->x_rank = rank;
+  c->x_world = world;
+  const size_t bytes = ((size_t)2 * world * std::max<int64_t>(c->n_mult, 1) + world) * 8;
+  int rc;
+  if ((rc = dev_alloc(c, (void**)&c->x_slab, bytes, true))) return rc;
+  CUDA_TRY(cudaMemset(c->x_slab, 0, bytes));   // zero slabs, flags = epoch 0
+  std::vector<int> touched;
+  for (int64_t g = 0; g < c->n_mult; ++g)
+    if (c->h_cptr[g + 1] > c->h_cptr[g]) touched.push_back((int)g);
+  c->x_n_touched = (int)touched.size();
+  if ((rc = upload(c, &c->d_x_touched, touched))) return rc;
+  if ((rc = dev_alloc(c, (void**)&c->d_x_done, 64, true))) return rc;
+  CUDA_TRY(cudaMemset(c->d_x_done, 0, 64));
+  c->d_x_error = reinterpret_cast<int*>(reinterpret_cast<char*>(c->d_x_done) + 32);
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->x_slab));
+  static_assert(sizeof(cudaIpcMemHandle_t) == FETI_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle_out, &h, sizeof(h));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return FETI_OK;
+}
+
+int feti_exchange_connect(feti_ctx* c, const char* handles) {
+  if (!c || !handles) return fail(FETI_ERR_ARG, "NULL argument");
+  if (!c->x_slab) return fail(FETI_ERR_LIFECYCLE, "exchange connect before setup");
+  CUDA_TRY(cudaSetDevice(c->device));
+  std::vector<double*> peers(c->x_world, nullptr);
+  for (int p = 0; p < c->x_world; ++p) {
+    if (p == c->x_rank) {
+      peers[p] = c->x_slab;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + (size_t)p * FETI_IPC_HANDLE_BYTES, sizeof(h));
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FETI_ERR_CUDA, "rank %d: opening the slab of rank %d failed: %s", c->x_rank, p,
+                  cudaGetErrorString(e));
+    }
+    peers[p] = static_cast<double*>(ptr);
+    c->x_open.push_back(peers[p]);
+  }
+  int rc;
+  if ((rc = upload(c, &c->d_x_peers, peers))) return rc;
+  c->x_ready = true;
+  return FETI_OK;
+}
+
+int feti_apply_exchange_device(feti_ctx* c, const double* d_p, double* d_q, void* stream) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "apply before preprocess for the current values");
+  if (!c->x_ready) return fail(FETI_ERR_LIFECYCLE, "exchange not connected");
+  if (!d_p || !d_q) return fail(FETI_ERR_ARG, "NULL vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_apply(c->apply_nw, c->apply_smem, c->d_subdev, c->d_w_apply, c->d_apply_seg_ptr, c->n_apply,
+               c->d_part_off, c->d_part, d_p, st);
+  XchgArgs a{c->d_x_peers, c->d_x_touched, c->d_cptr, c->d_cent, c->d_part_off, c->d_part, c->d_x_done,
+             c->d_x_error, ++c->x_epoch, c->x_n_touched, (int)c->n_mult, c->x_rank, c->x_world};
+  launch_exchange(a, d_q, st);
+  CUDA_TRY(cudaGetLastError());
+  return FETI_OK;
+}
+
+int feti_exchange_status(feti_ctx* c) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->d_x_error) return FETI_OK;
+  int err = 0;
+  CUDA_TRY(cudaMemcpy(&err, c->d_x_error, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) return fail(FETI_ERR_CUDA, "rank %d: a peer never published its contribution (exchange timed out)",
+                       c->x_rank);
   return FETI_OK;
 }
 

@@ -7,16 +7,19 @@ processes (PAPER.md:376).  Here:
 
 * assembly is embarrassingly parallel: rank r assembles the F~_i of cluster r
   on its own GPU, no communication;
-* apply has one exchange step: every rank applies its subdomains into a
-  full-length dual vector (zeros outside its multipliers) and the
-  contributions are summed with an NCCL all-reduce over NVLink
-  (``torch.distributed`` backend "nccl").  The p vector is broadcast from
-  rank 0 when it starts on the host.
+* apply has one exchange step.  Default (``exchange="p2p"``): the
+  exchange is fused into the apply's reduction (csrc/feti_exchange.cu): each
+  rank's reduction kernel stores its per-multiplier sums straight into every
+  rank's receive slab over NVLink (CUDA IPC peer memory), publishes an epoch
+  flag, and a second kernel sums the slabs in rank order once every flag
+  arrived -- no collective library call, deterministic, identical on every
+  rank.  ``exchange="nccl"``: the rank's contribution over all multipliers
+  is summed with an NCCL all-reduce (the baseline).  The p vector is
+  broadcast from rank 0 when it starts on the host.
 
-The summation order across ranks is NCCL's, so results agree with the
-reference's fixed gather order (dualop.py:375-379) to rounding (<=1e-10
-relative, the north-star bar), not bit for bit; within a rank the order is
-the reference's.
+Within a rank the summation order is the reference's fixed gather order
+(dualop.py:375-379); across ranks it is rank order (p2p) or NCCL's, so
+results agree with the reference to rounding (<=1e-10 relative).
 """
 
 from __future__ import annotations
@@ -48,20 +51,35 @@ class ClusterDualOperator:
     with ``subdomains=owned_subdomains(layout, rank)``).
     """
 
-    def __init__(self, local, n_multipliers: int, device, group=None):
+    def __init__(self, local, n_multipliers: int, device, group=None, exchange: str = "p2p"):
         import torch
+        import torch.distributed as dist
 
+        if exchange not in ("p2p", "nccl"):
+            raise ValueError("exchange must be 'p2p' or 'nccl'")
         self.local = local
         self.n = int(n_multipliers)
         self.device = device
         self.group = group
         self.p_dev = torch.empty(self.n, dtype=torch.float64, device=device)
         self.q_dev = torch.empty(self.n, dtype=torch.float64, device=device)
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+        self.p2p = exchange == "p2p" and multi and hasattr(local, "exchange_setup")
+        if self.p2p:
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+            handle = local.exchange_setup(rank, world)
+            handles = [None] * world
+            dist.all_gather_object(handles, handle, group=group)
+            local.exchange_connect(handles)
+            dist.barrier(group=group)
 
     def apply_device(self, p_dev, q_dev):
         import torch
 
         stream = torch.cuda.current_stream(self.device).cuda_stream
+        if self.p2p:
+            self.local.apply_exchange_device(p_dev, q_dev, stream)
+            return q_dev
         self.local.apply_device(p_dev, q_dev, stream)
         allreduce_sum_(q_dev, self.group)
         return q_dev

@@ -594,6 +594,33 @@ class DualOperator:
         _call(self._lib.feti_precond_apply_device(self._ctx, C.c_void_p(int(w.data_ptr())),
                                                   C.c_void_p(int(out.data_ptr())), C.c_void_p(int(stream))))
 
+    # -- multi-GPU apply with the fused exchange (feti_exchange.cu) -----------
+
+    def exchange_setup(self, rank: int, world: int) -> bytes:
+        """Allocate this rank's receive slab; returns its CUDA IPC handle."""
+        buf = C.create_string_buffer(_lib.FETI_IPC_HANDLE_BYTES)
+        _call(self._lib.feti_exchange_setup(self._ctx, int(rank), int(world), buf))
+        return buf.raw
+
+    def exchange_connect(self, handles) -> None:
+        """Open every rank's slab (handles in rank order, own included)."""
+        blob = b"".join(bytes(h) for h in handles)
+        _call(self._lib.feti_exchange_connect(self._ctx, blob))
+
+    def apply_exchange_device(self, p, q, stream=None) -> None:
+        """q = sum over ranks of B~^T F~ B~ p, exchanged over peer memory."""
+        if not self.step_ready:
+            raise LifecycleError("apply before preprocess for the current values")
+        if stream is None:
+            import torch
+
+            stream = torch.cuda.current_stream(p.device).cuda_stream
+        _call(self._lib.feti_apply_exchange_device(self._ctx, C.c_void_p(int(p.data_ptr())),
+                                                   C.c_void_p(int(q.data_ptr())), C.c_void_p(int(stream))))
+
+    def exchange_status(self) -> None:
+        _call(self._lib.feti_exchange_status(self._ctx))
+
     # -- K^+ access for the solver --------------------------------------------
 
     def solve_local(self, index: int, rhs, out=None):

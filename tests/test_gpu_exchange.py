@@ -1,0 +1,76 @@
+"""Fused cross-rank exchange of the apply (csrc/feti_exchange.cu) with two
+processes: each owns one cluster (decomposition.py:227-243) and exchanges its
+contributions through CUDA IPC peer memory.  On the one-GPU test box both
+ranks share the device (IPC across processes on one device); on a node each
+rank has its own GPU and the stores cross NVLink.  q must equal the
+single-operator apply of the whole problem to rounding, be identical on both
+ranks, and repeat bit for bit."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2502_08382_b200 import dualop, inputs
+
+pytestmark = pytest.mark.gpu
+CFG = dualop.DualOpConfig(strategy="explicit", path="syrk")
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_08382_b200 import distributed as fd
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ndev = torch.cuda.device_count()
+        dev = torch.device("cuda", rank % ndev)
+        torch.cuda.set_device(dev)
+        prob = inputs.Problem("heat", 3, 4, 2, n_clusters=world)
+        mats, cons, lay = inputs.reference_inputs(prob)
+        owned = fd.owned_subdomains(lay, rank)
+        with dualop.prepare(mats, cons, lay, CFG, device=dev.index, subdomains=owned) as op:
+            op.preprocess()
+            dco = fd.ClusterDualOperator(op, prob.n_multipliers, dev)
+            assert dco.p2p
+            p = torch.from_numpy(np.random.default_rng(0).normal(size=prob.n_multipliers)).to(dev)
+            qs = []
+            for _ in range(5):
+                q = torch.empty_like(p)
+                dco.apply_device(p, q)
+                torch.cuda.synchronize(dev)
+                qs.append(q.cpu().numpy())
+            op.exchange_status()
+            np.save(os.path.join(outdir, f"q{rank}.npy"), np.stack(qs))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_fused_exchange(tmp_path):
+    import torch.multiprocessing as mp
+
+    mp.spawn(_worker, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
+    prob = inputs.Problem("heat", 3, 4, 2)
+    mats, cons, lay = inputs.reference_inputs(prob)
+    with dualop.prepare(mats, cons, lay, CFG, device=0) as op:
+        op.preprocess()
+        ref = op.apply(np.random.default_rng(0).normal(size=prob.n_multipliers))
+    q0, q1 = np.load(tmp_path / "q0.npy"), np.load(tmp_path / "q1.npy")
+    assert np.array_equal(q0, q1)
+    for k in range(1, q0.shape[0]):
+        assert np.array_equal(q0[k], q0[0])
+    assert np.linalg.norm(q0[0] - ref) <= 1e-12 * np.linalg.norm(ref)
