@@ -83,7 +83,6 @@ __global__ void __launch_bounds__(256) sp_scatter_kernel(const SpSub* __restrict
 // tile GEMM tasks on the DMMA pipe (8 consumer warps, 1 bulk-copy producer)
 // ---------------------------------------------------------------------------
 constexpr int SG_STAGES = 3;
-constexpr int SG_THREADS = 288;
 
 // MI = 8: full 128-row tile; MI = 1: "thin" tile of the (P Q)^T block row,
 // whose rows >= r <= 8 are zero (only warp row-group 0, first 8 rows)
@@ -103,142 +102,6 @@ __device__ __forceinline__ void sg_mma_slice(const double* __restrict__ a_s, con
       for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
     }
   }
-}
-
-// Consumer side of sp_gemm_kernel: MI = 8 full tile, MI = 1 thin tile
-// (only warp row-group 0 computes, only rows < 8 are written).
-template <int MI>
-__device__ __forceinline__ void sg_consume(const double* __restrict__ sA, const double* __restrict__ sB,
-                                           uint64_t* full, uint64_t* empty, int nsl, double* Ct, bool panel,
-                                           int wm, int wn, int lane) {
-  const int g = lane >> 2, t = lane & 3;
-  const bool active = (MI == 8) || wm == 0;
-  double acc[MI][4][2];
-#pragma unroll
-  for (int a = 0; a < MI; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  int stage = 0;
-  uint32_t phase = 0;
-  for (int sl = 0; sl < nsl; ++sl) {
-    mbar_wait(&full[stage], phase);
-    if (active) sg_mma_slice<MI>(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
-    fence_proxy_async_shared();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
-    if (++stage == SG_STAGES) {
-      stage = 0;
-      phase ^= 1;
-    }
-  }
-  if (!active) return;
-  // every slice of a panel task's A (= C) was consumed above: in-place is safe
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi) {
-    const int m = wm * 64 + mi * 8 + g;
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int nn = wn * 32 + ni * 8 + 2 * t;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        double* cp = Ct + swz(nn + e, m);
-        if (panel)
-          *cp = acc[mi][ni][e];
-        else
-          *cp -= acc[mi][ni][e];
-      }
-    }
-  }
-}
-
-// sg_consume starting at ring position (stage0, phase0) of a persistent CTA
-template <int MI>
-__device__ __forceinline__ void sg_consume_at(const double* __restrict__ sA, const double* __restrict__ sB,
-                                              uint64_t* full, uint64_t* empty, int nsl, double* Ct, bool panel,
-                                              int wm, int wn, int lane, int stage0, uint32_t phase0) {
-  const int g = lane >> 2, t = lane & 3;
-  const bool active = (MI == 8) || wm == 0;
-  double acc[MI][4][2];
-#pragma unroll
-  for (int a = 0; a < MI; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  int stage = stage0;
-  uint32_t phase = phase0;
-  for (int sl = 0; sl < nsl; ++sl) {
-    mbar_wait(&full[stage], phase);
-    if (active) sg_mma_slice<MI>(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
-    fence_proxy_async_shared();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
-    if (++stage == SG_STAGES) {
-      stage = 0;
-      phase ^= 1;
-    }
-  }
-  if (!active) return;
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi) {
-    const int m = wm * 64 + mi * 8 + g;
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int nn = wn * 32 + ni * 8 + 2 * t;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        double* cp = Ct + swz(nn + e, m);
-        if (panel)
-          *cp = acc[mi][ni][e];
-        else
-          *cp -= acc[mi][ni][e];
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(SG_THREADS, 1) sp_gemm_kernel(const SpTask* __restrict__ tasks,
-                                                                const SpPair* __restrict__ pairs) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* sA = reinterpret_cast<double*>(smem_raw);
-  double* sB = sA + SG_STAGES * SLICE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + SG_STAGES * SLICE);
-  uint64_t* empty = full + SG_STAGES;
-  const SpTask tk = tasks[blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < SG_STAGES; ++st) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], 8);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  const int nsl = tk.npairs * (TB / KS);
-  if (warp == 8) {
-    if (lane == 0) {
-      // the epilogue read-modify-writes C: have it in L2 by then
-      if (!(tk.flags & 1)) bulk_prefetch_l2(tk.C, TILE * 8);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int sl = 0; sl < nsl; ++sl) {
-        const SpPair pr = pairs[tk.pair0 + sl / (TB / KS)];
-        const int so = (sl % (TB / KS)) * SLICE;
-        mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], 2 * SLICE * 8);
-        bulk_g2s(sA + stage * SLICE, pr.A + so, SLICE * 8, &full[stage]);
-        bulk_g2s(sB + stage * SLICE, pr.B + so, SLICE * 8, &full[stage]);
-        if (++stage == SG_STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-    return;
-  }
-  const int wm = warp >> 2, wn = warp & 3;
-  if (!(tk.flags & 2))
-    sg_consume<8>(sA, sB, full, empty, nsl, tk.C, tk.flags & 1, wm, wn, lane);
-  else
-    sg_consume<1>(sA, sB, full, empty, nsl, tk.C, tk.flags & 1, wm, wn, lane);
 }
 
 __global__ void __launch_bounds__(256, 1) sp_potrf_kernel(const SpDiag* __restrict__ d, int* __restrict__ bad) {
@@ -642,8 +505,6 @@ cudaError_t configure_sparse() {
     return e;
   if ((e = cudaFuncSetAttribute(sp_gemm8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem())))
     return e;
-  if ((e = cudaFuncSetAttribute(sp_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem())))
-    return e;
   return cudaFuncSetAttribute(sp_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_potrf_smem());
 }
 
@@ -655,14 +516,8 @@ void launch_sp_scatter(const SpSub* ss, int nsub, int max_n, cudaStream_t st) {
   if (nsub > 0 && max_n > 0) sp_scatter_kernel<<<dim3((max_n + 7) / 8, nsub), 256, 0, st>>>(ss);
 }
 
-static const bool g_gemm8 = getenv("FETI_SP_GEMM9") == nullptr;
-
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st) {
-  if (ntasks <= 0) return;
-  if (g_gemm8)
-    sp_gemm8_kernel<<<ntasks, DAG_THREADS, sg_smem(), st>>>(tasks, pairs);
-  else
-    sp_gemm_kernel<<<ntasks, SG_THREADS, sg_smem(), st>>>(tasks, pairs);
+  if (ntasks > 0) sp_gemm8_kernel<<<ntasks, DAG_THREADS, sg_smem(), st>>>(tasks, pairs);
 }
 
 void launch_sp_dag(const SpDag& g, int nctas, cudaStream_t st) {

@@ -210,6 +210,8 @@ class DualOperator:
         self._ctx = None
         self._lib = _lib.load()
         self._executor = None
+        self._upload_pool = None
+        self._handed_over = False
         self.timings = {}
 
     # -- helpers -------------------------------------------------------------
@@ -250,6 +252,9 @@ class DualOperator:
         if self._executor is not None:
             self._executor.shutdown(wait=True)
             self._executor = None
+        if getattr(self, "_upload_pool", None) is not None:
+            self._upload_pool.shutdown(wait=True)
+            self._upload_pool = None
         if self._ctx is not None:
             self._lib.feti_destroy(self._ctx)
             self._ctx = None
@@ -433,7 +438,8 @@ class DualOperator:
         import time
 
         t0 = time.perf_counter()
-        for sub in self._subs.values():
+
+        def hand_over(sub):
             n, ip, ix, dt = fct.csr_arrays(self.stiffness[sub.index])
             if n != sub.n:
                 raise ValueError("stiffness size does not match the subdomain")
@@ -452,6 +458,23 @@ class DualOperator:
             _call(self._lib.feti_set_stiffness(self._ctx, sub.slot, n, _lib.i64ptr(ip), _lib.i64ptr(ix),
                                                _lib.f64ptr(dt), ip[-1], _lib.f64ptr(q), q.shape[1], rho,
                                                _lib.i64ptr(sub.perm)))
+            return sub
+
+        subs = list(self._subs.values())
+        if self._handed_over and len(subs) > 1:
+            # later steps: the per-slot hand-overs (host copies of K values and
+            # Q, ctypes releases the GIL) run on a thread pool; the first step
+            # allocates device buffers and stays sequential
+            if self._upload_pool is None:
+                from concurrent.futures import ThreadPoolExecutor
+
+                self._upload_pool = ThreadPoolExecutor(max_workers=min(8, len(subs)),
+                                                       thread_name_prefix="feti-upload")
+            list(self._upload_pool.map(hand_over, subs))
+        else:
+            for sub in subs:
+                hand_over(sub)
+            self._handed_over = True
         t1 = time.perf_counter()
         # the sparse route reports a non-SPD pivot from feti_assemble (it
         # checks the pivots once the overlapped factorization/assembly ended)
