@@ -208,7 +208,7 @@ int feti_precond_apply_device(feti_ctx* ctx, const double* d_w, double* d_out, v
  * apply + all-reduce pair.  Setup: feti_exchange_setup returns this rank's
  * IPC handle (FETI_IPC_HANDLE_BYTES), the caller all-gathers the handles
  * (rank order) and passes them to feti_exchange_connect.  Every rank must
- * issue the same number of exchange applies; a rank that waits ~2 s for a
+ * issue the same number of exchange applies; a rank that waits ~10 s for a
  * peer gives up and feti_exchange_status reports it. */
 #define FETI_IPC_HANDLE_BYTES 64
 int feti_exchange_setup(feti_ctx* ctx, int rank, int world, char* handle_out);

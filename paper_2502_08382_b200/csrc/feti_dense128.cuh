@@ -100,10 +100,18 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, t4 = lane & 3;      // DMMA fragment coordinates
-  for (int idx = tid; idx < TILE; idx += 256) {
-    const int jl = idx >> 7;
-    const int il = (idx & 127) ^ ((jl & 3) << 2);
-    if (il >= jl) sA[il * PO_LD + jl] = tile[idx];
+  // 16 loads in flight per thread (the tile is usually cold in HBM)
+  for (int base = 0; base < TILE / 256; base += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldcg(tile + (base + u) * 256 + tid);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = (base + u) * 256 + tid;
+      const int jl = idx >> 7;
+      const int il = (idx & 127) ^ ((jl & 3) << 2);
+      if (il >= jl) sA[il * PO_LD + jl] = v[u];
+    }
   }
   po_sync();
   // Y(r, c) for r >= c (lower triangle of inv(L))

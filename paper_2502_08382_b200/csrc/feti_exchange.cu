@@ -16,7 +16,7 @@
 //   own sum of epoch e-1 returned, which needed every peer's flag e-1, which
 //   each peer publishes after its sum of epoch e-2 -- the last reader of
 //   that parity.
-// * The wait is bounded: after ~2 s without progress the kernel records an
+// * The wait is bounded: after ~10 s without progress the kernel records an
 //   error and returns instead of hanging the device.
 #include <cstdint>
 
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) sum_exchange_kernel(XchgArgs a, double* _
       const long long t0 = clock64();
       while (ld_acquire_sys_s64(flags + r) < a.epoch) {
         __nanosleep(200);
-        if (clock64() - t0 > 4000000000LL) {   // ~2 s at 2 GHz: a peer never arrived
+        if (clock64() - t0 > 20000000000LL) {   // ~10 s at 2 GHz: a peer never arrived
           atomicExch(a.error, 1);
           good = 0;
           break;
