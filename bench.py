@@ -566,7 +566,12 @@ def run_sparse(args, rank, world, local_rank):
                      "achieved": st["flops_factor_exec"] / fac_s / 1e12, "peak": peak_f64, "unit": "TFLOP/s",
                      "frac": st["flops_factor_exec"] / fac_s / 1e12 / peak_f64,
                      "peak_source": "measured in-run: cuBLAS DGEMM 8192^3 f64 (torch.matmul), best of 5",
-                     "traffic": None,
+                     "traffic": load_traffic(args.config, "sparse").get(
+                         "feti_factorize (sp_gemm8 + sp_potrf, per factorization)"),
+                     "traffic_note": "DRAM read+write of every sp_gemm8/sp_potrf launch of one factorization "
+                                     "(ncu dram__bytes_*.sum over all launches, profiles/ncu_traffic.json); the "
+                                     "pool's tiles are 8.2 GB at c3, so ~8x re-reads from DRAM (L2 holds 1.5 % of "
+                                     "the pool) at 1.1 TB/s: compute-bound",
                      "algorithmic": "tile flops of the block-sparse factorization (2*128^3 per tile product; "
                                     "the (PQ)^T block row included) over the whole feti_factorize time",
                      "executed_flops": st["flops_factor_exec"]},
