@@ -199,6 +199,9 @@ struct feti_ctx {
   int sp_groups = 1, sp_maxTq = 0;
   // persistent dependency-driven factorization (opt-in, FETI_SP_DAG=1)
   bool sp_use_dag = false;
+  cudaGraphExec_t sp_graph_exec = nullptr;   // captured column-launch sequence
+  int sp_graph_launches = 0;
+  bool sp_graph_used = false;
   int sp_dag_total = 0;
   std::vector<int> sp_dag_init, sp_acc_init, sp_pan_init;
   SpTask* d_dag_tasks = nullptr;
@@ -554,26 +557,48 @@ int factorize_sparse(feti_ctx* c) {
   } else {
   // the groups' column sequences are independent: issue them round-robin on
   // their own streams so the GPU interleaves one group's diagonal blocks with
-  // another's tile GEMMs
+  // another's tile GEMMs.  The ~900 launches are captured once into a CUDA
+  // graph (fork/join over the group streams) and replayed per factorization
+  // (FETI_SP_GRAPH=0 or FETI_DEBUG_SYNC: issued directly).
   const int G = c->sp_groups;
-  CUDA_TRY(cudaEventRecord(c->ev[2], st));
-  for (int g = 0; g < G; ++g) CUDA_TRY(cudaStreamWaitEvent(c->sp_streams[g], c->ev[2], 0));
-  for (int j = 0; j < c->sp_maxTq; ++j)
+  const bool use_graph = !g_debug_sync && !(getenv("FETI_SP_GRAPH") && atoi(getenv("FETI_SP_GRAPH")) == 0);
+  if (use_graph && c->sp_graph_exec) {
+    CUDA_TRY(cudaGraphLaunch(c->sp_graph_exec, st));
+    launches = 2 + c->sp_graph_launches;
+  } else {
+    if (use_graph) CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    CUDA_TRY(cudaEventRecord(c->ev[2], st));
+    for (int g = 0; g < G; ++g) CUDA_TRY(cudaStreamWaitEvent(c->sp_streams[g], c->ev[2], 0));
+    int nl = 0;
+    for (int j = 0; j < c->sp_maxTq; ++j)
+      for (int g = 0; g < G; ++g) {
+        const size_t gj = (size_t)g * c->sp_maxTq + j;
+        cudaStream_t gs = c->sp_streams[g];
+        const auto a = c->sp_acc_rng[gj], d = c->sp_diag_rng[gj], p = c->sp_panel_rng[gj];
+        launch_sp_gemm(c->d_sp_tasks + a.first, a.second, c->d_sp_pairs, gs);
+        launch_sp_potrf(c->d_sp_diag + d.first, d.second, c->d_bad, gs);
+        launch_sp_gemm(c->d_sp_tasks + p.first, p.second, c->d_sp_pairs, gs);
+        nl += (a.second > 0) + (d.second > 0) + (p.second > 0);
+        if (!use_graph) {
+          CUDA_TRY(cudaGetLastError());
+          FETI_DEBUG_SYNC(gs);
+        }
+      }
     for (int g = 0; g < G; ++g) {
-      const size_t gj = (size_t)g * c->sp_maxTq + j;
-      cudaStream_t gs = c->sp_streams[g];
-      const auto a = c->sp_acc_rng[gj], d = c->sp_diag_rng[gj], p = c->sp_panel_rng[gj];
-      launch_sp_gemm(c->d_sp_tasks + a.first, a.second, c->d_sp_pairs, gs);
-      launch_sp_potrf(c->d_sp_diag + d.first, d.second, c->d_bad, gs);
-      launch_sp_gemm(c->d_sp_tasks + p.first, p.second, c->d_sp_pairs, gs);
-      launches += (a.second > 0) + (d.second > 0) + (p.second > 0);
-      CUDA_TRY(cudaGetLastError());
-      FETI_DEBUG_SYNC(gs);
+      CUDA_TRY(cudaEventRecord(c->sp_join[g], c->sp_streams[g]));
+      CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
     }
-  for (int g = 0; g < G; ++g) {
-    CUDA_TRY(cudaEventRecord(c->sp_join[g], c->sp_streams[g]));
-    CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
+    launches += nl;
+    if (use_graph) {
+      cudaGraph_t graph = nullptr;
+      CUDA_TRY(cudaStreamEndCapture(st, &graph));
+      CUDA_TRY(cudaGraphInstantiate(&c->sp_graph_exec, graph, 0));
+      CUDA_TRY(cudaGraphDestroy(graph));
+      c->sp_graph_launches = nl;
+      CUDA_TRY(cudaGraphLaunch(c->sp_graph_exec, st));
+    }
   }
+  c->sp_graph_used = use_graph;
   }
   // the factorization end on the context stream (timing only); no host sync:
   // feti_assemble runs each group's assembly right behind its factorization
@@ -637,6 +662,7 @@ int feti_destroy(feti_ctx* c) {
   }
   for (auto& e : c->sp_ev)
     if (e) cudaEventDestroy(e);
+  if (c->sp_graph_exec) cudaGraphExecDestroy(c->sp_graph_exec);
   for (int g = 0; g < feti_ctx::kSpStreams; ++g) {
     if (c->sp_join[g]) cudaEventDestroy(c->sp_join[g]);
     if (c->sp_streams[g]) cudaStreamDestroy(c->sp_streams[g]);
@@ -1116,7 +1142,8 @@ int feti_assemble(feti_ctx* c) {
     const auto& r = c->wv_range;
     for (int g = 0; g < G; ++g) {
       cudaStream_t gs = c->sp_streams[g];
-      if (c->sp_use_dag) CUDA_TRY(cudaStreamWaitEvent(gs, c->ev[2], 0));
+      // the persistent kernel and the captured graph ran on the context stream
+      if (c->sp_use_dag || c->sp_graph_used) CUDA_TRY(cudaStreamWaitEvent(gs, c->ev[2], 0));
       std::vector<int> none;
       if ((rc = launch_assembly(c, gs, c->d_wv[0] + r[0][g].first, r[0][g].second, c->d_wv[1] + r[1][g].first,
                                 r[1][g].second, c->d_wv[2] + r[2][g].first, r[2][g].second,
