@@ -324,38 +324,55 @@ constexpr int MAXR = 8;
 
 // one CTA per (sub, panel c): U2[a] = sum_rows X[row][a] y[row], then
 // W[a] = C U1[a] - U2[a] with C = y^T y + I/rho = -tile(T,T) + I/rho
-__global__ void __launch_bounds__(TB) sp_u2_kernel(const SubDev* __restrict__ subs, const SpSub* __restrict__ ss,
-                                                   const int2* __restrict__ panels) {
+constexpr int U2_GROUPS = 4;   // row groups per CTA (U2_GROUPS x 128 threads)
+
+__global__ void __launch_bounds__(U2_GROUPS * TB) sp_u2_kernel(const SubDev* __restrict__ subs,
+                                                              const SpSub* __restrict__ ss,
+                                                              const int2* __restrict__ panels) {
   const int2 pc = panels[blockIdx.x];
   const SubDev& S = subs[pc.x];
   const SpSub& Q = ss[pc.x];
-  const int c = pc.y, col = threadIdx.x, r = Q.r;
+  const int c = pc.y, col = threadIdx.x & (TB - 1), rg = threadIdx.x >> 7, r = Q.r;
   const int a = c * TB + col;
   const int T = Q.T;
   __shared__ double Cm[MAXR * MAXR];
+  __shared__ double red[U2_GROUPS][MAXR][TB];
   const double* cq = Q.pool + (size_t)Q.tmap[T * Q.Tq + T] * TILE;
-  if (col < r * r) {
-    const int q = col / r, q2 = col % r;
-    Cm[col] = -cq[swz(q2, q)] + (q == q2 ? 1.0 / Q.rho : 0.0);
+  if (threadIdx.x < r * r) {
+    const int q = threadIdx.x / r, q2 = threadIdx.x % r;
+    Cm[threadIdx.x] = -cq[swz(q2, q)] + (q == q2 ? 1.0 / Q.rho : 0.0);
   }
-  __syncthreads();
-  double acc[MAXR];
+  // rows split over the row groups (row = kb*128 + il, il = rg mod U2_GROUPS),
+  // two independent accumulator chains per group
+  double acc[MAXR], acc2[MAXR];
 #pragma unroll
-  for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
+  for (int q = 0; q < MAXR; ++q) acc[q] = acc2[q] = 0.0;
   const int r0 = (S.panel_minrow[c] / TB) * TB;
   for (int kb = r0 / TB; kb < T; ++kb) {
     const double* yt = Q.pool + (size_t)Q.tmap[T * Q.Tq + kb] * TILE;
-    for (int il = 0; il < TB; ++il) {
-      const int row = kb * TB + il;
+    for (int il = rg; il < TB; il += 2 * U2_GROUPS) {
+      const int row = kb * TB + il, row2 = row + U2_GROUPS;
       const double x = xrow_ptr(S, c, row)[col ^ ((row & 3) << 2)];
+      const double x2 = xrow_ptr(S, c, row2)[col ^ ((row2 & 3) << 2)];
 #pragma unroll
       for (int q = 0; q < MAXR; ++q)
-        if (q < r) acc[q] = fma(x, yt[swz(il, q)], acc[q]);
+        if (q < r) {
+          acc[q] = fma(x, yt[swz(il, q)], acc[q]);
+          acc2[q] = fma(x2, yt[swz(il + U2_GROUPS, q)], acc2[q]);
+        }
     }
   }
-  if (a >= S.m) {
 #pragma unroll
-    for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
+  for (int q = 0; q < MAXR; ++q)
+    if (q < r) red[rg][q][col] = acc[q] + acc2[q];
+  __syncthreads();
+  if (rg != 0) return;
+#pragma unroll
+  for (int q = 0; q < MAXR; ++q) {
+    double v = 0.0;
+    if (q < r)
+      for (int g2 = 0; g2 < U2_GROUPS; ++g2) v += red[g2][q][col];
+    acc[q] = (a < S.m) ? v : 0.0;
   }
   double* out = Q.U2W + (size_t)a * 2 * r;
   const double* u1 = Q.U1 + (size_t)a * r;
@@ -530,7 +547,7 @@ void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st) {
 
 void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int sub0, int nsub,
                        int max_T32, cudaStream_t st) {
-  if (npanels > 0) sp_u2_kernel<<<npanels, TB, 0, st>>>(subs, ss, panels);
+  if (npanels > 0) sp_u2_kernel<<<npanels, U2_GROUPS * TB, 0, st>>>(subs, ss, panels);
   if (nsub > 0 && max_T32 > 0) sp_correct_kernel<<<dim3(max_T32, nsub), 256, 0, st>>>(subs, ss, sub0);
 }
 
