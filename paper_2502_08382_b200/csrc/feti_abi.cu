@@ -108,6 +108,7 @@ struct SubHost {
   // block-sparse tile pool, rank-2r correction after the assembly
   bool sp_pattern = false;
   int sp_r = 0;
+  int64_t sp_n = 0;                  // DOFs (rows of K); n above counts positions (>= sp_n)
   std::vector<int64_t> sp_perm, sp_iperm, sp_kptr, sp_kind, sp_fix;
   SpPlan sp;
   double* d_pool = nullptr;
@@ -322,7 +323,7 @@ int build_sparse_tasks(feti_ctx* c) {
     const SpPlan& P = s.sp;
     maxTq = std::max(maxTq, P.Tq);
     c->sp_max_T32 = std::max(c->sp_max_T32, s.T32);
-    c->sp_max_n = std::max<int>(c->sp_max_n, (int)s.n);
+    c->sp_max_n = std::max<int>(c->sp_max_n, (int)s.sp_n);
     for (int K = 0; K < P.Tq; ++K)
       for (int L = 0; L <= K; ++L) {
         const int slot = P.tmap[(size_t)K * P.Tq + L];
@@ -521,7 +522,7 @@ int factorize_sparse(feti_ctx* c) {
   for (int si = 0; si < ns; ++si) {
     SubHost& s = c->subs[si];
     ss[si] = SpSub{s.d_pool, s.d_tmap, s.d_perm, s.d_iperm, s.d_kptr, s.d_kind, s.d_kdata, s.d_Q,
-                   s.d_fix, s.d_U1, s.d_U2W, s.rho, s.sp.T, s.sp.Tq, (int)s.n, s.sp_r, s.sp_r, 0};
+                   s.d_fix, s.d_U1, s.d_U2W, s.rho, s.sp.T, s.sp.Tq, (int)s.sp_n, s.sp_r, s.sp_r, (int)s.n};
     s.src = SRC_TILES;
   }
   CUDA_TRY(cudaMemcpyAsync(c->d_spsub, ss.data(), ns * sizeof(SpSub), cudaMemcpyHostToDevice, st));
@@ -755,7 +756,7 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     for (size_t i = 0; i < c->subs.size(); ++i) {
       SubHost& s = c->subs[i];
       if (!s.sp_pattern) return fail(FETI_ERR_LIFECYCLE, "slot %zu has no sparse pattern", i);
-      sp_symbolic(s.n, s.sp_kptr.data(), s.sp_kind.data(), s.sp_iperm.data(), s.sp_r, s.smin, &s.sp);
+      sp_symbolic(s.sp_n, s.sp_kptr.data(), s.sp_kind.data(), s.sp_iperm.data(), s.n, s.sp_r, s.smin, &s.sp);
       need += (size_t)s.sp.ntiles * TILE * 8;
     }
   for (auto& s : c->subs) {
@@ -1487,16 +1488,22 @@ int feti_set_sparse_pattern(feti_ctx* c, int64_t slot, int64_t n, const int64_t*
   if (!c->sparse_factor) return fail(FETI_ERR_LIFECYCLE, "sparse factorization is not enabled");
   if (slot < 0 || slot >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot out of range");
   SubHost& s = c->subs[slot];
-  if (n != s.n) return fail(FETI_ERR_ARG, "pattern size %lld does not match the subdomain (%lld)", (long long)n,
-                            (long long)s.n);
+  // n DOFs; the slot was registered with s.n >= n positions (tile-aligned
+  // orderings pad segments to 128 rows; perm holds -1 at padding positions)
+  if (n <= 0 || n > s.n)
+    return fail(FETI_ERR_ARG, "pattern size %lld does not fit the subdomain's %lld positions", (long long)n,
+                (long long)s.n);
   if (!indptr || !indices || !perm || r < 0 || r > 8 || (r > 0 && !fix))
     return fail(FETI_ERR_ARG, "bad sparse pattern arguments (kernel dimension must be <= 8)");
   if (indptr[0] != 0) return fail(FETI_ERR_ARG, "pattern pointer must start at 0");
-  std::vector<int64_t> pv(perm, perm + n), ip(n, -1);
-  for (int64_t i = 0; i < n; ++i) {
+  std::vector<int64_t> pv(perm, perm + s.n), ip(n, -1);
+  for (int64_t i = 0; i < s.n; ++i) {
+    if (pv[i] == -1) continue;
     if (pv[i] < 0 || pv[i] >= n || ip[pv[i]] >= 0) return fail(FETI_ERR_ARG, "ordering is not a permutation");
     ip[pv[i]] = i;
   }
+  for (int64_t a = 0; a < n; ++a)
+    if (ip[a] < 0) return fail(FETI_ERR_ARG, "ordering misses DOF %lld", (long long)a);
   const int64_t nnz = indptr[n];
   for (int64_t a = 0; a < n; ++a) {
     if (indptr[a + 1] < indptr[a]) return fail(FETI_ERR_ARG, "pattern pointer is not monotone");
@@ -1515,6 +1522,7 @@ int feti_set_sparse_pattern(feti_ctx* c, int64_t slot, int64_t n, const int64_t*
   s.sp_kind.assign(indices, indices + nnz);
   s.sp_fix.assign(fix, fix + r);
   s.sp_r = (int)r;
+  s.sp_n = n;
   s.sp_pattern = true;
   return FETI_OK;
 }
@@ -1526,23 +1534,31 @@ int feti_set_stiffness(feti_ctx* c, int64_t slot, int64_t n, const int64_t* indp
     return fail(FETI_ERR_LIFECYCLE, "set_stiffness needs a finalized context with device factorization");
   if (slot < 0 || slot >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot out of range");
   SubHost& s = c->subs[slot];
-  if (n != s.n) return fail(FETI_ERR_ARG, "stiffness size %lld does not match the subdomain (%lld)", (long long)n,
-                            (long long)s.n);
+  const int64_t ndof = c->sparse_factor ? s.sp_n : s.n;
+  if (n != ndof) return fail(FETI_ERR_ARG, "stiffness size %lld does not match the subdomain (%lld)", (long long)n,
+                             (long long)ndof);
   if (!indptr || !indices || !data || (r > 0 && !Q) || !perm || r < 0 || r > 64 || nnz != indptr[n])
     return fail(FETI_ERR_ARG, "bad stiffness arguments");
   if (c->sparse_factor) {
     if ((int)r != s.sp_r) return fail(FETI_ERR_ARG, "kernel dimension differs from the sparse pattern's");
-    if (nnz != s.sp_kptr[n] || !std::equal(perm, perm + n, s.sp_perm.begin()) ||
+    if (nnz != s.sp_kptr[n] || !std::equal(perm, perm + s.n, s.sp_perm.begin()) ||
         !std::equal(indptr, indptr + n + 1, s.sp_kptr.begin()))
       return fail(FETI_ERR_ARG, "stiffness pattern or ordering differs from the sparse pattern");
   }
   CUDA_TRY(cudaSetDevice(c->device));
   int rc;
   if (!s.stiff_set) {
-    std::vector<int64_t> pv(perm, perm + n), ip(n, -1);
-    for (int64_t i = 0; i < n; ++i) {
-      if (pv[i] < 0 || pv[i] >= n || ip[pv[i]] >= 0) return fail(FETI_ERR_ARG, "ordering is not a permutation");
-      ip[pv[i]] = i;
+    std::vector<int64_t> pv, ip;
+    if (c->sparse_factor) {   // the pattern call validated the (padded) ordering
+      pv = s.sp_perm;
+      ip = s.sp_iperm;
+    } else {
+      pv.assign(perm, perm + n);
+      ip.assign(n, -1);
+      for (int64_t i = 0; i < n; ++i) {
+        if (pv[i] < 0 || pv[i] >= n || ip[pv[i]] >= 0) return fail(FETI_ERR_ARG, "ordering is not a permutation");
+        ip[pv[i]] = i;
+      }
     }
     std::vector<int64_t> kp(indptr, indptr + n + 1), ki(indices, indices + nnz);
     if ((rc = upload(c, &s.d_perm, pv))) return rc;

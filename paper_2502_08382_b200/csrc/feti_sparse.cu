@@ -41,17 +41,18 @@ __global__ void __launch_bounds__(256) sp_init_kernel(const SpInit* __restrict__
   const SpInit w = work[blockIdx.x];
   const SpSub& S = ss[w.sub];
   double* tile = w.tile;
-  const int n = S.n, r = S.r;
+  const int npos = S.npos, r = S.r;
   const bool qrow = (w.K == S.T);
   for (int idx = threadIdx.x; idx < TILE; idx += 256) {
     const int jl = idx >> 7;
     const int il = (idx & 127) ^ ((jl & 3) << 2);
     const int j = w.L * TB + jl;
+    const int64_t dof = j < npos ? S.perm[j] : -1;
     double v = 0.0;
     if (qrow) {
-      if (w.L < S.T && il < r && j < n) v = S.Q[S.perm[j] * r + il];
-    } else if (w.K == w.L && il == jl && j >= n) {
-      v = 1.0;   // identity padding keeps the last diagonal block SPD
+      if (w.L < S.T && il < r && dof >= 0) v = S.Q[dof * r + il];
+    } else if (w.K == w.L && il == jl && dof < 0) {
+      v = 1.0;   // identity rows at padding positions keep the diagonal blocks SPD
     }
     tile[idx] = v;
   }
@@ -416,10 +417,10 @@ __global__ void __launch_bounds__(256) sp_correct_kernel(const SubDev* __restric
 // ---------------------------------------------------------------------------
 // host: block symbolic factorization and task lists
 // ---------------------------------------------------------------------------
-void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* iperm, int r, int smin,
-                 SpPlan* out) {
+void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* iperm, int64_t npos,
+                 int r, int smin, SpPlan* out) {
   SpPlan& P = *out;
-  const int T = (int)((n + TB - 1) / TB);
+  const int T = (int)((npos + TB - 1) / TB);
   const int Tq = T + (r > 0 ? 1 : 0);
   P.T = T;
   P.Tq = Tq;

@@ -28,7 +28,8 @@ struct SpSub {
   double rho;
   int T;                    // block rows of K_s (the Q block row is T when r > 0)
   int Tq;                   // T + (r > 0)
-  int n, r, nfix, pad_;
+  int n, r, nfix;           // n: DOFs (rows of K)
+  int npos;                 // positions (>= n; perm[p] = -1 marks a padding position)
 };
 
 // One tile of the left-looking factorization:
@@ -72,8 +73,10 @@ struct SpPlan {
 // indptr/indices: symmetric pattern of K (original numbering); iperm: DOF ->
 // position; r: kernel dimension (adds the (P Q)^T block row T when > 0);
 // smin: first block row of the dense trailing triangle.
-void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* iperm, int r, int smin,
-                 SpPlan* out);
+// n DOFs (rows of K); positions live in [0, npos) (npos >= n: tile-aligned
+// orderings leave padding positions, which hold identity rows)
+void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* iperm, int64_t npos,
+                 int r, int smin, SpPlan* out);
 
 // Persistent, dependency-driven factorization (sp_dag_kernel): one CTA per
 // SM pulls ready tasks from a device queue; completing a task releases its

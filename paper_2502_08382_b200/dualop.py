@@ -132,7 +132,7 @@ def _constraint_rows(sc, n):
 
 class _Sub:
     __slots__ = ("index", "n", "m", "gids", "bcol", "bval", "perm", "iperm", "slot", "values", "pinned",
-                 "cluster", "fix", "solver", "diagpos", "kcache")
+                 "cluster", "fix", "solver", "diagpos", "kcache", "npos")
 
 
 class DualOperator:
@@ -167,7 +167,7 @@ class DualOperator:
     def __init__(self, matrices, constraints, layout, config: DualOpConfig, pool=None, workers: int = 1,
                  schur_cap: int = 2000, device: int | None = None, ordering: str = "rcm",
                  subdomains=None, pinned: bool = True, perms=None, factorization: str = "host",
-                 stiffness=None, kernels=None):
+                 stiffness=None, kernels=None, sparse_ordering: str = "auto"):
         if len(matrices) != len(constraints.per_subdomain):
             raise ValueError("one stiffness matrix per subdomain required")
         if config.strategy != "explicit":
@@ -198,6 +198,10 @@ class DualOperator:
             raise ValueError(f"{factorization} factorization needs stiffness= and kernels= per subdomain")
         self.owned = (list(range(self.n_subdomains)) if subdomains is None
                       else sorted(int(s) for s in subdomains))
+        if not (sparse_ordering in ("auto", "onion") or sparse_ordering.startswith("dissection:")):
+            raise ValueError("sparse_ordering must be 'auto', 'onion' or 'dissection:<depth>'")
+        self.sparse_ordering = sparse_ordering
+        self.sparse_recipe = None
 
         self.prepared = False
         self.step_ready = False
@@ -302,7 +306,8 @@ class DualOperator:
                 n, ip, ix, _ = fct.csr_arrays(self.stiffness[i])
                 if n != sub.n:
                     raise ValueError("stiffness size does not match the subdomain")
-                sub.perm = spr.onion_interface_last(n, ip, ix, sub.bcol)
+                sub.perm, sub.iperm = spr.sparse_route_ordering(n, ip, ix, sub.bcol, self.sparse_recipe)
+                sub.npos = int(sub.perm.shape[0])
             elif self.factorization == "device":
                 base = np.arange(sub.n - 1, -1, -1, dtype=np.int64)   # RCM of the dense K_reg
                 if self.ordering == "rcm":
@@ -315,7 +320,9 @@ class DualOperator:
                 sub.perm = fct.rcm_ordering(matrix)
             else:
                 sub.perm = fct.interface_last_ordering(matrix, sub.bcol)
-            sub.iperm = fct.inverse_permutation(sub.perm)
+            if self.factorization != "sparse":
+                sub.iperm = fct.inverse_permutation(sub.perm)
+                sub.npos = sub.n
             sub.values = None
             sub.pinned = None
             sub.solver = None
@@ -326,6 +333,15 @@ class DualOperator:
                 sub.fix = spr.fixing_dofs(self._kernel_basis(i, sub.n))
             return sub
 
+        if self.factorization == "sparse":
+            # one ordering recipe for the operator, chosen on its first subdomain
+            # by the tile flops it leaves (subdomains of one problem are alike)
+            i0 = order[0]
+            n0, ip0, ix0, _ = fct.csr_arrays(self.stiffness[i0])
+            sc0 = self.constraints.per_subdomain[i0]
+            bcol0, _ = _constraint_rows(sc0, n0)
+            r0 = self._kernel_basis(i0, n0).shape[1]
+            self.sparse_recipe = spr.choose_ordering(n0, ip0, ix0, bcol0, r0, self.sparse_ordering)
         subs = self._map(symbolic, order)
         ctx = C.c_void_p()
         _call(self._lib.feti_create(self._resolve_device(), C.byref(ctx)))
@@ -334,8 +350,8 @@ class DualOperator:
             first = np.ascontiguousarray(sub.iperm[sub.bcol], dtype=np.int64)
             slot = C.c_int64()
             _call(self._lib.feti_add_subdomain(
-                ctx, sub.n, sub.m, _lib.i64ptr(first), _lib.f64ptr(sub.bval), _lib.i64ptr(sub.gids),
-                None, None, fct.packed_size(sub.n), C.byref(slot)))
+                ctx, sub.npos, sub.m, _lib.i64ptr(first), _lib.f64ptr(sub.bval), _lib.i64ptr(sub.gids),
+                None, None, fct.packed_size(sub.npos), C.byref(slot)))
             sub.slot = slot.value
             self._subs[sub.index] = sub
         if self.pool is not None and hasattr(self.pool, "capacity"):

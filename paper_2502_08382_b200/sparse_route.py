@@ -105,3 +105,178 @@ class HostSparseSolver:
         b = np.asarray(b, dtype=np.float64)
         x = self._proj(self.lu.solve(self._proj(b)))
         return x + self.q @ (self.q.T @ b) / self.rho
+
+
+# ---------------------------------------------------------------------------
+# tile-aligned dissection ordering (padded positions)
+# ---------------------------------------------------------------------------
+
+TILE_ROWS = 128
+
+
+def _csr_graph(n, indptr, indices):
+    ip = np.asarray(indptr, np.int64)
+    ix = np.asarray(indices, np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ip))
+    return csr_matrix((np.ones(ix.size, np.int8), (rows, ix)), shape=(n, n))
+
+
+def _bfs_levels(g, src):
+    ip, ix = g.indptr, g.indices
+    lev = np.full(g.shape[0], -1, np.int64)
+    lev[src] = 0
+    front = np.array([src], np.int64)
+    depth = 0
+    while front.size:
+        starts, ends = ip[front], ip[front + 1]
+        nb = np.unique(np.concatenate([ix[a:b] for a, b in zip(starts, ends)]))
+        nb = nb[lev[nb] < 0]
+        depth += 1
+        lev[nb] = depth
+        front = nb
+    return lev
+
+
+def _dissect(g, ids, depth, min_size):
+    """[(kind, dof array)] in elimination order: both halves, then the separator
+    (a middle breadth-first level from a pseudo-peripheral vertex)."""
+    if depth == 0 or ids.size <= min_size:
+        return [("leaf", ids)]
+    from scipy.sparse.csgraph import connected_components
+
+    sub = g[ids][:, ids].tocsr()
+    nc, lab = connected_components(sub, directed=False)
+    if nc > 1:
+        out = []
+        for cc in range(nc):
+            out += _dissect(g, ids[lab == cc], depth, min_size)
+        return out
+    s = 0
+    for _ in range(2):
+        s = int(np.argmax(_bfs_levels(sub, s)))
+    lev = _bfs_levels(sub, s)
+    mid = int(np.searchsorted(np.cumsum(np.bincount(lev)), ids.size / 2))
+    return (_dissect(g, ids[lev < mid], depth - 1, min_size) + _dissect(g, ids[lev > mid], depth - 1, min_size)
+            + [("sep", ids[lev == mid])])
+
+
+def _onion_toward(g, region, boundary):
+    """region's DOFs by decreasing breadth-first distance from `boundary`."""
+    m = region.size
+    sub = np.concatenate([region, boundary])
+    h = g[sub][:, sub].tocsr()
+    nb = boundary.size
+    r = np.concatenate([np.full(nb, m + nb), np.arange(m, m + nb)])
+    c = np.concatenate([np.arange(m, m + nb), np.full(nb, m + nb)])
+    extra = csr_matrix((np.ones(2 * nb, np.int8), (r, c)), shape=(m + nb + 1, m + nb + 1))
+    hh = h.tocoo()
+    h2 = (extra + csr_matrix((hh.data, (hh.row, hh.col)), shape=(m + nb + 1, m + nb + 1))).tocsr()
+    order = breadth_first_order(h2, m + nb, directed=False, return_predecessors=False)
+    order = order[order < m]
+    seen = np.zeros(m, bool)
+    seen[order] = True
+    return region[np.concatenate([np.flatnonzero(~seen), order[::-1]])]
+
+
+def dissection_segments(n, indptr, indices, interface, depth=2, min_size=512):
+    """Segments (DOF arrays) of a tile-aligned ordering: a `depth`-level
+    dissection of the interior (leaves onion-ordered toward their own
+    boundary), then the interface ordered by the segment each DOF touches
+    first, so the interface rows coupled to a leaf share few tiles."""
+    g = _csr_graph(n, indptr, indices)
+    interface = np.unique(np.asarray(interface, np.int64))
+    mark = np.zeros(n, bool)
+    mark[interface] = True
+    interior = np.flatnonzero(~mark)
+    segs = []
+    for kind, ids in _dissect(g, interior, depth, min_size):
+        if ids.size == 0:
+            continue
+        if kind == "leaf":
+            inleaf = np.zeros(n, bool)
+            inleaf[ids] = True
+            nbr = np.unique(g[ids].indices)
+            segs.append(_onion_toward(g, ids, nbr[~inleaf[nbr]]))
+        else:
+            segs.append(ids)
+    seg_of = np.full(n, len(segs), np.int64)
+    for i, s in enumerate(segs):
+        seg_of[s] = i
+    key = np.full(interface.size, len(segs), np.int64)
+    ip = np.asarray(indptr, np.int64)
+    ix = np.asarray(indices, np.int64)
+    for t, d in enumerate(interface):
+        key[t] = seg_of[ix[ip[d]:ip[d + 1]]].min()
+    segs.append(interface[np.lexsort((interface, key))])
+    return segs
+
+
+def padded_positions(segments):
+    """perm_pos (position -> DOF, -1 for padding) with every segment starting
+    at a 128-row tile boundary, and iperm (DOF -> position)."""
+    npos = sum(-(-s.size // TILE_ROWS) * TILE_ROWS for s in segments)
+    n = sum(s.size for s in segments)
+    perm = np.full(npos, -1, np.int64)
+    iperm = np.empty(n, np.int64)
+    p = 0
+    for s in segments:
+        perm[p:p + s.size] = s
+        iperm[s] = p + np.arange(s.size)
+        p += -(-s.size // TILE_ROWS) * TILE_ROWS
+    return perm, iperm
+
+
+def tile_flops_estimate(n, indptr, indices, iperm, npos, kernel_dim, n_iface):
+    """Tile flops of the block-sparse factorization for an ordering (the
+    block symbolic of csrc/feti_sparse.cu sp_symbolic, in Python): used to
+    pick the ordering."""
+    TB = TILE_ROWS
+    T = -(-npos // TB)
+    ip = np.asarray(indptr, np.int64)
+    ix = np.asarray(indices, np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ip))
+    bi, bj = iperm[rows] // TB, iperm[ix] // TB
+    lo = bi > bj
+    struct = [set() for _ in range(T)]
+    for a, b in zip(bi[lo].tolist(), bj[lo].tolist()):
+        struct[b].add(a)
+    smin = (npos - -(-n_iface // TB) * TB) // TB
+    for J in range(smin, T):
+        struct[J].update(range(J + 1, T))
+    ops = 0.0
+    for k in range(T):
+        s = struct[k]
+        sn = len(s)
+        ops += sn * (sn + 1) / 2 + sn + (sn + 2) / 16.0 * (kernel_dim > 0)
+        if s:
+            p = min(s)
+            struct[p] |= (s - {p})
+    return ops * 2.0 * TB ** 3
+
+
+def sparse_route_ordering(n, indptr, indices, interface, recipe):
+    """(perm_pos, iperm) for a recipe ("onion",) or ("dissection", depth)."""
+    if recipe is None or recipe[0] == "onion":
+        perm = onion_interface_last(n, indptr, indices, interface)
+        iperm = np.empty(n, np.int64)
+        iperm[perm] = np.arange(n, dtype=np.int64)
+        return perm, iperm
+    return padded_positions(dissection_segments(n, indptr, indices, interface, depth=int(recipe[1])))
+
+
+def choose_ordering(n, indptr, indices, interface, kernel_dim, mode="auto", max_depth=4):
+    """The recipe with the fewest estimated tile flops (mode "auto"), or the
+    one named by `mode` ("onion", "dissection:<depth>")."""
+    if mode == "onion":
+        return ("onion",)
+    if mode.startswith("dissection:"):
+        return ("dissection", int(mode.split(":", 1)[1]))
+    n_iface = np.unique(np.asarray(interface, np.int64)).size
+    best, best_ops = ("onion",), None
+    candidates = [("onion",)] + ([("dissection", d) for d in range(1, max_depth + 1)] if n >= 16 * TILE_ROWS else [])
+    for rec in candidates:
+        perm, iperm = sparse_route_ordering(n, indptr, indices, interface, rec)
+        ops = tile_flops_estimate(n, indptr, indices, iperm, perm.shape[0], kernel_dim, n_iface)
+        if best_ops is None or ops < best_ops:
+            best, best_ops = rec, ops
+    return best

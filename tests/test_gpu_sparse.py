@@ -183,3 +183,26 @@ def test_sparse_route_persistent_kernel_bit_identical(monkeypatch):
         assert op2.stats()["launches_factorize"] == 3
     for a, b in zip(ref, got):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+def test_sparse_route_padded_dissection_matches_reference(case):
+    """The tile-aligned (padded) dissection ordering: identity rows at padding
+    positions, the same F~_i as the reference."""
+    g = load_golden(case)
+    prob = inputs.Problem(str(g["physics"]), int(g["dim"]), int(g["cells"]), int(g["subs"]))
+    ks, qs, fs = _systems(prob)
+    mats = [inputs.ShapeOnly((prob.n_dofs, prob.n_dofs)) for _ in range(prob.n_sub)]
+    with dualop.prepare(mats, prob.constraints(), prob.layout, CFG, device=0, factorization="sparse",
+                        stiffness=[ks[s] for s in range(prob.n_sub)], kernels=[qs[s] for s in range(prob.n_sub)],
+                        sparse_ordering="dissection:2") as op:
+        assert op.sparse_recipe == ("dissection", 2)
+        op.preprocess()
+        for s in range(prob.n_sub):
+            m = prob.gids[s].shape[0]
+            ref = np.zeros((m, m))
+            ref[np.triu_indices(m)] = g[f"s{s}_F_upper"]
+            f = op.local_operator(s)
+            assert np.linalg.norm(f - ref) <= 1e-10 * np.linalg.norm(ref), (case, s)
+        q = op.apply(g["p"])
+        assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])

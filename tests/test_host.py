@@ -148,3 +148,36 @@ def test_sparse_route_host_pieces(case):
         ref = np.zeros((m, m))
         ref[np.triu_indices(m)] = g[f"s{s}_F_upper"]
         assert np.linalg.norm(np.triu(f) - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_sparse_route_tile_aligned_dissection():
+    """Padded positions of the tile-aligned dissection ordering: every DOF
+    once, segments start on 128-row tiles, the interface last; the chosen
+    recipe for config 3 is a dissection with fewer estimated tile flops
+    than the onion ordering."""
+    from paper_2502_08382_b200 import inputs
+    from paper_2502_08382_b200 import sparse_route as spr
+
+    prob = inputs.Problem("heat", 3, 12, 2)
+    k, _, q = prob.subdomain_system(3)
+    n = k.shape[0]
+    bcol = prob.bcol[3]
+    segs = spr.dissection_segments(n, k.indptr, k.indices, bcol, depth=2)
+    perm, iperm = spr.padded_positions(segs)
+    assert perm.shape[0] % 128 == 0 and perm.shape[0] >= n
+    assert np.array_equal(np.sort(perm[perm >= 0]), np.arange(n))
+    assert np.array_equal(perm[iperm], np.arange(n))
+    p = 0
+    for s in segs:
+        assert p % 128 == 0 and np.array_equal(perm[p:p + s.size], s)
+        p += -(-s.size // 128) * 128
+    iface = np.unique(bcol)
+    assert np.array_equal(np.sort(segs[-1]), iface)
+    on_perm, on_iperm = spr.sparse_route_ordering(n, k.indptr, k.indices, bcol, ("onion",))
+    e_on = spr.tile_flops_estimate(n, k.indptr, k.indices, on_iperm, n, 1, iface.size)
+    e_nd = spr.tile_flops_estimate(n, k.indptr, k.indices, iperm, perm.shape[0], 1, iface.size)
+    assert e_on > 0 and e_nd > 0
+    big = inputs.Problem(*inputs.CONFIGS["c3"])
+    kb, _, qb = big.subdomain_system(21)
+    rec = spr.choose_ordering(kb.shape[0], kb.indptr, kb.indices, big.bcol[21], qb.shape[1])
+    assert rec[0] == "dissection"
