@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -203,6 +204,19 @@ struct feti_ctx {
   cudaGraphExec_t sp_graph_exec = nullptr;   // captured column-launch sequence
   int sp_graph_launches = 0;
   bool sp_graph_used = false;
+  // pipelined steps (after the first factorization): the last
+  // feti_set_stiffness of a group launches that group's factorization (one
+  // captured graph per group: init, scatter, column sequence) while the host
+  // still hands over the other groups' values
+  bool sp_pipelined = false;
+  std::vector<std::pair<int, int>> sp_init_rng;          // per group: SpInit range
+  static constexpr int kMaxGroups = 4;                    // == kSpStreams (checked below)
+  cudaGraphExec_t sp_ggraph[kMaxGroups] = {};
+  std::atomic<int> sp_left[kMaxGroups];
+  std::atomic<bool> sp_launched[kMaxGroups];
+  std::atomic<bool> sp_started{false};
+  int sp_group_launches[kMaxGroups] = {};
+  std::vector<int> sp_big;                                // pivot-report reset values
   int sp_dag_total = 0;
   std::vector<int> sp_dag_init, sp_acc_init, sp_pan_init;
   SpTask* d_dag_tasks = nullptr;
@@ -211,6 +225,7 @@ struct feti_ctx {
   int *d_dag_tcol = nullptr, *d_dag_dcol = nullptr, *d_dag_acc = nullptr, *d_dag_pan = nullptr;
   int *d_dag_queue = nullptr, *d_dag_ht = nullptr;
   static constexpr int kSpStreams = 4;
+  static_assert(kSpStreams == kMaxGroups, "one pipelined graph per group stream");
   std::vector<std::pair<int, int>> sp_corr_rng, sp_sub_rng;   // per group: panels, subdomains
   cudaEvent_t sp_ev[3] = {};   // factorize start, factorize end, assemble end
   std::vector<int> sp_bad_init;
@@ -331,6 +346,24 @@ int build_sparse_tasks(feti_ctx* c) {
       }
     c->sp_flops += P.flops_exec;
   }
+  // init work per group (the list is in subdomain order; groups are ranges)
+  c->sp_init_rng.assign(c->sp_groups, {0, 0});
+  for (int g = 0; g < c->sp_groups; ++g) {
+    const std::vector<int>& wv = c->waves[g];
+    if (wv.empty()) continue;
+    int b = -1, e = 0;
+    for (int i = 0; i < (int)init.size(); ++i)
+      if (init[i].sub >= wv.front() && init[i].sub <= wv.back()) {
+        if (b < 0) b = i;
+        e = i + 1;
+      }
+    c->sp_init_rng[g] = {std::max(b, 0), std::max(e - std::max(b, 0), 0)};
+  }
+  for (int g = 0; g < feti_ctx::kSpStreams; ++g) {
+    c->sp_left[g] = g < c->sp_groups ? (int)c->waves[g].size() : 0;
+    c->sp_launched[g] = false;
+  }
+  c->sp_big.assign(ns, 1 << 30);
   // correction work per group (contiguous subdomain ranges, as the waves)
   c->sp_corr_rng.assign(c->sp_groups, {0, 0});
   c->sp_sub_rng.assign(c->sp_groups, {0, 0});
@@ -515,9 +548,69 @@ int build_sparse_tasks(feti_ctx* c) {
   return FETI_OK;
 }
 
+// One group's factorization on its stream: reset its pivot reports, then the
+// group's captured graph (pool init, K_s scatter, column sequence).
+int launch_group(feti_ctx* c, int g) {
+  cudaStream_t gs = c->sp_streams[g];
+  const auto sr = c->sp_sub_rng[g];
+  const auto ir = c->sp_init_rng[g];
+  if (sr.second > 0)
+    CUDA_TRY(cudaMemcpyAsync(c->d_bad + sr.first, c->sp_big.data() + sr.first, (size_t)sr.second * sizeof(int),
+                             cudaMemcpyHostToDevice, gs));
+  bool first = false;
+  if (c->sp_started.compare_exchange_strong(first, true)) CUDA_TRY(cudaEventRecord(c->sp_ev[0], gs));
+  if (!c->sp_ggraph[g]) {
+    CUDA_TRY(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+    launch_sp_init(c->d_sp_init + ir.first, ir.second, c->d_spsub, gs);
+    launch_sp_scatter(c->d_spsub, sr.first, sr.second, c->sp_max_n, gs);
+    int nl = 2;
+    for (int j = 0; j < c->sp_maxTq; ++j) {
+      const size_t gj = (size_t)g * c->sp_maxTq + j;
+      const auto a = c->sp_acc_rng[gj], d = c->sp_diag_rng[gj], p = c->sp_panel_rng[gj];
+      launch_sp_gemm(c->d_sp_tasks + a.first, a.second, c->d_sp_pairs, gs);
+      launch_sp_potrf(c->d_sp_diag + d.first, d.second, c->d_bad, gs);
+      launch_sp_gemm(c->d_sp_tasks + p.first, p.second, c->d_sp_pairs, gs);
+      nl += (a.second > 0) + (d.second > 0) + (p.second > 0);
+    }
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(cudaStreamEndCapture(gs, &graph));
+    CUDA_TRY(cudaGraphInstantiate(&c->sp_ggraph[g], graph, 0));
+    CUDA_TRY(cudaGraphDestroy(graph));
+    c->sp_group_launches[g] = nl;
+  }
+  CUDA_TRY(cudaGraphLaunch(c->sp_ggraph[g], gs));
+  c->sp_launched[g] = true;
+  return FETI_OK;
+}
+
 int factorize_sparse(feti_ctx* c) {
   cudaStream_t st = c->stream;
   const int ns = (int)c->subs.size();
+  if (c->sp_pipelined) {
+    // later steps: groups whose stiffness hand-over completed are already
+    // running; launch the rest, then join on the context stream
+    int rc;
+    int launches = 0;
+    for (int g = 0; g < c->sp_groups; ++g) {
+      if (!c->sp_launched[g] && (rc = launch_group(c, g))) return rc;
+      launches += c->sp_group_launches[g];
+      CUDA_TRY(cudaEventRecord(c->sp_join[g], c->sp_streams[g]));
+      CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
+    }
+    CUDA_TRY(cudaEventRecord(c->sp_ev[1], st));
+    for (int g = 0; g < c->sp_groups; ++g) {
+      c->sp_left[g] = (int)c->waves[g].size();
+      c->sp_launched[g] = false;
+    }
+    c->sp_started = false;
+    c->stats.flops_factor_exec = c->sp_flops;
+    c->stats.launches_factorize = launches;
+    c->sp_graph_used = false;   // the graphs ran on the group streams
+    for (auto& s : c->subs) s.factor_set = true;
+    c->tiles_fresh = true;
+    c->sp_pending_check = true;
+    return FETI_OK;
+  }
   std::vector<SpSub> ss(ns);
   for (int si = 0; si < ns; ++si) {
     SubHost& s = c->subs[si];
@@ -533,7 +626,7 @@ int factorize_sparse(feti_ctx* c) {
   CUDA_TRY(cudaMemcpyAsync(c->d_bad, c->sp_bad_init.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaEventRecord(c->sp_ev[0], st));
   launch_sp_init(c->d_sp_init, c->n_sp_init, c->d_spsub, st);
-  launch_sp_scatter(c->d_spsub, ns, c->sp_max_n, st);
+  launch_sp_scatter(c->d_spsub, 0, ns, c->sp_max_n, st);
   CUDA_TRY(cudaGetLastError());
   FETI_DEBUG_SYNC(st);
   int launches = 2;
@@ -605,6 +698,13 @@ int factorize_sparse(feti_ctx* c) {
   // feti_assemble runs each group's assembly right behind its factorization
   // on the group's stream and checks the pivots once everything finished
   CUDA_TRY(cudaEventRecord(c->sp_ev[1], st));
+  // FETI_SP_PIPELINE=1: from the next step on, feti_set_stiffness launches
+  // each group as soon as its values are on the device.  Opt-in: it hides the
+  // host hand-over when that is long (c5 e2e 0.34 -> 0.29 s) but the
+  // staggered group starts cost concurrency (c3 device 60.5 -> 66 ms, e2e
+  // unchanged at 70 ms)
+  const char* penv = getenv("FETI_SP_PIPELINE");
+  c->sp_pipelined = !g_debug_sync && !c->sp_use_dag && penv && atoi(penv) == 1;
   c->stats.flops_factor_exec = c->sp_flops;
   c->stats.launches_factorize = launches;
   for (auto& s : c->subs) s.factor_set = true;
@@ -664,6 +764,8 @@ int feti_destroy(feti_ctx* c) {
   for (auto& e : c->sp_ev)
     if (e) cudaEventDestroy(e);
   if (c->sp_graph_exec) cudaGraphExecDestroy(c->sp_graph_exec);
+  for (auto& ge : c->sp_ggraph)
+    if (ge) cudaGraphExecDestroy(ge);
   for (int g = 0; g < feti_ctx::kSpStreams; ++g) {
     if (c->sp_join[g]) cudaEventDestroy(c->sp_join[g]);
     if (c->sp_streams[g]) cudaStreamDestroy(c->sp_streams[g]);
@@ -1576,6 +1678,7 @@ int feti_set_stiffness(feti_ctx* c, int64_t slot, int64_t n, const int64_t* indp
   CUDA_TRY(cudaMemcpy(s.d_kdata, data, (size_t)nnz * 8, cudaMemcpyHostToDevice));
   if (r > 0) CUDA_TRY(cudaMemcpy(s.d_Q, Q, (size_t)(n * r) * 8, cudaMemcpyHostToDevice));
   s.rho = rho;
+  const bool trigger = c->sparse_factor && c->sp_pipelined;
   if (c->sparse_factor && r > 0) {
     // U1 = B~ Q in sorted column order: row a = sign_a Q[dof_a]
     const size_t rows = (size_t)s.P * TB;
@@ -1589,6 +1692,16 @@ int feti_set_stiffness(feti_ctx* c, int64_t slot, int64_t n, const int64_t* indp
       if ((rc = dev_alloc(c, (void**)&s.d_U2W, rows * 2 * r * 8, true))) return rc;
     }
     CUDA_TRY(cudaMemcpy(s.d_U1, u1.data(), rows * r * 8, cudaMemcpyHostToDevice));
+  }
+  if (trigger) {
+    // this slot's descriptor (rho changes per step), then launch its group if
+    // it was the group's last hand-over of the step
+    const SpSub sd{s.d_pool, s.d_tmap, s.d_perm, s.d_iperm, s.d_kptr, s.d_kind, s.d_kdata, s.d_Q, s.d_fix,
+                   s.d_U1, s.d_U2W, s.rho, s.sp.T, s.sp.Tq, (int)s.sp_n, s.sp_r, s.sp_r, (int)s.n};
+    CUDA_TRY(cudaMemcpy(c->d_spsub + slot, &sd, sizeof(SpSub), cudaMemcpyHostToDevice));
+    int g = 0;
+    while (g + 1 < c->sp_groups && slot >= c->sp_sub_rng[g + 1].first) ++g;
+    if (c->sp_left[g].fetch_sub(1) == 1 && !c->sp_launched[g]) return launch_group(c, g);
   }
   return FETI_OK;
 }

@@ -60,8 +60,8 @@ __global__ void __launch_bounds__(256) sp_init_kernel(const SpInit* __restrict__
 
 // K_s entries into the lower block triangle of P K_s P^T: one warp per
 // original row a; the fixing shift rho lands on the diagonal entry.
-__global__ void __launch_bounds__(256) sp_scatter_kernel(const SpSub* __restrict__ ss) {
-  const SpSub& S = ss[blockIdx.y];
+__global__ void __launch_bounds__(256) sp_scatter_kernel(const SpSub* __restrict__ ss, int sub0) {
+  const SpSub& S = ss[sub0 + blockIdx.y];
   const int a = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (a >= S.n) return;
   const int lane = threadIdx.x & 31;
@@ -530,8 +530,8 @@ void launch_sp_init(const SpInit* w, int nw, const SpSub* ss, cudaStream_t st) {
   if (nw > 0) sp_init_kernel<<<nw, 256, 0, st>>>(w, ss);
 }
 
-void launch_sp_scatter(const SpSub* ss, int nsub, int max_n, cudaStream_t st) {
-  if (nsub > 0 && max_n > 0) sp_scatter_kernel<<<dim3((max_n + 7) / 8, nsub), 256, 0, st>>>(ss);
+void launch_sp_scatter(const SpSub* ss, int sub0, int nsub, int max_n, cudaStream_t st) {
+  if (nsub > 0 && max_n > 0) sp_scatter_kernel<<<dim3((max_n + 7) / 8, nsub), 256, 0, st>>>(ss, sub0);
 }
 
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st) {

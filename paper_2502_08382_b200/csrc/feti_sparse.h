@@ -107,7 +107,7 @@ enum { SPQ_TASK = 0, SPQ_DIAG = 1 };
 cudaError_t configure_sparse();
 void launch_sp_dag(const SpDag& g, int nctas, cudaStream_t st);
 void launch_sp_init(const SpInit* w, int nw, const SpSub* ss, cudaStream_t st);
-void launch_sp_scatter(const SpSub* ss, int nsub, int max_n, cudaStream_t st);
+void launch_sp_scatter(const SpSub* ss, int sub0, int nsub, int max_n, cudaStream_t st);
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st);
 void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st);
 // after the assembly: U2/W per (sub, panel), then the rank-2r update of F~

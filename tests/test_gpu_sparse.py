@@ -206,3 +206,25 @@ def test_sparse_route_padded_dissection_matches_reference(case):
             assert np.linalg.norm(f - ref) <= 1e-10 * np.linalg.norm(ref), (case, s)
         q = op.apply(g["p"])
         assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
+
+
+def test_sparse_route_pipelined_steps_bit_identical(monkeypatch):
+    """FETI_SP_PIPELINE=1: later steps launch each group's factorization from
+    its last stiffness hand-over (captured per-group graphs) -- same bits as
+    the first, non-pipelined step, also with a changed coefficient."""
+    monkeypatch.setenv("FETI_SP_PIPELINE", "1")
+    prob = inputs.Problem("elasticity", 2, 16, 2)
+    op, ks, qs, fs = _sparse_op(prob)
+    kl = [ks[s] for s in range(prob.n_sub)]
+    with op:
+        op.preprocess()
+        ref = [op.local_operator(s) for s in range(prob.n_sub)]
+        for _ in range(2):
+            op.preprocess()
+            for s in range(prob.n_sub):
+                assert np.array_equal(op.local_operator(s), ref[s])
+        # K -> 2K scales K_reg by 2 (rho = trace/n doubles too): F~ halves
+        op.preprocess(stiffness=[inputs.Csr(k.shape, k.indptr, k.indices, 2.0 * k.data) for k in kl])
+        for s in range(prob.n_sub):
+            f = op.local_operator(s)
+            assert np.linalg.norm(2.0 * f - ref[s]) <= 1e-12 * np.linalg.norm(ref[s])
