@@ -210,7 +210,7 @@ struct feti_ctx {
   // still hands over the other groups' values
   bool sp_pipelined = false;
   std::vector<std::pair<int, int>> sp_init_rng;          // per group: SpInit range
-  static constexpr int kMaxGroups = 4;                    // == kSpStreams (checked below)
+  static constexpr int kMaxGroups = 8;                    // == kSpStreams (checked below)
   cudaGraphExec_t sp_ggraph[kMaxGroups] = {};
   std::atomic<int> sp_left[kMaxGroups];
   std::atomic<bool> sp_launched[kMaxGroups];
@@ -224,7 +224,7 @@ struct feti_ctx {
   SpCol* d_dag_cols = nullptr;
   int *d_dag_tcol = nullptr, *d_dag_dcol = nullptr, *d_dag_acc = nullptr, *d_dag_pan = nullptr;
   int *d_dag_queue = nullptr, *d_dag_ht = nullptr;
-  static constexpr int kSpStreams = 4;
+  static constexpr int kSpStreams = 8;
   static_assert(kSpStreams == kMaxGroups, "one pipelined graph per group stream");
   std::vector<std::pair<int, int>> sp_corr_rng, sp_sub_rng;   // per group: panels, subdomains
   cudaEvent_t sp_ev[3] = {};   // factorize start, factorize end, assemble end
