@@ -85,6 +85,8 @@ typedef struct feti_stats {
   int32_t launches_factorize;
   int32_t pad_;
   double ms_preprocess;      /* sparse-factor route: factorize start -> assemble end (device) */
+  double flops_factor_alg;   /* sparse-factor route: scalar Cholesky flops of K_s in the chosen ordering
+                                (sum_j c_j (c_j + 3) from the exact column counts, + the y = L^-1 P Q solve) */
 } feti_stats;
 
 int feti_abi_version(void);

@@ -52,6 +52,7 @@ class FetiStats(C.Structure):
         ("launches_assemble", C.c_int32), ("launches_apply", C.c_int32),
         ("ms_factorize", C.c_double), ("ms_correct", C.c_double), ("flops_factor_exec", C.c_double),
         ("launches_factorize", C.c_int32), ("pad_", C.c_int32), ("ms_preprocess", C.c_double),
+        ("flops_factor_alg", C.c_double),
     ]
 
     def as_dict(self):

@@ -249,6 +249,7 @@ struct feti_ctx {
   cudaStream_t sp_streams[kSpStreams] = {};
   cudaEvent_t sp_join[kSpStreams] = {};
   double sp_flops = 0.0;
+  double sp_flops_scalar = 0.0;
 };
 
 namespace {
@@ -345,6 +346,7 @@ int build_sparse_tasks(feti_ctx* c) {
         if (slot >= 0) init.push_back(SpInit{s.d_pool + (size_t)slot * TILE, K, L, si, 0});
       }
     c->sp_flops += P.flops_exec;
+    c->sp_flops_scalar += P.flops_scalar;
   }
   // init work per group (the list is in subdomain order; groups are ranges)
   c->sp_init_rng.assign(c->sp_groups, {0, 0});
@@ -604,6 +606,7 @@ int factorize_sparse(feti_ctx* c) {
     }
     c->sp_started = false;
     c->stats.flops_factor_exec = c->sp_flops;
+    c->stats.flops_factor_alg = c->sp_flops_scalar;
     c->stats.launches_factorize = launches;
     c->sp_graph_used = false;   // the graphs ran on the group streams
     for (auto& s : c->subs) s.factor_set = true;
@@ -706,6 +709,7 @@ int factorize_sparse(feti_ctx* c) {
   const char* penv = getenv("FETI_SP_PIPELINE");
   c->sp_pipelined = !g_debug_sync && !c->sp_use_dag && penv && atoi(penv) == 1;
   c->stats.flops_factor_exec = c->sp_flops;
+    c->stats.flops_factor_alg = c->sp_flops_scalar;
   c->stats.launches_factorize = launches;
   for (auto& s : c->subs) s.factor_set = true;
   c->tiles_fresh = true;

@@ -449,6 +449,49 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
     for (int I = par + 1; I < Tq; ++I)
       if (cs[k][I]) cs[par][I] = 1;
   }
+  // scalar work of the same ordering (the algorithmic figure): elimination
+  // tree (Liu, path compression) and column counts by row-subtree walks,
+  // O(nnz(L)); flops = sum_j c_j (c_j + 3), c_j = nonzeros below the diagonal
+  {
+    std::vector<int64_t> pos_dof(npos, -1);
+    for (int64_t a = 0; a < n; ++a) pos_dof[iperm[a]] = a;
+    std::vector<int64_t> parent(npos, -1), anc(npos, -1), mark(npos, -1), cnt(npos, 0);
+    for (int64_t i = 0; i < npos; ++i) {
+      const int64_t a = pos_dof[i];
+      if (a < 0) continue;
+      for (int64_t p = indptr[a]; p < indptr[a + 1]; ++p) {
+        int64_t k = iperm[indices[p]];
+        while (k >= 0 && k < i) {          // etree with path compression
+          const int64_t nx = anc[k];
+          anc[k] = i;
+          if (nx < 0) {
+            parent[k] = i;
+            break;
+          }
+          k = nx;
+        }
+      }
+    }
+    for (int64_t i = 0; i < npos; ++i) {
+      const int64_t a = pos_dof[i];
+      if (a < 0) continue;
+      mark[i] = i;
+      for (int64_t p = indptr[a]; p < indptr[a + 1]; ++p) {
+        for (int64_t j = iperm[indices[p]]; j >= 0 && j < i && mark[j] != i; j = parent[j]) {
+          ++cnt[j];                          // L(i, j) != 0
+          mark[j] = i;
+        }
+      }
+    }
+    double fl = 0.0;
+    int64_t nl = 0;
+    for (int64_t j = 0; j < npos; ++j) {
+      fl += (double)cnt[j] * (double)(cnt[j] + 3);
+      nl += cnt[j] + (pos_dof[j] >= 0 ? 1 : 0);
+    }
+    P.nnz_l = nl;
+    P.flops_scalar = fl + 4.0 * r * (double)nl;   // + y = L^-1 P Q and y^T y
+  }
   // slots: everything outside the trailing triangle first, then the trailing
   // triangle in the assembly's tri_index order
   P.tmap.assign((size_t)Tq * Tq, -1);

@@ -69,6 +69,8 @@ struct SpPlan {
   std::vector<std::vector<std::pair<int, std::vector<std::pair<int, int>>>>> acc;
   std::vector<std::vector<int>> panel;  // per column j < T: slots of L_ij, i in struct(j)
   double flops_exec = 0.0;            // tile flops the factorization executes
+  double flops_scalar = 0.0;          // scalar Cholesky flops of K_s in this ordering (+ the y = L^-1 P Q solve)
+  int64_t nnz_l = 0;                  // nonzeros of the scalar factor
 };
 // indptr/indices: symmetric pattern of K (original numbering); iperm: DOF ->
 // position; r: kernel dimension (adds the (P Q)^T block row T when > 0);

@@ -228,3 +228,31 @@ def test_sparse_route_pipelined_steps_bit_identical(monkeypatch):
         for s in range(prob.n_sub):
             f = op.local_operator(s)
             assert np.linalg.norm(2.0 * f - ref[s]) <= 1e-12 * np.linalg.norm(ref[s])
+
+
+def test_sparse_route_algorithmic_flop_count():
+    """flops_factor_alg (structural column counts of the scalar factor of K_s
+    in the chosen ordering, sum_j c_j (c_j + 3) + 4 r nnz(L)) against the
+    nonzeros of a dense Cholesky of a matrix with K's stored CSR structure
+    and generic values (K itself stores exact zeros: P1 Laplacian couplings
+    along Kuhn diagonals vanish, and the device factors them as structure)."""
+    prob = inputs.Problem("heat", 3, 8, 2)
+    op, ks, qs, fs = _sparse_op(prob)
+    rng = np.random.default_rng(5)
+    with op:
+        op.preprocess()
+        got = op.stats()["flops_factor_alg"]
+        ref = 0.0
+        for s in range(prob.n_sub):
+            sub = op._subs[s]
+            pat = np.zeros((prob.n_dofs, prob.n_dofs), bool)      # the stored CSR structure
+            pat[np.repeat(np.arange(prob.n_dofs), np.diff(ks[s].indptr)), ks[s].indices] = True
+            a = pat * rng.uniform(0.1, 1.0, size=pat.shape)
+            a = np.triu(a, 1)
+            a = a + a.T
+            a[np.diag_indices_from(a)] = np.abs(a).sum(axis=1) + 1.0
+            order = sub.perm[sub.perm >= 0]
+            lf = np.linalg.cholesky(a[np.ix_(order, order)])
+            c = (lf != 0.0).sum(axis=0) - 1
+            ref += float((c * (c + 3.0)).sum()) + 4.0 * qs[s].shape[1] * float((c + 1).sum())
+    assert abs(got - ref) <= 1e-9 * ref, (got, ref)
