@@ -50,3 +50,21 @@ for dag in ("0", "1"):
         op.preprocess()
         q = op.apply(np.random.default_rng(0).normal(size=prob.n_multipliers))
         print("sparse route dag", dag, "apply norm", np.linalg.norm(q))
+# tile-aligned dissection (padded positions) and the lumped preconditioner
+os.environ.pop("FETI_SP_DAG", None)
+prob = inputs.Problem("heat", 3, 6, 2)
+ks, qs, fs = [], [], []
+for s in range(prob.n_sub):
+    k, f, qk = prob.subdomain_system(s)
+    ks.append(k)
+    qs.append(qk)
+    fs.append(f)
+mats = [inputs.ShapeOnly((prob.n_dofs, prob.n_dofs)) for _ in range(prob.n_sub)]
+with dualop.prepare(mats, prob.constraints(), prob.layout, CFG, device=0, factorization="sparse",
+                    stiffness=ks, kernels=qs, sparse_ordering="dissection:2") as op:
+    op.preprocess()
+    op.preprocess()
+    q = op.apply(np.random.default_rng(0).normal(size=prob.n_multipliers))
+    op.set_lumped_preconditioner(ks)
+    mq = op.precond_apply(q)
+    print("dissection route apply norm", np.linalg.norm(q), "lumped", np.linalg.norm(mq))
