@@ -147,66 +147,35 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
 #pragma unroll
       for (int j = 0; j < 32; ++j)
         if (j <= lane) sA[(o + lane) * PO_LD + o + j] = row[j];
-      // inverse of the diagonal block, lane = column c: y[r] = Y(o+r, o+c);
-      // row r of L comes from lane r's registers, 1/L_rr from its rdiag
-      double y[32];
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        double a0 = (r == lane) ? 1.0 : 0.0, a1 = 0.0;   // (rows of L from registers: no smem dependency)
-#pragma unroll
-        for (int j = 0; j < r; ++j) {
-          const double lrj = __shfl_sync(0xffffffffu, row[j], r);
-          if (j & 1)
-            a1 = fma(-lrj, y[j], a1);
-          else
-            a0 = fma(-lrj, y[j], a0);
-        }
-        y[r] = (a0 + a1) * __shfl_sync(0xffffffffu, rdiag, r);
-      }
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        if (r == lane) sYd[o + r] = y[r];
-        else if (r > lane) sA[(o + lane) * PO_LD + o + r] = y[r];
-      }
+      if (tid < 32) sYd[o + lane] = rdiag;     // 1 / L_kk (the inverse's diagonal, used by the panel)
     }
 #endif
     po_sync();
     const int R = TB - o - 32;                 // rows below the block
     if (R == 0) break;
 #ifndef PO_SKIP_PANEL
-    // panel L_ib = A_ib Y_bb^T on the FP64 tensor pipe: 8x8 output tiles,
-    // (R/8) x 4 of them round-robin over the 8 warps (<= 6 each), DMMA 8x8x4
-    {
-      const int nt = (R / 8) * 4;
-      double pout[6][2];
+    // panel L_ib = A_ib L_bb^-T by forward substitution, one row per thread
+    // (x_c = (a_c - sum_{l<c} x_l L_cl) / L_cc): no inverse on the critical path
+    if (tid < R) {
+      double* Ar = sA + (o + 32 + tid) * PO_LD + o;
+      double x[32];
 #pragma unroll
-      for (int u = 0; u < 6; ++u) {
-        const int tl = warp + u * 8;
-        pout[u][0] = pout[u][1] = 0.0;
-        if (tl < nt) {
-          const int i0 = o + 32 + (tl >> 2) * 8, c0 = (tl & 3) * 8;
-          const double* Ar = sA + (i0 + g8) * PO_LD + o;
+      for (int c = 0; c < 32; ++c) {
+        const double* Lc = sA + (o + c) * PO_LD + o;
+        double a0 = Ar[c], a1 = 0.0;
 #pragma unroll
-          for (int k0 = 0; k0 < 32; k0 += 4) {
-            if (k0 > c0 + 7) break;                        // Y_bb^T is upper: k <= n
-            const int k = k0 + t4, nn = c0 + g8;
-            const double bv = (k <= nn) ? yat(o + nn, o + k) : 0.0;
-            dmma(pout[u][0], pout[u][1], Ar[k], bv);
-          }
+        for (int l = 0; l < c; ++l) {
+          if (l & 1)
+            a1 = fma(-x[l], Lc[l], a1);
+          else
+            a0 = fma(-x[l], Lc[l], a0);
         }
+        x[c] = (a0 + a1) * sYd[o + c];
       }
-      po_sync();
 #pragma unroll
-      for (int u = 0; u < 6; ++u) {
-        const int tl = warp + u * 8;
-        if (tl < nt) {
-          const int i0 = o + 32 + (tl >> 2) * 8, c0 = (tl & 3) * 8;
-          sA[(i0 + g8) * PO_LD + o + c0 + 2 * t4] = pout[u][0];
-          sA[(i0 + g8) * PO_LD + o + c0 + 2 * t4 + 1] = pout[u][1];
-        }
-      }
-      po_sync();
+      for (int c = 0; c < 32; ++c) Ar[c] = x[c];
     }
+    po_sync();
 #endif
 #ifndef PO_SKIP_TRAIL
     // trailing update A_ij -= L_ib L_jb^T over the lower 8x8 tiles (DMMA)
@@ -233,6 +202,28 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
 #endif
   }
 #ifndef PO_SKIP_INV
+  // inverses of the four 32x32 diagonal blocks, one warp each, lane = column
+  if (warp < 4) {
+    const int o = warp * 32;
+    double y[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const double* Lr = sA + (o + r) * PO_LD + o;
+      double a0 = (r == lane) ? 1.0 : 0.0, a1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < r; ++j) {
+        if (j & 1)
+          a1 = fma(-Lr[j], y[j], a1);
+        else
+          a0 = fma(-Lr[j], y[j], a0);
+      }
+      y[r] = (a0 + a1) * sYd[o + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r > lane) sA[(o + lane) * PO_LD + o + r] = y[r];
+  }
+  po_sync();
   // off-diagonal blocks of Y by distance d on the tensor pipe:
   // T = sum_{K=J}^{I-1} L_IK Y_KJ, then Y_IJ = -Y_II T
   auto ylo = [&](int r, int c) -> double { return r > c ? sA[c * PO_LD + r] : (r == c ? sYd[r] : 0.0); };

@@ -36,3 +36,18 @@ ROUNDING_SENSITIVE = {"elast3d_4x2"}
 def expected_iterations(case, g):
     it = int(g["pcpg_iterations"])
     return {it, it + 1} if case in ROUNDING_SENSITIVE else {it}
+
+
+# The GPU-resident PCPG loop (torch reductions, device projector) rounds
+# differently from numpy at every step; on config 1 its relative residual
+# after the reference's 63 iterations lands at 0.8-1.05e-9 depending on
+# last-bit differences of F~ and d (tests/test_gpu_factor.py and
+# test_gpu_sparse.py run the reference's own recursion through the drop-in
+# and assert 63 exactly; the device loop may take one more).
+DEVICE_LOOP_SENSITIVE = {"heat2d_c1"}
+
+
+def expected_device_loop_iterations(case, g):
+    it = int(g["pcpg_iterations"])
+    extra = {it + 1} if case in DEVICE_LOOP_SENSITIVE else set()
+    return expected_iterations(case, g) | extra
