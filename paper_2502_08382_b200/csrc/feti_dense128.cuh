@@ -97,6 +97,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
   double* sA = smem;                    // [i][j] at i * PO_LD + j
   double* sYd = smem + TB * PO_LD;      // diagonal of Y
   double* sT = sYd + TB;                // 3 x 1024 scratch
+  double* colbuf = sT;                  // 32: one column of a diagonal block (scratch is free then)
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, t4 = lane & 3;      // DMMA fragment coordinates
@@ -138,11 +139,11 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
         if (lane == k) rdiag = rp;
         const double lik = (lane == k) ? pv : (lane > k ? row[k] * rp : 0.0);
         row[k] = lik;
+        colbuf[lane] = lik;                    // column k, read back as broadcasts
+        __syncwarp();
 #pragma unroll
-        for (int j = k + 1; j < 32; ++j) {
-          const double ljk = __shfl_sync(0xffffffffu, lik, j);
-          row[j] = fma(-lik, ljk, row[j]);
-        }
+        for (int j = k + 1; j < 32; ++j) row[j] = fma(-lik, colbuf[j], row[j]);
+        __syncwarp();
       }
 #pragma unroll
       for (int j = 0; j < 32; ++j)
