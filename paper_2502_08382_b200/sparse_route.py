@@ -137,9 +137,10 @@ def _bfs_levels(g, src):
     return lev
 
 
-def _dissect(g, ids, depth, min_size):
+def _dissect(g, ids, depth, min_size, sep_rule="mid"):
     """[(kind, dof array)] in elimination order: both halves, then the separator
-    (a middle breadth-first level from a pseudo-peripheral vertex)."""
+    (a breadth-first level from a pseudo-peripheral vertex: the median level,
+    or with sep_rule "minsep" the smallest level within 35-65 % of the DOFs)."""
     if depth == 0 or ids.size <= min_size:
         return [("leaf", ids)]
     from scipy.sparse.csgraph import connected_components
@@ -149,15 +150,22 @@ def _dissect(g, ids, depth, min_size):
     if nc > 1:
         out = []
         for cc in range(nc):
-            out += _dissect(g, ids[lab == cc], depth, min_size)
+            out += _dissect(g, ids[lab == cc], depth, min_size, sep_rule)
         return out
     s = 0
     for _ in range(2):
         s = int(np.argmax(_bfs_levels(sub, s)))
     lev = _bfs_levels(sub, s)
-    mid = int(np.searchsorted(np.cumsum(np.bincount(lev)), ids.size / 2))
-    return (_dissect(g, ids[lev < mid], depth - 1, min_size) + _dissect(g, ids[lev > mid], depth - 1, min_size)
-            + [("sep", ids[lev == mid])])
+    cnt = np.bincount(lev)
+    cum = np.cumsum(cnt)
+    mid = int(np.searchsorted(cum, ids.size / 2))
+    if sep_rule == "minsep":
+        cand = [lv for lv in range(1, cnt.size - 1) if 0.35 * ids.size <= cum[lv - 1] and cum[lv] - cnt[lv]
+                <= 0.65 * ids.size]
+        if cand:
+            mid = min(cand, key=lambda lv: cnt[lv])
+    return (_dissect(g, ids[lev < mid], depth - 1, min_size, sep_rule)
+            + _dissect(g, ids[lev > mid], depth - 1, min_size, sep_rule) + [("sep", ids[lev == mid])])
 
 
 def _onion_toward(g, region, boundary):
@@ -178,7 +186,7 @@ def _onion_toward(g, region, boundary):
     return region[np.concatenate([np.flatnonzero(~seen), order[::-1]])]
 
 
-def dissection_segments(n, indptr, indices, interface, depth=2, min_size=512):
+def dissection_segments(n, indptr, indices, interface, depth=2, min_size=512, sep_rule="mid"):
     """Segments (DOF arrays) of a tile-aligned ordering: a `depth`-level
     dissection of the interior (leaves onion-ordered toward their own
     boundary), then the interface ordered by the segment each DOF touches
@@ -189,7 +197,7 @@ def dissection_segments(n, indptr, indices, interface, depth=2, min_size=512):
     mark[interface] = True
     interior = np.flatnonzero(~mark)
     segs = []
-    for kind, ids in _dissect(g, interior, depth, min_size):
+    for kind, ids in _dissect(g, interior, depth, min_size, sep_rule):
         if ids.size == 0:
             continue
         if kind == "leaf":
@@ -255,13 +263,15 @@ def tile_flops_estimate(n, indptr, indices, iperm, npos, kernel_dim, n_iface):
 
 
 def sparse_route_ordering(n, indptr, indices, interface, recipe):
-    """(perm_pos, iperm) for a recipe ("onion",) or ("dissection", depth)."""
+    """(perm_pos, iperm) for a recipe ("onion",), ("dissection", depth) or
+    ("dissection", depth, sep_rule)."""
     if recipe is None or recipe[0] == "onion":
         perm = onion_interface_last(n, indptr, indices, interface)
         iperm = np.empty(n, np.int64)
         iperm[perm] = np.arange(n, dtype=np.int64)
         return perm, iperm
-    return padded_positions(dissection_segments(n, indptr, indices, interface, depth=int(recipe[1])))
+    rule = recipe[2] if len(recipe) > 2 else "mid"
+    return padded_positions(dissection_segments(n, indptr, indices, interface, depth=int(recipe[1]), sep_rule=rule))
 
 
 def choose_ordering(n, indptr, indices, interface, kernel_dim, mode="auto", max_depth=4):
@@ -273,7 +283,10 @@ def choose_ordering(n, indptr, indices, interface, kernel_dim, mode="auto", max_
         return ("dissection", int(mode.split(":", 1)[1]))
     n_iface = np.unique(np.asarray(interface, np.int64)).size
     best, best_ops = ("onion",), None
-    candidates = [("onion",)] + ([("dissection", d) for d in range(1, max_depth + 1)] if n >= 16 * TILE_ROWS else [])
+    candidates = [("onion",)]
+    if n >= 16 * TILE_ROWS:
+        candidates += [("dissection", d) for d in range(1, max_depth + 1)]
+        candidates += [("dissection", d, "minsep") for d in range(1, max_depth + 1)]
     for rec in candidates:
         perm, iperm = sparse_route_ordering(n, indptr, indices, interface, rec)
         ops = tile_flops_estimate(n, indptr, indices, iperm, perm.shape[0], kernel_dim, n_iface)
