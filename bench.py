@@ -548,6 +548,7 @@ def run_sparse(args, rank, world, local_rank):
         ta.append(time.perf_counter() - t0)
     apply_e2e_ms = max_over_ranks(statistics.median(ta) * 1e3)
     h2d = int(sum(ks[s].indptr[-1] * 8 + qs[s].size * 8 for s in owned)) + 8 * prob.n_multipliers
+    recipe = op.sparse_recipe
     op.close()
     del op, dco, p_dev, q_dev
     torch.cuda.empty_cache()
@@ -564,7 +565,7 @@ def run_sparse(args, rank, world, local_rank):
         "data": "synthetic: the reference's problem regenerated (inputs.py); sparse K + kernel basis per subdomain",
         "config": {"workload": f"{args.config}: {prob.physics} {prob.dim}D, {prob.n_sub} subdomains x {n} DOFs, "
                                f"{prob.n_multipliers} multipliers", "route": "sparse-factor (K_s + rank-2r correction)",
-                   "ordering": "constrained DOFs last, interior onion (BFS from the interface, reversed)",
+                   "ordering": f"constrained DOFs last; interior recipe {recipe!r} (tile-flop estimator, sparse_route.choose_ordering)",
                    "parallelism": f"cluster-per-gpu x{world}",
                    "l2": f"inputs larger than L2 (block-sparse factor tiles {st['bytes_temporary'] / 1e9:.0f} GB, "
                          f"packed F~ {8 * sum(m * (m + 1) / 2 for m in prob.m_per_subdomain()) / 1e9:.2f} GB "
