@@ -1076,7 +1076,10 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
 
   // per-warp accumulators in smem: (NW + 1) * M doubles
   c->apply_nw = 8;
-  while (c->apply_nw > 1 && (size_t)(c->apply_nw + 1) * max_M * 8 > 227 * 1024) c->apply_nw >>= 1;
+  // (as many warps as the accumulators leave room for: each warp keeps one
+  // 32x32 tile load in flight, and the kernel is HBM-bound on bytes in flight)
+  if (const char* wenv = getenv("FETI_APPLY_WARPS")) c->apply_nw = std::max(1, std::min(8, atoi(wenv)));   // tests
+  while (c->apply_nw > 1 && (size_t)(c->apply_nw + 1) * max_M * 8 > 227 * 1024) --c->apply_nw;
   c->apply_smem = (size_t)(c->apply_nw + 1) * max_M * 8;
   if (c->apply_smem > 227 * 1024)
     return fail(FETI_ERR_CAPACITY, "subdomain with %d multipliers exceeds the apply kernel's shared memory", max_M);

@@ -21,6 +21,7 @@
 //   7. reduce   q[g] = sum over (subdomain, local) contributions in the
 //               reference's fixed gather order (dualop.py:375-379).
 #include <cstdio>
+#include <cstdlib>
 
 #include "feti_common.cuh"
 #include "feti_dense128.cuh"
@@ -547,7 +548,7 @@ __device__ __forceinline__ void apply_advance(int& ti, int& tj, int step, int T3
   tj = ti + rem;
 }
 
-template <int NW>
+template <int NW, bool TRIPLE>
 __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict__ subs,
                                                         const int4* __restrict__ segs,
                                                         const int* __restrict__ seg_ptr,
@@ -584,6 +585,29 @@ __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict
     int tj = ti + (int)(tt - rowstart);
     const double* Fb = S.F;
     double fa[32], fb[32];
+    if constexpr (TRIPLE) {
+      // three tiles per warp in registers: two loads in flight while one is
+      // reduced (matters when the accumulators leave room for few warps)
+      double fc[32];
+      if (tt < t1) apply_tile_load(fa, Fb + tt * ATILE, lane);
+      if (tt + NW < t1) apply_tile_load(fb, Fb + (tt + NW) * ATILE, lane);
+      while (tt < t1) {
+        if (tt + 2 * NW < t1) apply_tile_load(fc, Fb + (tt + 2 * NW) * ATILE, lane);
+        apply_tile_compute(fa, ti, tj, sp, myq, lane);
+        tt += NW;
+        apply_advance(ti, tj, NW, T32);
+        if (tt >= t1) break;
+        if (tt + 2 * NW < t1) apply_tile_load(fa, Fb + (tt + 2 * NW) * ATILE, lane);
+        apply_tile_compute(fb, ti, tj, sp, myq, lane);
+        tt += NW;
+        apply_advance(ti, tj, NW, T32);
+        if (tt >= t1) break;
+        if (tt + 2 * NW < t1) apply_tile_load(fb, Fb + (tt + 2 * NW) * ATILE, lane);
+        apply_tile_compute(fc, ti, tj, sp, myq, lane);
+        tt += NW;
+        apply_advance(ti, tj, NW, T32);
+      }
+    } else {
     if (tt < t1) apply_tile_load(fa, Fb + tt * ATILE, lane);
     while (tt < t1) {
       int ti2 = ti, tj2 = tj;
@@ -602,6 +626,7 @@ __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict
       tt = nx;
       ti = ti2;
       tj = tj2;
+    }
     }
     __syncthreads();
     double* out = part + part_off[w.w];
@@ -651,14 +676,15 @@ cudaError_t configure_kernels() {
   if ((e = cudaFuncSetAttribute(diag_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (2 * 8256 + 3 * 1024) * 8)))
     return e;
-  if ((e = cudaFuncSetAttribute(apply_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
-    return e;
-  if ((e = cudaFuncSetAttribute(apply_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
-    return e;
-  if ((e = cudaFuncSetAttribute(apply_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
-    return e;
-  if ((e = cudaFuncSetAttribute(apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
-    return e;
+  const void* applies[16] = {
+      (const void*)apply_kernel<1, false>, (const void*)apply_kernel<2, false>, (const void*)apply_kernel<3, false>,
+      (const void*)apply_kernel<4, false>, (const void*)apply_kernel<5, false>, (const void*)apply_kernel<6, false>,
+      (const void*)apply_kernel<7, false>, (const void*)apply_kernel<8, false>, (const void*)apply_kernel<1, true>,
+      (const void*)apply_kernel<2, true>,  (const void*)apply_kernel<3, true>,  (const void*)apply_kernel<4, true>,
+      (const void*)apply_kernel<5, true>,  (const void*)apply_kernel<6, true>,  (const void*)apply_kernel<7, true>,
+      (const void*)apply_kernel<8, true>};
+  for (const void* k : applies)
+    if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024))) return e;
   return cudaSuccess;
 }
 
@@ -683,12 +709,25 @@ void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t s
 void launch_apply(int nw, size_t smem, const SubDev* subs, const int4* segs, const int* seg_ptr, int nctas,
                   const int64_t* part_off, double* part, const double* p, cudaStream_t st) {
   if (nctas <= 0) return;
+  const bool triple = getenv("FETI_APPLY_2BUF") == nullptr;   // A/B switch for measurements
+#define FETI_APPLY_CASE(W)                                                                            \
+  case W:                                                                                             \
+    if (triple)                                                                                       \
+      apply_kernel<W, true><<<nctas, W * 32, smem, st>>>(subs, segs, seg_ptr, part_off, part, p);    \
+    else                                                                                              \
+      apply_kernel<W, false><<<nctas, W * 32, smem, st>>>(subs, segs, seg_ptr, part_off, part, p);   \
+    break;
   switch (nw) {
-    case 8: apply_kernel<8><<<nctas, 256, smem, st>>>(subs, segs, seg_ptr, part_off, part, p); break;
-    case 4: apply_kernel<4><<<nctas, 128, smem, st>>>(subs, segs, seg_ptr, part_off, part, p); break;
-    case 2: apply_kernel<2><<<nctas, 64, smem, st>>>(subs, segs, seg_ptr, part_off, part, p); break;
-    default: apply_kernel<1><<<nctas, 32, smem, st>>>(subs, segs, seg_ptr, part_off, part, p); break;
+    FETI_APPLY_CASE(8)
+    FETI_APPLY_CASE(7)
+    FETI_APPLY_CASE(6)
+    FETI_APPLY_CASE(5)
+    FETI_APPLY_CASE(4)
+    FETI_APPLY_CASE(3)
+    FETI_APPLY_CASE(2)
+    default: FETI_APPLY_CASE(1)
   }
+#undef FETI_APPLY_CASE
 }
 void launch_reduce(int n_mult, const int* cptr, const int4* cent, const int64_t* part_off, const double* part,
                    double* q, cudaStream_t st) {
@@ -704,7 +743,7 @@ int kernel_attributes(char* buf, int len) {
       {"unpack_dense", (const void*)unpack_dense_kernel},   {"scatter_sparse", (const void*)scatter_sparse_kernel},
       {"diag_inverse", (const void*)diag_inverse_kernel},   {"block_scale", (const void*)block_scale_kernel},
       {"trsm_chain", (const void*)trsm_chain_kernel},       {"syrk", (const void*)syrk_kernel},
-      {"apply8", (const void*)apply_kernel<8>},             {"reduce", (const void*)reduce_kernel}};
+      {"apply8", (const void*)apply_kernel<8, true>},             {"reduce", (const void*)reduce_kernel}};
   int off = 0;
   for (auto& k : ks) {
     cudaFuncAttributes a;

@@ -327,3 +327,21 @@ def test_implicit_device_apply_matches_reference(case, ordering):
     assert np.array_equal(qi, qi2)
     assert np.linalg.norm(qi - g["q_implicit"]) <= 1e-11 * np.linalg.norm(g["q_implicit"])
     assert np.linalg.norm(qi - qe) <= 1e-11 * np.linalg.norm(qe)
+
+
+@pytest.mark.parametrize("two_buffers", [False, True])
+@pytest.mark.parametrize("warps", [1, 3, 5, 6, 7, 8])
+def test_apply_any_warp_count_matches_reference(warps, two_buffers, monkeypatch):
+    """The apply kernel runs with as many warps per CTA as its per-warp
+    accumulators leave room for (6 on c4's 3,873-multiplier subdomains),
+    with two or three register tile buffers per warp; every variant gives the
+    reference's q."""
+    monkeypatch.setenv("FETI_APPLY_WARPS", str(warps))
+    if two_buffers:
+        monkeypatch.setenv("FETI_APPLY_2BUF", "1")
+    g = load_golden(SMALL_CASES[-1])
+    prob, mats, cons, lay = _golden_problem(g)
+    with dualop.prepare(mats, cons, lay, CFG) as op:
+        op.preprocess()
+        q = op.apply(g["p"])
+    assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
