@@ -85,7 +85,10 @@ __device__ __forceinline__ void invert_lower_128(const double* __restrict__ sL, 
 // diagonal block in registers (shuffle broadcasts), all warps apply it to
 // the panel below and update the trailing matrix; the off-diagonal blocks of
 // Y follow by distance, Y_IJ = -Y_II sum_{K=J}^{I-1} L_IK Y_KJ.
-constexpr int PO_LD = TB + 1;
+#ifndef FETI_PO_LD
+#define FETI_PO_LD (TB + 1)
+#endif
+constexpr int PO_LD = FETI_PO_LD;
 
 // Barrier over the 256 threads (warps 0-7) that run potrf_invert_128: a named
 // barrier, so a persistent CTA with extra warps can call it.
