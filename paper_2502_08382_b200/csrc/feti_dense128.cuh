@@ -77,8 +77,10 @@ __device__ __forceinline__ void invert_lower_128(const double* __restrict__ sL, 
 // A non-positive pivot is reported as atomicMin(bad, rowbase + j) and
 // replaced by 1 so the sweep completes.  Must be called by all 256 threads.
 //
-// Shared memory: one 128 x 129 row-major array (odd stride: row and column
-// walks are bank-conflict free) holding L in its lower triangle and
+// Shared memory: one 128 x 132 row-major array (stride = 4 mod 16 doubles:
+// the DMMA fragment loads, rows g8 x columns t4, are bank-conflict free; the
+// odd stride 129 made them 4-way and measured 70.0 vs 61.4 us per tile,
+// scripts/gpu_potrf.sh, profiles/r01d_potrf_stride.md) holding L in its lower triangle and
 // Y = inv(L) transposed in its strict upper triangle (Y(i, j), i > j, at
 // [j][i]), the diagonal of Y apart, plus a 3 x 32 x 32 scratch.  Blocked
 // over four 32-wide block columns: one warp factors and inverts the 32x32
@@ -86,7 +88,7 @@ __device__ __forceinline__ void invert_lower_128(const double* __restrict__ sL, 
 // the panel below and update the trailing matrix; the off-diagonal blocks of
 // Y follow by distance, Y_IJ = -Y_II sum_{K=J}^{I-1} L_IK Y_KJ.
 #ifndef FETI_PO_LD
-#define FETI_PO_LD (TB + 1)
+#define FETI_PO_LD (TB + 4)
 #endif
 constexpr int PO_LD = FETI_PO_LD;
 
