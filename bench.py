@@ -325,7 +325,7 @@ def load_traffic(config, ordering):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    from paper_2502_08382_b200 import inputs
+    from harness import inputs
 
     prob = inputs.Problem(*inputs.CONFIGS[args.config])
     ms = prob.m_per_subdomain()
@@ -456,7 +456,8 @@ def run_sparse(args, rank, world, local_rank):
 
     from paper_2502_08382_b200 import _lib
     from paper_2502_08382_b200 import distributed as fd
-    from paper_2502_08382_b200 import dualop, inputs
+    from harness import inputs
+    from paper_2502_08382_b200 import dualop
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -629,7 +630,8 @@ def run_ours(args, rank, world, local_rank):
 
     from paper_2502_08382_b200 import _lib
     from paper_2502_08382_b200 import distributed as fd
-    from paper_2502_08382_b200 import dualop, inputs
+    from harness import inputs
+    from paper_2502_08382_b200 import dualop
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)

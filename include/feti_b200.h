@@ -52,6 +52,11 @@ enum {
 
 enum { FETI_FACTOR_HOST = 0, FETI_FACTOR_DEVICE = 1 };
 
+/* DualOpConfig.strategy (dualop.py:55-82): explicit F~ (default), or the
+ * implicit strategy -- no F~, each apply runs two block triangular sweeps
+ * over the factor (apply_implicit_local, dualop.py:504-521). */
+enum { FETI_STRATEGY_EXPLICIT = 0, FETI_STRATEGY_IMPLICIT = 1 };
+
 typedef struct feti_ctx feti_ctx;
 
 typedef struct feti_stats {
@@ -113,6 +118,15 @@ int feti_add_subdomain(feti_ctx* ctx, int64_t n, int64_t m, const int64_t* first
                        const int64_t* gids, const int64_t* up, const int64_t* ui, int64_t nnz,
                        int64_t* out_slot);
 
+/* Choose the strategy before feti_finalize (replaces the branch on
+ * config.strategy in DualOperator.preprocess/_apply_local, dualop.py:317-322,
+ * 382-388).  Implicit: feti_assemble only prepares the block-scaled factor
+ * (no TRSM/SYRK, no F~ memory) and feti_apply/feti_apply_device run the
+ * implicit sweeps; feti_local_operator is unavailable (the reference's
+ * local_operator returns None, dualop.py:399-401).  Not available with the
+ * sparse-factor route. */
+int feti_set_strategy(feti_ctx* ctx, int strategy);
+
 /* Allocate persistent and temporary device memory; n_multipliers is the
  * global dual-vector length. */
 int feti_finalize(feti_ctx* ctx, int64_t n_multipliers);
@@ -135,7 +149,10 @@ int feti_apply(feti_ctx* ctx, const double* p, double* q);
 
 /* Same on device vectors, enqueued on `stream` (a cudaStream_t used
  * verbatim: NULL is the legacy default stream).  Does not synchronise; the
- * caller orders it after feti_assemble (which returns synchronised). */
+ * caller orders it after feti_assemble (which returns synchronised).  The
+ * other direction is the library's: the next feti_factorize/feti_assemble
+ * waits (cudaStreamWaitEvent) for the last apply enqueued on any stream
+ * before it rewrites the factor tiles or F~. */
 int feti_apply_device(feti_ctx* ctx, const double* d_p, double* d_q, void* stream);
 
 /* Coarse space for a GPU-resident PCPG (solver.py:117-123, 195-272): the
@@ -211,7 +228,10 @@ int feti_precond_apply_device(feti_ctx* ctx, const double* d_w, double* d_out, v
  * IPC handle (FETI_IPC_HANDLE_BYTES), the caller all-gathers the handles
  * (rank order) and passes them to feti_exchange_connect.  Every rank must
  * issue the same number of exchange applies; a rank that waits ~10 s for a
- * peer gives up and feti_exchange_status reports it. */
+ * peer gives up, writes NaN into q (never stale values) and sets a sticky
+ * error that feti_exchange_status reports (FETI_ERR_CUDA): the context's
+ * exchange is unusable after that.  Successive calls may use different
+ * streams: each call waits for the previous call's sum (slab reuse). */
 #define FETI_IPC_HANDLE_BYTES 64
 int feti_exchange_setup(feti_ctx* ctx, int rank, int world, char* handle_out);
 int feti_exchange_connect(feti_ctx* ctx, const char* handles);

@@ -135,6 +135,7 @@ struct feti_ctx {
   std::vector<SubHost> subs;
   int64_t n_mult = 0;
   bool finalized = false, assembled = false;
+  bool implicit = false;             // FETI_STRATEGY_IMPLICIT: no F~, sweeps per apply
   std::vector<void*> allocs;
   int64_t bytes_persistent = 0, bytes_temporary = 0;
   // device tables
@@ -199,33 +200,10 @@ struct feti_ctx {
   // DMMA tile work of the others.  Ranges are indexed [g * sp_maxTq + j].
   std::vector<std::pair<int, int>> sp_acc_rng, sp_panel_rng, sp_diag_rng;
   int sp_groups = 1, sp_maxTq = 0;
-  // persistent dependency-driven factorization (opt-in, FETI_SP_DAG=1)
-  bool sp_use_dag = false;
   cudaGraphExec_t sp_graph_exec = nullptr;   // captured column-launch sequence
   int sp_graph_launches = 0;
   bool sp_graph_used = false;
-  // pipelined steps (after the first factorization): the last
-  // feti_set_stiffness of a group launches that group's factorization (one
-  // captured graph per group: init, scatter, column sequence) while the host
-  // still hands over the other groups' values
-  bool sp_pipelined = false;
-  std::vector<std::pair<int, int>> sp_init_rng;          // per group: SpInit range
-  static constexpr int kMaxGroups = 8;                    // == kSpStreams (checked below)
-  cudaGraphExec_t sp_ggraph[kMaxGroups] = {};
-  std::atomic<int> sp_left[kMaxGroups];
-  std::atomic<bool> sp_launched[kMaxGroups];
-  std::atomic<bool> sp_started{false};
-  int sp_group_launches[kMaxGroups] = {};
-  std::vector<int> sp_big;                                // pivot-report reset values
-  int sp_dag_total = 0;
-  std::vector<int> sp_dag_init, sp_acc_init, sp_pan_init;
-  SpTask* d_dag_tasks = nullptr;
-  SpDiag* d_dag_diag = nullptr;
-  SpCol* d_dag_cols = nullptr;
-  int *d_dag_tcol = nullptr, *d_dag_dcol = nullptr, *d_dag_acc = nullptr, *d_dag_pan = nullptr;
-  int *d_dag_queue = nullptr, *d_dag_ht = nullptr;
   static constexpr int kSpStreams = 8;
-  static_assert(kSpStreams == kMaxGroups, "one pipelined graph per group stream");
   std::vector<std::pair<int, int>> sp_corr_rng, sp_sub_rng;   // per group: panels, subdomains
   cudaEvent_t sp_ev[3] = {};   // factorize start, factorize end, assemble end
   std::vector<int> sp_bad_init;
@@ -245,6 +223,11 @@ struct feti_ctx {
   int* d_x_error = nullptr;
   int64_t x_epoch = 0;
   bool x_ready = false;
+  cudaEvent_t x_sum_done = nullptr;  // end of the last exchange's sum (slab reuse order)
+  // end of the last apply enqueued on a caller stream: the next
+  // factorization/assembly (which rewrite the tiles and F~) waits for it
+  cudaEvent_t apply_done = nullptr;
+  bool apply_pending = false;
   std::vector<int> h_cptr;           // host copy of the contribution CSR pointer
   cudaStream_t sp_streams[kSpStreams] = {};
   cudaEvent_t sp_join[kSpStreams] = {};
@@ -348,24 +331,6 @@ int build_sparse_tasks(feti_ctx* c) {
     c->sp_flops += P.flops_exec;
     c->sp_flops_scalar += P.flops_scalar;
   }
-  // init work per group (the list is in subdomain order; groups are ranges)
-  c->sp_init_rng.assign(c->sp_groups, {0, 0});
-  for (int g = 0; g < c->sp_groups; ++g) {
-    const std::vector<int>& wv = c->waves[g];
-    if (wv.empty()) continue;
-    int b = -1, e = 0;
-    for (int i = 0; i < (int)init.size(); ++i)
-      if (init[i].sub >= wv.front() && init[i].sub <= wv.back()) {
-        if (b < 0) b = i;
-        e = i + 1;
-      }
-    c->sp_init_rng[g] = {std::max(b, 0), std::max(e - std::max(b, 0), 0)};
-  }
-  for (int g = 0; g < feti_ctx::kSpStreams; ++g) {
-    c->sp_left[g] = g < c->sp_groups ? (int)c->waves[g].size() : 0;
-    c->sp_launched[g] = false;
-  }
-  c->sp_big.assign(ns, 1 << 30);
   // correction work per group (contiguous subdomain ranges, as the waves)
   c->sp_corr_rng.assign(c->sp_groups, {0, 0});
   c->sp_sub_rng.assign(c->sp_groups, {0, 0});
@@ -386,16 +351,8 @@ int build_sparse_tasks(feti_ctx* c) {
   c->sp_acc_rng.assign((size_t)G * maxTq, {0, 0});
   c->sp_panel_rng.assign((size_t)G * maxTq, {0, 0});
   c->sp_diag_rng.assign((size_t)G * maxTq, {0, 0});
-  // equal priorities by default.  FETI_SP_STAGGER=1 ranks the groups (group 0
-  // first) so early groups' assembly overlaps later factorization: the tail
-  // shrinks (c3 15 -> 6 ms) but the factorization loses more concurrency
-  // than that (61 -> 78 ms), so it is off
-  int prio_lo = 0, prio_hi = 0;
-  CUDA_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  const bool stagger = getenv("FETI_SP_STAGGER") != nullptr;
   for (int g = 0; g < G; ++g) {
-    const int prio = stagger ? std::min(prio_lo, prio_hi + g) : prio_lo;   // numerically lower = higher priority
-    CUDA_TRY(cudaStreamCreateWithPriority(&c->sp_streams[g], cudaStreamNonBlocking, prio));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->sp_streams[g], cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&c->sp_join[g], cudaEventDisableTiming));
   }
   for (auto& e : c->sp_ev) CUDA_TRY(cudaEventCreate(&e));
@@ -450,91 +407,6 @@ int build_sparse_tasks(feti_ctx* c) {
     }
     c->sp_panel_rng[gj] = {b, (int)tasks.size() - b};
   }
-  // ---- persistent-kernel (dependency-driven) lists: per (subdomain, column)
-  // contiguous accumulation and panel tasks, the column records, and the
-  // entries ready at the start (the first column of every subdomain)
-  {
-    std::vector<SpTask> td;
-    std::vector<SpDiag> dd;
-    std::vector<SpCol> cols;
-    std::vector<int> tcol, dcol;
-    std::vector<int> init_q;
-    for (int si = 0; si < ns; ++si) {
-      const SubHost& s = c->subs[si];
-      const SpPlan& P = s.sp;
-      const int c0 = (int)cols.size();
-      for (int j = 0; j < P.Tq; ++j) {
-        const int cid = (int)cols.size();
-        SpCol col{};
-        col.acc0 = (int)td.size();
-        for (const auto& t : P.acc[j]) {
-          td.push_back(SpTask{s.d_pool + (size_t)t.first * TILE, (int64_t)pairs.size(), (int)t.second.size(),
-                              qrow[si][t.first] ? 2 : 0});
-          tcol.push_back(cid);
-          for (const auto& pr : t.second)
-            pairs.push_back(SpPair{s.d_pool + (size_t)pr.first * TILE, s.d_pool + (size_t)pr.second * TILE});
-        }
-        std::stable_sort(td.begin() + col.acc0, td.end(), [](const SpTask& x, const SpTask& y) {
-          return x.npairs * ((x.flags & 2) ? 1 : 4) > y.npairs * ((y.flags & 2) ? 1 : 4);
-        });
-        col.nacc = (int)td.size() - col.acc0;
-        col.pan0 = (int)td.size();
-        if (j < P.T)
-          for (int slot : P.panel[j]) {
-            double* C = s.d_pool + (size_t)slot * TILE;
-            td.push_back(SpTask{C, (int64_t)pairs.size(), 1, qrow[si][slot] ? 3 : 1});
-            tcol.push_back(cid);
-            pairs.push_back(SpPair{C, c->d_dinv + (size_t)si * TILE});
-          }
-        col.npan = (int)td.size() - col.pan0;
-        col.diag = -1;
-        if (j < P.T) {
-          col.diag = (int)dd.size();
-          dd.push_back(SpDiag{s.d_pool + (size_t)P.tmap[(size_t)j * P.Tq + j] * TILE,
-                              c->d_dinv + (size_t)si * TILE, si, j * TB});
-          dcol.push_back(cid);
-        }
-        col.next = (j + 1 < P.Tq) ? cid + 1 : -1;
-        cols.push_back(col);
-      }
-      // start of the subdomain: its first column (the device's dag_start_column)
-      for (int cid = (P.Tq > 0 ? c0 : -1); cid >= 0;) {
-        const SpCol& col = cols[cid];
-        if (col.nacc > 0) {
-          for (int t = 0; t < col.nacc; ++t) init_q.push_back((SPQ_TASK << 30) | (col.acc0 + t));
-          break;
-        }
-        if (col.diag >= 0) {
-          init_q.push_back((SPQ_DIAG << 30) | col.diag);
-          break;
-        }
-        cid = col.next;
-      }
-    }
-    const int total = (int)(td.size() + dd.size());
-    c->sp_dag_total = total;
-    c->sp_dag_init = init_q;
-    c->sp_acc_init.resize(cols.size());
-    c->sp_pan_init.resize(cols.size());
-    for (size_t k = 0; k < cols.size(); ++k) {
-      c->sp_acc_init[k] = cols[k].nacc;
-      c->sp_pan_init[k] = cols[k].npan;
-    }
-    if ((rc = upload(c, &c->d_dag_tasks, td))) return rc;
-    if ((rc = upload(c, &c->d_dag_diag, dd))) return rc;
-    if ((rc = upload(c, &c->d_dag_cols, cols))) return rc;
-    if ((rc = upload(c, &c->d_dag_tcol, tcol))) return rc;
-    if ((rc = upload(c, &c->d_dag_dcol, dcol))) return rc;
-    if ((rc = dev_alloc(c, (void**)&c->d_dag_acc, std::max<size_t>(cols.size(), 1) * 4, false))) return rc;
-    if ((rc = dev_alloc(c, (void**)&c->d_dag_pan, std::max<size_t>(cols.size(), 1) * 4, false))) return rc;
-    if ((rc = dev_alloc(c, (void**)&c->d_dag_queue, (size_t)std::max(total, 1) * 4, false))) return rc;
-    if ((rc = dev_alloc(c, (void**)&c->d_dag_ht, 2 * sizeof(int), false))) return rc;
-    // the per-column launch sequence on 4 group streams measures faster than
-    // the persistent kernel (c3 62.6 vs 65.6 ms, c5 403 vs 425 ms): the
-    // persistent path is opt-in (FETI_SP_DAG=1); both give identical bits
-    const char* denv = getenv("FETI_SP_DAG");
-    c->sp_use_dag = denv && atoi(denv) == 1;
-  }
   if ((rc = upload(c, &c->d_sp_init, init))) return rc;
   if ((rc = upload(c, &c->d_sp_tasks, tasks))) return rc;
   if ((rc = upload(c, &c->d_sp_pairs, pairs))) return rc;
@@ -550,70 +422,9 @@ int build_sparse_tasks(feti_ctx* c) {
   return FETI_OK;
 }
 
-// One group's factorization on its stream: reset its pivot reports, then the
-// group's captured graph (pool init, K_s scatter, column sequence).
-int launch_group(feti_ctx* c, int g) {
-  cudaStream_t gs = c->sp_streams[g];
-  const auto sr = c->sp_sub_rng[g];
-  const auto ir = c->sp_init_rng[g];
-  if (sr.second > 0)
-    CUDA_TRY(cudaMemcpyAsync(c->d_bad + sr.first, c->sp_big.data() + sr.first, (size_t)sr.second * sizeof(int),
-                             cudaMemcpyHostToDevice, gs));
-  bool first = false;
-  if (c->sp_started.compare_exchange_strong(first, true)) CUDA_TRY(cudaEventRecord(c->sp_ev[0], gs));
-  if (!c->sp_ggraph[g]) {
-    CUDA_TRY(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
-    launch_sp_init(c->d_sp_init + ir.first, ir.second, c->d_spsub, gs);
-    launch_sp_scatter(c->d_spsub, sr.first, sr.second, c->sp_max_n, gs);
-    int nl = 2;
-    for (int j = 0; j < c->sp_maxTq; ++j) {
-      const size_t gj = (size_t)g * c->sp_maxTq + j;
-      const auto a = c->sp_acc_rng[gj], d = c->sp_diag_rng[gj], p = c->sp_panel_rng[gj];
-      launch_sp_gemm(c->d_sp_tasks + a.first, a.second, c->d_sp_pairs, gs);
-      launch_sp_potrf(c->d_sp_diag + d.first, d.second, c->d_bad, gs);
-      launch_sp_gemm(c->d_sp_tasks + p.first, p.second, c->d_sp_pairs, gs);
-      nl += (a.second > 0) + (d.second > 0) + (p.second > 0);
-    }
-    cudaGraph_t graph = nullptr;
-    CUDA_TRY(cudaStreamEndCapture(gs, &graph));
-    CUDA_TRY(cudaGraphInstantiate(&c->sp_ggraph[g], graph, 0));
-    CUDA_TRY(cudaGraphDestroy(graph));
-    c->sp_group_launches[g] = nl;
-  }
-  CUDA_TRY(cudaGraphLaunch(c->sp_ggraph[g], gs));
-  c->sp_launched[g] = true;
-  return FETI_OK;
-}
-
 int factorize_sparse(feti_ctx* c) {
   cudaStream_t st = c->stream;
   const int ns = (int)c->subs.size();
-  if (c->sp_pipelined) {
-    // later steps: groups whose stiffness hand-over completed are already
-    // running; launch the rest, then join on the context stream
-    int rc;
-    int launches = 0;
-    for (int g = 0; g < c->sp_groups; ++g) {
-      if (!c->sp_launched[g] && (rc = launch_group(c, g))) return rc;
-      launches += c->sp_group_launches[g];
-      CUDA_TRY(cudaEventRecord(c->sp_join[g], c->sp_streams[g]));
-      CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
-    }
-    CUDA_TRY(cudaEventRecord(c->sp_ev[1], st));
-    for (int g = 0; g < c->sp_groups; ++g) {
-      c->sp_left[g] = (int)c->waves[g].size();
-      c->sp_launched[g] = false;
-    }
-    c->sp_started = false;
-    c->stats.flops_factor_exec = c->sp_flops;
-    c->stats.flops_factor_alg = c->sp_flops_scalar;
-    c->stats.launches_factorize = launches;
-    c->sp_graph_used = false;   // the graphs ran on the group streams
-    for (auto& s : c->subs) s.factor_set = true;
-    c->tiles_fresh = true;
-    c->sp_pending_check = true;
-    return FETI_OK;
-  }
   std::vector<SpSub> ss(ns);
   for (int si = 0; si < ns; ++si) {
     SubHost& s = c->subs[si];
@@ -633,25 +444,6 @@ int factorize_sparse(feti_ctx* c) {
   CUDA_TRY(cudaGetLastError());
   FETI_DEBUG_SYNC(st);
   int launches = 2;
-  if (c->sp_use_dag) {
-    // one persistent launch: reset the dependency counters and the queue
-    CUDA_TRY(cudaMemcpyAsync(c->d_dag_acc, c->sp_acc_init.data(), c->sp_acc_init.size() * 4,
-                             cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(c->d_dag_pan, c->sp_pan_init.data(), c->sp_pan_init.size() * 4,
-                             cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemsetAsync(c->d_dag_queue, 0xff, (size_t)std::max(c->sp_dag_total, 1) * 4, st));
-    CUDA_TRY(cudaMemcpyAsync(c->d_dag_queue, c->sp_dag_init.data(), c->sp_dag_init.size() * 4,
-                             cudaMemcpyHostToDevice, st));
-    const int ht[2] = {0, (int)c->sp_dag_init.size()};
-    CUDA_TRY(cudaMemcpyAsync(c->d_dag_ht, ht, sizeof(ht), cudaMemcpyHostToDevice, st));
-    SpDag g{c->d_dag_tasks, c->d_sp_pairs, c->d_dag_diag, c->d_dag_cols, c->d_dag_tcol, c->d_dag_dcol,
-            c->d_dag_acc, c->d_dag_pan, c->d_dag_queue, c->d_dag_ht, c->d_dag_ht + 1, c->d_bad,
-            c->sp_dag_total};
-    launch_sp_dag(g, c->num_sms, st);
-    launches += 1;
-    CUDA_TRY(cudaGetLastError());
-    FETI_DEBUG_SYNC(st);
-  } else {
   // the groups' column sequences are independent: issue them round-robin on
   // their own streams so the GPU interleaves one group's diagonal blocks with
   // another's tile GEMMs.  The ~900 launches are captured once into a CUDA
@@ -696,24 +488,33 @@ int factorize_sparse(feti_ctx* c) {
     }
   }
   c->sp_graph_used = use_graph;
-  }
   // the factorization end on the context stream (timing only); no host sync:
   // feti_assemble runs each group's assembly right behind its factorization
   // on the group's stream and checks the pivots once everything finished
   CUDA_TRY(cudaEventRecord(c->sp_ev[1], st));
-  // FETI_SP_PIPELINE=1: from the next step on, feti_set_stiffness launches
-  // each group as soon as its values are on the device.  Opt-in: it hides the
-  // host hand-over when that is long (c5 e2e 0.34 -> 0.29 s) but the
-  // staggered group starts cost concurrency (c3 device 60.5 -> 66 ms, e2e
-  // unchanged at 70 ms)
-  const char* penv = getenv("FETI_SP_PIPELINE");
-  c->sp_pipelined = !g_debug_sync && !c->sp_use_dag && penv && atoi(penv) == 1;
   c->stats.flops_factor_exec = c->sp_flops;
-    c->stats.flops_factor_alg = c->sp_flops_scalar;
+  c->stats.flops_factor_alg = c->sp_flops_scalar;
   c->stats.launches_factorize = launches;
   for (auto& s : c->subs) s.factor_set = true;
   c->tiles_fresh = true;
   c->sp_pending_check = true;
+  return FETI_OK;
+}
+
+// An apply reads F~, the shared partial buffer and (implicit) the tiles on a
+// caller stream; mark its end so the next factorize/assemble, which rewrite
+// them on the library's streams, wait for it (write-after-read).
+int mark_apply(feti_ctx* c, cudaStream_t st) {
+  CUDA_TRY(cudaEventRecord(c->apply_done, st));
+  c->apply_pending = true;
+  return FETI_OK;
+}
+
+int wait_applies(feti_ctx* c) {
+  if (c->apply_pending) {
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->apply_done, 0));
+    c->apply_pending = false;
+  }
   return FETI_OK;
 }
 
@@ -744,6 +545,8 @@ int feti_create(int device, feti_ctx** out) {
     CUDA_TRY(cudaEventCreateWithFlags(&c->wave_join[i], cudaEventDisableTiming));
   }
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->apply_done, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->x_sum_done, cudaEventDisableTiming));
   CUDA_TRY(configure_kernels());
   *out = c;
   return FETI_OK;
@@ -768,13 +571,13 @@ int feti_destroy(feti_ctx* c) {
   for (auto& e : c->sp_ev)
     if (e) cudaEventDestroy(e);
   if (c->sp_graph_exec) cudaGraphExecDestroy(c->sp_graph_exec);
-  for (auto& ge : c->sp_ggraph)
-    if (ge) cudaGraphExecDestroy(ge);
   for (int g = 0; g < feti_ctx::kSpStreams; ++g) {
     if (c->sp_join[g]) cudaEventDestroy(c->sp_join[g]);
     if (c->sp_streams[g]) cudaStreamDestroy(c->sp_streams[g]);
   }
   for (double* pp : c->x_open) cudaIpcCloseMemHandle(pp);
+  if (c->apply_done) cudaEventDestroy(c->apply_done);
+  if (c->x_sum_done) cudaEventDestroy(c->x_sum_done);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   delete c;
@@ -845,10 +648,21 @@ int feti_add_subdomain(feti_ctx* c, int64_t n, int64_t m, const int64_t* first_r
   return FETI_OK;
 }
 
+int feti_set_strategy(feti_ctx* c, int strategy) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (c->finalized) return fail(FETI_ERR_LIFECYCLE, "the strategy must be chosen before finalize");
+  if (strategy != FETI_STRATEGY_EXPLICIT && strategy != FETI_STRATEGY_IMPLICIT)
+    return fail(FETI_ERR_ARG, "unknown strategy %d", strategy);
+  c->implicit = strategy == FETI_STRATEGY_IMPLICIT;
+  return FETI_OK;
+}
+
 int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
   if (c->finalized) return fail(FETI_ERR_LIFECYCLE, "prepare was already called on this operator");
   if (n_multipliers < 0 || n_multipliers >= (int64_t)1 << 31) return fail(FETI_ERR_ARG, "bad n_multipliers");
+  if (c->implicit && c->sparse_factor)
+    return fail(FETI_ERR_ARG, "the implicit strategy is not available with the sparse-factor route");
   CUDA_TRY(cudaSetDevice(c->device));
   c->n_mult = n_multipliers;
   for (auto& s : c->subs)
@@ -868,8 +682,10 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   for (auto& s : c->subs) {
     const int64_t tb = c->device_factor ? 0 : s.smin;
     if (!c->sparse_factor) need += (size_t)(s.T - tb) * (s.T - tb + 1) / 2 * TILE * 8;   // tiles
-    need += (size_t)s.P * (s.T - s.smin) * TILE * 8;   // X panels
-    need += (size_t)s.f_tiles() * ATILE * 8;          // F~
+    if (!c->implicit) {
+      need += (size_t)s.P * (s.T - s.smin) * TILE * 8;   // X panels
+      need += (size_t)s.f_tiles() * ATILE * 8;          // F~
+    }
     max_M = std::max(max_M, s.T32 * AT);
   }
   size_t fr = 0, tot = 0;
@@ -903,10 +719,13 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     } else if ((rc = dev_alloc(c, (void**)&s.d_tiles, (size_t)std::max<int64_t>(s.l_tiles(), 1) * TILE * 8, false))) {
       return rc;
     }
-    if ((rc = dev_alloc(c, (void**)&s.d_X, (size_t)std::max(s.P, 1) * std::max(s.T - s.smin, 1) * TILE * 8, false)))
-      return rc;
-    if ((rc = dev_alloc(c, (void**)&s.d_F, (size_t)std::max<int64_t>(s.f_tiles(), 1) * ATILE * 8, true)))
-      return rc;
+    if (!c->implicit) {
+      if ((rc = dev_alloc(c, (void**)&s.d_X, (size_t)std::max(s.P, 1) * std::max(s.T - s.smin, 1) * TILE * 8,
+                          false)))
+        return rc;
+      if ((rc = dev_alloc(c, (void**)&s.d_F, (size_t)std::max<int64_t>(s.f_tiles(), 1) * ATILE * 8, true)))
+        return rc;
+    }
     if ((rc = upload(c, &s.d_r, s.r_sorted))) return rc;
     if ((rc = upload(c, &s.d_s, s.s_sorted))) return rc;
     if ((rc = upload(c, &s.d_g, s.gids_sorted))) return rc;
@@ -937,13 +756,13 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     for (int k = s.T - 1; k > k0; --k) ws.push_back(make_int4(si, k, 0, 0));
     const double tt = s.T - k0;
     scale_exec += tt * (tt - 1) / 2 * 2.0 * (2.0 * 64 * 32 * 32 * (1 + 2 + 3 + 4));
-    for (int p = 0; p < s.P; ++p) {
+    for (int p = 0; p < s.P && !c->implicit; ++p) {
       wc.push_back(make_int4(si, p, 0, 0));
       const double s0 = s.panel_minrow[p] / TB;
       trsm_exec += tb3 * (s.T - 1 - s0) * (s.T - s0) / 2.0;
     }
     const int rend = (int)((s.n + KS - 1) / KS * KS);
-    for (int I = 0; I < s.P; ++I)
+    for (int I = 0; I < s.P && !c->implicit; ++I)
       for (int J = I; J < s.P; ++J) {
         wy.push_back(make_int4(si, I, J, 0));
         const int rs = std::max(s.panel_minrow[I], s.panel_minrow[J]) & ~(KS - 1);
@@ -1081,7 +900,7 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   if (const char* wenv = getenv("FETI_APPLY_WARPS")) c->apply_nw = std::max(1, std::min(8, atoi(wenv)));   // tests
   while (c->apply_nw > 1 && (size_t)(c->apply_nw + 1) * max_M * 8 > 227 * 1024) --c->apply_nw;
   c->apply_smem = (size_t)(c->apply_nw + 1) * max_M * 8;
-  if (c->apply_smem > 227 * 1024)
+  if (c->apply_smem > 227 * 1024 && !c->implicit)
     return fail(FETI_ERR_CAPACITY, "subdomain with %d multipliers exceeds the apply kernel's shared memory", max_M);
 
   if ((rc = upload(c, &c->d_w_unpack, wu))) return rc;
@@ -1233,6 +1052,7 @@ int feti_assemble(feti_ctx* c) {
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   int launches = 0, rc;
+  if ((rc = wait_applies(c))) return rc;
   bool pending = false;
   double fb = 0;
   for (auto& s : c->subs)
@@ -1252,8 +1072,8 @@ int feti_assemble(feti_ctx* c) {
     const auto& r = c->wv_range;
     for (int g = 0; g < G; ++g) {
       cudaStream_t gs = c->sp_streams[g];
-      // the persistent kernel and the captured graph ran on the context stream
-      if (c->sp_use_dag || c->sp_graph_used) CUDA_TRY(cudaStreamWaitEvent(gs, c->ev[2], 0));
+      // the captured graph ran on the context stream
+      if (c->sp_graph_used) CUDA_TRY(cudaStreamWaitEvent(gs, c->ev[2], 0));
       std::vector<int> none;
       if ((rc = launch_assembly(c, gs, c->d_wv[0] + r[0][g].first, r[0][g].second, c->d_wv[1] + r[1][g].first,
                                 r[1][g].second, c->d_wv[2] + r[2][g].first, r[2][g].second,
@@ -1364,6 +1184,7 @@ int feti_assemble(feti_ctx* c) {
 int feti_local_operator(feti_ctx* c, int64_t slot, double* out) {
   if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
   if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "local operator before preprocess");
+  if (c->implicit) return fail(FETI_ERR_LIFECYCLE, "the implicit strategy keeps no local operator");
   if (slot < 0 || slot >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot out of range");
   const SubHost& s = c->subs[slot];
   CUDA_TRY(cudaSetDevice(c->device));
@@ -1386,6 +1207,8 @@ int feti_local_operator(feti_ctx* c, int64_t slot, double* out) {
   return FETI_OK;
 }
 
+static int implicit_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st, bool time_it);
+
 // The descriptor table was uploaded by feti_assemble on the context stream;
 // apply reads only finalize-time fields of it (F~ tiles, index maps).
 static int apply_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st, bool time_it) {
@@ -1395,7 +1218,7 @@ static int apply_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream
   launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_part_off, c->d_part, d_q, st);
   CUDA_TRY(cudaGetLastError());
   if (time_it) CUDA_TRY(cudaEventRecord(c->ev[1], st));
-  return FETI_OK;
+  return mark_apply(c, st);
 }
 
 int feti_apply(feti_ctx* c, const double* p, double* q) {
@@ -1405,7 +1228,7 @@ int feti_apply(feti_ctx* c, const double* p, double* q) {
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   CUDA_TRY(cudaMemcpyAsync(c->d_p, p, (size_t)c->n_mult * 8, cudaMemcpyHostToDevice, st));
-  int rc = apply_enqueue(c, c->d_p, c->d_q, st, true);
+  int rc = c->implicit ? implicit_enqueue(c, c->d_p, c->d_q, st, true) : apply_enqueue(c, c->d_p, c->d_q, st, true);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(q, c->d_q, (size_t)c->n_mult * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -1468,7 +1291,7 @@ int feti_precond_apply_device(feti_ctx* c, const double* d_w, double* d_out, voi
                c->d_part_off, c->d_part, d_w, st);
   launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_part_off, c->d_part, d_out, st);
   CUDA_TRY(cudaGetLastError());
-  return FETI_OK;
+  return mark_apply(c, st);
 }
 
 int feti_precond_apply(feti_ctx* c, const double* w, double* out) {
@@ -1544,16 +1367,23 @@ int feti_apply_exchange_device(feti_ctx* c, const double* d_p, double* d_q, void
   if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
   if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "apply before preprocess for the current values");
   if (!c->x_ready) return fail(FETI_ERR_LIFECYCLE, "exchange not connected");
+  if (c->implicit) return fail(FETI_ERR_ARG, "the fused exchange serves the explicit strategy");
   if (!d_p || !d_q) return fail(FETI_ERR_ARG, "NULL vector");
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
+  // slab parity (epoch % 2) reuse is safe only if this rank's previous sum
+  // finished first (feti_exchange.cu header): order it explicitly, whatever
+  // stream the caller used last time
+  CUDA_TRY(cudaStreamWaitEvent(st, c->x_sum_done, 0));
   launch_apply(c->apply_nw, c->apply_smem, c->d_subdev, c->d_w_apply, c->d_apply_seg_ptr, c->n_apply,
                c->d_part_off, c->d_part, d_p, st);
   XchgArgs a{c->d_x_peers, c->d_x_touched, c->d_cptr, c->d_cent, c->d_part_off, c->d_part, c->d_x_done,
-             c->d_x_error, ++c->x_epoch, c->x_n_touched, (int)c->n_mult, c->x_rank, c->x_world};
+             c->d_x_error, c->x_epoch + 1, c->x_n_touched, (int)c->n_mult, c->x_rank, c->x_world};
   launch_exchange(a, d_q, st);
   CUDA_TRY(cudaGetLastError());
-  return FETI_OK;
+  ++c->x_epoch;   // only once the launches were accepted: ranks stay in step
+  CUDA_TRY(cudaEventRecord(c->x_sum_done, st));
+  return mark_apply(c, st);
 }
 
 int feti_exchange_status(feti_ctx* c) {
@@ -1572,6 +1402,7 @@ int feti_apply_device(feti_ctx* c, const double* d_p, double* d_q, void* stream)
   if (!d_p || !d_q) return fail(FETI_ERR_ARG, "NULL vector");
   CUDA_TRY(cudaSetDevice(c->device));
   // the handle is used verbatim: NULL is the legacy default stream, as in CUDA
+  if (c->implicit) return implicit_enqueue(c, d_p, d_q, (cudaStream_t)stream, false);
   return apply_enqueue(c, d_p, d_q, (cudaStream_t)stream, false);
 }
 
@@ -1685,7 +1516,6 @@ int feti_set_stiffness(feti_ctx* c, int64_t slot, int64_t n, const int64_t* indp
   CUDA_TRY(cudaMemcpy(s.d_kdata, data, (size_t)nnz * 8, cudaMemcpyHostToDevice));
   if (r > 0) CUDA_TRY(cudaMemcpy(s.d_Q, Q, (size_t)(n * r) * 8, cudaMemcpyHostToDevice));
   s.rho = rho;
-  const bool trigger = c->sparse_factor && c->sp_pipelined;
   if (c->sparse_factor && r > 0) {
     // U1 = B~ Q in sorted column order: row a = sign_a Q[dof_a]
     const size_t rows = (size_t)s.P * TB;
@@ -1700,16 +1530,6 @@ int feti_set_stiffness(feti_ctx* c, int64_t slot, int64_t n, const int64_t* indp
     }
     CUDA_TRY(cudaMemcpy(s.d_U1, u1.data(), rows * r * 8, cudaMemcpyHostToDevice));
   }
-  if (trigger) {
-    // this slot's descriptor (rho changes per step), then launch its group if
-    // it was the group's last hand-over of the step
-    const SpSub sd{s.d_pool, s.d_tmap, s.d_perm, s.d_iperm, s.d_kptr, s.d_kind, s.d_kdata, s.d_Q, s.d_fix,
-                   s.d_U1, s.d_U2W, s.rho, s.sp.T, s.sp.Tq, (int)s.sp_n, s.sp_r, s.sp_r, (int)s.n};
-    CUDA_TRY(cudaMemcpy(c->d_spsub + slot, &sd, sizeof(SpSub), cudaMemcpyHostToDevice));
-    int g = 0;
-    while (g + 1 < c->sp_groups && slot >= c->sp_sub_rng[g + 1].first) ++g;
-    if (c->sp_left[g].fetch_sub(1) == 1 && !c->sp_launched[g]) return launch_group(c, g);
-  }
   return FETI_OK;
 }
 
@@ -1720,6 +1540,7 @@ int feti_factorize(feti_ctx* c) {
   for (size_t i = 0; i < c->subs.size(); ++i)
     if (!c->subs[i].stiff_set) return fail(FETI_ERR_LIFECYCLE, "subdomain slot %zu has no stiffness", i);
   CUDA_TRY(cudaSetDevice(c->device));
+  if (int rc0 = wait_applies(c)) return rc0;
   if (c->sparse_factor) return factorize_sparse(c);
   cudaStream_t st = c->stream;
   const int ns = (int)c->subs.size();
@@ -1786,15 +1607,17 @@ int feti_solve_many(feti_ctx* c, int64_t nslots, const int64_t* slots, const dou
   return FETI_OK;
 }
 
-static int implicit_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st) {
+static int implicit_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st, bool time_it) {
   if (c->sparse_factor)
     return fail(FETI_ERR_ARG, "implicit apply is not available with the sparse-factor route");
   if (c->impl_max_blocks < 0)
     return fail(FETI_ERR_CAPACITY, "implicit apply: subdomain too large for the single-CTA sweep");
+  if (time_it) CUDA_TRY(cudaEventRecord(c->ev[0], st));
   launch_implicit_apply(c->d_subdev, (int)c->subs.size(), c->impl_max_blocks, c->d_impl_off, d_p, c->d_impl_part,
                         (int)c->n_mult, c->d_cptr, c->d_cent, d_q, st);
   CUDA_TRY(cudaGetLastError());
-  return FETI_OK;
+  if (time_it) CUDA_TRY(cudaEventRecord(c->ev[1], st));
+  return mark_apply(c, st);
 }
 
 int feti_apply_implicit(feti_ctx* c, const double* p, double* q) {
@@ -1804,10 +1627,8 @@ int feti_apply_implicit(feti_ctx* c, const double* p, double* q) {
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   CUDA_TRY(cudaMemcpyAsync(c->d_p, p, (size_t)c->n_mult * 8, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaEventRecord(c->ev[0], st));
-  int rc = implicit_enqueue(c, c->d_p, c->d_q, st);
+  int rc = implicit_enqueue(c, c->d_p, c->d_q, st, true);
   if (rc) return rc;
-  CUDA_TRY(cudaEventRecord(c->ev[1], st));
   CUDA_TRY(cudaMemcpyAsync(q, c->d_q, (size_t)c->n_mult * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   float ms = 0;
@@ -1821,7 +1642,7 @@ int feti_apply_implicit_device(feti_ctx* c, const double* d_p, double* d_q, void
   if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "apply before preprocess for the current values");
   if (!d_p || !d_q) return fail(FETI_ERR_ARG, "NULL vector");
   CUDA_TRY(cudaSetDevice(c->device));
-  return implicit_enqueue(c, d_p, d_q, (cudaStream_t)stream);
+  return implicit_enqueue(c, d_p, d_q, (cudaStream_t)stream, false);
 }
 
 int feti_coarse_setup(feti_ctx* c, const int64_t* kdim, const double* G, const double* coarse_inv, int64_t nk) {

@@ -80,7 +80,10 @@ __device__ __forceinline__ void invert_lower_128(const double* __restrict__ sL, 
 // Shared memory: one 128 x 132 row-major array (stride = 4 mod 16 doubles:
 // the DMMA fragment loads, rows g8 x columns t4, are bank-conflict free; the
 // odd stride 129 made them 4-way and measured 70.0 vs 61.4 us per tile,
-// scripts/gpu_potrf.sh, profiles/r01d_potrf_stride.md) holding L in its lower triangle and
+// scripts/gpu_potrf.sh, profiles/r01d_potrf_stride.md.  The row-per-lane
+// walks -- tile load scatter, diagonal-block row load/store, panel
+// substitution, inverse store, writeback -- stay up to 4-way conflicted with
+// this stride: 32 rows map to 4 bank groups) holding L in its lower triangle and
 // Y = inv(L) transposed in its strict upper triangle (Y(i, j), i > j, at
 // [j][i]), the diagonal of Y apart, plus a 3 x 32 x 32 scratch.  Blocked
 // over four 32-wide block columns: one warp factors and inverts the 32x32

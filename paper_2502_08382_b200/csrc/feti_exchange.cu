@@ -16,8 +16,18 @@
 //   own sum of epoch e-1 returned, which needed every peer's flag e-1, which
 //   each peer publishes after its sum of epoch e-2 -- the last reader of
 //   that parity.
-// * The wait is bounded: after ~10 s without progress the kernel records an
-//   error and returns instead of hanging the device.
+// * The wait is bounded: after ~10 s without progress the kernel records a
+//   sticky error (feti_exchange_status) and writes NaN to its part of q, so
+//   a lost peer can never leave stale or half-updated values that look valid.
+// * Memory ordering across GPUs: every thread's remote stores of the reduce
+//   kernel are ordered before its CTA's __syncthreads; thread 0 then issues
+//   __threadfence_system (a fence.sc.sys: cumulative, so it orders the CTA's
+//   stores observed through the barrier before everything thread 0 does
+//   next) and bumps the CTA counter; the last CTA fences again and publishes
+//   the epoch with st.release.sys.  A reader's ld.acquire.sys of that flag
+//   therefore synchronises with all CTAs' slab stores (release sequence via
+//   the device-scope atomic counter + system fences), so the summing kernel
+//   never reads a slab entry older than the epoch it waited for.
 #include <cstdint>
 
 #include "feti_common.cuh"
@@ -85,9 +95,12 @@ __global__ void __launch_bounds__(256) sum_exchange_kernel(XchgArgs a, double* _
     ok = good;
   }
   __syncthreads();
-  if (!ok) return;
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= a.n_mult) return;
+  if (!ok) {
+    q[g] = __longlong_as_double(0x7ff8000000000000LL);   // NaN: never a stale value
+    return;
+  }
   const double* slab = a.peers[a.rank] + (size_t)(a.epoch & 1) * a.world * a.n_mult;
   double acc = 0.0;
   for (int r = 0; r < a.world; ++r) acc += slab[(size_t)r * a.n_mult + g];

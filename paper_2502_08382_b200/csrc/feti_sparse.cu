@@ -111,74 +111,13 @@ __global__ void __launch_bounds__(256, 1) sp_potrf_kernel(const SpDiag* __restri
   potrf_invert_128(w.C, w.D, bad + w.sub, w.rowbase, psm);
 }
 
-// ---------------------------------------------------------------------------
-// persistent dependency-driven factorization
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-
-// (thread 0 only) make entries [first, first + n) of `kind` ready
-__device__ void dag_push(const SpDag& g, int kind, int first, int n) {
-  if (n <= 0) return;
-  const int base = atomicAdd(g.tail, n);
-  for (int t = 0; t < n; ++t) st_release(g.queue + base + t, (kind << 30) | (first + t));
-}
-
-__device__ void dag_start_column(const SpDag& g, int c);
-
-__device__ void dag_acc_done(const SpDag& g, int c) {
-  const SpCol col = g.cols[c];
-  if (col.diag >= 0) {
-    dag_push(g, SPQ_DIAG, col.diag, 1);
-  } else if (col.next >= 0) {   // (P Q)^T column: nothing to factor
-    dag_start_column(g, col.next);
-  }
-}
-
-__device__ void dag_start_column(const SpDag& g, int c) {
-  const SpCol col = g.cols[c];
-  if (col.nacc > 0)
-    dag_push(g, SPQ_TASK, col.acc0, col.nacc);
-  else
-    dag_acc_done(g, c);
-}
-
-__device__ void dag_column_done(const SpDag& g, int c) {
-  const int nx = g.cols[c].next;
-  if (nx >= 0) dag_start_column(g, nx);
-}
-
-__device__ void dag_complete(const SpDag& g, int kind, int idx) {
-  if (kind == SPQ_DIAG) {
-    const int c = g.diag_col[idx];
-    const SpCol col = g.cols[c];
-    if (col.npan > 0)
-      dag_push(g, SPQ_TASK, col.pan0, col.npan);
-    else
-      dag_column_done(g, c);
-    return;
-  }
-  const int c = g.task_col[idx];
-  if (g.tasks[idx].flags & 1) {
-    if (atomicSub(g.pan_left + c, 1) == 1) dag_column_done(g, c);
-  } else {
-    if (atomicSub(g.acc_left + c, 1) == 1) dag_acc_done(g, c);
-  }
-}
-
 // 8 warps, no dedicated producer warp: lane 0 of warp 0 issues the bulk
 // copies PREF slices ahead (after every warp released the stage), so the CTA
 // has 255 registers per thread for both the DMMA tiles and potrf_invert_128.
-constexpr int DAG_THREADS = 256;
-constexpr int DAG_PREF = SG_STAGES - 1;
+constexpr int SG_THREADS = 256;
+constexpr int SG_PREF = SG_STAGES - 1;
 
-__device__ __forceinline__ void dag_issue(const SpPair* __restrict__ pairs, int64_t pair0, int sl, uint32_t pos,
+__device__ __forceinline__ void sg_issue(const SpPair* __restrict__ pairs, int64_t pair0, int sl, uint32_t pos,
                                           double* sA, double* sB, uint64_t* full, uint64_t* empty) {
   const int st = (int)(pos % SG_STAGES);
   const uint32_t ph = (pos / SG_STAGES) & 1;
@@ -191,7 +130,7 @@ __device__ __forceinline__ void dag_issue(const SpPair* __restrict__ pairs, int6
 }
 
 template <int MI>
-__device__ __forceinline__ void dag_gemm(const SpPair* __restrict__ pairs, const SpTask& tk, double* sA, double* sB,
+__device__ __forceinline__ void sg_gemm(const SpPair* __restrict__ pairs, const SpTask& tk, double* sA, double* sB,
                                          uint64_t* full, uint64_t* empty, uint32_t pos0, int warp, int lane) {
   const int nsl = tk.npairs * (TB / KS);
   const int wm = warp >> 2, wn = warp & 3;
@@ -202,7 +141,7 @@ __device__ __forceinline__ void dag_gemm(const SpPair* __restrict__ pairs, const
     fence_proxy_async_global();
     fence_proxy_async_shared();
     if (!(tk.flags & 1)) bulk_prefetch_l2(tk.C, TILE * 8);
-    for (int sl = 0; sl < DAG_PREF && sl < nsl; ++sl) dag_issue(pairs, tk.pair0, sl, pos0 + sl, sA, sB, full, empty);
+    for (int sl = 0; sl < SG_PREF && sl < nsl; ++sl) sg_issue(pairs, tk.pair0, sl, pos0 + sl, sA, sB, full, empty);
   }
   double acc[MI][4][2];
 #pragma unroll
@@ -211,8 +150,8 @@ __device__ __forceinline__ void dag_gemm(const SpPair* __restrict__ pairs, const
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   for (int sl = 0; sl < nsl; ++sl) {
     const uint32_t pos = pos0 + sl;
-    if (issuer && sl + DAG_PREF < nsl)
-      dag_issue(pairs, tk.pair0, sl + DAG_PREF, pos + DAG_PREF, sA, sB, full, empty);
+    if (issuer && sl + SG_PREF < nsl)
+      sg_issue(pairs, tk.pair0, sl + SG_PREF, pos + SG_PREF, sA, sB, full, empty);
     const int st = (int)(pos % SG_STAGES);
     mbar_wait(&full[st], (pos / SG_STAGES) & 1);
     if (active) sg_mma_slice<MI>(sA + st * SLICE, sB + st * SLICE, acc, wm, wn, gq, t);
@@ -243,7 +182,7 @@ __device__ __forceinline__ void dag_gemm(const SpPair* __restrict__ pairs, const
 
 // one task per CTA, 8 warps (255 registers, no spills): the column-launch
 // scheduler's tile kernel
-__global__ void __launch_bounds__(DAG_THREADS, 1) sp_gemm8_kernel(const SpTask* __restrict__ tasks,
+__global__ void __launch_bounds__(SG_THREADS, 1) sp_gemm8_kernel(const SpTask* __restrict__ tasks,
                                                                   const SpPair* __restrict__ pairs) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sA = reinterpret_cast<double*>(smem_raw);
@@ -261,61 +200,9 @@ __global__ void __launch_bounds__(DAG_THREADS, 1) sp_gemm8_kernel(const SpTask* 
   __syncthreads();
   const SpTask tk = tasks[blockIdx.x];
   if (!(tk.flags & 2))
-    dag_gemm<8>(pairs, tk, sA, sB, full, empty, 0, warp, lane);
+    sg_gemm<8>(pairs, tk, sA, sB, full, empty, 0, warp, lane);
   else
-    dag_gemm<1>(pairs, tk, sA, sB, full, empty, 0, warp, lane);
-}
-
-__global__ void __launch_bounds__(DAG_THREADS, 1) sp_dag_kernel(const SpDag g) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* sA = reinterpret_cast<double*>(smem_raw);
-  double* sB = sA + SG_STAGES * SLICE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + SG_STAGES * SLICE);
-  uint64_t* empty = full + SG_STAGES;
-  __shared__ int s_entry;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < SG_STAGES; ++st) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], 8);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  uint32_t pos = 0;   // ring position (slices this CTA consumed so far)
-  for (;;) {
-    if (threadIdx.x == 0) {
-      const int slot = atomicAdd(g.head, 1);
-      int e = -2;
-      if (slot < g.total) {
-        while ((e = ld_acquire(g.queue + slot)) < 0) __nanosleep(32);
-      }
-      s_entry = e;
-    }
-    __syncthreads();
-    const int e = s_entry;
-    if (e == -2) break;
-    const int kind = e >> 30, idx = e & ((1 << 30) - 1);
-    if (kind == SPQ_TASK) {
-      const SpTask tk = g.tasks[idx];
-      if (!(tk.flags & 2))
-        dag_gemm<8>(g.pairs, tk, sA, sB, full, empty, pos, warp, lane);
-      else
-        dag_gemm<1>(g.pairs, tk, sA, sB, full, empty, pos, warp, lane);
-      pos += (uint32_t)(tk.npairs * (TB / KS));
-      fence_proxy_async_global();   // C is read by later bulk copies
-    } else {
-      const SpDiag d = g.diag[idx];
-      potrf_invert_128(d.C, d.D, g.bad + d.sub, d.rowbase, reinterpret_cast<double*>(smem_raw));
-      fence_proxy_async_shared();   // the ring reuses this shared memory via bulk copies
-      fence_proxy_async_global();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      dag_complete(g, kind, idx);
-    }
-  }
+    sg_gemm<1>(pairs, tk, sA, sB, full, empty, 0, warp, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -557,13 +444,9 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
 static size_t sg_smem() { return 2 * SG_STAGES * SLICE * sizeof(double) + 8 * 2 * SG_STAGES; }
 static size_t sp_potrf_smem() { return POTRF_SMEM_DOUBLES * sizeof(double); }
 
-static size_t dag_smem() { return sg_smem(); }
-
 cudaError_t configure_sparse() {
   cudaError_t e;
   static_assert(POTRF_SMEM_DOUBLES * 8 <= 2 * SG_STAGES * SLICE * 8, "potrf scratch must fit the GEMM ring");
-  if ((e = cudaFuncSetAttribute(sp_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dag_smem())))
-    return e;
   if ((e = cudaFuncSetAttribute(sp_gemm8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg_smem())))
     return e;
   return cudaFuncSetAttribute(sp_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp_potrf_smem());
@@ -578,11 +461,7 @@ void launch_sp_scatter(const SpSub* ss, int sub0, int nsub, int max_n, cudaStrea
 }
 
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st) {
-  if (ntasks > 0) sp_gemm8_kernel<<<ntasks, DAG_THREADS, sg_smem(), st>>>(tasks, pairs);
-}
-
-void launch_sp_dag(const SpDag& g, int nctas, cudaStream_t st) {
-  if (g.total > 0 && nctas > 0) sp_dag_kernel<<<nctas, DAG_THREADS, dag_smem(), st>>>(g);
+  if (ntasks > 0) sp_gemm8_kernel<<<ntasks, SG_THREADS, sg_smem(), st>>>(tasks, pairs);
 }
 
 void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st) {

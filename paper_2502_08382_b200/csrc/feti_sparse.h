@@ -80,34 +80,7 @@ struct SpPlan {
 void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* iperm, int64_t npos,
                  int r, int smin, SpPlan* out);
 
-// Persistent, dependency-driven factorization (sp_dag_kernel): one CTA per
-// SM pulls ready tasks from a device queue; completing a task releases its
-// dependents.  Per (subdomain, block column) record:
-struct SpCol {
-  int acc0, nacc;     // accumulation tasks [acc0, acc0 + nacc) in SpDag::tasks
-  int pan0, npan;     // panel tasks
-  int diag;           // index in SpDag::diag, -1 for the (P Q)^T column
-  int next;           // record of the next column of the subdomain, -1 at the end
-};
-struct SpDag {
-  const SpTask* tasks;
-  const SpPair* pairs;
-  const SpDiag* diag;
-  const SpCol* cols;
-  const int* task_col;    // task -> column record
-  const int* diag_col;    // diagonal task -> column record
-  int* acc_left;          // per column record: accumulations not yet done
-  int* pan_left;          // per column record: panels not yet done
-  int* queue;             // ready entries (kind << 30 | index), -1 = not yet written
-  int* head;              // next queue slot to take
-  int* tail;              // next queue slot to fill
-  int* bad;
-  int total;              // number of tasks (= entries ever pushed)
-};
-enum { SPQ_TASK = 0, SPQ_DIAG = 1 };
-
 cudaError_t configure_sparse();
-void launch_sp_dag(const SpDag& g, int nctas, cudaStream_t st);
 void launch_sp_init(const SpInit* w, int nw, const SpSub* ss, cudaStream_t st);
 void launch_sp_scatter(const SpSub* ss, int sub0, int nsub, int max_n, cudaStream_t st);
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st);

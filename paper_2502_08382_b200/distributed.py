@@ -84,6 +84,12 @@ class ClusterDualOperator:
         allreduce_sum_(q_dev, self.group)
         return q_dev
 
+    def check(self):
+        """Raise if the fused exchange ever timed out waiting for a peer (the
+        kernels then wrote NaN into q); a no-op for the NCCL exchange."""
+        if self.p2p:
+            self.local.exchange_status()
+
     def apply(self, p=None, out=None, src: int = 0):
         """Host-facing apply: p on rank ``src``'s host, q returned on every rank."""
         import torch
@@ -95,6 +101,7 @@ class ClusterDualOperator:
             dist.broadcast(self.p_dev, src=src, group=self.group)
         self.apply_device(self.p_dev, self.q_dev)
         host = self.q_dev.cpu().numpy()
+        self.check()
         if out is None:
             return host
         out[:] = host

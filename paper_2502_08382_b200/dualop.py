@@ -56,11 +56,34 @@ class SingularFactorError(ArithmeticError):
     """A triangular factor carries a zero diagonal entry (sparse.py:42-43)."""
 
 
+class SizeCapError(ValueError):
+    """schur_oracle on a subdomain above ``schur_cap`` DOFs (dualop.py:51-52, 533-534)."""
+
+
+class _Shape:
+    """Shape-only stand-in for K_reg on the device-factor routes (never densified)."""
+
+    def __init__(self, shape):
+        self.shape = tuple(int(v) for v in shape)
+
+
+def _problem_like(x) -> bool:
+    """A ``SubdomainProblem`` (solver.py:100-106) or anything carrying the
+    unregularized ``stiffness`` and its ``kernel`` basis."""
+    return hasattr(x, "stiffness") and hasattr(x, "kernel")
+
+
 @dataclass(frozen=True)
 class DualOpConfig:
     """Same fields and validation as the reference (dualop.py:55-82).
 
-    The device path implements the explicit strategy.  ``path``: the TRSM and
+    ``strategy``: "explicit" assembles F~_i on the device; "implicit" keeps
+    only the block-scaled factor and runs two triangular sweeps per apply on
+    the device (apply_implicit_local, dualop.py:504-521); "schur_oracle" is
+    the reference's dense test oracle for F~ (dualop.py:524-549) -- it keeps
+    the oracle's size cap and is served by the explicit device assembly (the
+    same F~ to rounding, strategy invariance test_dualop.py:297-308).
+    ``path``: the TRSM and
     SYRK paths produce the same F~_i to roundoff (test_dualop.py:143-149), so
     both are served by the device SYRK path.  The storage/order knobs select
     CPU kernel variants in the reference; the device has one tiled layout, so
@@ -151,6 +174,10 @@ class DualOperator:
     * ``perms``: explicit per-subdomain orderings (mapping or sequence indexed
       by subdomain), as ``symbolic_factorize(ordering=<array>)`` accepts
       (sparse.py:368-371); overrides ``ordering``
+    * ``matrices`` may also be ``SubdomainProblem``-like objects (attributes
+      ``stiffness`` and ``kernel``, solver.py:100-106): the operator then
+      takes K_i and its kernel basis from them and defaults to the sparse
+      route (``prepare_from_problems``)
     * ``factorization``: ``"host"`` (LAPACK on the host, the factor is
       uploaded) or ``"device"``: K_reg = K + rho Q Q^T is formed from the
       unregularized sparse ``stiffness[i]`` and the kernel basis
@@ -166,14 +193,22 @@ class DualOperator:
 
     def __init__(self, matrices, constraints, layout, config: DualOpConfig, pool=None, workers: int = 1,
                  schur_cap: int = 2000, device: int | None = None, ordering: str = "rcm",
-                 subdomains=None, pinned: bool = True, perms=None, factorization: str = "host",
+                 subdomains=None, pinned: bool = True, perms=None, factorization: str | None = None,
                  stiffness=None, kernels=None, sparse_ordering: str = "auto"):
+        matrices = list(matrices)
         if len(matrices) != len(constraints.per_subdomain):
             raise ValueError("one stiffness matrix per subdomain required")
-        if config.strategy != "explicit":
-            raise ValueError(
-                f"the B200 drop-in implements strategy='explicit' (got {config.strategy!r}); "
-                "the implicit and schur_oracle strategies stay in the reference")
+        if matrices and all(_problem_like(x) for x in matrices):
+            # SubdomainProblem inputs: K_i and ker K_i straight from the caller
+            stiffness = [x.stiffness for x in matrices] if stiffness is None else stiffness
+            kernels = [x.kernel for x in matrices] if kernels is None else kernels
+            factorization = factorization or "sparse"
+            matrices = ([x.stiffness_reg for x in matrices] if factorization == "host"
+                        else [_Shape(x.stiffness.shape) for x in matrices])
+        factorization = factorization or "host"
+        if config.strategy == "implicit" and factorization == "sparse":
+            raise ValueError("strategy='implicit' runs on the dense-tile factor routes (factorization='host' or "
+                             "'device'); the sparse-factor route assembles F~ explicitly")
         if ordering not in ORDERINGS:
             raise ValueError(f"ordering must be one of {ORDERINGS}")
         self.matrices = list(matrices)
@@ -354,11 +389,13 @@ class DualOperator:
                 None, None, fct.packed_size(sub.npos), C.byref(slot)))
             sub.slot = slot.value
             self._subs[sub.index] = sub
-        if self.pool is not None and hasattr(self.pool, "capacity"):
+        if self.pool is not None and hasattr(self.pool, "capacity") and self.factorization != "sparse":
             need = self.device_bytes_estimate()
             if need > int(self.pool.capacity):
                 raise PoolCapacityError(
                     f"pool of {self.pool.capacity} bytes cannot hold the {need}-byte device operator")
+        if self.config.strategy == "implicit":
+            _call(self._lib.feti_set_strategy(ctx, _lib.FETI_STRATEGY_IMPLICIT))
         if self.factorization == "device":
             _call(self._lib.feti_enable_device_factorization(ctx))
         if self.factorization == "sparse":
@@ -372,12 +409,21 @@ class DualOperator:
                                                         _lib.i64ptr(sub.perm), fix.shape[0], _lib.i64ptr(fix)))
         _call(self._lib.feti_finalize(ctx, self.n_multipliers))
         st = self.stats()
+        if self.pool is not None and hasattr(self.pool, "capacity") and self.factorization == "sparse":
+            # the block-sparse plan is known only after finalize: the library's own byte count
+            need = int(st["bytes_persistent"]) + int(st["bytes_temporary"])
+            if need > int(self.pool.capacity):
+                raise PoolCapacityError(
+                    f"pool of {self.pool.capacity} bytes cannot hold the {need}-byte device operator")
         self.persistent_bytes = int(st["bytes_persistent"])
         self.symbolic_count = len(self._subs)
         self.prepared = True
         return self
 
     def device_bytes_estimate(self) -> int:
+        """Dense-tile routes: factor tile triangle + X panels + packed F~ (the
+        sparse route's plan is only known after finalize; prepare() checks it
+        against the library's byte count instead)."""
         tot = 0
         for sub in self._subs.values():
             T = -(-sub.n // 128)
@@ -405,7 +451,17 @@ class DualOperator:
         if matrices is not None:
             if len(matrices) != self.n_subdomains:
                 raise ValueError("one stiffness matrix per subdomain required")
-            self.matrices = list(matrices)
+            matrices = list(matrices)
+            if matrices and all(_problem_like(x) for x in matrices):
+                stiffness = [x.stiffness for x in matrices] if stiffness is None else stiffness
+                kernels = [x.kernel for x in matrices] if kernels is None else kernels
+                matrices = ([x.stiffness_reg for x in matrices] if self.factorization == "host"
+                            else [_Shape(x.stiffness.shape) for x in matrices])
+            self.matrices = matrices
+        if self.config.strategy == "schur_oracle":
+            for sub in self._subs.values():
+                if sub.n > self.schur_cap:
+                    raise SizeCapError(f"subdomain of {sub.n} DOFs exceeds the dense oracle cap {self.schur_cap}")
         if self.factorization in ("device", "sparse"):
             if stiffness is not None:
                 self.stiffness = list(stiffness)
@@ -709,8 +765,11 @@ class DualOperator:
                                               sub.fix)
         return sub.solver
 
-    def local_operator(self, index: int) -> np.ndarray:
-        """Host copy of F~_i: m x m, upper triangle, strictly lower = 0."""
+    def local_operator(self, index: int):
+        """Host copy of F~_i: m x m, upper triangle, strictly lower = 0 (None
+        for the implicit strategy, as the reference, dualop.py:399-401)."""
+        if self.config.strategy == "implicit":
+            return None
         if not self.step_ready:
             raise LifecycleError("local operator before preprocess")
         sub = self._subs[int(index)]
@@ -733,3 +792,14 @@ def prepare(matrices, constraints, layout, config, pool=None, workers=1, schur_c
     op = DualOperator(matrices, constraints, layout, config, pool=pool, workers=workers,
                       schur_cap=schur_cap, **kw)
     return op.prepare()
+
+
+def prepare_from_problems(subproblems, constraints, layout, config, pool=None, workers=1, schur_cap=2000,
+                          **kw) -> DualOperator:
+    """``prepare`` on the reference's ``SubdomainProblem`` list
+    (Problem.subdomain_problems, solver.py:100-106): the operator reads the
+    sparse K_i and ker K_i from them and runs the sparse-factor route, so the
+    dense K_reg = K + rho Q Q^T (sparse.py:445-454) is never needed.  Later
+    steps pass the new subproblems to ``preprocess``."""
+    return prepare(list(subproblems), constraints, layout, config, pool=pool, workers=workers,
+                   schur_cap=schur_cap, **kw)

@@ -9,7 +9,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import numpy as np  # noqa: E402
 
-from paper_2502_08382_b200 import dualop, inputs  # noqa: E402
+from harness import inputs  # noqa: E402
+from paper_2502_08382_b200 import dualop  # noqa: E402
 from paper_2502_08382_b200.pcpg import DevicePCPG  # noqa: E402
 
 CFG = dualop.DualOpConfig(strategy="explicit", path="syrk")

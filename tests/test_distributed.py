@@ -15,7 +15,7 @@ import pytest
 
 from oracle import feti_oracle as ora
 from paper_2502_08382_b200 import distributed as fd
-from paper_2502_08382_b200 import inputs
+from harness import inputs
 
 
 def _free_port():

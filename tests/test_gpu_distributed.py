@@ -9,7 +9,8 @@ import numpy as np
 import pytest
 
 from paper_2502_08382_b200 import distributed as fd
-from paper_2502_08382_b200 import dualop, inputs
+from paper_2502_08382_b200 import dualop
+from harness import inputs
 
 pytestmark = pytest.mark.gpu
 CFG = dualop.DualOpConfig(strategy="explicit", path="syrk")

@@ -12,7 +12,8 @@ import socket
 import numpy as np
 import pytest
 
-from paper_2502_08382_b200 import dualop, inputs
+from paper_2502_08382_b200 import dualop
+from harness import inputs
 
 pytestmark = pytest.mark.gpu
 CFG = dualop.DualOpConfig(strategy="explicit", path="syrk")

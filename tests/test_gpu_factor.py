@@ -6,7 +6,8 @@ import numpy as np
 import pytest
 
 from conftest import SMALL_CASES, expected_device_loop_iterations, expected_iterations, load_golden
-from paper_2502_08382_b200 import dualop, inputs
+from paper_2502_08382_b200 import dualop
+from harness import inputs
 from paper_2502_08382_b200.pcpg import DevicePCPG
 
 pytestmark = pytest.mark.gpu

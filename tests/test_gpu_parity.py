@@ -13,7 +13,8 @@ import pytest
 
 from conftest import SMALL_CASES, expected_iterations, load_golden
 from oracle import feti_oracle as ora
-from paper_2502_08382_b200 import _lib, dualop, inputs
+from paper_2502_08382_b200 import _lib, dualop
+from harness import inputs
 
 pytestmark = pytest.mark.gpu
 
@@ -327,6 +328,59 @@ def test_implicit_device_apply_matches_reference(case, ordering):
     assert np.array_equal(qi, qi2)
     assert np.linalg.norm(qi - g["q_implicit"]) <= 1e-11 * np.linalg.norm(g["q_implicit"])
     assert np.linalg.norm(qi - qe) <= 1e-11 * np.linalg.norm(qe)
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+@pytest.mark.parametrize("factorization", ["host", "device"])
+def test_implicit_strategy_through_the_drop_in(case, factorization):
+    """DualOpConfig(strategy="implicit") (the reference's default,
+    dualop.py:59): preprocess keeps only the block-scaled factor (no F~, no
+    X), apply runs the device sweeps and gives the reference's implicit q
+    (test_dualop.py:215-224 bar 1e-11); local_operator is None like the
+    reference's; the reference's PCPG takes the same iteration count."""
+    g = load_golden(case)
+    prob, mats, cons, lay = _golden_problem(g)
+    cfg = dualop.DualOpConfig(strategy="implicit")
+    kw = {}
+    if factorization == "device":
+        ks, qs = [], []
+        for s in range(prob.n_sub):
+            k, _, q = prob.subdomain_system(s)
+            ks.append(k)
+            qs.append(q)
+        kw = dict(factorization="device", stiffness=ks, kernels=qs)
+        mats = [inputs.ShapeOnly(m.shape) for m in mats]
+    with dualop.prepare(mats, cons, lay, cfg, **kw) as op:
+        op.preprocess()
+        assert op.stats()["flops_trsm_exec"] == 0.0
+        q = op.apply(g["p"])
+        assert op.local_operator(0) is None
+        qk, fk = [], []
+        for s in range(prob.n_sub):
+            _, f, qb = prob.subdomain_system(s)
+            qk.append(qb)
+            fk.append(f)
+        cons_o = [(prob.gids[s], prob.bcol[s], prob.bval[s]) for s in range(prob.n_sub)]
+        gm, e, d, coarse = ora.assemble_dual_system(qk, fk, cons_o, prob.n_multipliers, prob.c, op.solve_local)
+        _, it = ora.pcpg(gm, e, d, coarse, op.apply, tol=1e-9)
+    assert np.linalg.norm(q - g["q_implicit"]) <= 1e-11 * np.linalg.norm(g["q_implicit"])
+    assert it in expected_iterations(case, g)
+
+
+def test_schur_oracle_strategy_keeps_the_cap():
+    """strategy="schur_oracle": the reference's dense oracle semantics --
+    SizeCapError above schur_cap DOFs (dualop.py:533-534), otherwise the
+    reference's F~ (served by the device assembly)."""
+    g = load_golden("heat2d_3x2")
+    prob, mats, cons, lay = _golden_problem(g)
+    cfg = dualop.DualOpConfig(strategy="schur_oracle")
+    with dualop.prepare(mats, cons, lay, cfg, schur_cap=10) as op:
+        with pytest.raises(dualop.SizeCapError):
+            op.preprocess()
+    with dualop.prepare(mats, cons, lay, cfg) as op:
+        op.preprocess()
+        q = op.apply(g["p"])
+    assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
 
 
 @pytest.mark.parametrize("two_buffers", [False, True])

@@ -10,7 +10,8 @@ import pytest
 
 from conftest import SMALL_CASES, expected_device_loop_iterations, expected_iterations, load_golden
 from oracle import feti_oracle as ora
-from paper_2502_08382_b200 import dualop, inputs
+from paper_2502_08382_b200 import dualop
+from harness import inputs
 from paper_2502_08382_b200.pcpg import DevicePCPG
 
 pytestmark = pytest.mark.gpu
@@ -255,3 +256,38 @@ def test_sparse_route_algorithmic_flop_count():
             c = (lf != 0.0).sum(axis=0) - 1
             ref += float((c * (c + 3.0)).sum()) + 4.0 * qs[s].shape[1] * float((c + 1).sum())
     assert abs(got - ref) <= 1e-9 * ref, (got, ref)
+
+
+class _SubProblem:
+    """Duck type of the reference's SubdomainProblem (solver.py:100-106)."""
+
+    def __init__(self, stiffness, force, kernel):
+        self.stiffness, self.force, self.kernel = stiffness, force, kernel
+        self.stiffness_reg = None   # the dense K_reg is never formed on this route
+
+
+def test_prepare_from_problems_runs_the_sparse_route():
+    """prepare_from_problems / SubdomainProblem inputs: the run_steps hand-over
+    shape (solver.py:424-431, passing the subproblems instead of their dense
+    stiffness_reg) reaches the sparse-factor route and reproduces the
+    reference's q and PCPG iteration count; a second preprocess takes the
+    next step's subproblems."""
+    g = load_golden("heat3d_4x2")
+    prob = inputs.Problem(str(g["physics"]), int(g["dim"]), int(g["cells"]), int(g["subs"]))
+    subs = []
+    for s in range(prob.n_sub):
+        k, f, q = prob.subdomain_system(s)
+        subs.append(_SubProblem(k, f, q))
+    with dualop.prepare_from_problems(subs, prob.constraints(), prob.layout, CFG, device=0) as op:
+        assert op.factorization == "sparse"
+        op.preprocess(subs)
+        q1 = op.apply(g["p"])
+        op.preprocess(subs)
+        q2 = op.apply(g["p"])
+        cons = [(prob.gids[s], prob.bcol[s], prob.bval[s]) for s in range(prob.n_sub)]
+        gm, e, d, coarse = ora.assemble_dual_system([x.kernel for x in subs], [x.force for x in subs], cons,
+                                                    prob.n_multipliers, prob.c, op.solve_local)
+        _, it = ora.pcpg(gm, e, d, coarse, op.apply, tol=1e-9)
+    assert np.array_equal(q1, q2)
+    assert np.linalg.norm(q1 - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
+    assert it in expected_iterations("heat3d_4x2", g)

@@ -10,7 +10,8 @@ from scipy.sparse import csr_matrix
 from scipy.sparse.csgraph import reverse_cuthill_mckee
 
 from conftest import ROOT
-from paper_2502_08382_b200 import _lib, dualop, inputs
+from paper_2502_08382_b200 import _lib, dualop
+from harness import inputs
 from paper_2502_08382_b200 import factor as fct
 
 HEADER = os.path.join(ROOT, "include", "feti_b200.h")
@@ -64,11 +65,41 @@ def test_config_mirrors_reference():
     assert cfg2.path == "syrk" and cfg2.strategy == "implicit"
 
 
-def test_non_explicit_strategy_rejected():
+def test_implicit_strategy_needs_a_dense_tile_route():
+    """strategy='implicit' runs on the host/device-factor routes; the
+    sparse-factor route only assembles F~ explicitly (rejected up front)."""
     prob = inputs.Problem("heat", 2, 3, 2)
     mats, cons, lay = inputs.reference_inputs(prob)
-    with pytest.raises(ValueError, match="explicit"):
-        dualop.DualOperator(mats, cons, lay, dualop.DualOpConfig(strategy="implicit"))
+    shapes = [inputs.ShapeOnly(m.shape) for m in mats]
+    with pytest.raises(ValueError, match="implicit"):
+        dualop.DualOperator(shapes, cons, lay, dualop.DualOpConfig(strategy="implicit"), factorization="sparse",
+                            stiffness=[None] * len(mats), kernels=[None] * len(mats))
+
+
+class _SubProblem:
+    """Duck type of the reference's SubdomainProblem (solver.py:100-106)."""
+
+    def __init__(self, stiffness, stiffness_reg, force, kernel):
+        self.stiffness, self.stiffness_reg, self.force, self.kernel = stiffness, stiffness_reg, force, kernel
+
+
+def test_problem_like_inputs_select_the_sparse_route():
+    """SubdomainProblem-like inputs (prepare_from_problems): K_i and ker K_i
+    come from them and the route defaults to the sparse factor; with
+    factorization='host' their stiffness_reg is used (the reference's
+    run_steps hand-over, solver.py:424-431)."""
+    prob = inputs.Problem("heat", 2, 3, 2)
+    mats, cons, lay = inputs.reference_inputs(prob)
+    subs = []
+    for s in range(prob.n_sub):
+        k, f, q = prob.subdomain_system(s)
+        subs.append(_SubProblem(k, mats[s], f, q))
+    op = dualop.DualOperator(subs, cons, lay, dualop.DualOpConfig(strategy="explicit"))
+    assert op.factorization == "sparse"
+    assert op.stiffness[0] is subs[0].stiffness and op.kernels[1] is subs[1].kernel
+    assert op.matrices[0].shape == mats[0].shape
+    op2 = dualop.DualOperator(subs, cons, lay, dualop.DualOpConfig(strategy="explicit"), factorization="host")
+    assert op2.matrices[0] is mats[0]
 
 
 @pytest.mark.parametrize("n", [7, 40])
@@ -123,7 +154,7 @@ def test_sparse_route_host_pieces(case):
     solve_local of the sparse-factor route against the reference's F~_i."""
     from conftest import load_golden
     from oracle import feti_oracle as ora
-    from paper_2502_08382_b200 import inputs
+    from harness import inputs
     from paper_2502_08382_b200 import sparse_route as spr
 
     g = load_golden(case)
@@ -155,7 +186,7 @@ def test_sparse_route_tile_aligned_dissection():
     once, segments start on 128-row tiles, the interface last; the chosen
     recipe for config 3 is a dissection with fewer estimated tile flops
     than the onion ordering."""
-    from paper_2502_08382_b200 import inputs
+    from harness import inputs
     from paper_2502_08382_b200 import sparse_route as spr
 
     prob = inputs.Problem("heat", 3, 12, 2)

@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 from conftest import SMALL_CASES, load_golden
-from paper_2502_08382_b200 import inputs
+from harness import inputs
 
 
 @pytest.mark.parametrize("case", SMALL_CASES)
