@@ -161,107 +161,166 @@ def device_factor(prob, s, perm, dev, mask_cache):
 # ---------------------------------------------------------------------------
 
 
-def cpu_reference(prob, sample_sub, values=None, threads=None, reps=1, impl_reps=1):
-    """Time the reference's CPU explicit path on a bounded sample.
+class CpuReference:
+    """The reference's CPU paths for this path, timed on the box's host cores
+    per multiplier-count class: CPU BLAS cost depends only on
+    (n, m), so one subdomain per m-class, weighted by the class's subdomain
+    count, times the whole job exactly up to noise.
 
-    * explicit assembly: the reference's fastest CPU variant (dense storage:
-      factor_to_dense + BLAS dtrsm + dsyrk, dualop.py:427-501,
-      sparse.py:512-563) on one full c3 subdomain with all host threads in
-      BLAS; scaled to the job by the BLAS cost model n^2 m + n m^2 per
-      subdomain (the reference's dense path does not prune);
-    * explicit apply: symv_upper over every subdomain's F~ (sample F~ cut to
-      each m_i), workers = threads (dualop.py:348-388);
-    * implicit apply: spmv + U^-T + U^-1 + spmv on the dense-pattern factor
-      (dualop.py:504-521), `threads` concurrent solves on the sample factor,
-      scaled to all subdomains.
+    * explicit assembly, the reference's dense-storage config as is
+      (assemble_explicit_local, dualop.py:427-501: densify P B~^T,
+      factor_to_dense fancy scatter sparse.py:539-563, BLAS dtrsm
+      sparse.py:517-536, dsyrk dualop.py:488-501, zero_lower) on the
+      reference-layout factor of the dense K_reg -- the faster of
+      {1 worker x all BLAS threads} and {`nconc` workers x 1 BLAS thread},
+      decided on the largest class;
+    * the reference's default config (sparse storage: utsolve_rows,
+      _kernels.py:168-181, one thread per subdomain) on a 128-column sample
+      of the largest class, scaled by sum(m) / 128 (its cost is linear in
+      the number of right-hand sides), over `threads` workers;
+    * explicit apply: symv_upper over every subdomain (dualop.py:348-388);
+    * implicit apply: apply_implicit_local (dualop.py:504-521) per class,
+      `nconc` concurrent, weighted by the class counts.
+    The dense K_reg factorizations (LAPACK) are setup, outside every timing.
     """
-    from concurrent.futures import ThreadPoolExecutor
 
-    from oracle import feti_oracle as ora
-    from paper_2502_08382_b200 import factor as fct
+    def __init__(self, prob, threads=None, log_fn=None):
+        from oracle import feti_oracle as ora
+        from paper_2502_08382_b200 import factor as fct
 
-    threads = threads or os.cpu_count()
-    n = prob.n_dofs
-    bcol, bval = prob.bcol[sample_sub], prob.bval[sample_sub]
-    m_s = bcol.shape[0]
-    perm = rcm_perm_dense(n)
-    iperm = fct.inverse_permutation(perm)
-    out = {"threads": threads, "sample_subdomain": int(sample_sub), "sample_m": int(m_s)}
-    t0 = time.perf_counter()
-    if values is None:
-        kreg = prob.kreg_dense(sample_sub)
-        values = ora.dense_factor_values(kreg, perm)
-        del kreg
-    out["host_factorization_lapack_s"] = time.perf_counter() - t0
-    up, ui = ora.dense_pattern(n)
-    times = []
-    f = None
-    for _ in range(reps):
+        self.ora = ora
+        self.prob = prob
+        self.threads = threads or os.cpu_count()
+        n = prob.n_dofs
+        ms = prob.m_per_subdomain()
+        self.n = n
+        self.perm = rcm_perm_dense(n)
+        self.iperm = fct.inverse_permutation(self.perm)
+        self.up, self.ui = ora.dense_pattern(n)
+        self.classes = []      # (m, representative subdomain, count)
+        for m in sorted(set(int(x) for x in ms)):
+            members = np.flatnonzero(ms == m)
+            self.classes.append((m, int(members[0]), int(members.size)))
         t0 = time.perf_counter()
-        f = ora.assemble_explicit_local(up, ui, values, n, iperm, bcol, bval, storage="dense")
-        times.append(time.perf_counter() - t0)
-    t_sample = min(times)
-    ms = prob.m_per_subdomain().astype(np.float64)
-    cost = lambda m: n * n * m + n * m * m  # noqa: E731
-    scale = float(sum(cost(m) for m in ms) / cost(m_s))
-    out["assembly_sample_s"] = t_sample
-    out["assembly_scale"] = scale
-    total_blas = t_sample * scale
-    # the other threading of SURVEY §8d: subdomains in parallel, one BLAS
-    # thread each (the reference's `workers` pool); `nconc` concurrent copies
-    # of the sample (bounded for host memory: ~1 GB each), scaled by the same
-    # cost model over nconc-wide waves
-    from threadpoolctl import threadpool_limits
+        self.values = {}
+        for m, s, _ in self.classes:
+            kreg = prob.kreg_dense(s)
+            self.values[s] = ora.dense_factor_values(kreg, self.perm)
+            del kreg
+        self.setup_s = time.perf_counter() - t0
+        self.host_factorization_s = self.setup_s / len(self.classes)
+        if log_fn:
+            log_fn(f"[cpu] {len(self.classes)} m-classes, dense K_reg + LAPACK factor per class in {self.setup_s:.1f} s")
+        self.fmats = {}
+        self.variant = None
 
-    nconc = max(1, min(threads, 8, prob.n_sub))
+    def _assemble(self, s):
+        ora, prob = self.ora, self.prob
+        return ora.assemble_explicit_local(self.up, self.ui, self.values[s], self.n, self.iperm, prob.bcol[s],
+                                           prob.bval[s], storage="dense")
 
-    def one_assembly(_):
-        return ora.assemble_explicit_local(up, ui, values, n, iperm, bcol, bval, storage="dense")
+    def choose_threading(self):
+        """Faster of 1 worker x all BLAS threads / nconc workers x 1 BLAS thread,
+        per subdomain-equivalent, on the largest class."""
+        from concurrent.futures import ThreadPoolExecutor
 
-    with threadpool_limits(limits=1, user_api="blas"):
+        from threadpoolctl import threadpool_limits
+
+        m, s, _ = self.classes[-1]
+        self._assemble(s)
         t0 = time.perf_counter()
-        with ThreadPoolExecutor(nconc) as ex:
-            list(ex.map(one_assembly, range(nconc)))
-        t_workers = time.perf_counter() - t0
-    total_workers = t_workers * scale / nconc
-    out["assembly_workers_sample_s"] = t_workers
-    out["assembly_workers_concurrency"] = nconc
-    out["assembly_variants_total_s"] = {"1 worker x all BLAS threads": total_blas,
-                                        f"{nconc} workers x 1 BLAS thread": total_workers}
-    out["assembly_total_s"] = min(total_blas, total_workers)
-    out["assembly_variant"] = ("1 worker x all BLAS threads" if total_blas <= total_workers
-                               else f"{nconc} workers x 1 BLAS thread")
-    # explicit apply over all subdomains (F~ cut to each m_i)
-    fm = [np.ascontiguousarray(f[:int(m), :int(m)]) for m in ms]
-    cons = [(prob.gids[s], prob.bcol[s], prob.bval[s]) for s in range(prob.n_sub)]
-    # restrict gids to the cut size (only sizes matter for timing)
-    cons = [(c[0][:fm[s].shape[0]], c[1], c[2]) for s, c in enumerate(cons)]
-    op = ora.OracleOperator([None] * prob.n_sub, cons, workers=threads)
-    op.fmats = fm
-    p = np.random.default_rng(0).normal(size=prob.n_multipliers)
-    op.apply(p)
-    tt = []
-    for _ in range(3):
-        t0 = time.perf_counter()
-        op.apply(p)
-        tt.append(time.perf_counter() - t0)
-    out["explicit_apply_s"] = min(tt)
-    # implicit apply: `threads` concurrent solves on the sample factor
-    pl = np.random.default_rng(1).normal(size=m_s)
-    nconc = min(threads, prob.n_sub)
-
-    def one(_):
-        return ora.apply_implicit_local(up, ui, values, iperm, bcol, bval, pl)
-
-    ti = []
-    with ThreadPoolExecutor(nconc) as ex:
-        for _ in range(impl_reps):
+        self._assemble(s)
+        t_blas = time.perf_counter() - t0
+        nconc = max(1, min(self.threads, 8, self.prob.n_sub))
+        with threadpool_limits(limits=1, user_api="blas"):
             t0 = time.perf_counter()
-            list(ex.map(one, range(nconc)))
-            ti.append(time.perf_counter() - t0)
-    out["implicit_apply_sample_s"] = min(ti)
-    out["implicit_apply_s"] = min(ti) * math.ceil(prob.n_sub / nconc)
-    return out
+            with ThreadPoolExecutor(nconc) as ex:
+                list(ex.map(lambda _: self._assemble(s), range(nconc)))
+            t_workers = (time.perf_counter() - t0) / nconc
+        self.nconc = nconc
+        self.variant = "blas" if t_blas <= t_workers else "workers"
+        self.threading = {"1 worker x all BLAS threads (s per max-m subdomain)": t_blas,
+                          f"{nconc} workers x 1 BLAS thread (s per max-m subdomain, amortized)": t_workers}
+        return self.variant
+
+    def time_assembly(self):
+        """One timed pass over the classes; returns (total s, {m: s per subdomain})."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        from threadpoolctl import threadpool_limits
+
+        if self.variant is None:
+            self.choose_threading()
+        per, total = {}, 0.0
+        for m, s, cnt in self.classes:
+            if self.variant == "blas":
+                t0 = time.perf_counter()
+                self.fmats[m] = self._assemble(s)
+                t = time.perf_counter() - t0
+            else:
+                k = min(self.nconc, cnt)
+                with threadpool_limits(limits=1, user_api="blas"):
+                    t0 = time.perf_counter()
+                    with ThreadPoolExecutor(k) as ex:
+                        outs = list(ex.map(lambda _: self._assemble(s), range(k)))
+                    t = (time.perf_counter() - t0) / k
+                self.fmats[m] = outs[0]
+            per[m] = t
+            total += t * cnt
+        return total, per
+
+    def time_sparse_storage(self, cols=128):
+        """The reference's default (sparse-storage) forward solve on `cols`
+        columns of the largest class, scaled by sum(m) / cols over `threads`
+        concurrent subdomains."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        ora, prob = self.ora, self.prob
+        m, s, _ = self.classes[-1]
+        cols = min(cols, m)
+        bc, bv = prob.bcol[s][:cols], prob.bval[s][:cols]
+        k = max(1, min(self.threads, prob.n_sub))
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(k) as ex:
+            list(ex.map(lambda _: ora.assemble_explicit_local(self.up, self.ui, self.values[s], self.n, self.iperm,
+                                                              bc, bv, storage="sparse"), range(k)))
+        t = (time.perf_counter() - t0) / k
+        sum_m = float(prob.m_per_subdomain().sum())
+        return t * sum_m / cols, {"sample_cols": cols, "sample_s_per_copy": t, "concurrent_copies": k}
+
+    def time_applies(self, reps=3):
+        """(explicit apply s, implicit apply s) for the whole job."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        ora, prob = self.ora, self.prob
+        if not self.fmats:
+            self.time_assembly()
+        ms = prob.m_per_subdomain()
+        cons = [(prob.gids[s], prob.bcol[s], prob.bval[s]) for s in range(prob.n_sub)]
+        op = ora.OracleOperator([None] * prob.n_sub, cons, workers=self.threads)
+        op.fmats = [self.fmats[int(ms[s])] for s in range(prob.n_sub)]
+        p = np.random.default_rng(0).normal(size=prob.n_multipliers)
+        op.apply(p)
+        tt = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            op.apply(p)
+            tt.append(time.perf_counter() - t0)
+        t_expl = min(tt)
+        k = max(1, min(self.threads, prob.n_sub))
+        t_impl = 0.0
+        with ThreadPoolExecutor(k) as ex:
+            for m, s, cnt in self.classes:
+                pl = np.random.default_rng(1).normal(size=m)
+                c = min(k, cnt)
+                t0 = time.perf_counter()
+                list(ex.map(lambda _: ora.apply_implicit_local(self.up, self.ui, self.values[s], self.iperm,
+                                                               prob.bcol[s], prob.bval[s], pl), range(c)))
+                t_impl += (time.perf_counter() - t0) * math.ceil(cnt / c)
+        return t_expl, t_impl
+
+    def describe(self, per):
+        return ", ".join(f"m={m}: {per[m]:.3f} s x{cnt}" for m, _, cnt in self.classes)
 
 
 def amortization_point(impl, expl):
@@ -357,18 +416,21 @@ def run_reference(args, rank, world):
         }
         print(json.dumps(line), flush=True)
         return
-    results = []
-    first = None
+    cpu = CpuReference(prob, threads, log_fn=log)
+    cpu.choose_threading()
+    totals = []
+    per = None
     for i in range(args.warmup + args.steps):
-        r = cpu_reference(prob, sample, threads=threads, impl_reps=1)
-        if first is None:
-            first = r
+        total, per = cpu.time_assembly()
         if i >= args.warmup:
-            results.append(r)
-        log(f"[reference] step {i}: assembly {r['assembly_total_s']:.2f} s (sample {r['assembly_sample_s']:.2f} s)")
-    value = statistics.median(r["assembly_total_s"] for r in results)
-    app_e = statistics.median(r["explicit_apply_s"] for r in results)
-    app_i = statistics.median(r["implicit_apply_s"] for r in results)
+            totals.append(total)
+        log(f"[reference] step {i}: assembly {total:.2f} s over {len(cpu.classes)} m-classes")
+    value = statistics.median(totals)
+    t_sparse, sp_info = cpu.time_sparse_storage()
+    app_e, app_i = cpu.time_applies()
+    sample = (f"explicit SYRK assembly, the reference's dense-storage config as is (densify, factor_to_dense, "
+              f"dtrsm, dsyrk, zero_lower), one subdomain per multiplier-count class weighted by the class "
+              f"counts ({cpu.describe(per)}), {cpu.variant} threading on {threads} host threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
@@ -376,13 +438,13 @@ def run_reference(args, rank, world):
         "config": {"workload": f"{args.config}: {prob.physics} {prob.dim}D, {prob.n_sub} subdomains x "
                                f"{prob.n_dofs} DOFs, {prob.n_multipliers} multipliers", "ordering": "rcm",
                    "parallelism": f"cpu{threads}"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"explicit SYRK assembly, dense storage (factor_to_dense + dtrsm + dsyrk), "
-                                   f"subdomain {sample} (m={int(ms[sample])}) with {threads} BLAS threads, "
-                                   f"scaled x{first['assembly_scale']:.2f} by the n^2 m + n m^2 BLAS cost model"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         "per_class_s": {str(k): v for k, v in per.items()},
+                         "threading_s": cpu.threading,
+                         "default_sparse_storage_s": t_sparse, "default_sparse_storage_sample": sp_info},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "apply": {"explicit_ms_per_iter": app_e * 1e3, "implicit_ms_per_iter": app_i * 1e3},
-        "host_factorization": {"lapack_s_per_subdomain": first["host_factorization_lapack_s"]},
+        "host_factorization": {"lapack_s_per_subdomain": cpu.host_factorization_s},
     }
     print(json.dumps(line), flush=True)
 
@@ -819,7 +881,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.empty_cache()
         return res
 
-    main_res = measure(args.ordering, keep_host=(rank == 0 and world == 1 and not args.no_cpu_baseline))
+    main_res = measure(args.ordering)
     alt = None
     if not args.single_ordering:
         alt = measure("interface_last" if args.ordering == "rcm" else "rcm")
@@ -895,8 +957,6 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_cpu_baseline:
         ms = prob.m_per_subdomain()
         sample = int(np.argmax(ms))
-        vals = main_res["host_factors"][sample].array if args.ordering == "rcm" else None
-        cpu = cpu_reference(prob, sample, values=vals)
         from paper_2502_08382_b200 import factor as fct
 
         t0 = time.perf_counter()
@@ -905,20 +965,27 @@ def run_ours(args, rank, world, local_rank):
         t0 = time.perf_counter()
         fct.numeric_factorize_dense(kreg, main_res["perms"][sample])
         t_fac = time.perf_counter() - t0
+        del kreg
+        cpu_ref = CpuReference(prob, log_fn=log)
+        cpu_ref.choose_threading()
+        total, per = cpu_ref.time_assembly()
+        t_sparse, sp_info = cpu_ref.time_sparse_storage()
+        t_expl, t_impl = cpu_ref.time_applies()
+        cpu = {"assembly_total_s": total, "explicit_apply_s": t_expl, "implicit_apply_s": t_impl,
+               "threads": cpu_ref.threads}
         line["cpu_baseline"] = {
-            "value": cpu["assembly_total_s"], "unit": UNIT, "cores": cpu["threads"], "kind": "port",
-            "sample": f"CPU explicit SYRK assembly, dense storage (factor_to_dense + dtrsm + dsyrk as "
-                      f"dualop.py:427-501), subdomain {sample} (m={int(ms[sample])}): faster of {cpu['threads']} "
-                      f"BLAS threads on one subdomain ({cpu['assembly_sample_s']:.2f} s) and "
-                      f"{cpu['assembly_workers_concurrency']} concurrent single-thread assemblies "
-                      f"({cpu['assembly_workers_sample_s']:.2f} s), scaled to all {prob.n_sub} subdomains by the "
-                      f"n^2 m + n m^2 BLAS cost model (x{cpu['assembly_scale']:.2f}); used: {cpu['assembly_variant']}",
-            "variants_s": cpu["assembly_variants_total_s"],
-            "explicit_apply_ms": cpu["explicit_apply_s"] * 1e3,
-            "implicit_apply_ms": cpu["implicit_apply_s"] * 1e3,
-            "implicit_sample": f"{min(cpu['threads'], prob.n_sub)} concurrent implicit applies on subdomain "
-                               f"{sample} = {cpu['implicit_apply_sample_s'] * 1e3:.1f} ms, "
-                               f"x{math.ceil(prob.n_sub / min(cpu['threads'], prob.n_sub))}"}
+            "value": total, "unit": UNIT, "cores": cpu_ref.threads, "kind": "port",
+            "sample": f"CPU explicit SYRK assembly, the reference's dense-storage config as is (densify, "
+                      f"factor_to_dense, dtrsm, dsyrk, zero_lower; dualop.py:427-501), one subdomain per "
+                      f"multiplier-count class weighted by the class counts ({cpu_ref.describe(per)}), "
+                      f"{cpu_ref.variant} threading on {cpu_ref.threads} host threads",
+            "per_class_s": {str(k): v for k, v in per.items()},
+            "threading_s": cpu_ref.threading,
+            "default_sparse_storage_s": t_sparse, "default_sparse_storage_sample": sp_info,
+            "explicit_apply_ms": t_expl * 1e3,
+            "implicit_apply_ms": t_impl * 1e3,
+            "implicit_sample": f"apply_implicit_local per m-class, {min(cpu_ref.threads, prob.n_sub)} concurrent, "
+                               f"weighted by the class counts"}
         line["host_factorization"] = {
             "lapack_dpotrf_s_per_subdomain": t_fac, "dense_kreg_build_s": t_dense,
             "note": "host numeric factorization (before the path; common to implicit and explicit, cancels "

@@ -476,3 +476,53 @@ def fmatrix_via_solver(solver, n, bcol, bval):
     z[bcol, np.arange(m)] = bval
     x = solver.solve(z)
     return bval[:, None] * x[bcol, :]
+
+
+# ---------------------------------------------------------------------------
+# whole-job oracle at the headline sizes (configs 3-4): dense LAPACK + BLAS
+# ---------------------------------------------------------------------------
+
+
+class DenseKregOracle:
+    """F~_i = B~ K_reg^-1 B~^T and K_reg^-1 b from the reference's dense
+    K_reg = K + rho Q Q^T (regularize, sparse.py:427-454), by the reference's
+    dense-storage arithmetic: LAPACK dpotrf of K_reg (its dense pattern makes
+    the RCM ordering a pure relabelling, so it is omitted),
+    X = L^-1 B~^T by BLAS dtrsm (triangular_solve_multi with dense storage,
+    sparse.py:512-536), F = X^T X by BLAS dsyrk (_syrk_into, dualop.py:488-501).
+    Full symmetric m x m result.  Used where the reference's own numba
+    factorization (332 s per config-3 subdomain) is too slow to rerun."""
+
+    def __init__(self, kreg_dense: np.ndarray, consume: bool = False):
+        """``consume``: factor in place (the symmetric C-ordered array is read
+        as its Fortran-ordered transpose, no copy)."""
+        import scipy.linalg.lapack as lapack
+
+        a = kreg_dense.T if (consume and kreg_dense.flags.c_contiguous) else np.asfortranarray(kreg_dense)
+        c, info = lapack.dpotrf(a, lower=1, clean=1, overwrite_a=1 if consume else 0)
+        if info != 0:
+            raise ArithmeticError(f"dpotrf info={info}")
+        self.l = c
+
+    def fmatrix(self, bcol, bval) -> np.ndarray:
+        n, m = self.l.shape[0], bcol.shape[0]
+        z = np.zeros((n, m), order="F")
+        z[bcol, np.arange(m)] = bval
+        x = dtrsm(1.0, self.l, z, side=0, lower=1, trans_a=0, overwrite_b=1)
+        f = dsyrk(1.0, x, trans=1, lower=0)
+        return np.triu(f) + np.triu(f, 1).T
+
+    def solve(self, b) -> np.ndarray:
+        from scipy.linalg.lapack import dpotrs
+
+        x, info = dpotrs(self.l, np.asarray(b, dtype=np.float64), lower=1)
+        return x
+
+
+def apply_dense_full(fmats, cons, p) -> np.ndarray:
+    """q = sum_i B~_i^T F_i B~_i p over full symmetric F_i, in the given
+    (gather) order (dualop.py:348-380); BLAS dgemv per subdomain."""
+    out = np.zeros(p.shape[0])
+    for f, (g, _, _) in zip(fmats, cons):
+        out[g] += f @ p[g]
+    return out

