@@ -200,11 +200,25 @@ int feti_factorize(feti_ctx* ctx);
  * Call feti_enable_sparse_factorization and, per slot, feti_set_sparse_pattern
  * (K's CSR pattern, the ordering -- constrained DOFs last -- and the fixing
  * DOFs) before feti_finalize; then per step feti_set_stiffness (values, Q,
- * rho = trace(K)/n, same ordering), feti_factorize, feti_assemble.
- * feti_solve_many and the implicit apply are not available in this mode. */
+ * same ordering; rho = trace(K)/n, sparse.py:450, is computed on the device
+ * in this mode and the argument is ignored) -- or, after the first step,
+ * the batched feti_set_stiffness_values -- then feti_factorize,
+ * feti_assemble.  In this mode the K values are copied asynchronously
+ * (overlapping the zeroing of the tile pool): keep `data` alive and
+ * unchanged until feti_assemble returns.
+ * The implicit apply is not available in this mode. */
 int feti_enable_sparse_factorization(feti_ctx* ctx);
 int feti_set_sparse_pattern(feti_ctx* ctx, int64_t slot, int64_t n, const int64_t* indptr, const int64_t* indices,
                             const int64_t* perm, int64_t r, const int64_t* fix_dofs);
+/* Per-step numeric hand-over of the sparse route over a frozen pattern (the
+ * refill of CholFactor over its symbolic stage, sparse.py:287-299, without
+ * re-validating the pattern): for each listed slot, nnz[i] values of K in
+ * the CSR order of its first feti_set_stiffness, and Q[i] its n x r kernel
+ * basis or NULL when unchanged (Q may itself be NULL: all unchanged).
+ * Copies are queued asynchronously; keep the buffers alive until
+ * feti_assemble returns. */
+int feti_set_stiffness_values(feti_ctx* ctx, int64_t nslots, const int64_t* slots, const double* const* data,
+                              const int64_t* nnz, const double* const* Q);
 /* x = K_reg^-1 b for the listed slots (host vectors concatenated in list
  * order), through the device factor (CholFactor.solve, sparse.py:324-337). */
 int feti_solve_many(feti_ctx* ctx, int64_t nslots, const int64_t* slots, const double* b, double* x);

@@ -36,7 +36,7 @@ EXPORTED = (
     "feti_factorize", "feti_solve_many", "feti_enable_sparse_factorization", "feti_set_sparse_pattern",
     "feti_set_preconditioner", "feti_precond_apply", "feti_precond_apply_device",
     "feti_exchange_setup", "feti_exchange_connect", "feti_apply_exchange_device", "feti_exchange_status",
-    "feti_set_strategy",
+    "feti_set_strategy", "feti_set_stiffness_values",
 )
 FETI_IPC_HANDLE_BYTES = 64
 
@@ -99,6 +99,7 @@ def load() -> C.CDLL:
         "feti_coarse_apply_device": ([P, P, P, P], C.c_int),
         "feti_apply_implicit": ([P, f64p, f64p], C.c_int),
         "feti_set_strategy": ([P, C.c_int], C.c_int),
+        "feti_set_stiffness_values": ([P, C.c_int64, P, P, P, P], C.c_int),
         "feti_apply_implicit_device": ([P, P, P, P], C.c_int),
         "feti_enable_device_factorization": ([P], C.c_int),
         "feti_set_stiffness": ([P, C.c_int64, C.c_int64, i64p, i64p, f64p, C.c_int64, f64p, C.c_int64, C.c_double,

@@ -117,6 +117,9 @@ struct SubHost {
   int64_t* d_fix = nullptr;
   double* d_U1 = nullptr;
   double* d_U2W = nullptr;
+  int64_t* d_kdiag = nullptr;        // diagonal position of each row of K (rho on the device)
+  double* d_rho = nullptr;
+  std::vector<double> h_Q, h_U1;     // last kernel basis handed over and its U1 = B~ Q (async sources)
   int64_t f_tiles() const { return (int64_t)T32 * (T32 + 1) / 2; }
   int64_t l_tiles() const { return (int64_t)(T - tbase) * (T - tbase + 1) / 2; }
   int64_t upload_count() const { return nnz - raw_off; }
@@ -141,16 +144,16 @@ struct feti_ctx {
   // device tables
   SubDev* d_subdev = nullptr;
   int4 *d_w_unpack = nullptr, *d_w_diag = nullptr, *d_w_scale = nullptr, *d_w_chain = nullptr,
-       *d_w_syrk = nullptr, *d_w_apply = nullptr;
+       *d_w_syrk = nullptr;
+  ApplySeg* d_apply_segs = nullptr;
   int n_unpack = 0, n_diag = 0, n_scale = 0, n_chain = 0, n_syrk = 0, n_apply = 0;
-  int64_t* d_part_off = nullptr;
+  int64_t* d_ridx = nullptr;        // partial positions per (subdomain, multiplier) contribution
   int* d_apply_seg_ptr = nullptr;
   double* d_part = nullptr;
   int* d_cptr = nullptr;
   int4* d_cent = nullptr;
   double *d_p = nullptr, *d_q = nullptr;
   int apply_nw = 8;
-  size_t apply_smem = 0;
   feti_stats stats{};
   cudaEvent_t ev[8] = {};
   bool subdev_dirty = true;
@@ -206,6 +209,11 @@ struct feti_ctx {
   static constexpr int kSpStreams = 8;
   std::vector<std::pair<int, int>> sp_corr_rng, sp_sub_rng;   // per group: panels, subdomains
   cudaEvent_t sp_ev[3] = {};   // factorize start, factorize end, assemble end
+  // sparse-route stiffness hand-over: values are copied on copy_stream while
+  // the pool is zeroed; k_ready = copies issued so far landed, k_free = the
+  // last scatter finished reading the previous values
+  cudaEvent_t k_ready = nullptr, k_free = nullptr;
+  bool k_pending = false;
   std::vector<int> sp_bad_init;
   bool sp_pending_check = false;   // pivots of the last factorize not yet checked
   // lumped preconditioner (feti_set_preconditioner): a second descriptor table
@@ -428,8 +436,8 @@ int factorize_sparse(feti_ctx* c) {
   std::vector<SpSub> ss(ns);
   for (int si = 0; si < ns; ++si) {
     SubHost& s = c->subs[si];
-    ss[si] = SpSub{s.d_pool, s.d_tmap, s.d_perm, s.d_iperm, s.d_kptr, s.d_kind, s.d_kdata, s.d_Q,
-                   s.d_fix, s.d_U1, s.d_U2W, s.rho, s.sp.T, s.sp.Tq, (int)s.sp_n, s.sp_r, s.sp_r, (int)s.n};
+    ss[si] = SpSub{s.d_pool, s.d_tmap, s.d_perm, s.d_iperm, s.d_kptr, s.d_kind, s.d_kdata, s.d_Q, s.d_kdiag,
+                   s.d_fix, s.d_U1, s.d_U2W, s.d_rho, s.sp.T, s.sp.Tq, (int)s.sp_n, s.sp_r, s.sp_r, (int)s.n};
     s.src = SRC_TILES;
   }
   CUDA_TRY(cudaMemcpyAsync(c->d_spsub, ss.data(), ns * sizeof(SpSub), cudaMemcpyHostToDevice, st));
@@ -440,7 +448,15 @@ int factorize_sparse(feti_ctx* c) {
   CUDA_TRY(cudaMemcpyAsync(c->d_bad, c->sp_bad_init.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaEventRecord(c->sp_ev[0], st));
   launch_sp_init(c->d_sp_init, c->n_sp_init, c->d_spsub, st);
+  // the step's K values / kernel bases were copied on copy_stream while the
+  // pool was being zeroed
+  if (c->k_pending) {
+    CUDA_TRY(cudaStreamWaitEvent(st, c->k_ready, 0));
+    c->k_pending = false;
+  }
+  launch_sp_trace(c->d_spsub, ns, st);
   launch_sp_scatter(c->d_spsub, 0, ns, c->sp_max_n, st);
+  CUDA_TRY(cudaEventRecord(c->k_free, st));
   CUDA_TRY(cudaGetLastError());
   FETI_DEBUG_SYNC(st);
   int launches = 2;
@@ -518,6 +534,41 @@ int wait_applies(feti_ctx* c) {
   return FETI_OK;
 }
 
+// Sparse route: queue one slot's K values (and, when it changed, its kernel
+// basis + U1 = B~ Q) on copy_stream; factorize_sparse waits for k_ready
+// after zeroing the pool.  The caller keeps `data` alive and unchanged
+// until feti_assemble returns; Q and U1 are staged in the slot's own host
+// buffers.
+int stiffness_values_async(feti_ctx* c, SubHost& s, const double* data, const double* Q) {
+  if (!c->k_pending) {
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->k_free, 0));   // the last scatter read the old values
+    c->k_pending = true;
+  }
+  CUDA_TRY(cudaMemcpyAsync(s.d_kdata, data, (size_t)s.k_nnz * 8, cudaMemcpyHostToDevice, c->copy_stream));
+  const int64_t n = s.sp_n, r = s.kr;
+  if (r > 0 && Q && (s.h_Q.empty() || std::memcmp(s.h_Q.data(), Q, (size_t)(n * r) * 8) != 0)) {
+    s.h_Q.assign(Q, Q + n * r);
+    // U1 = B~ Q in sorted column order: row a = sign_a Q[dof_a]
+    const size_t rows = (size_t)s.P * TB;
+    s.h_U1.assign(rows * r, 0.0);
+    for (int64_t a = 0; a < s.m; ++a) {
+      const int64_t dof = s.sp_perm[s.r_sorted[a]];
+      for (int64_t q = 0; q < r; ++q) s.h_U1[a * r + q] = s.s_sorted[a] * Q[dof * r + q];
+    }
+    if (!s.d_U1) {
+      int rc;
+      if ((rc = dev_alloc(c, (void**)&s.d_U1, rows * r * 8, true))) return rc;
+      if ((rc = dev_alloc(c, (void**)&s.d_U2W, rows * 2 * r * 8, true))) return rc;
+    }
+    CUDA_TRY(cudaMemcpyAsync(s.d_Q, s.h_Q.data(), (size_t)(n * r) * 8, cudaMemcpyHostToDevice, c->copy_stream));
+    CUDA_TRY(cudaMemcpyAsync(s.d_U1, s.h_U1.data(), rows * r * 8, cudaMemcpyHostToDevice, c->copy_stream));
+  } else if (r > 0 && s.h_Q.empty()) {
+    return fail(FETI_ERR_ARG, "the first hand-over of a slot needs its kernel basis");
+  }
+  CUDA_TRY(cudaEventRecord(c->k_ready, c->copy_stream));
+  return FETI_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -547,6 +598,9 @@ int feti_create(int device, feti_ctx** out) {
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(cudaEventCreateWithFlags(&c->apply_done, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&c->x_sum_done, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->k_ready, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->k_free, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(c->k_free, c->stream));
   CUDA_TRY(configure_kernels());
   *out = c;
   return FETI_OK;
@@ -578,6 +632,8 @@ int feti_destroy(feti_ctx* c) {
   for (double* pp : c->x_open) cudaIpcCloseMemHandle(pp);
   if (c->apply_done) cudaEventDestroy(c->apply_done);
   if (c->x_sum_done) cudaEventDestroy(c->x_sum_done);
+  if (c->k_ready) cudaEventDestroy(c->k_ready);
+  if (c->k_free) cudaEventDestroy(c->k_free);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   delete c;
@@ -671,7 +727,6 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
 
   // capacity check before allocating anything large
   size_t need = 0;
-  int max_M = 0;
   if (c->sparse_factor)
     for (size_t i = 0; i < c->subs.size(); ++i) {
       SubHost& s = c->subs[i];
@@ -686,7 +741,6 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
       need += (size_t)s.P * (s.T - s.smin) * TILE * 8;   // X panels
       need += (size_t)s.f_tiles() * ATILE * 8;          // F~
     }
-    max_M = std::max(max_M, s.T32 * AT);
   }
   size_t fr = 0, tot = 0;
   CUDA_TRY(cudaMemGetInfo(&fr, &tot));
@@ -740,7 +794,7 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   if ((rc = dev_alloc(c, (void**)&c->d_subdev, c->subs.size() * sizeof(SubDev), true))) return rc;
 
   // ---- work lists (largest work first where it varies)
-  std::vector<int4> wu, wd, ws, wc, wy, wa;
+  std::vector<int4> wu, wd, ws, wc, wy;
   double trsm_alg = 0, syrk_alg = 0, trsm_exec = 0, syrk_exec = 0, scale_exec = 0;
   const double tb3 = 2.0 * TB * TB * TB;
   for (int si = 0; si < (int)c->subs.size(); ++si) {
@@ -841,37 +895,55 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     for (auto& e : c->wave_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
 
-  // ---- apply work: the concatenated tile list of all subdomains is cut into
-  // one contiguous, equal range per SM (persistent CTAs); each range becomes
-  // segments (sub, t0, t1, partial slot) where it crosses subdomain bounds
+  // ---- apply work: every subdomain's packed upper triangle of 32x32 tiles is
+  // split into SB x SB-tile super-blocks (I <= J); the concatenated tile list
+  // of all super-blocks is cut into one contiguous, equal range per SM
+  // (persistent CTAs), each range into segments at super-block bounds.  The
+  // kernel's accumulators span one super-block (<= 2 x SBE multipliers), so
+  // neither the warp count nor the subdomain size is limited by shared memory.
+  struct Blk { int sub, I, J; int64_t tiles; };
+  std::vector<Blk> blks;
   int64_t total_tiles = 0;
-  for (auto& s : c->subs) total_tiles += s.f_tiles();
+  for (int si = 0; si < (int)c->subs.size(); ++si) {
+    const SubHost& s = c->subs[si];
+    if (s.m == 0) continue;
+    const int nb = (s.T32 + SB - 1) / SB;
+    for (int I = 0; I < nb; ++I)
+      for (int J = I; J < nb; ++J) {
+        const int64_t h = std::min(SB, s.T32 - I * SB), w = std::min(SB, s.T32 - J * SB);
+        const int64_t nt = (I == J) ? h * (h + 1) / 2 : h * w;
+        blks.push_back(Blk{si, I, J, nt});
+        total_tiles += nt;
+      }
+  }
   const int64_t ncta = std::max<int64_t>(1, std::min<int64_t>(c->num_sms, (total_tiles + 63) / 64));
-  std::vector<int64_t> part_off;
-  std::vector<int> cta_begin(c->subs.size()), cta_end(c->subs.size());
+  std::vector<ApplySeg> asegs;
   std::vector<int> seg_ptr;
   int64_t poff = 0;
   double apply_alg = 16.0 * (double)c->n_mult, apply_exec = 16.0 * (double)c->n_mult;
   {
-    std::vector<int64_t> base(c->subs.size() + 1, 0);
-    for (size_t si = 0; si < c->subs.size(); ++si) base[si + 1] = base[si] + c->subs[si].f_tiles();
-    for (size_t si = 0; si < c->subs.size(); ++si) cta_begin[si] = cta_end[si] = -1;
+    size_t bi = 0;
+    int64_t bbase = 0;    // first global tile of block bi
     for (int64_t b = 0; b < ncta; ++b) {
-      seg_ptr.push_back((int)wa.size());
+      seg_ptr.push_back((int)asegs.size());
       const int64_t g0 = total_tiles * b / ncta, g1 = total_tiles * (b + 1) / ncta;
-      for (size_t si = 0; si < c->subs.size(); ++si) {
-        const int64_t lo = std::max(g0, base[si]), hi = std::min(g1, base[si + 1]);
-        if (lo >= hi || c->subs[si].m == 0) continue;
-        if (cta_begin[si] < 0) cta_begin[si] = (int)part_off.size();
-        wa.push_back(make_int4((int)si, (int)(lo - base[si]), (int)(hi - base[si]), (int)part_off.size()));
-        part_off.push_back(poff);
-        poff += c->subs[si].m;
-        cta_end[si] = (int)part_off.size();
+      while (bi < blks.size() && bbase + blks[bi].tiles <= g0) bbase += blks[bi++].tiles;
+      for (size_t k = bi, kb = bbase; k < blks.size() && (int64_t)kb < g1; kb += blks[k++].tiles) {
+        const int64_t lo = std::max<int64_t>(g0, kb), hi = std::min<int64_t>(g1, kb + blks[k].tiles);
+        if (lo >= hi) continue;
+        const Blk& B = blks[k];
+        const SubHost& s = c->subs[B.sub];
+        const int h = std::min(SB, s.T32 - B.I * SB), w = std::min(SB, s.T32 - B.J * SB);
+        ApplySeg sg{B.sub, B.I, B.J, (int)(lo - kb), (int)(hi - kb), 0, poff, -1};
+        poff += (int64_t)h * AT;
+        if (B.I != B.J) {
+          sg.out_c = poff;
+          poff += (int64_t)w * AT;
+        }
+        asegs.push_back(sg);
       }
     }
-    seg_ptr.push_back((int)wa.size());
-    for (size_t si = 0; si < c->subs.size(); ++si)
-      if (cta_begin[si] < 0) cta_begin[si] = cta_end[si] = 0;
+    seg_ptr.push_back((int)asegs.size());
   }
   for (int si = 0; si < (int)c->subs.size(); ++si) {
     const SubHost& s = c->subs[si];
@@ -879,12 +951,34 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     apply_exec += 8.0 * ATILE * s.f_tiles() + s.T32 * AT * 12.0;
   }
   apply_exec += 16.0 * poff;
+  // partial positions of every (subdomain, local multiplier), in segment order
+  std::vector<std::vector<std::vector<int64_t>>> lp(c->subs.size());
+  for (int si = 0; si < (int)c->subs.size(); ++si) lp[si].assign(c->subs[si].m, {});
+  for (const ApplySeg& sg : asegs) {
+    const SubHost& s = c->subs[sg.sub];
+    const int h = std::min(SB, s.T32 - sg.I * SB), w = std::min(SB, s.T32 - sg.J * SB);
+    for (int a = 0; a < h * AT; ++a) {
+      const int la = sg.I * SBE + a;
+      if (la < s.m) lp[sg.sub][la].push_back(sg.out_r + a);
+    }
+    if (sg.I != sg.J)
+      for (int a = 0; a < w * AT; ++a) {
+        const int la = sg.J * SBE + a;
+        if (la < s.m) lp[sg.sub][la].push_back(sg.out_c + a);
+      }
+  }
   // contributions per global multiplier, in registration (gather) order
+  std::vector<int64_t> ridx;
   std::vector<std::vector<int4>> per_g((size_t)c->n_mult);
   for (int si = 0; si < (int)c->subs.size(); ++si) {
     const SubHost& s = c->subs[si];
-    for (int a = 0; a < s.m; ++a) per_g[s.gids_sorted[a]].push_back(make_int4(a, cta_begin[si], cta_end[si], si));
+    for (int a = 0; a < s.m; ++a) {
+      const int b0 = (int)ridx.size();
+      ridx.insert(ridx.end(), lp[si][a].begin(), lp[si][a].end());
+      per_g[s.gids_sorted[a]].push_back(make_int4(a, b0, (int)ridx.size(), si));
+    }
   }
+  std::vector<std::vector<std::vector<int64_t>>>().swap(lp);
   std::vector<int> cptr((size_t)c->n_mult + 1, 0);
   std::vector<int4> cent;
   for (int64_t g = 0; g < c->n_mult; ++g) {
@@ -893,24 +987,19 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   }
   cptr[c->n_mult] = (int)cent.size();
 
-  // per-warp accumulators in smem: (NW + 1) * M doubles
+  // warps per apply CTA: bytes in flight bound the kernel (two 8 KB tile
+  // loads per warp); the accumulators no longer depend on m
   c->apply_nw = 8;
-  // (as many warps as the accumulators leave room for: each warp keeps one
-  // 32x32 tile load in flight, and the kernel is HBM-bound on bytes in flight)
-  if (const char* wenv = getenv("FETI_APPLY_WARPS")) c->apply_nw = std::max(1, std::min(8, atoi(wenv)));   // tests
-  while (c->apply_nw > 1 && (size_t)(c->apply_nw + 1) * max_M * 8 > 227 * 1024) --c->apply_nw;
-  c->apply_smem = (size_t)(c->apply_nw + 1) * max_M * 8;
-  if (c->apply_smem > 227 * 1024 && !c->implicit)
-    return fail(FETI_ERR_CAPACITY, "subdomain with %d multipliers exceeds the apply kernel's shared memory", max_M);
+  if (const char* wenv = getenv("FETI_APPLY_WARPS")) c->apply_nw = std::max(1, std::min(APPLY_MAX_WARPS, atoi(wenv)));
 
   if ((rc = upload(c, &c->d_w_unpack, wu))) return rc;
   if ((rc = upload(c, &c->d_w_diag, wd))) return rc;
   if ((rc = upload(c, &c->d_w_scale, ws))) return rc;
   if ((rc = upload(c, &c->d_w_chain, wc))) return rc;
   if ((rc = upload(c, &c->d_w_syrk, wy))) return rc;
-  if ((rc = upload(c, &c->d_w_apply, wa))) return rc;
+  if ((rc = upload(c, &c->d_apply_segs, asegs))) return rc;
   if ((rc = upload(c, &c->d_apply_seg_ptr, seg_ptr))) return rc;
-  if ((rc = upload(c, &c->d_part_off, part_off))) return rc;
+  if ((rc = upload(c, &c->d_ridx, ridx))) return rc;
   c->h_cptr = cptr;
   if ((rc = upload(c, &c->d_cptr, cptr))) return rc;
   if ((rc = upload(c, &c->d_cent, cent))) return rc;
@@ -1213,9 +1302,8 @@ static int implicit_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStr
 // apply reads only finalize-time fields of it (F~ tiles, index maps).
 static int apply_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st, bool time_it) {
   if (time_it) CUDA_TRY(cudaEventRecord(c->ev[0], st));
-  launch_apply(c->apply_nw, c->apply_smem, c->d_subdev, c->d_w_apply, c->d_apply_seg_ptr, c->n_apply,
-               c->d_part_off, c->d_part, d_p, st);
-  launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_part_off, c->d_part, d_q, st);
+  launch_apply(c->apply_nw, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, d_p, st);
+  launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_ridx, c->d_part, d_q, st);
   CUDA_TRY(cudaGetLastError());
   if (time_it) CUDA_TRY(cudaEventRecord(c->ev[1], st));
   return mark_apply(c, st);
@@ -1287,9 +1375,8 @@ int feti_precond_apply_device(feti_ctx* c, const double* d_w, double* d_out, voi
   if (!d_w || !d_out) return fail(FETI_ERR_ARG, "NULL vector");
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
-  launch_apply(c->apply_nw, c->apply_smem, c->d_subdev_p, c->d_w_apply, c->d_apply_seg_ptr, c->n_apply,
-               c->d_part_off, c->d_part, d_w, st);
-  launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_part_off, c->d_part, d_out, st);
+  launch_apply(c->apply_nw, c->d_subdev_p, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, d_w, st);
+  launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_ridx, c->d_part, d_out, st);
   CUDA_TRY(cudaGetLastError());
   return mark_apply(c, st);
 }
@@ -1375,9 +1462,8 @@ int feti_apply_exchange_device(feti_ctx* c, const double* d_p, double* d_q, void
   // finished first (feti_exchange.cu header): order it explicitly, whatever
   // stream the caller used last time
   CUDA_TRY(cudaStreamWaitEvent(st, c->x_sum_done, 0));
-  launch_apply(c->apply_nw, c->apply_smem, c->d_subdev, c->d_w_apply, c->d_apply_seg_ptr, c->n_apply,
-               c->d_part_off, c->d_part, d_p, st);
-  XchgArgs a{c->d_x_peers, c->d_x_touched, c->d_cptr, c->d_cent, c->d_part_off, c->d_part, c->d_x_done,
+  launch_apply(c->apply_nw, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, d_p, st);
+  XchgArgs a{c->d_x_peers, c->d_x_touched, c->d_cptr, c->d_cent, c->d_ridx, c->d_part, c->d_x_done,
              c->d_x_error, c->x_epoch + 1, c->x_n_touched, (int)c->n_mult, c->x_rank, c->x_world};
   launch_exchange(a, d_q, st);
   CUDA_TRY(cudaGetLastError());
@@ -1513,22 +1599,41 @@ int feti_set_stiffness(feti_ctx* c, int64_t slot, int64_t n, const int64_t* indp
   } else if (nnz != s.k_nnz || (int)r != s.kr) {
     return fail(FETI_ERR_ARG, "stiffness pattern changed after the first call");
   }
+  if (c->sparse_factor) {
+    if (!s.d_kdiag) {
+      std::vector<int64_t> kd(n, -1);
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p)
+          if (indices[p] == i) kd[i] = p;
+      if ((rc = upload(c, &s.d_kdiag, kd))) return rc;
+      if ((rc = dev_alloc(c, (void**)&s.d_rho, sizeof(double), true))) return rc;
+    }
+    return stiffness_values_async(c, s, data, Q);
+  }
   CUDA_TRY(cudaMemcpy(s.d_kdata, data, (size_t)nnz * 8, cudaMemcpyHostToDevice));
   if (r > 0) CUDA_TRY(cudaMemcpy(s.d_Q, Q, (size_t)(n * r) * 8, cudaMemcpyHostToDevice));
   s.rho = rho;
-  if (c->sparse_factor && r > 0) {
-    // U1 = B~ Q in sorted column order: row a = sign_a Q[dof_a]
-    const size_t rows = (size_t)s.P * TB;
-    std::vector<double> u1(rows * r, 0.0);
-    for (int64_t a = 0; a < s.m; ++a) {
-      const int64_t dof = s.sp_perm[s.r_sorted[a]];
-      for (int64_t q = 0; q < r; ++q) u1[a * r + q] = s.s_sorted[a] * Q[dof * r + q];
-    }
-    if (!s.d_U1) {
-      if ((rc = dev_alloc(c, (void**)&s.d_U1, rows * r * 8, true))) return rc;
-      if ((rc = dev_alloc(c, (void**)&s.d_U2W, rows * 2 * r * 8, true))) return rc;
-    }
-    CUDA_TRY(cudaMemcpy(s.d_U1, u1.data(), rows * r * 8, cudaMemcpyHostToDevice));
+  return FETI_OK;
+}
+
+int feti_set_stiffness_values(feti_ctx* c, int64_t nslots, const int64_t* slots, const double* const* data,
+                              const int64_t* nnz, const double* const* Q) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->finalized || !c->sparse_factor)
+    return fail(FETI_ERR_LIFECYCLE, "set_stiffness_values needs a finalized context with sparse factorization");
+  if (nslots < 0 || (nslots > 0 && (!slots || !data || !nnz))) return fail(FETI_ERR_ARG, "bad batch arguments");
+  CUDA_TRY(cudaSetDevice(c->device));
+  for (int64_t i = 0; i < nslots; ++i) {
+    if (slots[i] < 0 || slots[i] >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot out of range");
+    SubHost& s = c->subs[slots[i]];
+    if (!s.stiff_set)
+      return fail(FETI_ERR_LIFECYCLE, "slot %lld: the first hand-over goes through feti_set_stiffness",
+                  (long long)slots[i]);
+    if (nnz[i] != s.k_nnz || !data[i])
+      return fail(FETI_ERR_ARG, "slot %lld: %lld values for a pattern of %lld", (long long)slots[i],
+                  (long long)nnz[i], (long long)s.k_nnz);
+    int rc = stiffness_values_async(c, s, data[i], Q ? Q[i] : nullptr);
+    if (rc) return rc;
   }
   return FETI_OK;
 }

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) reduce_exchange_kernel(XchgArgs a) {
     for (int e = a.cptr[g]; e < a.cptr[g + 1]; ++e) {
       const int4 c = a.cent[e];
       double v = 0.0;
-      for (int s = c.y; s < c.z; ++s) v += a.part[a.part_off[s] + c.x];
+      for (int k = c.y; k < c.z; ++k) v += a.part[a.ridx[k]];
       acc += v;
     }
     const size_t off = ((size_t)(a.epoch & 1) * a.world + a.rank) * a.n_mult + g;

@@ -10,7 +10,7 @@ struct XchgArgs {
   const int* touched;       // multipliers this rank contributes to (ascending)
   const int* cptr;          // contribution CSR of this rank (as reduce_kernel)
   const int4* cent;
-  const int64_t* part_off;
+  const int64_t* ridx;      // partial positions per contribution (as reduce_kernel)
   const double* part;
   unsigned* done;           // CTA completion counter (own memory)
   int* error;               // set when a peer never arrived

@@ -504,25 +504,33 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) syrk_kernel(const SubDev* __r
 // ---------------------------------------------------------------------------
 // 6. apply: batched packed SYMV fused with the B~ gather/scatter
 // ---------------------------------------------------------------------------
-// work: (sub, tile_begin, tile_end, partial slot)
+// Work unit: a segment of one super-block (I, J) of SB x SB tiles of a
+// subdomain's packed upper triangle (ApplySeg).  The concatenated tile list
+// of all super-blocks of all subdomains is cut into one contiguous, equal
+// range per CTA (persistent, one CTA per SM), so the load is balanced to a
+// tile and the per-warp accumulators span at most 2 x SBE multipliers,
+// whatever the subdomain's m (no size limit, and NW warps always fit).
 //
 // Lane l of a warp owns column l of a 32x32 tile (32 coalesced 256-byte row
-// reads per tile); the next tile's 32 loads are issued before the current one
-// is reduced (register double buffering) so each warp keeps 16 KB in flight.
+// reads per tile); three tiles per warp live in registers so two loads are in
+// flight while one is reduced.
 __device__ __forceinline__ void apply_tile_load(double (&f)[32], const double* __restrict__ Ft, int lane) {
 #pragma unroll
   for (int r = 0; r < 32; ++r) f[r] = __ldcs(Ft + r * AT + lane);
 }
 
-__device__ __forceinline__ void apply_tile_compute(double (&f)[32], int ti, int tj, const double* __restrict__ sp,
-                                                   double* __restrict__ myq, int lane) {
-  if (ti != tj) {
+// row sums into myr[li], column sums (transposed contribution of an
+// off-diagonal tile) into myc[lj]
+__device__ __forceinline__ void apply_tile_compute(double (&f)[32], int li, int lj, bool offdiag,
+                                                   const double* __restrict__ pr, const double* __restrict__ pc,
+                                                   double* __restrict__ myr, double* __restrict__ myc, int lane) {
+  if (offdiag) {
     double cs = 0.0;
 #pragma unroll
-    for (int r = 0; r < 32; ++r) cs = fma(f[r], sp[ti * AT + r], cs);
-    myq[tj * AT + lane] += cs;
+    for (int r = 0; r < 32; ++r) cs = fma(f[r], pr[li * AT + r], cs);
+    myc[lj * AT + lane] += cs;
   }
-  const double pj = sp[tj * AT + lane];
+  const double pj = pc[lj * AT + lane];
 #pragma unroll
   for (int r = 0; r < 32; ++r) f[r] *= pj;
   // butterfly transpose-reduce: lane r ends with sum_l F[r][l] p_J[l]
@@ -536,115 +544,118 @@ __device__ __forceinline__ void apply_tile_compute(double (&f)[32], int ti, int 
       f[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
     }
   }
-  myq[ti * AT + lane] += f[0];
+  myr[li * AT + lane] += f[0];
 }
 
-__device__ __forceinline__ void apply_advance(int& ti, int& tj, int step, int T32) {
-  int rem = (tj - ti) + step;
-  while (ti < T32 && rem >= T32 - ti) {
-    rem -= T32 - ti;
-    ++ti;
+// Tile cursor inside a super-block: h x w tiles (rectangle), or for a
+// diagonal block the upper triangle of h x h tiles, row-major.
+struct SbCursor {
+  int li, lj;
+  __device__ __forceinline__ void locate(int t, int h, int w, bool diag) {
+    if (!diag) {
+      li = t / w;
+      lj = t - li * w;
+      return;
+    }
+    // row li starts at li*h - li*(li-1)/2
+    const double b = 2.0 * h + 1.0;
+    int r = (int)((b - sqrt(b * b - 8.0 * t)) * 0.5);
+    while (r > 0 && r * h - r * (r - 1) / 2 > t) --r;
+    while ((r + 1) * h - (r + 1) * r / 2 <= t) ++r;
+    li = r;
+    lj = r + (t - (r * h - r * (r - 1) / 2));
   }
-  tj = ti + rem;
-}
+};
 
-template <int NW, bool TRIPLE>
+template <int NW>
 __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict__ subs,
-                                                        const int4* __restrict__ segs,
+                                                        const ApplySeg* __restrict__ segs,
                                                         const int* __restrict__ seg_ptr,
-                                                        const int64_t* __restrict__ part_off,
                                                         double* __restrict__ part,
                                                         const double* __restrict__ p) {
-  // persistent: CTA b walks its segments (sub, tile range, partial slot)
   extern __shared__ double asmem[];
+  double* spr = asmem;                  // p of the block's rows
+  double* spc = asmem + SBE;            // p of the block's columns (off-diagonal blocks)
+  double* acc = asmem + 2 * SBE;        // warp w: rows at acc + 2 w SBE, columns at + SBE
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int sg = seg_ptr[blockIdx.x]; sg < seg_ptr[blockIdx.x + 1]; ++sg) {
-    const int4 w = segs[sg];
-    const SubDev& S = subs[w.x];
+    const ApplySeg w = segs[sg];
+    const SubDev& S = subs[w.sub];
     const int T32 = S.T32;
-    const int M = T32 * AT;
-    double* sp = asmem;
-    double* sq = asmem + M;
-    __syncthreads();   // previous segment's combine is done with smem
-    for (int a = tid; a < M; a += NW * 32) {
-      const int gi = S.gids_sorted[a];
-      sp[a] = gi >= 0 ? __ldg(p + gi) : 0.0;
+    const int r0 = w.I * SB, c0 = w.J * SB;
+    const int h = min(SB, T32 - r0), wd = min(SB, T32 - c0);
+    const bool diag = w.I == w.J;
+    __syncthreads();   // the previous segment's combine is done with smem
+    for (int a = tid; a < h * AT; a += NW * 32) {
+      const int gi = S.gids_sorted[r0 * AT + a];
+      spr[a] = gi >= 0 ? __ldg(p + gi) : 0.0;
     }
-    for (int a = tid; a < NW * M; a += NW * 32) sq[a] = 0.0;
-    __syncthreads();
-    double* myq = sq + warp * M;
-
-    int64_t tt = (int64_t)w.y + warp;
-    const int64_t t1 = w.z;
-    int ti = 0;
-    int64_t rowstart = 0;
-    while (ti < T32 && rowstart + (T32 - ti) <= tt) {
-      rowstart += T32 - ti;
-      ++ti;
-    }
-    int tj = ti + (int)(tt - rowstart);
-    const double* Fb = S.F;
-    double fa[32], fb[32];
-    if constexpr (TRIPLE) {
-      // three tiles per warp in registers: two loads in flight while one is
-      // reduced (matters when the accumulators leave room for few warps)
-      double fc[32];
-      if (tt < t1) apply_tile_load(fa, Fb + tt * ATILE, lane);
-      if (tt + NW < t1) apply_tile_load(fb, Fb + (tt + NW) * ATILE, lane);
-      while (tt < t1) {
-        if (tt + 2 * NW < t1) apply_tile_load(fc, Fb + (tt + 2 * NW) * ATILE, lane);
-        apply_tile_compute(fa, ti, tj, sp, myq, lane);
-        tt += NW;
-        apply_advance(ti, tj, NW, T32);
-        if (tt >= t1) break;
-        if (tt + 2 * NW < t1) apply_tile_load(fa, Fb + (tt + 2 * NW) * ATILE, lane);
-        apply_tile_compute(fb, ti, tj, sp, myq, lane);
-        tt += NW;
-        apply_advance(ti, tj, NW, T32);
-        if (tt >= t1) break;
-        if (tt + 2 * NW < t1) apply_tile_load(fb, Fb + (tt + 2 * NW) * ATILE, lane);
-        apply_tile_compute(fc, ti, tj, sp, myq, lane);
-        tt += NW;
-        apply_advance(ti, tj, NW, T32);
+    if (!diag)
+      for (int a = tid; a < wd * AT; a += NW * 32) {
+        const int gi = S.gids_sorted[c0 * AT + a];
+        spc[a] = gi >= 0 ? __ldg(p + gi) : 0.0;
       }
-    } else {
-    if (tt < t1) apply_tile_load(fa, Fb + tt * ATILE, lane);
+    for (int a = tid; a < NW * 2 * SBE; a += NW * 32) acc[a] = 0.0;
+    __syncthreads();
+    double* myr = acc + 2 * warp * SBE;
+    double* myc = diag ? myr : myr + SBE;
+    const double* pc = diag ? spr : spc;
+    const double* Fb = S.F;
+    auto tile_ptr = [&](int t) -> const double* {
+      SbCursor cu;
+      cu.locate(t, h, wd, diag);
+      return Fb + apply_tile_index(r0 + cu.li, c0 + cu.lj, T32) * ATILE;
+    };
+    int tt = w.t0 + warp;
+    const int t1 = w.t1;
+    double fa[32], fb[32], fc[32];
+    if (tt < t1) apply_tile_load(fa, tile_ptr(tt), lane);
+    if (tt + NW < t1) apply_tile_load(fb, tile_ptr(tt + NW), lane);
+    SbCursor cu;
     while (tt < t1) {
-      int ti2 = ti, tj2 = tj;
-      apply_advance(ti2, tj2, NW, T32);
-      int64_t nx = tt + NW;
-      if (nx < t1) apply_tile_load(fb, Fb + nx * ATILE, lane);
-      apply_tile_compute(fa, ti, tj, sp, myq, lane);
-      tt = nx;
-      ti = ti2;
-      tj = tj2;
+      if (tt + 2 * NW < t1) apply_tile_load(fc, tile_ptr(tt + 2 * NW), lane);
+      cu.locate(tt, h, wd, diag);
+      apply_tile_compute(fa, cu.li, cu.lj, !diag || cu.li != cu.lj, spr, pc, myr, myc, lane);
+      tt += NW;
       if (tt >= t1) break;
-      apply_advance(ti2, tj2, NW, T32);
-      nx = tt + NW;
-      if (nx < t1) apply_tile_load(fa, Fb + nx * ATILE, lane);
-      apply_tile_compute(fb, ti, tj, sp, myq, lane);
-      tt = nx;
-      ti = ti2;
-      tj = tj2;
-    }
+      if (tt + 2 * NW < t1) apply_tile_load(fa, tile_ptr(tt + 2 * NW), lane);
+      cu.locate(tt, h, wd, diag);
+      apply_tile_compute(fb, cu.li, cu.lj, !diag || cu.li != cu.lj, spr, pc, myr, myc, lane);
+      tt += NW;
+      if (tt >= t1) break;
+      if (tt + 2 * NW < t1) apply_tile_load(fb, tile_ptr(tt + 2 * NW), lane);
+      cu.locate(tt, h, wd, diag);
+      apply_tile_compute(fc, cu.li, cu.lj, !diag || cu.li != cu.lj, spr, pc, myr, myc, lane);
+      tt += NW;
     }
     __syncthreads();
-    double* out = part + part_off[w.w];
-    for (int a = tid; a < S.m; a += NW * 32) {
+    // combine the warps in fixed order (deterministic)
+    for (int a = tid; a < h * AT; a += NW * 32) {
       double s = 0.0;
 #pragma unroll
-      for (int wi = 0; wi < NW; ++wi) s += sq[wi * M + a];
-      out[a] = s;
+      for (int wi = 0; wi < NW; ++wi) s += acc[2 * wi * SBE + a];
+      part[w.out_r + a] = s;
     }
+    if (!diag)
+      for (int a = tid; a < wd * AT; a += NW * 32) {
+        double s = 0.0;
+#pragma unroll
+        for (int wi = 0; wi < NW; ++wi) s += acc[2 * wi * SBE + SBE + a];
+        part[w.out_c + a] = s;
+      }
   }
 }
 
 // ---------------------------------------------------------------------------
 // 7. ordered reduction into the global dual vector
 // ---------------------------------------------------------------------------
+// per global multiplier: its (subdomain, local) contributions in the
+// reference's gather order (dualop.py:375-379); contribution e sums the
+// partials ridx[cent[e].y .. cent[e].z) of the super-block segments that
+// touched it, in segment order
 __global__ void __launch_bounds__(256) reduce_kernel(int n_mult, const int* __restrict__ cptr,
                                                      const int4* __restrict__ cent,
-                                                     const int64_t* __restrict__ part_off,
+                                                     const int64_t* __restrict__ ridx,
                                                      const double* __restrict__ part, double* __restrict__ q) {
   const int gidx = blockIdx.x * blockDim.x + threadIdx.x;
   if (gidx >= n_mult) return;
@@ -652,7 +663,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(int n_mult, const int* __re
   for (int e = cptr[gidx]; e < cptr[gidx + 1]; ++e) {
     const int4 c = cent[e];
     double v = 0.0;
-    for (int s = c.y; s < c.z; ++s) v += part[part_off[s] + c.x];
+    for (int k = c.y; k < c.z; ++k) v += part[ridx[k]];
     acc += v;
   }
   q[gidx] = acc;
@@ -676,15 +687,13 @@ cudaError_t configure_kernels() {
   if ((e = cudaFuncSetAttribute(diag_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (2 * 8256 + 3 * 1024) * 8)))
     return e;
-  const void* applies[16] = {
-      (const void*)apply_kernel<1, false>, (const void*)apply_kernel<2, false>, (const void*)apply_kernel<3, false>,
-      (const void*)apply_kernel<4, false>, (const void*)apply_kernel<5, false>, (const void*)apply_kernel<6, false>,
-      (const void*)apply_kernel<7, false>, (const void*)apply_kernel<8, false>, (const void*)apply_kernel<1, true>,
-      (const void*)apply_kernel<2, true>,  (const void*)apply_kernel<3, true>,  (const void*)apply_kernel<4, true>,
-      (const void*)apply_kernel<5, true>,  (const void*)apply_kernel<6, true>,  (const void*)apply_kernel<7, true>,
-      (const void*)apply_kernel<8, true>};
-  for (const void* k : applies)
-    if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024))) return e;
+  const void* applies[APPLY_MAX_WARPS] = {
+      (const void*)apply_kernel<1>,  (const void*)apply_kernel<2>,  (const void*)apply_kernel<3>,
+      (const void*)apply_kernel<4>,  (const void*)apply_kernel<5>,  (const void*)apply_kernel<6>,
+      (const void*)apply_kernel<7>,  (const void*)apply_kernel<8>};
+  for (int w = 1; w <= APPLY_MAX_WARPS; ++w)
+    if ((e = cudaFuncSetAttribute(applies[w - 1], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem(w))))
+      return e;
   return cudaSuccess;
 }
 
@@ -706,16 +715,14 @@ void launch_trsm_chain(const SubDev* subs, const int4* work, int nwork, cudaStre
 void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
   if (nwork > 0) syrk_kernel<<<nwork, PIPE_THREADS, pipe_smem(), st>>>(subs, work);
 }
-void launch_apply(int nw, size_t smem, const SubDev* subs, const int4* segs, const int* seg_ptr, int nctas,
-                  const int64_t* part_off, double* part, const double* p, cudaStream_t st) {
+size_t apply_smem(int nw) { return (size_t)(2 + 2 * nw) * SBE * sizeof(double); }
+
+void launch_apply(int nw, const SubDev* subs, const ApplySeg* segs, const int* seg_ptr, int nctas, double* part,
+                  const double* p, cudaStream_t st) {
   if (nctas <= 0) return;
-  const bool triple = getenv("FETI_APPLY_2BUF") == nullptr;   // A/B switch for measurements
-#define FETI_APPLY_CASE(W)                                                                            \
-  case W:                                                                                             \
-    if (triple)                                                                                       \
-      apply_kernel<W, true><<<nctas, W * 32, smem, st>>>(subs, segs, seg_ptr, part_off, part, p);    \
-    else                                                                                              \
-      apply_kernel<W, false><<<nctas, W * 32, smem, st>>>(subs, segs, seg_ptr, part_off, part, p);   \
+#define FETI_APPLY_CASE(W) \
+  case W:                  \
+    apply_kernel<W><<<nctas, W * 32, apply_smem(W), st>>>(subs, segs, seg_ptr, part, p); \
     break;
   switch (nw) {
     FETI_APPLY_CASE(8)
@@ -729,9 +736,9 @@ void launch_apply(int nw, size_t smem, const SubDev* subs, const int4* segs, con
   }
 #undef FETI_APPLY_CASE
 }
-void launch_reduce(int n_mult, const int* cptr, const int4* cent, const int64_t* part_off, const double* part,
+void launch_reduce(int n_mult, const int* cptr, const int4* cent, const int64_t* ridx, const double* part,
                    double* q, cudaStream_t st) {
-  if (n_mult > 0) reduce_kernel<<<(n_mult + 255) / 256, 256, 0, st>>>(n_mult, cptr, cent, part_off, part, q);
+  if (n_mult > 0) reduce_kernel<<<(n_mult + 255) / 256, 256, 0, st>>>(n_mult, cptr, cent, ridx, part, q);
 }
 
 }  // namespace feti
@@ -743,7 +750,7 @@ int kernel_attributes(char* buf, int len) {
       {"unpack_dense", (const void*)unpack_dense_kernel},   {"scatter_sparse", (const void*)scatter_sparse_kernel},
       {"diag_inverse", (const void*)diag_inverse_kernel},   {"block_scale", (const void*)block_scale_kernel},
       {"trsm_chain", (const void*)trsm_chain_kernel},       {"syrk", (const void*)syrk_kernel},
-      {"apply8", (const void*)apply_kernel<8, true>},             {"reduce", (const void*)reduce_kernel}};
+      {"apply8", (const void*)apply_kernel<8>},             {"reduce", (const void*)reduce_kernel}};
   int off = 0;
   for (auto& k : ks) {
     cudaFuncAttributes a;

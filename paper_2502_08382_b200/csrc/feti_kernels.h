@@ -15,9 +15,11 @@ void launch_diag_inverse(const SubDev* subs, const int4* work, int nwork, cudaSt
 void launch_block_scale(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
 void launch_trsm_chain(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
 void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
-void launch_apply(int nw, size_t smem, const SubDev* subs, const int4* segs, const int* seg_ptr, int nctas,
-                  const int64_t* part_off, double* part, const double* p, cudaStream_t st);
-void launch_reduce(int n_mult, const int* cptr, const int4* cent, const int64_t* part_off, const double* part,
+constexpr int APPLY_MAX_WARPS = 8;   // 3 tile buffers x 32 doubles: > 8 warps spill
+size_t apply_smem(int nw);
+void launch_apply(int nw, const SubDev* subs, const ApplySeg* segs, const int* seg_ptr, int nctas, double* part,
+                  const double* p, cudaStream_t st);
+void launch_reduce(int n_mult, const int* cptr, const int4* cent, const int64_t* ridx, const double* part,
                    double* q, cudaStream_t st);
 
 }  // namespace feti

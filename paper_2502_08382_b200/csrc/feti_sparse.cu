@@ -58,6 +58,22 @@ __global__ void __launch_bounds__(256) sp_init_kernel(const SpInit* __restrict__
   }
 }
 
+// rho = trace(K) / n (regularize, sparse.py:450): one CTA per subdomain,
+// strided partial sums reduced in a fixed tree order (bit-reproducible)
+__global__ void __launch_bounds__(256) sp_trace_kernel(const SpSub* __restrict__ ss) {
+  const SpSub& S = ss[blockIdx.x];
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int a = threadIdx.x; a < S.n; a += 256) acc += S.kdata[S.kdiag[a]];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *S.rho = red[0] / S.n;
+}
+
 // K_s entries into the lower block triangle of P K_s P^T: one warp per
 // original row a; the fixing shift rho lands on the diagonal entry.
 __global__ void __launch_bounds__(256) sp_scatter_kernel(const SpSub* __restrict__ ss, int sub0) {
@@ -73,7 +89,7 @@ __global__ void __launch_bounds__(256) sp_scatter_kernel(const SpSub* __restrict
     const int64_t pb = S.iperm[b];
     if (pa < pb) continue;
     double v = S.kdata[p];
-    if (fixed && b == a) v += S.rho;
+    if (fixed && b == a) v += *S.rho;
     const int slot = S.tmap[(pa / TB) * S.Tq + pb / TB];
     double* tile = S.pool + (size_t)slot * TILE;
     tile[swz((int)(pb % TB), (int)(pa % TB))] += v;
@@ -228,7 +244,7 @@ __global__ void __launch_bounds__(U2_GROUPS * TB) sp_u2_kernel(const SubDev* __r
   const double* cq = Q.pool + (size_t)Q.tmap[T * Q.Tq + T] * TILE;
   if (threadIdx.x < r * r) {
     const int q = threadIdx.x / r, q2 = threadIdx.x % r;
-    Cm[threadIdx.x] = -cq[swz(q2, q)] + (q == q2 ? 1.0 / Q.rho : 0.0);
+    Cm[threadIdx.x] = -cq[swz(q2, q)] + (q == q2 ? 1.0 / *Q.rho : 0.0);
   }
   // rows split over the row groups (row = kb*128 + il, il = rg mod U2_GROUPS),
   // two independent accumulator chains per group
@@ -458,6 +474,10 @@ void launch_sp_init(const SpInit* w, int nw, const SpSub* ss, cudaStream_t st) {
 
 void launch_sp_scatter(const SpSub* ss, int sub0, int nsub, int max_n, cudaStream_t st) {
   if (nsub > 0 && max_n > 0) sp_scatter_kernel<<<dim3((max_n + 7) / 8, nsub), 256, 0, st>>>(ss, sub0);
+}
+
+void launch_sp_trace(const SpSub* ss, int nsub, cudaStream_t st) {
+  if (nsub > 0) sp_trace_kernel<<<nsub, 256, 0, st>>>(ss);
 }
 
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st) {

@@ -22,10 +22,11 @@ struct SpSub {
   const int64_t* kind;
   const double* kdata;
   const double* Q;          // n x r kernel basis, row-major
+  const int64_t* kdiag;     // n: position of K's diagonal entry of each row in kdata
   const int64_t* fix;       // fixing DOFs (original numbering), nfix = r
   const double* U1;         // P*128 x r: sign_a * Q[dof_a], sorted column order
   double* U2W;              // P*128 x 2r: U2 = X^T y_b, then W = C U1 - U2
-  double rho;
+  double* rho;              // device scalar: trace(K) / n (sparse.py:450), written by sp_trace_kernel
   int T;                    // block rows of K_s (the Q block row is T when r > 0)
   int Tq;                   // T + (r > 0)
   int n, r, nfix;           // n: DOFs (rows of K)
@@ -83,6 +84,8 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
 cudaError_t configure_sparse();
 void launch_sp_init(const SpInit* w, int nw, const SpSub* ss, cudaStream_t st);
 void launch_sp_scatter(const SpSub* ss, int sub0, int nsub, int max_n, cudaStream_t st);
+// rho = trace(K) / n per subdomain on the device (fixed-order reduction)
+void launch_sp_trace(const SpSub* ss, int nsub, cudaStream_t st);
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st);
 void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st);
 // after the assembly: U2/W per (sub, panel), then the rank-2r update of F~

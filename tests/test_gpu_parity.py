@@ -383,19 +383,58 @@ def test_schur_oracle_strategy_keeps_the_cap():
     assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
 
 
-@pytest.mark.parametrize("two_buffers", [False, True])
 @pytest.mark.parametrize("warps", [1, 3, 5, 6, 7, 8])
-def test_apply_any_warp_count_matches_reference(warps, two_buffers, monkeypatch):
-    """The apply kernel runs with as many warps per CTA as its per-warp
-    accumulators leave room for (6 on c4's 3,873-multiplier subdomains),
-    with two or three register tile buffers per warp; every variant gives the
-    reference's q."""
+def test_apply_any_warp_count_matches_reference(warps, monkeypatch):
+    """The apply kernel with any warp count per CTA (its super-block
+    accumulators no longer depend on m) gives the reference's q."""
     monkeypatch.setenv("FETI_APPLY_WARPS", str(warps))
-    if two_buffers:
-        monkeypatch.setenv("FETI_APPLY_2BUF", "1")
     g = load_golden(SMALL_CASES[-1])
     prob, mats, cons, lay = _golden_problem(g)
     with dualop.prepare(mats, cons, lay, CFG) as op:
         op.preprocess()
         q = op.apply(g["p"])
     assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
+
+
+def test_apply_without_multiplier_limit():
+    """Two subdomains with m = 15,500 and 2,100 multipliers (the round-1
+    kernel capped m at ~14.5k: (NW+1) M doubles of shared memory) through
+    the apply kernels, via the C-ABI's explicit-tile entry
+    (feti_set_preconditioner + feti_precond_apply run the same SYMV + gather/
+    scatter + ordered reduction as feti_apply): q = sum_i B~_i^T P_i B~_i p
+    against numpy (symv_upper semantics, _kernels.py:274-287)."""
+    lib = _lib.load()
+    ctx = C.c_void_p()
+    _lib.check(lib.feti_create(0, C.byref(ctx)))
+    rng = np.random.default_rng(21)
+    n_mult = 17000
+    sizes = (15500, 2100)
+    try:
+        _lib.check(lib.feti_set_strategy(ctx, _lib.FETI_STRATEGY_IMPLICIT))   # no F~/X workspace needed
+        subs = []
+        for m in sizes:
+            n = m + 3
+            gids = np.sort(rng.choice(n_mult, size=m, replace=False)).astype(np.int64)
+            first = rng.permutation(n)[:m].astype(np.int64)
+            sign = rng.choice([-1.0, 1.0], size=m)
+            slot = C.c_int64()
+            _lib.check(lib.feti_add_subdomain(ctx, n, m, _lib.i64ptr(first), _lib.f64ptr(sign), _lib.i64ptr(gids),
+                                              None, None, n * (n + 1) // 2, C.byref(slot)))
+            subs.append((slot.value, m, gids))
+        _lib.check(lib.feti_finalize(ctx, n_mult))
+        mats = []
+        for slot, m, gids in subs:
+            a = rng.standard_normal((m, m))
+            a = np.ascontiguousarray(a + a.T)
+            _lib.check(lib.feti_set_preconditioner(ctx, slot, _lib.f64ptr(a)))
+            mats.append((a, gids))
+            del a
+        p = rng.standard_normal(n_mult)
+        q = np.empty(n_mult)
+        _lib.check(lib.feti_precond_apply(ctx, _lib.f64ptr(p), _lib.f64ptr(q)))
+        qr = np.zeros(n_mult)
+        for a, gids in mats:
+            qr[gids] += a @ p[gids]
+        assert np.linalg.norm(q - qr) <= 1e-12 * np.linalg.norm(qr)
+    finally:
+        lib.feti_destroy(ctx)
