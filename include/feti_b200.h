@@ -47,7 +47,9 @@ enum {
   FETI_ERR_CAPACITY = 4,   /* device memory too small: PoolCapacityError */
   FETI_ERR_SINGULAR = 5,   /* zero diagonal in the factor: SingularFactorError (sparse.py:491-492) */
   FETI_ERR_INTERNAL = 6,
-  FETI_ERR_NOT_SPD = 7     /* non-positive pivot in the device factorization: SpdError (sparse.py:297-298) */
+  FETI_ERR_NOT_SPD = 7,    /* non-positive pivot in the device factorization: SpdError (sparse.py:297-298) */
+  FETI_ERR_BREAKDOWN = 8,  /* PCPG: p^T F p <= 0, BreakdownError (solver.py:40-41, 246-247) */
+  FETI_ERR_NOT_CONVERGED = 9 /* PCPG: iteration cap reached, ConvergenceError (solver.py:44-45, 263-267) */
 };
 
 enum { FETI_FACTOR_HOST = 0, FETI_FACTOR_DEVICE = 1 };
@@ -92,6 +94,8 @@ typedef struct feti_stats {
   double ms_preprocess;      /* sparse-factor route: factorize start -> assemble end (device) */
   double flops_factor_alg;   /* sparse-factor route: scalar Cholesky flops of K_s in the chosen ordering
                                 (sum_j c_j (c_j + 3) from the exact column counts, + the y = L^-1 P Q solve) */
+  double ms_pcpg;            /* device time of the last feti_pcpg_solve iteration loop */
+  int64_t pcpg_iterations;   /* its iteration count */
 } feti_stats;
 
 int feti_abi_version(void);
@@ -167,6 +171,19 @@ int feti_project_device(feti_ctx* ctx, const double* d_x, double* d_out, void* s
 /* out = G (G^T G)^-1 v for v of length nk (feasible start G (G^T G)^-1 e). */
 int feti_coarse_apply_device(feti_ctx* ctx, const double* d_v, double* d_out, void* stream);
 
+/* Device-native PCPG (pcpg, solver.py:195-272) on this context's explicit
+ * operator (which must own every subdomain) after feti_coarse_setup: the
+ * whole iteration -- apply, projections, inner products, the stopping test
+ * -- runs on the device (CUDA graph of several iterations, the host polls a
+ * status word per graph launch).  d (n_multipliers) and e (nk) host vectors
+ * of the dual system (solver.py:125-148); precond 0 = none, 1 = lumped
+ * (feti_set_preconditioner); lam (host, n_multipliers) receives the
+ * multipliers.  The reference's feasible start, roundoff guard and stopping
+ * test (||w_k|| <= tol ||w_0||); maxit <= 0 means n_multipliers.  Returns
+ * FETI_ERR_BREAKDOWN / FETI_ERR_NOT_CONVERGED as the reference raises. */
+int feti_pcpg_solve(feti_ctx* ctx, const double* d, const double* e, double tol, int64_t maxit, int precond,
+                    double* lam, int64_t* iterations, double* rel_residual);
+
 /* Implicit strategy on the device (apply_implicit_local, dualop.py:504-521):
  * q = sum_i B~_i^T K_reg,i^-1 B~_i p through two block triangular sweeps over
  * the scaled factor the last feti_assemble left in HBM (same result as
@@ -219,6 +236,19 @@ int feti_set_sparse_pattern(feti_ctx* ctx, int64_t slot, int64_t n, const int64_
  * feti_assemble returns. */
 int feti_set_stiffness_values(feti_ctx* ctx, int64_t nslots, const int64_t* slots, const double* const* data,
                               const int64_t* nnz, const double* const* Q);
+/* Device dual right-hand side of the sparse route (replaces the solve_local
+ * calls of assemble_dual_system, solver.py:141-143, for d = B~ K_reg^-1 f - c):
+ * feti_enable_dual_rhs before feti_finalize appends a force row to every
+ * slot's (P Q)^T block row; per step feti_set_forces hands over
+ * f' = (I - Q Q^T) f (n) and Q^T f (r) per slot before feti_factorize (same
+ * asynchronous rules as the stiffness values); after feti_assemble,
+ * feti_dual_rhs writes d = sum_i B~_i K_reg,i^-1 f_i - c (c may be NULL) to
+ * the host.  With K_reg^-1 = Pi K_s^-1 Pi + rho^-1 Q Q^T:
+ * B~ K_reg^-1 f = X^T y_f - U1 (y^T y_f) + rho^-1 U1 Q^T f, y_f = L^-1 P f'. */
+int feti_enable_dual_rhs(feti_ctx* ctx);
+int feti_set_forces(feti_ctx* ctx, int64_t nslots, const int64_t* slots, const double* const* fproj,
+                    const double* const* qtf);
+int feti_dual_rhs(feti_ctx* ctx, const double* c, double* d);
 /* x = K_reg^-1 b for the listed slots (host vectors concatenated in list
  * order), through the device factor (CholFactor.solve, sparse.py:324-337). */
 int feti_solve_many(feti_ctx* ctx, int64_t nslots, const int64_t* slots, const double* b, double* x);

@@ -22,6 +22,8 @@ FETI_ERR_CAPACITY = 4
 FETI_ERR_SINGULAR = 5
 FETI_ERR_INTERNAL = 6
 FETI_ERR_NOT_SPD = 7
+FETI_ERR_BREAKDOWN = 8
+FETI_ERR_NOT_CONVERGED = 9
 FETI_FACTOR_HOST = 0
 FETI_FACTOR_DEVICE = 1
 FETI_STRATEGY_EXPLICIT = 0
@@ -36,7 +38,8 @@ EXPORTED = (
     "feti_factorize", "feti_solve_many", "feti_enable_sparse_factorization", "feti_set_sparse_pattern",
     "feti_set_preconditioner", "feti_precond_apply", "feti_precond_apply_device",
     "feti_exchange_setup", "feti_exchange_connect", "feti_apply_exchange_device", "feti_exchange_status",
-    "feti_set_strategy", "feti_set_stiffness_values",
+    "feti_set_strategy", "feti_set_stiffness_values", "feti_pcpg_solve", "feti_enable_dual_rhs",
+    "feti_set_forces", "feti_dual_rhs",
 )
 FETI_IPC_HANDLE_BYTES = 64
 
@@ -55,7 +58,7 @@ class FetiStats(C.Structure):
         ("launches_assemble", C.c_int32), ("launches_apply", C.c_int32),
         ("ms_factorize", C.c_double), ("ms_correct", C.c_double), ("flops_factor_exec", C.c_double),
         ("launches_factorize", C.c_int32), ("pad_", C.c_int32), ("ms_preprocess", C.c_double),
-        ("flops_factor_alg", C.c_double),
+        ("flops_factor_alg", C.c_double), ("ms_pcpg", C.c_double), ("pcpg_iterations", C.c_int64),
     ]
 
     def as_dict(self):
@@ -100,6 +103,10 @@ def load() -> C.CDLL:
         "feti_apply_implicit": ([P, f64p, f64p], C.c_int),
         "feti_set_strategy": ([P, C.c_int], C.c_int),
         "feti_set_stiffness_values": ([P, C.c_int64, P, P, P, P], C.c_int),
+        "feti_pcpg_solve": ([P, f64p, f64p, C.c_double, C.c_int64, C.c_int, f64p, P, P], C.c_int),
+        "feti_enable_dual_rhs": ([P], C.c_int),
+        "feti_set_forces": ([P, C.c_int64, P, P, P], C.c_int),
+        "feti_dual_rhs": ([P, P, f64p], C.c_int),
         "feti_apply_implicit_device": ([P, P, P, P], C.c_int),
         "feti_enable_device_factorization": ([P], C.c_int),
         "feti_set_stiffness": ([P, C.c_int64, C.c_int64, i64p, i64p, f64p, C.c_int64, f64p, C.c_int64, C.c_double,

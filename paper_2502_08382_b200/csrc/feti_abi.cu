@@ -25,6 +25,7 @@
 #include "feti_factor.h"
 #include "feti_implicit.h"
 #include "feti_kernels.h"
+#include "feti_pcpg.h"
 #include "feti_sparse.h"
 
 using namespace feti;
@@ -118,6 +119,8 @@ struct SubHost {
   double* d_U1 = nullptr;
   double* d_U2W = nullptr;
   int64_t* d_kdiag = nullptr;        // diagonal position of each row of K (rho on the device)
+  double *d_fproj = nullptr, *d_qtf = nullptr, *d_U2f = nullptr;   // device dual rhs (feti_enable_dual_rhs)
+  std::vector<double> h_qtf;
   double* d_rho = nullptr;
   std::vector<double> h_Q, h_U1;     // last kernel basis handed over and its U1 = B~ Q (async sources)
   int64_t f_tiles() const { return (int64_t)T32 * (T32 + 1) / 2; }
@@ -154,6 +157,7 @@ struct feti_ctx {
   int4* d_cent = nullptr;
   double *d_p = nullptr, *d_q = nullptr;
   int apply_nw = 8;
+  int apply_sb = 32;                 // apply super-block edge (32x32 tiles)
   feti_stats stats{};
   cudaEvent_t ev[8] = {};
   bool subdev_dirty = true;
@@ -191,6 +195,7 @@ struct feti_ctx {
   std::vector<std::pair<int, int>> wv_range[5];
   // sparse-factor route: per block column task ranges into the device lists
   bool sparse_factor = false;
+  bool dual_rhs = false;             // factor f' along (appended row) for d = B~ K_reg^-1 f
   SpSub* d_spsub = nullptr;
   SpInit* d_sp_init = nullptr;
   SpTask* d_sp_tasks = nullptr;
@@ -214,8 +219,18 @@ struct feti_ctx {
   // last scatter finished reading the previous values
   cudaEvent_t k_ready = nullptr, k_free = nullptr;
   bool k_pending = false;
+  bool k_early = false;              // Q or f' changed: sp_init reads them, so wait before it
   std::vector<int> sp_bad_init;
   bool sp_pending_check = false;   // pivots of the last factorize not yet checked
+  // device-native PCPG (feti_pcpg_solve): iteration vectors, coarse scratch,
+  // block partials, device scalars (+ a pinned host copy polled per graph)
+  double* pc_vec = nullptr;
+  double* pc_k = nullptr;
+  double* pc_bpart = nullptr;
+  PcpgScal* pc_sc = nullptr;
+  PcpgScal* pc_sc_host = nullptr;
+  cudaGraphExec_t pc_graph[2] = {};
+  static constexpr int kPcpgGraphIters = 8;
   // lumped preconditioner (feti_set_preconditioner): a second descriptor table
   // whose F points at the preconditioner tiles, applied by the same kernels
   SubDev* d_subdev_p = nullptr;
@@ -346,7 +361,7 @@ int build_sparse_tasks(feti_ctx* c) {
     const std::vector<int>& wv = c->waves[g];
     const int b = (int)panels.size();
     for (int si : wv)
-      if (c->subs[si].sp_r > 0)
+      if (c->subs[si].sp_r > 0 || c->dual_rhs)
         for (int p = 0; p < c->subs[si].P; ++p) panels.push_back(make_int2(si, p));
     c->sp_corr_rng[g] = {b, (int)panels.size() - b};
     c->sp_sub_rng[g] = {wv.empty() ? 0 : wv.front(), (int)wv.size()};
@@ -437,7 +452,8 @@ int factorize_sparse(feti_ctx* c) {
   for (int si = 0; si < ns; ++si) {
     SubHost& s = c->subs[si];
     ss[si] = SpSub{s.d_pool, s.d_tmap, s.d_perm, s.d_iperm, s.d_kptr, s.d_kind, s.d_kdata, s.d_Q, s.d_kdiag,
-                   s.d_fix, s.d_U1, s.d_U2W, s.d_rho, s.sp.T, s.sp.Tq, (int)s.sp_n, s.sp_r, s.sp_r, (int)s.n};
+                   s.d_fix, s.d_U1, s.d_U2W, s.d_rho, s.d_fproj, s.d_qtf, s.d_U2f, c->dual_rhs ? s.sp_r : -1,
+                   s.sp.T, s.sp.Tq, (int)s.sp_n, s.sp_r, s.sp_r, (int)s.n};
     s.src = SRC_TILES;
   }
   CUDA_TRY(cudaMemcpyAsync(c->d_spsub, ss.data(), ns * sizeof(SpSub), cudaMemcpyHostToDevice, st));
@@ -447,9 +463,14 @@ int factorize_sparse(feti_ctx* c) {
   c->sp_bad_init.assign(ns, 1 << 30);
   CUDA_TRY(cudaMemcpyAsync(c->d_bad, c->sp_bad_init.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaEventRecord(c->sp_ev[0], st));
+  // the step's K values were copied on copy_stream while the pool was being
+  // zeroed; a changed kernel basis or force (read by the pool init itself)
+  // has to land before it
+  if (c->k_pending && c->k_early) {
+    CUDA_TRY(cudaStreamWaitEvent(st, c->k_ready, 0));
+    c->k_pending = c->k_early = false;
+  }
   launch_sp_init(c->d_sp_init, c->n_sp_init, c->d_spsub, st);
-  // the step's K values / kernel bases were copied on copy_stream while the
-  // pool was being zeroed
   if (c->k_pending) {
     CUDA_TRY(cudaStreamWaitEvent(st, c->k_ready, 0));
     c->k_pending = false;
@@ -561,6 +582,7 @@ int stiffness_values_async(feti_ctx* c, SubHost& s, const double* data, const do
       if ((rc = dev_alloc(c, (void**)&s.d_U2W, rows * 2 * r * 8, true))) return rc;
     }
     CUDA_TRY(cudaMemcpyAsync(s.d_Q, s.h_Q.data(), (size_t)(n * r) * 8, cudaMemcpyHostToDevice, c->copy_stream));
+    c->k_early = true;
     CUDA_TRY(cudaMemcpyAsync(s.d_U1, s.h_U1.data(), rows * r * 8, cudaMemcpyHostToDevice, c->copy_stream));
   } else if (r > 0 && s.h_Q.empty()) {
     return fail(FETI_ERR_ARG, "the first hand-over of a slot needs its kernel basis");
@@ -633,6 +655,9 @@ int feti_destroy(feti_ctx* c) {
   if (c->apply_done) cudaEventDestroy(c->apply_done);
   if (c->x_sum_done) cudaEventDestroy(c->x_sum_done);
   if (c->k_ready) cudaEventDestroy(c->k_ready);
+  for (auto& ge : c->pc_graph)
+    if (ge) cudaGraphExecDestroy(ge);
+  if (c->pc_sc_host) cudaFreeHost(c->pc_sc_host);
   if (c->k_free) cudaEventDestroy(c->k_free);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -731,7 +756,8 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     for (size_t i = 0; i < c->subs.size(); ++i) {
       SubHost& s = c->subs[i];
       if (!s.sp_pattern) return fail(FETI_ERR_LIFECYCLE, "slot %zu has no sparse pattern", i);
-      sp_symbolic(s.sp_n, s.sp_kptr.data(), s.sp_kind.data(), s.sp_iperm.data(), s.n, s.sp_r, s.smin, &s.sp);
+      sp_symbolic(s.sp_n, s.sp_kptr.data(), s.sp_kind.data(), s.sp_iperm.data(), s.n, s.sp_r, s.smin, &s.sp,
+                  c->dual_rhs);
       need += (size_t)s.sp.ntiles * TILE * 8;
     }
   for (auto& s : c->subs) {
@@ -770,6 +796,13 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
       s.d_tiles = s.d_pool + (size_t)s.sp.trail_base * TILE;
       if ((rc = upload(c, &s.d_tmap, s.sp.tmap))) return rc;
       if ((rc = upload(c, &s.d_fix, s.sp_fix))) return rc;
+      if (c->dual_rhs) {
+        if ((rc = dev_alloc(c, (void**)&s.d_fproj, (size_t)std::max<int64_t>(s.sp_n, 1) * 8, true))) return rc;
+        if ((rc = dev_alloc(c, (void**)&s.d_qtf, (size_t)std::max(s.sp_r, 1) * 8, true))) return rc;
+        if ((rc = dev_alloc(c, (void**)&s.d_U2f, (size_t)std::max(s.P, 1) * TB * 8, true))) return rc;
+        CUDA_TRY(cudaMemset(s.d_fproj, 0, (size_t)std::max<int64_t>(s.sp_n, 1) * 8));
+        CUDA_TRY(cudaMemset(s.d_qtf, 0, (size_t)std::max(s.sp_r, 1) * 8));
+      }
     } else if ((rc = dev_alloc(c, (void**)&s.d_tiles, (size_t)std::max<int64_t>(s.l_tiles(), 1) * TILE * 8, false))) {
       return rc;
     }
@@ -901,6 +934,21 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   // (persistent CTAs), each range into segments at super-block bounds.  The
   // kernel's accumulators span one super-block (<= 2 x SBE multipliers), so
   // neither the warp count nor the subdomain size is limited by shared memory.
+  // warps per apply CTA: bytes in flight bound the kernel (two 8 KB tile
+  // loads per warp); the super-block edge is the largest the warps'
+  // accumulators fit, balanced so the largest subdomain splits into equal
+  // blocks (fewer, larger segments: less per-segment refill and combine)
+  c->apply_nw = 8;
+  if (const char* wenv = getenv("FETI_APPLY_WARPS")) c->apply_nw = std::max(1, std::min(APPLY_MAX_WARPS, atoi(wenv)));
+  {
+    int maxT32 = 1;
+    for (auto& s : c->subs) maxT32 = std::max(maxT32, s.T32);
+    const int cap = std::min(apply_max_sb(c->apply_nw), 64);
+    const int nbk = (maxT32 + cap - 1) / cap;
+    c->apply_sb = (maxT32 + nbk - 1) / nbk;
+    if (const char* senv = getenv("FETI_APPLY_SB")) c->apply_sb = std::max(1, std::min(cap, atoi(senv)));
+  }
+  const int SB = c->apply_sb, SBE = SB * AT;
   struct Blk { int sub, I, J; int64_t tiles; };
   std::vector<Blk> blks;
   int64_t total_tiles = 0;
@@ -987,10 +1035,6 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   }
   cptr[c->n_mult] = (int)cent.size();
 
-  // warps per apply CTA: bytes in flight bound the kernel (two 8 KB tile
-  // loads per warp); the accumulators no longer depend on m
-  c->apply_nw = 8;
-  if (const char* wenv = getenv("FETI_APPLY_WARPS")) c->apply_nw = std::max(1, std::min(APPLY_MAX_WARPS, atoi(wenv)));
 
   if ((rc = upload(c, &c->d_w_unpack, wu))) return rc;
   if ((rc = upload(c, &c->d_w_diag, wd))) return rc;
@@ -1302,7 +1346,7 @@ static int implicit_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStr
 // apply reads only finalize-time fields of it (F~ tiles, index maps).
 static int apply_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st, bool time_it) {
   if (time_it) CUDA_TRY(cudaEventRecord(c->ev[0], st));
-  launch_apply(c->apply_nw, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, d_p, st);
+  launch_apply(c->apply_nw, c->apply_sb, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, d_p, st);
   launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_ridx, c->d_part, d_q, st);
   CUDA_TRY(cudaGetLastError());
   if (time_it) CUDA_TRY(cudaEventRecord(c->ev[1], st));
@@ -1375,7 +1419,7 @@ int feti_precond_apply_device(feti_ctx* c, const double* d_w, double* d_out, voi
   if (!d_w || !d_out) return fail(FETI_ERR_ARG, "NULL vector");
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
-  launch_apply(c->apply_nw, c->d_subdev_p, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, d_w, st);
+  launch_apply(c->apply_nw, c->apply_sb, c->d_subdev_p, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, d_w, st);
   launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_ridx, c->d_part, d_out, st);
   CUDA_TRY(cudaGetLastError());
   return mark_apply(c, st);
@@ -1462,7 +1506,7 @@ int feti_apply_exchange_device(feti_ctx* c, const double* d_p, double* d_q, void
   // finished first (feti_exchange.cu header): order it explicitly, whatever
   // stream the caller used last time
   CUDA_TRY(cudaStreamWaitEvent(st, c->x_sum_done, 0));
-  launch_apply(c->apply_nw, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, d_p, st);
+  launch_apply(c->apply_nw, c->apply_sb, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, d_p, st);
   XchgArgs a{c->d_x_peers, c->d_x_touched, c->d_cptr, c->d_cent, c->d_ridx, c->d_part, c->d_x_done,
              c->d_x_error, c->x_epoch + 1, c->x_n_touched, (int)c->n_mult, c->x_rank, c->x_world};
   launch_exchange(a, d_q, st);
@@ -1635,6 +1679,56 @@ int feti_set_stiffness_values(feti_ctx* c, int64_t nslots, const int64_t* slots,
     int rc = stiffness_values_async(c, s, data[i], Q ? Q[i] : nullptr);
     if (rc) return rc;
   }
+  return FETI_OK;
+}
+
+int feti_enable_dual_rhs(feti_ctx* c) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (c->finalized) return fail(FETI_ERR_LIFECYCLE, "the dual right-hand side must be enabled before finalize");
+  if (!c->sparse_factor) return fail(FETI_ERR_ARG, "the device dual right-hand side needs the sparse-factor route");
+  c->dual_rhs = true;
+  return FETI_OK;
+}
+
+int feti_set_forces(feti_ctx* c, int64_t nslots, const int64_t* slots, const double* const* fproj,
+                    const double* const* qtf) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->finalized || !c->dual_rhs) return fail(FETI_ERR_LIFECYCLE, "set_forces needs feti_enable_dual_rhs");
+  if (nslots < 0 || (nslots > 0 && (!slots || !fproj))) return fail(FETI_ERR_ARG, "bad force arguments");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (!c->k_pending) {
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->k_free, 0));   // the last init read the old values
+    c->k_pending = true;
+  }
+  for (int64_t i = 0; i < nslots; ++i) {
+    if (slots[i] < 0 || slots[i] >= (int64_t)c->subs.size() || !fproj[i]) return fail(FETI_ERR_ARG, "bad slot");
+    SubHost& s = c->subs[slots[i]];
+    CUDA_TRY(cudaMemcpyAsync(s.d_fproj, fproj[i], (size_t)s.sp_n * 8, cudaMemcpyHostToDevice, c->copy_stream));
+    c->k_early = true;
+    if (s.sp_r > 0) {
+      if (!qtf || !qtf[i]) return fail(FETI_ERR_ARG, "slot %lld needs Q^T f", (long long)slots[i]);
+      s.h_qtf.assign(qtf[i], qtf[i] + s.sp_r);
+      CUDA_TRY(cudaMemcpyAsync(s.d_qtf, s.h_qtf.data(), (size_t)s.sp_r * 8, cudaMemcpyHostToDevice, c->copy_stream));
+    }
+  }
+  CUDA_TRY(cudaEventRecord(c->k_ready, c->copy_stream));
+  return FETI_OK;
+}
+
+int feti_dual_rhs(feti_ctx* c, const double* cvec, double* d) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->dual_rhs) return fail(FETI_ERR_LIFECYCLE, "feti_dual_rhs needs feti_enable_dual_rhs");
+  if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "dual right-hand side before preprocess");
+  if (!d) return fail(FETI_ERR_ARG, "d is NULL");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  int rc;
+  if ((rc = wait_applies(c))) return rc;
+  if (cvec) CUDA_TRY(cudaMemcpyAsync(c->d_p, cvec, (size_t)c->n_mult * 8, cudaMemcpyHostToDevice, st));
+  launch_sp_dual_rhs(c->d_spsub, (int)c->n_mult, c->d_cptr, c->d_cent, cvec ? c->d_p : nullptr, c->d_q, st);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(d, c->d_q, (size_t)c->n_mult * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
   return FETI_OK;
 }
 
@@ -1818,6 +1912,151 @@ int feti_coarse_apply_device(feti_ctx* c, const double* d_v, double* d_out, void
   launch_coarse(c->nk, c->d_cinv, d_v, c->d_kz, st);
   launch_project((int)c->n_mult, c->d_cptr, c->d_cent, c->d_coarse, c->d_kz, nullptr, -1.0, d_out, st);
   CUDA_TRY(cudaGetLastError());
+  return FETI_OK;
+}
+
+int feti_pcpg_solve(feti_ctx* c, const double* d, const double* e, double tol, int64_t maxit, int precond,
+                    double* lam, int64_t* iterations, double* rel_residual) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (!c->assembled) return fail(FETI_ERR_LIFECYCLE, "PCPG before preprocess");
+  if (c->implicit) return fail(FETI_ERR_ARG, "the device PCPG runs on the explicit operator");
+  if (!c->d_coarse) return fail(FETI_ERR_LIFECYCLE, "PCPG before feti_coarse_setup");
+  if (precond != 0 && precond != 1) return fail(FETI_ERR_ARG, "precond must be 0 (none) or 1 (lumped)");
+  if (precond == 1 && (!c->d_subdev_p || c->n_precond_set != (int)c->subs.size()))
+    return fail(FETI_ERR_LIFECYCLE, "lumped PCPG before feti_set_preconditioner for every slot");
+  if (!d || (c->nk > 0 && !e) || !lam || !(tol >= 0.0)) return fail(FETI_ERR_ARG, "bad PCPG arguments");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int n = (int)c->n_mult, nk = c->nk;
+  int rc;
+  if (!c->pc_vec) {
+    if ((rc = dev_alloc(c, (void**)&c->pc_vec, (size_t)8 * std::max(n, 1) * 8, true))) return rc;
+    if ((rc = dev_alloc(c, (void**)&c->pc_k, (size_t)4 * std::max(nk, 1) * 8, true))) return rc;
+    if ((rc = dev_alloc(c, (void**)&c->pc_bpart, pcpg_bpart_doubles(n, nk) * 8, true))) return rc;
+    if ((rc = dev_alloc(c, (void**)&c->pc_sc, sizeof(PcpgScal), true))) return rc;
+    CUDA_TRY(cudaMemset(c->pc_sc, 0, sizeof(PcpgScal)));
+    CUDA_TRY(cudaHostAlloc((void**)&c->pc_sc_host, sizeof(PcpgScal), cudaHostAllocDefault));
+  }
+  double* v = c->pc_vec;
+  const size_t N = (size_t)std::max(n, 1);
+  PcpgDev P{};
+  P.n_mult = n;
+  P.nk = nk;
+  P.ncols = nk;
+  P.cptr = c->d_cptr;
+  P.cent = c->d_cent;
+  P.ridx = c->d_ridx;
+  P.part = c->d_part;
+  P.cs = c->d_coarse;
+  P.kcols = c->d_kcols;
+  P.cinv = c->d_cinv;
+  double* dd = v + 7 * N;
+  P.d = dd;
+  P.lam = v;
+  P.r = v + N;
+  P.p = v + 2 * N;
+  P.q = v + 3 * N;
+  P.y = v + 4 * N;
+  P.w = v + 5 * N;
+  P.z = v + 6 * N;
+  const size_t K = (size_t)std::max(nk, 1);
+  P.kv = c->pc_k;
+  P.kz = c->pc_k + K;
+  P.kv2 = c->pc_k + 2 * K;
+  P.kz2 = c->pc_k + 3 * K;
+  P.bpart = c->pc_bpart;
+  P.sc = c->pc_sc;
+  cudaStream_t st = c->stream;
+  if ((rc = wait_applies(c))) return rc;
+  CUDA_TRY(cudaMemcpyAsync(dd, d, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  if (nk > 0) CUDA_TRY(cudaMemcpyAsync(P.kv, e, (size_t)nk * 8, cudaMemcpyHostToDevice, st));
+  // lam0 = G (G^T G)^-1 e (feasible_start, solver.py:121-123)
+  launch_coarse(nk, c->d_cinv, P.kv, P.kz, st);
+  launch_project(n, c->d_cptr, c->d_cent, c->d_coarse, P.kz, nullptr, -1.0, P.lam, st);
+  // r = d - F lam
+  launch_apply(c->apply_nw, c->apply_sb, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, P.lam, st);
+  launch_reduce(n, c->d_cptr, c->d_cent, c->d_ridx, c->d_part, P.q, st);
+  launch_pcpg_sub(n, dd, P.q, P.r, st);
+  // w = P r, z = M w, y = P z
+  launch_gtx(c->d_coarse, c->d_kcols, nk, P.r, P.kv, st);
+  launch_coarse(nk, c->d_cinv, P.kv, P.kz, st);
+  launch_project(n, c->d_cptr, c->d_cent, c->d_coarse, P.kz, P.r, 1.0, P.w, st);
+  const double* zsrc = P.w;
+  if (precond == 1) {
+    launch_apply(c->apply_nw, c->apply_sb, c->d_subdev_p, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, P.w, st);
+    launch_reduce(n, c->d_cptr, c->d_cent, c->d_ridx, c->d_part, P.z, st);
+    zsrc = P.z;
+  }
+  launch_gtx(c->d_coarse, c->d_kcols, nk, zsrc, P.kv, st);
+  launch_coarse(nk, c->d_cinv, P.kv, P.kz, st);
+  launch_project(n, c->d_cptr, c->d_cent, c->d_coarse, P.kz, zsrc, 1.0, P.y, st);
+  launch_pcpg_init_dots(P, st);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(c->pc_sc_host, c->pc_sc, sizeof(PcpgScal), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  PcpgScal h = *c->pc_sc_host;
+  const int64_t cap = maxit > 0 ? maxit : (int64_t)n;
+  c->stats.pcpg_iterations = 0;
+  c->stats.ms_pcpg = 0.0;
+  if (h.w0 <= 1e-14 * std::max(1.0, h.dnorm)) {   // roundoff guard (solver.py:233-241)
+    CUDA_TRY(cudaMemcpy(lam, P.lam, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    if (iterations) *iterations = 0;
+    if (rel_residual) *rel_residual = 0.0;
+    return FETI_OK;
+  }
+  h.tolw0 = tol * h.w0;
+  h.maxit = cap;
+  *c->pc_sc_host = h;
+  CUDA_TRY(cudaMemcpyAsync(c->pc_sc, c->pc_sc_host, sizeof(PcpgScal), cudaMemcpyHostToDevice, st));
+  // the iteration body, kPcpgGraphIters iterations per graph (no-ops once done)
+  cudaGraphExec_t& ge = c->pc_graph[precond];
+  if (!ge) {
+    CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    const int* done = &c->pc_sc->done;
+    const double* beta = &c->pc_sc->beta;
+    for (int it = 0; it < feti_ctx::kPcpgGraphIters; ++it) {
+      launch_apply(c->apply_nw, c->apply_sb, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, P.p, st,
+                   P.y, beta, done);
+      launch_pcpg_reduce_pq(P, st);
+      launch_pcpg_gtx_r(P, st);
+      if (precond == 0) {
+        launch_pcpg_gtx_w(P, st);
+        launch_pcpg_update(P, 0, st);
+      } else {
+        launch_pcpg_update(P, 1, st);
+        launch_apply(c->apply_nw, c->apply_sb, c->d_subdev_p, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, P.w,
+                     st, nullptr, nullptr, done);
+        launch_reduce(n, c->d_cptr, c->d_cent, c->d_ridx, c->d_part, P.z, st);
+        launch_pcpg_gtx_x(P, P.z, st);
+        launch_pcpg_update(P, 2, st);
+      }
+    }
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(cudaStreamEndCapture(st, &graph));
+    CUDA_TRY(cudaGraphInstantiate(&ge, graph, 0));
+    CUDA_TRY(cudaGraphDestroy(graph));
+  }
+  CUDA_TRY(cudaEventRecord(c->ev[0], st));
+  for (;;) {
+    CUDA_TRY(cudaGraphLaunch(ge, st));
+    CUDA_TRY(cudaMemcpyAsync(c->pc_sc_host, c->pc_sc, sizeof(PcpgScal), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (c->pc_sc_host->done) break;
+  }
+  CUDA_TRY(cudaEventRecord(c->ev[1], st));
+  CUDA_TRY(cudaMemcpyAsync(lam, P.lam, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  h = *c->pc_sc_host;
+  c->stats.ms_pcpg = ms;
+  c->stats.pcpg_iterations = h.k;
+  if (iterations) *iterations = h.k;
+  if (rel_residual) *rel_residual = h.w0 > 0 ? h.wn / h.w0 : 0.0;
+  if (h.status == PCPG_BREAKDOWN)
+    return fail(FETI_ERR_BREAKDOWN, "p^T F p = %.3e at iteration %lld", h.pq, (long long)h.k);
+  if (h.status == PCPG_MAXIT)
+    return fail(FETI_ERR_NOT_CONVERGED, "PCPG did not reach tol %.1e in %lld iterations (relative residual %.3e)",
+                tol, (long long)h.k, h.w0 > 0 ? h.wn / h.w0 : 0.0);
   return FETI_OK;
 }
 

@@ -19,9 +19,6 @@ constexpr int SLICE = KS * TB;     // doubles per slice (32 KB)
 constexpr int AT = 32;             // apply-side tile edge (32x32 = 8 KB)
 constexpr int ATILE = AT * AT;
 constexpr int BIG_ROW = 1 << 30;   // sentinel first-row of padding columns
-constexpr int SB = 32;             // apply super-block edge in 32x32 tiles (1024 multipliers)
-constexpr int SBE = SB * AT;
-
 // One apply work segment: tiles [t0, t1) (row-major) of the super-block
 // (I, J), I <= J, of subdomain `sub`'s packed upper triangle of 32x32 tiles.
 // Partial sums: rows of block I at part[out_r ...], columns of block J at

@@ -548,22 +548,31 @@ __device__ __forceinline__ void apply_tile_compute(double (&f)[32], int li, int 
 }
 
 // Tile cursor inside a super-block: h x w tiles (rectangle), or for a
-// diagonal block the upper triangle of h x h tiles, row-major.
+// diagonal block the upper triangle of h x h tiles, row-major.  Located once
+// per segment, then advanced incrementally (no division or square root on
+// the path that computes the next load's address).
 struct SbCursor {
   int li, lj;
   __device__ __forceinline__ void locate(int t, int h, int w, bool diag) {
+    li = 0;
+    lj = diag ? 0 : 0;
+    advance(t, h, w, diag);
+  }
+  __device__ __forceinline__ void advance(int step, int h, int w, bool diag) {
     if (!diag) {
-      li = t / w;
-      lj = t - li * w;
+      lj += step;
+      while (lj >= w && li < h) {
+        lj -= w;
+        ++li;
+      }
       return;
     }
-    // row li starts at li*h - li*(li-1)/2
-    const double b = 2.0 * h + 1.0;
-    int r = (int)((b - sqrt(b * b - 8.0 * t)) * 0.5);
-    while (r > 0 && r * h - r * (r - 1) / 2 > t) --r;
-    while ((r + 1) * h - (r + 1) * r / 2 <= t) ++r;
-    li = r;
-    lj = r + (t - (r * h - r * (r - 1) / 2));
+    int rem = (lj - li) + step;
+    while (li < h && rem >= h - li) {
+      rem -= h - li;
+      ++li;
+    }
+    lj = li + rem;
   }
 };
 
@@ -572,60 +581,79 @@ __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict
                                                         const ApplySeg* __restrict__ segs,
                                                         const int* __restrict__ seg_ptr,
                                                         double* __restrict__ part,
-                                                        const double* __restrict__ p) {
+                                                        const double* __restrict__ p,
+                                                        const double* __restrict__ py,
+                                                        const double* __restrict__ pbeta,
+                                                        const int* __restrict__ done, int sb) {
+  // PCPG mode (py != nullptr): the gathered vector is p_new = y + beta p
+  // (fma, bit-identical to the reduce-side update, feti_pcpg.cu); `done`
+  // turns the launch into a no-op once the device loop has finished
+  if (done && *done) return;
+  const double beta = py ? *pbeta : 0.0;
+  auto pval = [&](int gi) -> double { return py ? fma(beta, __ldg(p + gi), __ldg(py + gi)) : __ldg(p + gi); };
   extern __shared__ double asmem[];
+  const int SBE = sb * AT;              // multipliers per super-block edge
   double* spr = asmem;                  // p of the block's rows
   double* spc = asmem + SBE;            // p of the block's columns (off-diagonal blocks)
   double* acc = asmem + 2 * SBE;        // warp w: rows at acc + 2 w SBE, columns at + SBE
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // accumulators are zeroed once; each combine re-zeroes what it read
+  for (int a = tid; a < NW * 2 * SBE; a += NW * 32) acc[a] = 0.0;
   for (int sg = seg_ptr[blockIdx.x]; sg < seg_ptr[blockIdx.x + 1]; ++sg) {
     const ApplySeg w = segs[sg];
     const SubDev& S = subs[w.sub];
     const int T32 = S.T32;
-    const int r0 = w.I * SB, c0 = w.J * SB;
-    const int h = min(SB, T32 - r0), wd = min(SB, T32 - c0);
+    const int r0 = w.I * sb, c0 = w.J * sb;
+    const int h = min(sb, T32 - r0), wd = min(sb, T32 - c0);
     const bool diag = w.I == w.J;
+    const double* Fb = S.F;
+    auto tile_ptr = [&](const SbCursor& c) -> const double* {
+      return Fb + apply_tile_index(r0 + c.li, c0 + c.lj, T32) * ATILE;
+    };
+    int tt = w.t0 + warp;
+    const int t1 = w.t1;
+    // cu: the tile being reduced; ld: the tile two loads ahead.  The first
+    // two tile loads are issued before the p gather so their latency
+    // overlaps it (each segment restarts the pipeline)
+    SbCursor cu, ld;
+    cu.locate(tt, h, wd, diag);
+    ld = cu;
+    double fa[32], fb[32], fc[32];
+    if (tt < t1) apply_tile_load(fa, tile_ptr(ld), lane);
+    ld.advance(NW, h, wd, diag);
+    if (tt + NW < t1) apply_tile_load(fb, tile_ptr(ld), lane);
+    ld.advance(NW, h, wd, diag);
     __syncthreads();   // the previous segment's combine is done with smem
     for (int a = tid; a < h * AT; a += NW * 32) {
       const int gi = S.gids_sorted[r0 * AT + a];
-      spr[a] = gi >= 0 ? __ldg(p + gi) : 0.0;
+      spr[a] = gi >= 0 ? pval(gi) : 0.0;
     }
     if (!diag)
       for (int a = tid; a < wd * AT; a += NW * 32) {
         const int gi = S.gids_sorted[c0 * AT + a];
-        spc[a] = gi >= 0 ? __ldg(p + gi) : 0.0;
+        spc[a] = gi >= 0 ? pval(gi) : 0.0;
       }
-    for (int a = tid; a < NW * 2 * SBE; a += NW * 32) acc[a] = 0.0;
     __syncthreads();
     double* myr = acc + 2 * warp * SBE;
     double* myc = diag ? myr : myr + SBE;
     const double* pc = diag ? spr : spc;
-    const double* Fb = S.F;
-    auto tile_ptr = [&](int t) -> const double* {
-      SbCursor cu;
-      cu.locate(t, h, wd, diag);
-      return Fb + apply_tile_index(r0 + cu.li, c0 + cu.lj, T32) * ATILE;
-    };
-    int tt = w.t0 + warp;
-    const int t1 = w.t1;
-    double fa[32], fb[32], fc[32];
-    if (tt < t1) apply_tile_load(fa, tile_ptr(tt), lane);
-    if (tt + NW < t1) apply_tile_load(fb, tile_ptr(tt + NW), lane);
-    SbCursor cu;
     while (tt < t1) {
-      if (tt + 2 * NW < t1) apply_tile_load(fc, tile_ptr(tt + 2 * NW), lane);
-      cu.locate(tt, h, wd, diag);
+      if (tt + 2 * NW < t1) apply_tile_load(fc, tile_ptr(ld), lane);
+      ld.advance(NW, h, wd, diag);
       apply_tile_compute(fa, cu.li, cu.lj, !diag || cu.li != cu.lj, spr, pc, myr, myc, lane);
+      cu.advance(NW, h, wd, diag);
       tt += NW;
       if (tt >= t1) break;
-      if (tt + 2 * NW < t1) apply_tile_load(fa, tile_ptr(tt + 2 * NW), lane);
-      cu.locate(tt, h, wd, diag);
+      if (tt + 2 * NW < t1) apply_tile_load(fa, tile_ptr(ld), lane);
+      ld.advance(NW, h, wd, diag);
       apply_tile_compute(fb, cu.li, cu.lj, !diag || cu.li != cu.lj, spr, pc, myr, myc, lane);
+      cu.advance(NW, h, wd, diag);
       tt += NW;
       if (tt >= t1) break;
-      if (tt + 2 * NW < t1) apply_tile_load(fb, tile_ptr(tt + 2 * NW), lane);
-      cu.locate(tt, h, wd, diag);
+      if (tt + 2 * NW < t1) apply_tile_load(fb, tile_ptr(ld), lane);
+      ld.advance(NW, h, wd, diag);
       apply_tile_compute(fc, cu.li, cu.lj, !diag || cu.li != cu.lj, spr, pc, myr, myc, lane);
+      cu.advance(NW, h, wd, diag);
       tt += NW;
     }
     __syncthreads();
@@ -633,14 +661,20 @@ __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict
     for (int a = tid; a < h * AT; a += NW * 32) {
       double s = 0.0;
 #pragma unroll
-      for (int wi = 0; wi < NW; ++wi) s += acc[2 * wi * SBE + a];
+      for (int wi = 0; wi < NW; ++wi) {
+        s += acc[2 * wi * SBE + a];
+        acc[2 * wi * SBE + a] = 0.0;
+      }
       part[w.out_r + a] = s;
     }
     if (!diag)
       for (int a = tid; a < wd * AT; a += NW * 32) {
         double s = 0.0;
 #pragma unroll
-        for (int wi = 0; wi < NW; ++wi) s += acc[2 * wi * SBE + SBE + a];
+        for (int wi = 0; wi < NW; ++wi) {
+          s += acc[2 * wi * SBE + SBE + a];
+          acc[2 * wi * SBE + SBE + a] = 0.0;
+        }
         part[w.out_c + a] = s;
       }
   }
@@ -692,7 +726,7 @@ cudaError_t configure_kernels() {
       (const void*)apply_kernel<4>,  (const void*)apply_kernel<5>,  (const void*)apply_kernel<6>,
       (const void*)apply_kernel<7>,  (const void*)apply_kernel<8>};
   for (int w = 1; w <= APPLY_MAX_WARPS; ++w)
-    if ((e = cudaFuncSetAttribute(applies[w - 1], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem(w))))
+    if ((e = cudaFuncSetAttribute(applies[w - 1], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)))
       return e;
   return cudaSuccess;
 }
@@ -715,14 +749,17 @@ void launch_trsm_chain(const SubDev* subs, const int4* work, int nwork, cudaStre
 void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
   if (nwork > 0) syrk_kernel<<<nwork, PIPE_THREADS, pipe_smem(), st>>>(subs, work);
 }
-size_t apply_smem(int nw) { return (size_t)(2 + 2 * nw) * SBE * sizeof(double); }
+size_t apply_smem(int nw, int sb) { return (size_t)(2 + 2 * nw) * sb * AT * sizeof(double); }
 
-void launch_apply(int nw, const SubDev* subs, const ApplySeg* segs, const int* seg_ptr, int nctas, double* part,
-                  const double* p, cudaStream_t st) {
+int apply_max_sb(int nw) { return (int)((227 * 1024) / ((size_t)(2 + 2 * nw) * AT * sizeof(double))); }
+
+void launch_apply(int nw, int sb, const SubDev* subs, const ApplySeg* segs, const int* seg_ptr, int nctas,
+                  double* part, const double* p, cudaStream_t st, const double* py, const double* pbeta,
+                  const int* done) {
   if (nctas <= 0) return;
 #define FETI_APPLY_CASE(W) \
   case W:                  \
-    apply_kernel<W><<<nctas, W * 32, apply_smem(W), st>>>(subs, segs, seg_ptr, part, p); \
+    apply_kernel<W><<<nctas, W * 32, apply_smem(W, sb), st>>>(subs, segs, seg_ptr, part, p, py, pbeta, done, sb); \
     break;
   switch (nw) {
     FETI_APPLY_CASE(8)

@@ -16,9 +16,13 @@ void launch_block_scale(const SubDev* subs, const int4* work, int nwork, cudaStr
 void launch_trsm_chain(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
 void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
 constexpr int APPLY_MAX_WARPS = 8;   // 3 tile buffers x 32 doubles: > 8 warps spill
-size_t apply_smem(int nw);
-void launch_apply(int nw, const SubDev* subs, const ApplySeg* segs, const int* seg_ptr, int nctas, double* part,
-                  const double* p, cudaStream_t st);
+size_t apply_smem(int nw, int sb);
+int apply_max_sb(int nw);   // largest super-block edge (tiles) whose accumulators fit 227 KB
+// sb: super-block edge in 32x32 tiles (the segments' blocking, chosen at finalize);
+// py/pbeta/done: PCPG mode (gather p_new = y + beta p; no-op once *done)
+void launch_apply(int nw, int sb, const SubDev* subs, const ApplySeg* segs, const int* seg_ptr, int nctas,
+                  double* part, const double* p, cudaStream_t st, const double* py = nullptr,
+                  const double* pbeta = nullptr, const int* done = nullptr);
 void launch_reduce(int n_mult, const int* cptr, const int4* cent, const int64_t* ridx, const double* part,
                    double* q, cudaStream_t st);
 

@@ -1,0 +1,47 @@
+// Device-native PCPG kernels (feti_pcpg.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "feti_coarse.h"
+
+namespace feti {
+
+enum { PCPG_RUNNING = 0, PCPG_CONVERGED = 1, PCPG_BREAKDOWN = 2, PCPG_MAXIT = 3 };
+
+// device scalars of one solve (also read by the host once per graph launch)
+struct PcpgScal {
+  double wy, w0, tolw0, delta, beta, pq, wn, ww, dnorm;
+  long long k, maxit;
+  int status, done;
+  unsigned cnt[4];   // last-block counters (reset by the last block)
+};
+
+struct PcpgDev {
+  int n_mult, nk, ncols, pad_;
+  // apply partials (reduce_kernel's layout) and the coarse space
+  const int* cptr;
+  const int4* cent;
+  const int64_t* ridx;
+  const double* part;
+  const CoarseSub* cs;
+  const int2* kcols;
+  const double* cinv;
+  const double* d;
+  // iteration vectors
+  double *lam, *r, *p, *q, *y, *w, *z;
+  double *kv, *kz, *kv2, *kz2;
+  double* bpart;
+  PcpgScal* sc;
+};
+
+void launch_pcpg_sub(int n, const double* a, const double* b, double* out, cudaStream_t st);
+void launch_pcpg_init_dots(const PcpgDev& P, cudaStream_t st);
+void launch_pcpg_reduce_pq(const PcpgDev& P, cudaStream_t st);
+void launch_pcpg_gtx_r(const PcpgDev& P, cudaStream_t st);
+void launch_pcpg_gtx_w(const PcpgDev& P, cudaStream_t st);
+void launch_pcpg_gtx_x(const PcpgDev& P, const double* x, cudaStream_t st);
+void launch_pcpg_update(const PcpgDev& P, int mode, cudaStream_t st);
+size_t pcpg_bpart_doubles(int n_mult, int ncols);
+
+}  // namespace feti

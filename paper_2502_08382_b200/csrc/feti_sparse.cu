@@ -50,7 +50,12 @@ __global__ void __launch_bounds__(256) sp_init_kernel(const SpInit* __restrict__
     const int64_t dof = j < npos ? S.perm[j] : -1;
     double v = 0.0;
     if (qrow) {
-      if (w.L < S.T && il < r && dof >= 0) v = S.Q[dof * r + il];
+      if (w.L < S.T && dof >= 0) {
+        if (il < r)
+          v = S.Q[dof * r + il];
+        else if (il == S.frow)
+          v = S.fproj[dof];
+      }
     } else if (w.K == w.L && il == jl && dof < 0) {
       v = 1.0;   // identity rows at padding positions keep the diagonal blocks SPD
     }
@@ -237,6 +242,7 @@ __global__ void __launch_bounds__(U2_GROUPS * TB) sp_u2_kernel(const SubDev* __r
   const SubDev& S = subs[pc.x];
   const SpSub& Q = ss[pc.x];
   const int c = pc.y, col = threadIdx.x & (TB - 1), rg = threadIdx.x >> 7, r = Q.r;
+  const int nr = Q.frow >= 0 ? Q.frow + 1 : r;   // rows of y used: Q columns, then f' (device dual rhs)
   const int a = c * TB + col;
   const int T = Q.T;
   __shared__ double Cm[MAXR * MAXR];
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(U2_GROUPS * TB) sp_u2_kernel(const SubDev* __r
       const double x2 = xrow_ptr(S, c, row2)[col ^ ((row2 & 3) << 2)];
 #pragma unroll
       for (int q = 0; q < MAXR; ++q)
-        if (q < r) {
+        if (q < nr) {
           acc[q] = fma(x, yt[swz(il, q)], acc[q]);
           acc2[q] = fma(x2, yt[swz(il + U2_GROUPS, q)], acc2[q]);
         }
@@ -268,16 +274,22 @@ __global__ void __launch_bounds__(U2_GROUPS * TB) sp_u2_kernel(const SubDev* __r
   }
 #pragma unroll
   for (int q = 0; q < MAXR; ++q)
-    if (q < r) red[rg][q][col] = acc[q] + acc2[q];
+    if (q < nr) red[rg][q][col] = acc[q] + acc2[q];
   __syncthreads();
   if (rg != 0) return;
 #pragma unroll
   for (int q = 0; q < MAXR; ++q) {
     double v = 0.0;
-    if (q < r)
+    if (q < nr)
       for (int g2 = 0; g2 < U2_GROUPS; ++g2) v += red[g2][q][col];
     acc[q] = (a < S.m) ? v : 0.0;
   }
+  if (Q.frow >= 0) {
+#pragma unroll
+    for (int q = 0; q < MAXR; ++q)
+      if (q == Q.frow) Q.U2f[a] = acc[q];   // X^T y_f = B~ K_s^-1 f'
+  }
+  if (r == 0) return;
   double* out = Q.U2W + (size_t)a * 2 * r;
   const double* u1 = Q.U1 + (size_t)a * r;
   for (int q = 0; q < r; ++q) {
@@ -317,14 +329,45 @@ __global__ void __launch_bounds__(256) sp_correct_kernel(const SubDev* __restric
 }
 
 
+// d[g] = sum_(s,a) [ (X^T y_f)_a - U1_a . (y^T y_f) + U1_a . (Q^T f) / rho ] - c[g]
+// with K_reg^-1 = Pi K_s^-1 Pi + rho^-1 Q Q^T (Pi = I - Q Q^T, f' = Pi f):
+//   B~ K_reg^-1 f = B~ K_s^-1 f' - U1 Q^T K_s^-1 f' + rho^-1 U1 Q^T f,
+//   Q^T K_s^-1 f' = y^T y_f = -tile(T, T)[q][frow].  Contributions in the
+// reference's gather order (assemble_dual_system, solver.py:141-143).
+__global__ void __launch_bounds__(256) sp_dual_rhs_kernel(const SpSub* __restrict__ ss, int n_mult,
+                                                          const int* __restrict__ cptr, const int4* __restrict__ cent,
+                                                          const double* __restrict__ c, double* __restrict__ d) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_mult) return;
+  double acc = 0.0;
+  for (int e = cptr[g]; e < cptr[g + 1]; ++e) {
+    const int4 ce = cent[e];
+    const SpSub& S = ss[ce.w];
+    const int a = ce.x, r = S.r;
+    double v = S.U2f[a];
+    if (r > 0) {
+      const double* cq = S.pool + (size_t)S.tmap[S.T * S.Tq + S.T] * TILE;
+      const double irho = 1.0 / *S.rho;
+      double corr = 0.0;
+      for (int q = 0; q < r; ++q) {
+        const double yyf = -cq[swz(S.frow, q)];
+        corr = fma(S.U1[(size_t)a * r + q], irho * S.qtf[q] - yyf, corr);
+      }
+      v += corr;
+    }
+    acc += v;
+  }
+  d[g] = acc - (c ? c[g] : 0.0);
+}
+
 // ---------------------------------------------------------------------------
 // host: block symbolic factorization and task lists
 // ---------------------------------------------------------------------------
 void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* iperm, int64_t npos,
-                 int r, int smin, SpPlan* out) {
+                 int r, int smin, SpPlan* out, bool extra_row) {
   SpPlan& P = *out;
   const int T = (int)((npos + TB - 1) / TB);
-  const int Tq = T + (r > 0 ? 1 : 0);
+  const int Tq = T + ((r > 0 || extra_row) ? 1 : 0);
   P.T = T;
   P.Tq = Tq;
   P.smin = smin = std::min(std::max(smin, 0), T);
@@ -338,7 +381,7 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
     }
   for (int J = smin; J < T; ++J)
     for (int I = J + 1; I < T; ++I) cs[J][I] = 1;     // dense interface block
-  if (r > 0)
+  if (Tq > T)
     for (int J = 0; J < T; ++J) cs[J][T] = 1;         // (P Q)^T row: y is dense
   // block fill along the elimination tree: struct(parent) >= struct(k) \ {parent}
   for (int k = 0; k < T; ++k) {
@@ -398,7 +441,7 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
   // slots: everything outside the trailing triangle first, then the trailing
   // triangle in the assembly's tri_index order
   P.tmap.assign((size_t)Tq * Tq, -1);
-  auto stored = [&](int I, int J) { return (I == J && J < T) || (J < T && I > J && cs[J][I]) || (I == T && J == T && r > 0); };
+  auto stored = [&](int I, int J) { return (I == J && J < T) || (J < T && I > J && cs[J][I]) || (I == T && J == T && Tq > T); };
   auto trailing = [&](int I, int J) { return I < T && J >= smin; };
   int64_t ns = 0;
   for (int J = 0; J < Tq; ++J)
@@ -440,7 +483,7 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
           ++v;
         }
       }
-      const double tfi = (i == T && r > 0) ? tf / 16.0 : tf;   // thin (P Q)^T row tiles
+      const double tfi = (i == T && Tq > T) ? tf / 16.0 : tf;   // thin (P Q)^T row tiles
       if (!pr.empty()) {
         P.flops_exec += tfi * pr.size();
         P.acc[j].emplace_back(P.tmap[(size_t)i * Tq + j], std::move(pr));
@@ -486,6 +529,11 @@ void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaSt
 
 void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st) {
   if (nd > 0) sp_potrf_kernel<<<nd, 256, sp_potrf_smem(), st>>>(d, bad);
+}
+
+void launch_sp_dual_rhs(const SpSub* ss, int n_mult, const int* cptr, const int4* cent, const double* c, double* d,
+                        cudaStream_t st) {
+  if (n_mult > 0) sp_dual_rhs_kernel<<<(n_mult + 255) / 256, 256, 0, st>>>(ss, n_mult, cptr, cent, c, d);
 }
 
 void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int sub0, int nsub,

@@ -27,6 +27,10 @@ struct SpSub {
   const double* U1;         // P*128 x r: sign_a * Q[dof_a], sorted column order
   double* U2W;              // P*128 x 2r: U2 = X^T y_b, then W = C U1 - U2
   double* rho;              // device scalar: trace(K) / n (sparse.py:450), written by sp_trace_kernel
+  const double* fproj;      // n: f' = (I - Q Q^T) f, factored along as row `frow` of the (P Q)^T block row
+  const double* qtf;        // r: Q^T f
+  double* U2f;              // P*128: X^T y_f = B~ K_s^-1 f' (sorted column order)
+  int frow;                 // -1, or the block-row-T row holding f' (= r)
   int T;                    // block rows of K_s (the Q block row is T when r > 0)
   int Tq;                   // T + (r > 0)
   int n, r, nfix;           // n: DOFs (rows of K)
@@ -78,8 +82,10 @@ struct SpPlan {
 // smin: first block row of the dense trailing triangle.
 // n DOFs (rows of K); positions live in [0, npos) (npos >= n: tile-aligned
 // orderings leave padding positions, which hold identity rows)
+// extra_row: keep the appended block row T even when r = 0 (it then carries
+// only the force row of the device dual right-hand side)
 void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const int64_t* iperm, int64_t npos,
-                 int r, int smin, SpPlan* out);
+                 int r, int smin, SpPlan* out, bool extra_row = false);
 
 cudaError_t configure_sparse();
 void launch_sp_init(const SpInit* w, int nw, const SpSub* ss, cudaStream_t st);
@@ -88,6 +94,10 @@ void launch_sp_scatter(const SpSub* ss, int sub0, int nsub, int max_n, cudaStrea
 void launch_sp_trace(const SpSub* ss, int nsub, cudaStream_t st);
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st);
 void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st);
+// d[g] = sum over (sub, a) contributions of B~ K_reg^-1 f, minus c[g]
+// (assemble_dual_system, solver.py:141-143), from U2f, U1, y^T y_f, rho, Q^T f
+void launch_sp_dual_rhs(const SpSub* ss, int n_mult, const int* cptr, const int4* cent, const double* c, double* d,
+                        cudaStream_t st);
 // after the assembly: U2/W per (sub, panel), then the rank-2r update of F~
 void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int sub0, int nsub,
                        int max_T32,

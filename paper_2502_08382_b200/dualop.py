@@ -194,7 +194,7 @@ class DualOperator:
     def __init__(self, matrices, constraints, layout, config: DualOpConfig, pool=None, workers: int = 1,
                  schur_cap: int = 2000, device: int | None = None, ordering: str = "rcm",
                  subdomains=None, pinned: bool = True, perms=None, factorization: str | None = None,
-                 stiffness=None, kernels=None, sparse_ordering: str = "auto"):
+                 stiffness=None, kernels=None, sparse_ordering: str = "auto", forces=None):
         matrices = list(matrices)
         if len(matrices) != len(constraints.per_subdomain):
             raise ValueError("one stiffness matrix per subdomain required")
@@ -202,6 +202,8 @@ class DualOperator:
             # SubdomainProblem inputs: K_i and ker K_i straight from the caller
             stiffness = [x.stiffness for x in matrices] if stiffness is None else stiffness
             kernels = [x.kernel for x in matrices] if kernels is None else kernels
+            if forces is None and all(hasattr(x, "force") for x in matrices):
+                forces = [x.force for x in matrices]
             factorization = factorization or "sparse"
             matrices = ([x.stiffness_reg for x in matrices] if factorization == "host"
                         else [_Shape(x.stiffness.shape) for x in matrices])
@@ -231,6 +233,10 @@ class DualOperator:
         self.kernels = None if kernels is None else list(kernels)
         if factorization in ("device", "sparse") and (self.stiffness is None or self.kernels is None):
             raise ValueError(f"{factorization} factorization needs stiffness= and kernels= per subdomain")
+        # loads f_i: on the sparse route they are factored along (an appended
+        # row) so that d = B~ K^+ f comes out of the device (dual_rhs)
+        self.forces = None if forces is None else list(forces)
+        self._forces_dev = None
         self.owned = (list(range(self.n_subdomains)) if subdomains is None
                       else sorted(int(s) for s in subdomains))
         if not (sparse_ordering in ("auto", "onion") or sparse_ordering.startswith("dissection:")):
@@ -400,6 +406,8 @@ class DualOperator:
             _call(self._lib.feti_enable_device_factorization(ctx))
         if self.factorization == "sparse":
             _call(self._lib.feti_enable_sparse_factorization(ctx))
+            if self.forces is not None:
+                _call(self._lib.feti_enable_dual_rhs(ctx))
             for sub in subs:
                 n, ip, ix, _ = fct.csr_arrays(self.stiffness[sub.index])
                 ip = np.ascontiguousarray(ip, np.int64)
@@ -442,7 +450,7 @@ class DualOperator:
                 sub.values = np.empty(n)
         return sub.values
 
-    def preprocess(self, matrices=None, stiffness=None, kernels=None) -> None:
+    def preprocess(self, matrices=None, stiffness=None, kernels=None, forces=None) -> None:
         """Numeric factorization (host, or device), then device assembly of every F~_i."""
         import time
 
@@ -455,6 +463,8 @@ class DualOperator:
             if matrices and all(_problem_like(x) for x in matrices):
                 stiffness = [x.stiffness for x in matrices] if stiffness is None else stiffness
                 kernels = [x.kernel for x in matrices] if kernels is None else kernels
+                if forces is None and all(hasattr(x, "force") for x in matrices):
+                    forces = [x.force for x in matrices]
                 matrices = ([x.stiffness_reg for x in matrices] if self.factorization == "host"
                             else [_Shape(x.stiffness.shape) for x in matrices])
             self.matrices = matrices
@@ -467,6 +477,8 @@ class DualOperator:
                 self.stiffness = list(stiffness)
             if kernels is not None:
                 self.kernels = list(kernels)
+            if forces is not None:
+                self.forces = list(forces)
             self._preprocess_device()
             return
 
@@ -576,6 +588,8 @@ class DualOperator:
             for sub in subs:
                 hand_over(sub)
             self._handed_over = True
+        if self.factorization == "sparse" and self.forces is not None:
+            self._hand_over_forces(subs, keep)
         t1 = time.perf_counter()
         self._factorize_and_assemble()
         del keep
@@ -583,6 +597,25 @@ class DualOperator:
         self.timings = {"stiffness_upload_s": t1 - t0, "device_factorization_and_assembly_s": t2 - t1,
                         "device_factorization_ms": self.stats()["ms_factorize"]}
         self.numeric_count += len(self._subs)
+
+    def _hand_over_forces(self, subs, keep) -> None:
+        """f' = (I - Q Q^T) f and Q^T f per slot (O(n r) on the host), factored
+        along with K_s so the dual right-hand side needs no solve_local."""
+        ns = len(subs)
+        slots = np.empty(ns, np.int64)
+        fptr = (C.c_void_p * ns)()
+        qptr = (C.c_void_p * ns)()
+        for k, sub in enumerate(subs):
+            f = np.asarray(self.forces[sub.index], dtype=np.float64)
+            q = self._kernel_basis(sub.index, sub.n)
+            qtf = np.ascontiguousarray(q.T @ f)
+            fp = np.ascontiguousarray(f - q @ qtf)
+            keep.append((fp, qtf))
+            slots[k] = sub.slot
+            fptr[k] = fp.ctypes.data
+            qptr[k] = qtf.ctypes.data if qtf.size else None
+        _call(self._lib.feti_set_forces(self._ctx, ns, _lib.i64ptr(slots), fptr, qptr))
+        self._forces_dev = list(self.forces)
 
     def _factorize_and_assemble(self) -> None:
         # the sparse route reports a non-SPD pivot from feti_assemble (it
@@ -797,6 +830,26 @@ class DualOperator:
             out.append(x[off:off + s.n].copy())
             off += s.n
         return out
+
+    def dual_rhs(self, forces) -> np.ndarray:
+        """B~ K^+ f summed over the owned subdomains (the d of
+        assemble_dual_system without the -c, solver.py:141-143)."""
+        if not self.step_ready:
+            raise LifecycleError("dual_rhs before preprocess")
+        fd = self._forces_dev
+        if fd is not None and len(fd) == len(forces) and all(
+                a is b or (a is not None and b is not None and np.array_equal(a, b))
+                for a, b in ((fd[s.index], forces[s.index]) for s in self._subs.values())):
+            # the loads were factored along with K_s: d straight from the device
+            d = np.empty(self.n_multipliers)
+            _call(self._lib.feti_dual_rhs(self._ctx, None, _lib.f64ptr(d)))
+            return d
+        d = np.zeros(self.n_multipliers)
+        subs = sorted(self._subs.values(), key=lambda s: s.index)
+        kfs = self.solve_local_many([s.index for s in subs], [forces[s.index] for s in subs])
+        for s, kf in zip(subs, kfs):
+            d[s.gids] += s.bval * kf[s.bcol]
+        return d
 
     def _sparse_solver(self, sub):
         """Host K_reg^-1 through a sparse LU of K_s (solve_local is off the

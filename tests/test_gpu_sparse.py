@@ -27,14 +27,15 @@ def _systems(prob, subs=None):
     return ks, qs, fs
 
 
-def _sparse_op(prob, subs=None):
+def _sparse_op(prob, subs=None, forces=False):
     ks, qs, fs = _systems(prob, subs)
     full = list(range(prob.n_sub))
     kl = [ks.get(s) for s in full]
     ql = [qs.get(s) for s in full]
     mats = [inputs.ShapeOnly((prob.n_dofs, prob.n_dofs)) for _ in full]
     op = dualop.prepare(mats, prob.constraints(), prob.layout, CFG, device=0, factorization="sparse",
-                        stiffness=kl, kernels=ql, subdomains=subs)
+                        stiffness=kl, kernels=ql, subdomains=subs,
+                        forces=[fs.get(s) for s in full] if forces else None)
     return op, ks, qs, fs
 
 
@@ -42,7 +43,7 @@ def _sparse_op(prob, subs=None):
 def test_sparse_route_matches_reference(case):
     g = load_golden(case)
     prob = inputs.Problem(str(g["physics"]), int(g["dim"]), int(g["cells"]), int(g["subs"]))
-    op, ks, qs, fs = _sparse_op(prob)
+    op, ks, qs, fs = _sparse_op(prob, forces=True)
     with op:
         op.preprocess()
         for s in range(prob.n_sub):
@@ -61,6 +62,10 @@ def test_sparse_route_matches_reference(case):
         qk, fk = [qs[s] for s in range(prob.n_sub)], [fs[s] for s in range(prob.n_sub)]
         cons = [(prob.gids[s], prob.bcol[s], prob.bval[s]) for s in range(prob.n_sub)]
         gm, e, d, coarse = ora.assemble_dual_system(qk, fk, cons, prob.n_multipliers, prob.c, op.solve_local)
+        # d = B~ K^+ f from the factorization itself (the loads factored along
+        # as an appended row) against the host solve_local route
+        dd = op.dual_rhs(fk) - prob.c
+        assert np.linalg.norm(dd - d) <= 1e-10 * np.linalg.norm(d), case
         lam_h, it_h = ora.pcpg(gm, e, d, coarse, op.apply, tol=1e-9)
         assert it_h in expected_iterations(case, g)
         assert np.linalg.norm(lam_h - g["pcpg_lambda"]) <= 1e-9 * np.linalg.norm(g["pcpg_lambda"])
