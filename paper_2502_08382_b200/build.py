@@ -49,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     def compile_one(src_obj):
         src, obj = src_obj
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-c", os.path.join(CSRC, src), "-o", obj]
+               *os.environ.get("FETI_NVCC_FLAGS", "").split(), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

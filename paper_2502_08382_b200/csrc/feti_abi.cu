@@ -211,7 +211,7 @@ struct feti_ctx {
   cudaGraphExec_t sp_graph_exec = nullptr;   // captured column-launch sequence
   int sp_graph_launches = 0;
   bool sp_graph_used = false;
-  static constexpr int kSpStreams = 8;
+  static constexpr int kSpStreams = 16;   // upper bound on factorization groups (FETI_SP_GROUPS, default 8)
   std::vector<std::pair<int, int>> sp_corr_rng, sp_sub_rng;   // per group: panels, subdomains
   cudaEvent_t sp_ev[3] = {};   // factorize start, factorize end, assemble end
   // sparse-route stiffness hand-over: values are copied on copy_stream while
@@ -899,7 +899,7 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
       // factorization on its stream
       const char* genv = getenv("FETI_SP_GROUPS");
       const int ns = (int)c->subs.size();
-      int G = genv ? atoi(genv) : feti_ctx::kSpStreams;
+      int G = genv ? atoi(genv) : 8;
       G = std::max(1, std::min(std::min(G, (int)feti_ctx::kSpStreams), std::max(ns, 1)));
       c->sp_groups = G;
       nw = G;
@@ -940,13 +940,21 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   // blocks (fewer, larger segments: less per-segment refill and combine)
   c->apply_nw = 8;
   if (const char* wenv = getenv("FETI_APPLY_WARPS")) c->apply_nw = std::max(1, std::min(APPLY_MAX_WARPS, atoi(wenv)));
+  bool compact = false;
   {
     int maxT32 = 1;
     for (auto& s : c->subs) maxT32 = std::max(maxT32, s.T32);
     const int cap = std::min(apply_max_sb(c->apply_nw), 64);
     const int nbk = (maxT32 + cap - 1) / cap;
     c->apply_sb = (maxT32 + nbk - 1) / nbk;
-    if (const char* senv = getenv("FETI_APPLY_SB")) c->apply_sb = std::max(1, std::min(cap, atoi(senv)));
+    // every subdomain in one block with the compact layout when it fits
+    // (one segment per subdomain slice: the fewest pipeline restarts)
+    compact = maxT32 <= apply_max_compact(c->apply_nw);
+    if (compact) c->apply_sb = maxT32;
+    if (const char* senv = getenv("FETI_APPLY_SB")) {
+      c->apply_sb = std::max(1, std::min(cap, atoi(senv)));
+      compact = false;
+    }
   }
   const int SB = c->apply_sb, SBE = SB * AT;
   struct Blk { int sub, I, J; int64_t tiles; };
@@ -999,6 +1007,7 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     apply_exec += 8.0 * ATILE * s.f_tiles() + s.T32 * AT * 12.0;
   }
   apply_exec += 16.0 * poff;
+  if (compact) c->apply_sb = -SB;   // the kernel's compact-layout flag
   // partial positions of every (subdomain, local multiplier), in segment order
   std::vector<std::vector<std::vector<int64_t>>> lp(c->subs.size());
   for (int si = 0; si < (int)c->subs.size(); ++si) lp[si].assign(c->subs[si].m, {});

@@ -592,13 +592,19 @@ __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict
   const double beta = py ? *pbeta : 0.0;
   auto pval = [&](int gi) -> double { return py ? fma(beta, __ldg(p + gi), __ldg(py + gi)) : __ldg(p + gi); };
   extern __shared__ double asmem[];
-  const int SBE = sb * AT;              // multipliers per super-block edge
+  // sb > 0: super-blocks of sb tiles, per warp row + column accumulators;
+  // sb < 0: every subdomain is one diagonal block of -sb tiles (compact
+  // layout: row accumulators only, as many as fit for small m)
+  const bool compact = sb < 0;
+  const int SBE = (compact ? -sb : sb) * AT;   // multipliers per super-block edge
+  const int WS = compact ? SBE : 2 * SBE;      // accumulator stride per warp
   double* spr = asmem;                  // p of the block's rows
   double* spc = asmem + SBE;            // p of the block's columns (off-diagonal blocks)
-  double* acc = asmem + 2 * SBE;        // warp w: rows at acc + 2 w SBE, columns at + SBE
+  double* acc = asmem + (compact ? SBE : 2 * SBE);   // warp w: rows at acc + w WS, columns at + SBE
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (compact) sb = -sb;
   // accumulators are zeroed once; each combine re-zeroes what it read
-  for (int a = tid; a < NW * 2 * SBE; a += NW * 32) acc[a] = 0.0;
+  for (int a = tid; a < NW * WS; a += NW * 32) acc[a] = 0.0;
   for (int sg = seg_ptr[blockIdx.x]; sg < seg_ptr[blockIdx.x + 1]; ++sg) {
     const ApplySeg w = segs[sg];
     const SubDev& S = subs[w.sub];
@@ -634,7 +640,7 @@ __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict
         spc[a] = gi >= 0 ? pval(gi) : 0.0;
       }
     __syncthreads();
-    double* myr = acc + 2 * warp * SBE;
+    double* myr = acc + warp * WS;
     double* myc = diag ? myr : myr + SBE;
     const double* pc = diag ? spr : spc;
     while (tt < t1) {
@@ -662,8 +668,8 @@ __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict
       double s = 0.0;
 #pragma unroll
       for (int wi = 0; wi < NW; ++wi) {
-        s += acc[2 * wi * SBE + a];
-        acc[2 * wi * SBE + a] = 0.0;
+        s += acc[wi * WS + a];
+        acc[wi * WS + a] = 0.0;
       }
       part[w.out_r + a] = s;
     }
@@ -672,8 +678,8 @@ __global__ void __launch_bounds__(NW * 32) apply_kernel(const SubDev* __restrict
         double s = 0.0;
 #pragma unroll
         for (int wi = 0; wi < NW; ++wi) {
-          s += acc[2 * wi * SBE + SBE + a];
-          acc[2 * wi * SBE + SBE + a] = 0.0;
+          s += acc[wi * WS + SBE + a];
+          acc[wi * WS + SBE + a] = 0.0;
         }
         part[w.out_c + a] = s;
       }
@@ -749,9 +755,12 @@ void launch_trsm_chain(const SubDev* subs, const int4* work, int nwork, cudaStre
 void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
   if (nwork > 0) syrk_kernel<<<nwork, PIPE_THREADS, pipe_smem(), st>>>(subs, work);
 }
-size_t apply_smem(int nw, int sb) { return (size_t)(2 + 2 * nw) * sb * AT * sizeof(double); }
+size_t apply_smem(int nw, int sb) {
+  return sb < 0 ? (size_t)(1 + nw) * (-sb) * AT * sizeof(double) : (size_t)(2 + 2 * nw) * sb * AT * sizeof(double);
+}
 
 int apply_max_sb(int nw) { return (int)((227 * 1024) / ((size_t)(2 + 2 * nw) * AT * sizeof(double))); }
+int apply_max_compact(int nw) { return (int)((227 * 1024) / ((size_t)(1 + nw) * AT * sizeof(double))); }
 
 void launch_apply(int nw, int sb, const SubDev* subs, const ApplySeg* segs, const int* seg_ptr, int nctas,
                   double* part, const double* p, cudaStream_t st, const double* py, const double* pbeta,

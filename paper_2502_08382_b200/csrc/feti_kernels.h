@@ -18,7 +18,9 @@ void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t s
 constexpr int APPLY_MAX_WARPS = 8;   // 3 tile buffers x 32 doubles: > 8 warps spill
 size_t apply_smem(int nw, int sb);
 int apply_max_sb(int nw);   // largest super-block edge (tiles) whose accumulators fit 227 KB
-// sb: super-block edge in 32x32 tiles (the segments' blocking, chosen at finalize);
+int apply_max_compact(int nw);   // largest subdomain (tiles) for the one-block compact layout
+// sb: super-block edge in 32x32 tiles (the segments' blocking, chosen at finalize),
+//     negative: one block per subdomain of -sb tiles, compact accumulators;
 // py/pbeta/done: PCPG mode (gather p_new = y + beta p; no-op once *done)
 void launch_apply(int nw, int sb, const SubDev* subs, const ApplySeg* segs, const int* seg_ptr, int nctas,
                   double* part, const double* p, cudaStream_t st, const double* py = nullptr,

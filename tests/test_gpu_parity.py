@@ -383,11 +383,15 @@ def test_schur_oracle_strategy_keeps_the_cap():
     assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
 
 
+@pytest.mark.parametrize("sb", [None, 1, 2, 3])
 @pytest.mark.parametrize("warps", [1, 3, 5, 6, 7, 8])
-def test_apply_any_warp_count_matches_reference(warps, monkeypatch):
-    """The apply kernel with any warp count per CTA (its super-block
-    accumulators no longer depend on m) gives the reference's q."""
+def test_apply_any_warp_count_matches_reference(warps, sb, monkeypatch):
+    """The apply kernel with any warp count per CTA and any super-block edge
+    (None: one compact block per subdomain; 1-3 tiles: many off-diagonal
+    super-blocks and segments on this small case) gives the reference's q."""
     monkeypatch.setenv("FETI_APPLY_WARPS", str(warps))
+    if sb is not None:
+        monkeypatch.setenv("FETI_APPLY_SB", str(sb))
     g = load_golden(SMALL_CASES[-1])
     prob, mats, cons, lay = _golden_problem(g)
     with dualop.prepare(mats, cons, lay, CFG) as op:
