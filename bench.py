@@ -539,7 +539,10 @@ def run_sparse(args, rank, world, local_rank):
 
     prob = inputs.Problem(*inputs.CONFIGS[args.config], n_clusters=world)
     cons = prob.constraints()
-    owned = fd.owned_subdomains(prob.layout, rank)
+    if args.assign == "lpt":
+        owned = fd.lpt_subdomains(fd.apply_weights(cons), world, rank)
+    else:
+        owned = fd.owned_subdomains(prob.layout, rank)
     n = prob.n_dofs
     cfg = dualop.DualOpConfig(strategy="explicit", path="syrk")
     t0 = time.time()
@@ -679,7 +682,7 @@ def run_sparse(args, rank, world, local_rank):
         "config": {"workload": f"{args.config}: {prob.physics} {prob.dim}D, {prob.n_sub} subdomains x {n} DOFs, "
                                f"{prob.n_multipliers} multipliers", "route": "sparse-factor (K_s + rank-2r correction)",
                    "ordering": f"constrained DOFs last; interior recipe {recipe!r} (tile-flop estimator, sparse_route.choose_ordering)",
-                   "parallelism": f"cluster-per-gpu x{world}",
+                   "parallelism": f"cluster-per-gpu x{world} ({args.assign})",
                    "l2": f"inputs larger than L2 (block-sparse factor tiles {st['bytes_temporary'] / 1e9:.0f} GB, "
                          f"packed F~ {8 * sum(m * (m + 1) / 2 for m in prob.m_per_subdomain()) / 1e9:.2f} GB "
                          f"per apply)"},
@@ -1072,6 +1075,8 @@ def main():
     ap.add_argument("--sparse-only", action="store_true",
                     help="sparse route: skip the reference-factor-path measurements")
     ap.add_argument("--ordering", default="rcm", choices=("rcm", "interface_last"))
+    ap.add_argument("--assign", default="contiguous", choices=("contiguous", "lpt"),
+                    help="subdomain -> rank: the reference's contiguous clusters or LPT by packed F~ bytes")
     ap.add_argument("--applies", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-device-factor", dest="device_factor", action="store_false",

@@ -34,6 +34,33 @@ def owned_subdomains(layout, rank: int):
     return [int(s) for s in layout.clusters[rank].subdomain_ids]
 
 
+def lpt_subdomains(weights, world: int, rank: int):
+    """Longest-processing-time-first assignment of subdomains to ranks: by
+    decreasing weight (ties by index), each subdomain goes to the currently
+    least-loaded rank (ties by rank).  Deterministic on every rank.  Weights:
+    ``apply_weights`` (packed F~ bytes, the per-iteration HBM stream) or any
+    per-subdomain work estimate.  The reference's contiguous layout
+    (decomposition.py:227-243) leaves max/mean 1.20 at 4 and 8 GPUs on configs
+    3-4; LPT gets within one subdomain of the mean.  Returns the
+    rank's subdomain ids in ascending order (the operator applies them in the
+    reference's gather order, dualop.py:375-379)."""
+    w = [float(x) for x in weights]
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    loads = [0.0] * world
+    owner = [0] * len(w)
+    for s in sorted(range(len(w)), key=lambda i: (-w[i], i)):
+        r = min(range(world), key=lambda k: (loads[k], k))
+        owner[s] = r
+        loads[r] += w[s]
+    return [s for s in range(len(w)) if owner[s] == rank]
+
+
+def apply_weights(constraints):
+    """Per-subdomain apply work: packed F~ bytes 8 m (m + 1) / 2."""
+    return [4.0 * m * (m + 1) for m in (len(sc.multiplier_ids) for sc in constraints.per_subdomain)]
+
+
 def allreduce_sum_(q, group=None):
     """In-place sum of per-rank dual-vector contributions."""
     import torch.distributed as dist

@@ -40,7 +40,7 @@ def _oracle_parts(prob):
     return op
 
 
-def _worker(rank, world, port, outdir):
+def _worker(rank, world, port, outdir, assign="contiguous"):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -49,7 +49,10 @@ def _worker(rank, world, port, outdir):
     try:
         prob = inputs.Problem("heat", 2, 3, 2, n_clusters=world)
         op = _oracle_parts(prob)
-        owned = fd.owned_subdomains(prob.layout, rank)
+        if assign == "lpt":
+            owned = fd.lpt_subdomains(fd.apply_weights(prob.constraints()), world, rank)
+        else:
+            owned = fd.owned_subdomains(prob.layout, rank)
         p = np.random.default_rng(0).normal(size=prob.n_multipliers)
 
         def local_apply(vec):
@@ -93,3 +96,38 @@ def test_owned_subdomains_layout():
     assert got == [[0, 1], [2, 3], [4, 5], [6, 7]]
     with pytest.raises(ValueError):
         fd.owned_subdomains(prob.layout, 4)
+
+
+def test_two_rank_lpt_apply_equals_single_operator(tmp_path):
+    """The LPT assignment (mixed subdomain sets per rank) composes to the same q."""
+    pytest.importorskip("torch")
+    import torch.multiprocessing as mp
+
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), "lpt"), nprocs=2, join=True)
+    prob = inputs.Problem("heat", 2, 3, 2, n_clusters=2)
+    op = _oracle_parts(prob)
+    p = np.random.default_rng(0).normal(size=prob.n_multipliers)
+    ref = op.apply(p)
+    q0, q1 = np.load(tmp_path / "q0.npy"), np.load(tmp_path / "q1.npy")
+    assert np.array_equal(q0, q1)
+    assert np.linalg.norm(q0 - ref) <= 1e-14 * np.linalg.norm(ref)
+    owned = [set(np.load(tmp_path / f"owned{r}.npy").tolist()) for r in range(2)]
+    assert owned[0] | owned[1] == set(range(prob.n_sub)) and not owned[0] & owned[1]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_lpt_balances_config3_apply_work(world):
+    """Config 3: contiguous clusters leave max/mean 1.20 of packed
+    F~ bytes at 4 and 8 ranks; LPT is within one subdomain's share of the mean,
+    deterministic, and a partition."""
+    prob = inputs.Problem(*inputs.CONFIGS["c3"], n_clusters=world)
+    w = fd.apply_weights(prob.constraints())
+    parts = [fd.lpt_subdomains(w, world, r) for r in range(world)]
+    assert sorted(s for p in parts for s in p) == list(range(prob.n_sub))
+    assert parts == [fd.lpt_subdomains(w, world, r) for r in range(world)]
+    loads = [sum(w[s] for s in p) for p in parts]
+    mean = sum(w) / world
+    assert max(loads) - mean <= max(w)
+    contiguous = [sum(w[s] for s in fd.owned_subdomains(prob.layout, r)) for r in range(world)]
+    assert max(loads) <= 1.001 * max(contiguous)
+    assert max(loads) / mean < 1.05

@@ -27,7 +27,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, outdir):
+def _worker(rank, world, port, outdir, assign="contiguous"):
     import torch
     import torch.distributed as dist
 
@@ -42,7 +42,8 @@ def _worker(rank, world, port, outdir):
         torch.cuda.set_device(dev)
         prob = inputs.Problem("heat", 3, 4, 2, n_clusters=world)
         mats, cons, lay = inputs.reference_inputs(prob)
-        owned = fd.owned_subdomains(lay, rank)
+        owned = (fd.lpt_subdomains(fd.apply_weights(cons), world, rank) if assign == "lpt"
+                 else fd.owned_subdomains(lay, rank))
         with dualop.prepare(mats, cons, lay, CFG, device=dev.index, subdomains=owned) as op:
             op.preprocess()
             dco = fd.ClusterDualOperator(op, prob.n_multipliers, dev)
@@ -61,17 +62,23 @@ def _worker(rank, world, port, outdir):
         dist.destroy_process_group()
 
 
-def test_two_rank_fused_exchange(tmp_path):
+@pytest.mark.parametrize("world,assign", [(2, "contiguous"), (4, "contiguous"), (8, "contiguous"), (4, "lpt")])
+def test_fused_exchange_multi_rank(tmp_path, world, assign):
+    """2, 4 and 8 ranks (one subdomain per rank at 8) time-sharing the box's
+    GPU through CUDA IPC, contiguous clusters or the LPT assignment: q equals
+    the single-operator apply, is identical on every rank and repeats bit for
+    bit over successive epochs (slab parity reuse)."""
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _port(), str(tmp_path), assign), nprocs=world, join=True)
     prob = inputs.Problem("heat", 3, 4, 2)
     mats, cons, lay = inputs.reference_inputs(prob)
     with dualop.prepare(mats, cons, lay, CFG, device=0) as op:
         op.preprocess()
         ref = op.apply(np.random.default_rng(0).normal(size=prob.n_multipliers))
-    q0, q1 = np.load(tmp_path / "q0.npy"), np.load(tmp_path / "q1.npy")
-    assert np.array_equal(q0, q1)
-    for k in range(1, q0.shape[0]):
-        assert np.array_equal(q0[k], q0[0])
-    assert np.linalg.norm(q0[0] - ref) <= 1e-12 * np.linalg.norm(ref)
+    qs = [np.load(tmp_path / f"q{r}.npy") for r in range(world)]
+    for q in qs[1:]:
+        assert np.array_equal(q, qs[0])
+    for k in range(1, qs[0].shape[0]):
+        assert np.array_equal(qs[0][k], qs[0][0])
+    assert np.linalg.norm(qs[0][0] - ref) <= 1e-12 * np.linalg.norm(ref)
