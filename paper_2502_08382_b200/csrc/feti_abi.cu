@@ -2018,6 +2018,9 @@ int feti_pcpg_solve(feti_ctx* c, const double* d, const double* e, double tol, i
   CUDA_TRY(cudaMemcpyAsync(c->pc_sc, c->pc_sc_host, sizeof(PcpgScal), cudaMemcpyHostToDevice, st));
   // the iteration body, kPcpgGraphIters iterations per graph (no-ops once done)
   cudaGraphExec_t& ge = c->pc_graph[precond];
+  // FETI_PCPG_COOP=0: the five-launch iteration (B, D, F, G separately)
+  const int coop = (getenv("FETI_PCPG_COOP") && atoi(getenv("FETI_PCPG_COOP")) == 0)
+                       ? 0 : std::min(pcpg_coop_grid(c->num_sms), 1024);
   if (!ge) {
     CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     const int* done = &c->pc_sc->done;
@@ -2025,6 +2028,11 @@ int feti_pcpg_solve(feti_ctx* c, const double* d, const double* e, double tol, i
     for (int it = 0; it < feti_ctx::kPcpgGraphIters; ++it) {
       launch_apply(c->apply_nw, c->apply_sb, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, P.p, st,
                    P.y, beta, done);
+      if (precond == 0 && coop > 0) {
+        // the vector work of the iteration in one cooperative launch
+        CUDA_TRY(launch_pcpg_iter_coop(P, coop, st));
+        continue;
+      }
       launch_pcpg_reduce_pq(P, st);
       launch_pcpg_gtx_r(P, st);
       if (precond == 0) {

@@ -2,9 +2,11 @@
 // (solver.py:195-272) with every vector operation, inner product and the
 // stopping test on the device.
 //
-// One iteration (precond "none") is five launches, captured in a CUDA graph
-// of several iterations and replayed; the host polls a status word once per
-// graph launch:
+// One iteration (precond "none") is two launches -- the apply and one
+// cooperative kernel doing B, D, F and G below between grid-wide barriers
+// (pcpg_iter_coop; FETI_PCPG_COOP=0 falls back to five separate launches) --
+// captured in a CUDA graph of several iterations and replayed; the host polls
+// a status word once per graph launch.  The phases:
 //   A  apply_kernel      SYMV partials of F p_new, gathering p_new = y + beta p
 //                        on the fly (the conjugation of the previous iteration)
 //   B  reduce_pq         q = F p_new in the reference's gather order, p <- p_new,
@@ -19,6 +21,8 @@
 // and G2 forms y = z - G kz2 and finalises.)  Reductions are fixed-order
 // trees, and the cross-block sums are done by the last block to finish (a
 // counter) in block order: bit-reproducible runs.
+#include <cooperative_groups.h>
+
 #include <cstdint>
 
 #include "feti_coarse.h"
@@ -248,6 +252,141 @@ __global__ void __launch_bounds__(PT) pcpg_update(PcpgDev P) {
   }
 }
 
+// ---- the iteration's vector work as ONE cooperative kernel (precond none) --
+// grid = one CTA per SM (co-resident), grid-wide barriers between the phases
+// of kernels B, D, F and G above; every cross-CTA sum is read back by the CTAs
+// that need it in CTA order (deterministic, identical everywhere), so the
+// scalar results need no broadcast barrier.
+__device__ __forceinline__ double cta_ordered(const double* v, int n, int stride, double* red) {
+  const double t = ordered_sum(v, n, stride, red);
+  __shared__ double bc;
+  if (threadIdx.x == 0) bc = t;
+  __syncthreads();
+  const double r = bc;
+  __syncthreads();
+  return r;
+}
+
+// z = C v, rows split over the grid (written to global)
+__device__ __forceinline__ void coarse_rows(const PcpgDev& P, const double* v, double* z) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * (PT / 32) + warp; row < P.nk; row += gridDim.x * (PT / 32)) {
+    double acc = 0.0;
+    for (int c = lane; c < P.nk; c += 32) acc = fma(P.cinv[(int64_t)row * P.nk + c], __ldcg(v + c), acc);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) z[row] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(PT) pcpg_iter_coop(PcpgDev P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[PT / 32];
+  PcpgScal* sc = P.sc;
+  if (sc->done) return;                       // uniform: written by the previous launch only
+  const int G = gridDim.x, b = blockIdx.x;
+  const int nthr = G * PT, gt = b * PT + threadIdx.x;
+  // B: q = reduce(partials), p <- y + beta p, p.q
+  const double beta = sc->beta;
+  double v = 0.0;
+  for (int g = gt; g < P.n_mult; g += nthr) {
+    double qg = 0.0;
+    for (int e = P.cptr[g]; e < P.cptr[g + 1]; ++e) {
+      const int4 c = P.cent[e];
+      double s2 = 0.0;
+      for (int k = c.y; k < c.z; ++k) s2 += P.part[P.ridx[k]];
+      qg += s2;
+    }
+    const double pn = fma(beta, P.p[g], P.y[g]);
+    P.q[g] = qg;
+    P.p[g] = pn;
+    v += pn * qg;
+  }
+  double t = block_sum(v, red);
+  if (threadIdx.x == 0) P.bpart[b] = t;
+  grid.sync();
+  const double pq = cta_ordered(P.bpart, G, 1, red);
+  if (!(pq > 0.0)) {                          // BreakdownError (solver.py:246-247)
+    if (b == 0 && threadIdx.x == 0) {
+      sc->pq = pq;
+      sc->status = PCPG_BREAKDOWN;
+      sc->done = 1;
+    }
+    return;                                   // every CTA saw the same pq
+  }
+  const double delta = sc->wy / pq;
+  // D: kv = G^T (r - delta q), one CTA per kernel column
+  for (int col = b; col < P.ncols; col += G) {
+    const int2 cc = P.kcols[col];
+    const CoarseSub& S = P.cs[cc.x];
+    double acc = 0.0;
+    for (int a = threadIdx.x; a < S.m; a += PT)
+      acc = fma(S.G[(int64_t)a * S.r + cc.y], __ldcg(P.r + S.gids[a]) - delta * __ldcg(P.q + S.gids[a]), acc);
+    const double tt = block_sum(acc, red);
+    if (threadIdx.x == 0) P.kv[S.koff + cc.y] = tt;
+  }
+  grid.sync();
+  coarse_rows(P, P.kv, P.kz);
+  grid.sync();
+  // F: kv2 = G^T w, w = (r - delta q) - G kz on the fly
+  for (int col = b; col < P.ncols; col += G) {
+    const int2 cc = P.kcols[col];
+    const CoarseSub& S = P.cs[cc.x];
+    double acc = 0.0;
+    for (int a = threadIdx.x; a < S.m; a += PT) {
+      const int g = S.gids[a];
+      const double wg = (__ldcg(P.r + g) - delta * __ldcg(P.q + g)) - gz(P, g, P.kz);
+      acc = fma(S.G[(int64_t)a * S.r + cc.y], wg, acc);
+    }
+    const double tt = block_sum(acc, red);
+    if (threadIdx.x == 0) P.kv2[S.koff + cc.y] = tt;
+  }
+  grid.sync();
+  coarse_rows(P, P.kv2, P.kz2);
+  grid.sync();
+  // G: r, lam, w = P r, y = P w; w.y, w.w
+  double wy = 0.0, ww = 0.0;
+  for (int g = gt; g < P.n_mult; g += nthr) {
+    const double rn = __ldcg(P.r + g) - delta * __ldcg(P.q + g);
+    P.lam[g] = P.lam[g] + delta * P.p[g];
+    const double wg = rn - gz(P, g, P.kz);
+    const double yg = wg - gz(P, g, P.kz2);
+    P.r[g] = rn;
+    P.y[g] = yg;
+    wy += wg * yg;
+    ww += wg * wg;
+  }
+  const double a1 = block_sum(wy, red);
+  const double a2 = block_sum(ww, red);
+  if (threadIdx.x == 0) {
+    P.bpart[2 * G + 2 * b] = a1;
+    P.bpart[2 * G + 2 * b + 1] = a2;
+  }
+  grid.sync();
+  if (b != 0) return;
+  const double s_wy = ordered_sum(P.bpart + 2 * G, G, 2, red);
+  const double s_ww = ordered_sum(P.bpart + 2 * G + 1, G, 2, red);
+  if (threadIdx.x == 0) {
+    sc->pq = pq;
+    sc->delta = delta;
+    finalize(P, s_wy, s_ww);
+  }
+}
+
+int pcpg_coop_grid(int num_sms) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcpg_iter_coop, PT, 0) != cudaSuccess || per_sm < 1)
+    return 0;
+  return num_sms;   // one CTA per SM: co-resident by construction
+}
+
+cudaError_t launch_pcpg_iter_coop(const PcpgDev& P, int grid, cudaStream_t st) {
+  PcpgDev arg = P;
+  void* args[] = {&arg};
+  return cudaLaunchCooperativeKernel((const void*)pcpg_iter_coop, dim3(grid), dim3(PT), args, 0, st);
+}
+
 // ---- setup kernels -----------------------------------------------------
 // out = a - b (elementwise)
 __global__ void __launch_bounds__(PT) pcpg_sub(int n, const double* __restrict__ a, const double* __restrict__ b,
@@ -316,6 +455,6 @@ void launch_pcpg_update(const PcpgDev& P, int mode, cudaStream_t st) {
   else
     pcpg_update<2><<<nblocks(P.n_mult), PT, 0, st>>>(P);
 }
-size_t pcpg_bpart_doubles(int n_mult, int ncols) { return (size_t)3 * (nblocks(n_mult) + ncols + 1); }
+size_t pcpg_bpart_doubles(int n_mult, int ncols) { return (size_t)3 * (nblocks(n_mult) + ncols + 1) + 4 * 1024; }
 
 }  // namespace feti

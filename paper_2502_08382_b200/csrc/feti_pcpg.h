@@ -43,5 +43,8 @@ void launch_pcpg_gtx_w(const PcpgDev& P, cudaStream_t st);
 void launch_pcpg_gtx_x(const PcpgDev& P, const double* x, cudaStream_t st);
 void launch_pcpg_update(const PcpgDev& P, int mode, cudaStream_t st);
 size_t pcpg_bpart_doubles(int n_mult, int ncols);
+// one cooperative launch for B + D + F + G (grid-wide barriers); grid <= 0: unavailable
+int pcpg_coop_grid(int num_sms);
+cudaError_t launch_pcpg_iter_coop(const PcpgDev& P, int grid, cudaStream_t st);
 
 }  // namespace feti

@@ -150,9 +150,14 @@ __device__ __forceinline__ void sg_issue(const SpPair* __restrict__ pairs, int64
   bulk_g2s(sB + st * SLICE, pr.B + so, SLICE * 8, &full[st]);
 }
 
+// One tile task on the ring (positions pos0 ...).  `pre` slices of it were
+// already issued by the previous task of this CTA; when `next` is given, its
+// first slices are issued before this task's epilogue (cross-task prefetch:
+// the next task's fill overlaps this epilogue).  Returns the number issued.
 template <int MI>
-__device__ __forceinline__ void sg_gemm(const SpPair* __restrict__ pairs, const SpTask& tk, double* sA, double* sB,
-                                         uint64_t* full, uint64_t* empty, uint32_t pos0, int warp, int lane) {
+__device__ __forceinline__ int sg_gemm(const SpPair* __restrict__ pairs, const SpTask& tk, double* sA, double* sB,
+                                       uint64_t* full, uint64_t* empty, uint32_t pos0, int warp, int lane, int pre,
+                                       const SpTask* next) {
   const int nsl = tk.npairs * (TB / KS);
   const int wm = warp >> 2, wn = warp & 3;
   const int gq = lane >> 2, t = lane & 3;
@@ -161,8 +166,8 @@ __device__ __forceinline__ void sg_gemm(const SpPair* __restrict__ pairs, const 
   if (issuer) {
     fence_proxy_async_global();
     fence_proxy_async_shared();
-    if (!(tk.flags & 1)) bulk_prefetch_l2(tk.C, TILE * 8);
-    for (int sl = 0; sl < SG_PREF && sl < nsl; ++sl) sg_issue(pairs, tk.pair0, sl, pos0 + sl, sA, sB, full, empty);
+    if (!pre && !(tk.flags & 1)) bulk_prefetch_l2(tk.C, TILE * 8);
+    for (int sl = pre; sl < SG_PREF && sl < nsl; ++sl) sg_issue(pairs, tk.pair0, sl, pos0 + sl, sA, sB, full, empty);
   }
   double acc[MI][4][2];
 #pragma unroll
@@ -180,7 +185,16 @@ __device__ __forceinline__ void sg_gemm(const SpPair* __restrict__ pairs, const 
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
-  if (!active) return;
+  int issued = 0;
+  if (next) {
+    const int nsl2 = next->npairs * (TB / KS);
+    issued = min(SG_PREF, nsl2);
+    if (issuer) {
+      if (!(next->flags & 1)) bulk_prefetch_l2(next->C, TILE * 8);
+      for (int sl = 0; sl < issued; ++sl) sg_issue(pairs, next->pair0, sl, pos0 + nsl + sl, sA, sB, full, empty);
+    }
+  }
+  if (!active) return issued;
   double* Ct = tk.C;
   const bool panel = tk.flags & 1;
 #pragma unroll
@@ -199,11 +213,12 @@ __device__ __forceinline__ void sg_gemm(const SpPair* __restrict__ pairs, const 
       }
     }
   }
+  return issued;
 }
 
-// one task per CTA, 8 warps (255 registers, no spills): the column-launch
-// scheduler's tile kernel
-__global__ void __launch_bounds__(SG_THREADS, 1) sp_gemm8_kernel(const SpTask* __restrict__ tasks,
+// persistent over the launch's tasks: CTA b runs tasks b, b + grid, ...
+// (sorted by decreasing size), the ring continuing across them
+__global__ void __launch_bounds__(SG_THREADS, 1) sp_gemm8_kernel(const SpTask* __restrict__ tasks, int ntasks,
                                                                   const SpPair* __restrict__ pairs) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sA = reinterpret_cast<double*>(smem_raw);
@@ -219,11 +234,17 @@ __global__ void __launch_bounds__(SG_THREADS, 1) sp_gemm8_kernel(const SpTask* _
     mbar_fence_init();
   }
   __syncthreads();
-  const SpTask tk = tasks[blockIdx.x];
-  if (!(tk.flags & 2))
-    sg_gemm<8>(pairs, tk, sA, sB, full, empty, 0, warp, lane);
-  else
-    sg_gemm<1>(pairs, tk, sA, sB, full, empty, 0, warp, lane);
+  uint32_t pos = 0;
+  int pre = 0;
+  for (int ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
+    const SpTask tk = tasks[ti];
+    const SpTask* nx = (ti + (int)gridDim.x < ntasks) ? tasks + ti + gridDim.x : nullptr;
+    if (!(tk.flags & 2))
+      pre = sg_gemm<8>(pairs, tk, sA, sB, full, empty, pos, warp, lane, pre, nx);
+    else
+      pre = sg_gemm<1>(pairs, tk, sA, sB, full, empty, pos, warp, lane, pre, nx);
+    pos += (uint32_t)(tk.npairs * (TB / KS));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -524,7 +545,8 @@ void launch_sp_trace(const SpSub* ss, int nsub, cudaStream_t st) {
 }
 
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st) {
-  if (ntasks > 0) sp_gemm8_kernel<<<ntasks, SG_THREADS, sg_smem(), st>>>(tasks, pairs);
+  static const int tpc = getenv("FETI_SP_TPC") ? std::max(1, atoi(getenv("FETI_SP_TPC"))) : 2;   // tasks per CTA
+  if (ntasks > 0) sp_gemm8_kernel<<<(ntasks + tpc - 1) / tpc, SG_THREADS, sg_smem(), st>>>(tasks, ntasks, pairs);
 }
 
 void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st) {
