@@ -545,7 +545,11 @@ void launch_sp_trace(const SpSub* ss, int nsub, cudaStream_t st) {
 }
 
 void launch_sp_gemm(const SpTask* tasks, int ntasks, const SpPair* pairs, cudaStream_t st) {
-  static const int tpc = getenv("FETI_SP_TPC") ? std::max(1, atoi(getenv("FETI_SP_TPC"))) : 2;   // tasks per CTA
+  // tasks per CTA: 1 by default.  Measured (c3, scripts/gpu_exp_tpc.sh):
+  // 1/2/3/4 tasks per CTA give 42.3/45.4/49.8/55.9 ms -- fewer, longer CTAs
+  // per launch cost more cross-stream concurrency than the cross-task
+  // prefetch saves
+  static const int tpc = getenv("FETI_SP_TPC") ? std::max(1, atoi(getenv("FETI_SP_TPC"))) : 1;
   if (ntasks > 0) sp_gemm8_kernel<<<(ntasks + tpc - 1) / tpc, SG_THREADS, sg_smem(), st>>>(tasks, ntasks, pairs);
 }
 
