@@ -182,6 +182,12 @@ struct feti_ctx {
   double* d_cinv = nullptr;
   double* d_kv = nullptr;
   double* d_kz = nullptr;
+  // G flattened by kernel column and cut into pieces (device PCPG's G^T x)
+  double* d_gval = nullptr;
+  int* d_gidx = nullptr;
+  int4* d_pieces = nullptr;
+  int npieces = 0;
+  double* d_ppart = nullptr;
   // upload/compute pipeline for host factors: subdomains grouped in waves
   // (largest work first); wave w's H2D on copy_stream, its kernels on
   // wave_streams[w % 2] once its copies landed
@@ -392,6 +398,7 @@ int build_sparse_tasks(feti_ctx* c) {
         if (slot >= 0) qrow[si][slot] = 1;
       }
   }
+  const bool sort_by_sub = getenv("FETI_SP_ORDER") && std::string(getenv("FETI_SP_ORDER")) == "sub";
   for (int g = 0; g < G; ++g)
   for (int j = 0; j < maxTq; ++j) {
     const size_t gj = (size_t)g * maxTq + j;
@@ -406,9 +413,12 @@ int build_sparse_tasks(feti_ctx* c) {
           pairs.push_back(SpPair{s.d_pool + (size_t)pr.first * TILE, s.d_pool + (size_t)pr.second * TILE});
       }
     }
-    std::stable_sort(tasks.begin() + b, tasks.end(), [](const SpTask& x, const SpTask& y) {
-      return x.npairs * ((x.flags & 2) ? 1 : 4) > y.npairs * ((y.flags & 2) ? 1 : 4);
-    });
+    // largest first (shortest launch tail); FETI_SP_ORDER=sub keeps the
+    // subdomain order instead (consecutive CTAs share operand tiles in L2)
+    if (!sort_by_sub)
+      std::stable_sort(tasks.begin() + b, tasks.end(), [](const SpTask& x, const SpTask& y) {
+        return x.npairs * ((x.flags & 2) ? 1 : 4) > y.npairs * ((y.flags & 2) ? 1 : 4);
+      });
     c->sp_acc_rng[gj] = {b, (int)tasks.size() - b};
     const int db = (int)diag.size();
     for (int si = 0; si < ns; ++si) {
@@ -1893,6 +1903,34 @@ int feti_coarse_setup(feti_ctx* c, const int64_t* kdim, const double* G, const d
   if ((rc = upload(c, &c->d_kcols, cols))) return rc;
   std::vector<double> ci(coarse_inv, coarse_inv + nk * nk);
   if ((rc = upload(c, &c->d_cinv, ci))) return rc;
+  {
+    // G by kernel column, entries of a column contiguous (sorted local order),
+    // cut into pieces of <= kPiece entries that never straddle columns
+    std::vector<double> gv;
+    std::vector<int> gi;
+    std::vector<int4> pcs;
+    int64_t go = 0;
+    for (size_t si = 0; si < c->subs.size(); ++si) {
+      const SubHost& sh = c->subs[si];
+      const int r = (int)kdim[si];
+      for (int k = 0; k < r; ++k) {
+        const int col = hs[si].koff + k;
+        const int e0 = (int)gv.size();
+        for (int64_t a = 0; a < sh.m; ++a) {
+          gv.push_back(gs[go + a * r + k]);
+          gi.push_back(sh.gids_sorted[a]);
+        }
+        for (int e = e0; e < (int)gv.size(); e += kPiece)
+          pcs.push_back(make_int4(col, e, std::min<int>(e + kPiece, (int)gv.size()), 0));
+      }
+      go += sh.m * r;
+    }
+    if ((rc = upload(c, &c->d_gval, gv))) return rc;
+    if ((rc = upload(c, &c->d_gidx, gi))) return rc;
+    if ((rc = upload(c, &c->d_pieces, pcs))) return rc;
+    c->npieces = (int)pcs.size();
+    if ((rc = dev_alloc(c, (void**)&c->d_ppart, (size_t)std::max(c->npieces, 1) * 8, true))) return rc;
+  }
   if ((rc = dev_alloc(c, (void**)&c->d_kv, (size_t)std::max<int64_t>(nk, 1) * 8, true))) return rc;
   if ((rc = dev_alloc(c, (void**)&c->d_kz, (size_t)std::max<int64_t>(nk, 1) * 8, true))) return rc;
   c->nk = (int)nk;
@@ -1974,6 +2012,11 @@ int feti_pcpg_solve(feti_ctx* c, const double* d, const double* e, double tol, i
   P.kz2 = c->pc_k + 3 * K;
   P.bpart = c->pc_bpart;
   P.sc = c->pc_sc;
+  P.gval = c->d_gval;
+  P.gidx = c->d_gidx;
+  P.pieces = c->d_pieces;
+  P.npieces = c->npieces;
+  P.ppart = c->d_ppart;
   cudaStream_t st = c->stream;
   if ((rc = wait_applies(c))) return rc;
   CUDA_TRY(cudaMemcpyAsync(dd, d, (size_t)n * 8, cudaMemcpyHostToDevice, st));

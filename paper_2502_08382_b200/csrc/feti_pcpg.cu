@@ -267,12 +267,34 @@ __device__ __forceinline__ double cta_ordered(const double* v, int n, int stride
   return r;
 }
 
-// z = C v, rows split over the grid (written to global)
-__device__ __forceinline__ void coarse_rows(const PcpgDev& P, const double* v, double* z) {
+// piece sums of G^T x (warp per piece, lanes strided over its entries);
+// with `qx`, x = r - delta q is formed on the fly (two independent gathers)
+__device__ __forceinline__ void gtx_pieces(const PcpgDev& P, const double* x, const double* qx, double delta) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int pc = blockIdx.x * (PT / 32) + warp; pc < P.npieces; pc += gridDim.x * (PT / 32)) {
+    const int4 pi = P.pieces[pc];
+    double acc = 0.0;
+#pragma unroll 4
+    for (int e = pi.y + lane; e < pi.z; e += 32) {
+      const int g = P.gidx[e];
+      const double xv = qx ? __ldcg(x + g) - delta * __ldcg(qx + g) : __ldcg(x + g);
+      acc = fma(P.gval[e], xv, acc);
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) P.ppart[pc] = acc;
+  }
+}
+
+// z = C (G^T x) from the piece sums: z[row] = sum_pieces C[row][col(p)] part[p]
+// (a row per warp; the pieces of a column are summed in order within the
+// warp's fixed lane/tree order: deterministic)
+__device__ __forceinline__ void coarse_pieces(const PcpgDev& P, double* z) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int row = blockIdx.x * (PT / 32) + warp; row < P.nk; row += gridDim.x * (PT / 32)) {
+    const double* crow = P.cinv + (int64_t)row * P.nk;
     double acc = 0.0;
-    for (int c = lane; c < P.nk; c += 32) acc = fma(P.cinv[(int64_t)row * P.nk + c], __ldcg(v + c), acc);
+    for (int pc = lane; pc < P.npieces; pc += 32) acc = fma(crow[P.pieces[pc].x], __ldcg(P.ppart + pc), acc);
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     if (lane == 0) z[row] = acc;
@@ -287,7 +309,7 @@ __global__ void __launch_bounds__(PT) pcpg_iter_coop(PcpgDev P) {
   if (sc->done) return;                       // uniform: written by the previous launch only
   const int G = gridDim.x, b = blockIdx.x;
   const int nthr = G * PT, gt = b * PT + threadIdx.x;
-  // B: q = reduce(partials), p <- y + beta p, p.q
+  // q = reduce(partials), p <- y + beta p, p.q
   const double beta = sc->beta;
   double v = 0.0;
   for (int g = gt; g < P.n_mult; g += nthr) {
@@ -316,43 +338,29 @@ __global__ void __launch_bounds__(PT) pcpg_iter_coop(PcpgDev P) {
     return;                                   // every CTA saw the same pq
   }
   const double delta = sc->wy / pq;
-  // D: kv = G^T (r - delta q), one CTA per kernel column
-  for (int col = b; col < P.ncols; col += G) {
-    const int2 cc = P.kcols[col];
-    const CoarseSub& S = P.cs[cc.x];
-    double acc = 0.0;
-    for (int a = threadIdx.x; a < S.m; a += PT)
-      acc = fma(S.G[(int64_t)a * S.r + cc.y], __ldcg(P.r + S.gids[a]) - delta * __ldcg(P.q + S.gids[a]), acc);
-    const double tt = block_sum(acc, red);
-    if (threadIdx.x == 0) P.kv[S.koff + cc.y] = tt;
-  }
+  // kz = (G^T G)^-1 G^T (r - delta q)
+  gtx_pieces(P, P.r, P.q, delta);
   grid.sync();
-  coarse_rows(P, P.kv, P.kz);
+  coarse_pieces(P, P.kz);
   grid.sync();
-  // F: kv2 = G^T w, w = (r - delta q) - G kz on the fly
-  for (int col = b; col < P.ncols; col += G) {
-    const int2 cc = P.kcols[col];
-    const CoarseSub& S = P.cs[cc.x];
-    double acc = 0.0;
-    for (int a = threadIdx.x; a < S.m; a += PT) {
-      const int g = S.gids[a];
-      const double wg = (__ldcg(P.r + g) - delta * __ldcg(P.q + g)) - gz(P, g, P.kz);
-      acc = fma(S.G[(int64_t)a * S.r + cc.y], wg, acc);
-    }
-    const double tt = block_sum(acc, red);
-    if (threadIdx.x == 0) P.kv2[S.koff + cc.y] = tt;
-  }
-  grid.sync();
-  coarse_rows(P, P.kv2, P.kz2);
-  grid.sync();
-  // G: r, lam, w = P r, y = P w; w.y, w.w
-  double wy = 0.0, ww = 0.0;
+  // r <- r - delta q, lam <- lam + delta p, w = P r (materialised)
   for (int g = gt; g < P.n_mult; g += nthr) {
     const double rn = __ldcg(P.r + g) - delta * __ldcg(P.q + g);
     P.lam[g] = P.lam[g] + delta * P.p[g];
-    const double wg = rn - gz(P, g, P.kz);
-    const double yg = wg - gz(P, g, P.kz2);
     P.r[g] = rn;
+    P.w[g] = rn - gz(P, g, P.kz);
+  }
+  grid.sync();
+  // kz2 = (G^T G)^-1 G^T w
+  gtx_pieces(P, P.w, nullptr, 0.0);
+  grid.sync();
+  coarse_pieces(P, P.kz2);
+  grid.sync();
+  // y = P w; w.y, w.w
+  double wy = 0.0, ww = 0.0;
+  for (int g = gt; g < P.n_mult; g += nthr) {
+    const double wg = __ldcg(P.w + g);
+    const double yg = wg - gz(P, g, P.kz2);
     P.y[g] = yg;
     wy += wg * yg;
     ww += wg * wg;

@@ -33,7 +33,17 @@ struct PcpgDev {
   double *kv, *kz, *kv2, *kz2;
   double* bpart;
   PcpgScal* sc;
+  // G flattened by kernel column (entries of a column contiguous) and cut into
+  // pieces of <= kPiece entries that never straddle columns: G^T x is one
+  // fully parallel pass over the pieces, then rows of (G^T G)^-1 times the
+  // piece sums (pcpg_iter_coop)
+  const double* gval;       // G entry
+  const int* gidx;          // its global multiplier
+  const int4* pieces;       // (column, first entry, end entry, -)
+  int npieces, pad2_;
+  double* ppart;            // per-piece partial sums
 };
+constexpr int kPiece = 512;
 
 void launch_pcpg_sub(int n, const double* a, const double* b, double* out, cudaStream_t st);
 void launch_pcpg_init_dots(const PcpgDev& P, cudaStream_t st);
