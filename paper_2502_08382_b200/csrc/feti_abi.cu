@@ -158,6 +158,7 @@ struct feti_ctx {
   double *d_p = nullptr, *d_q = nullptr;
   int apply_nw = 8;
   int apply_sb = 32;                 // apply super-block edge (32x32 tiles)
+  int apply_cps = 1;                 // apply CTAs per SM
   feti_stats stats{};
   cudaEvent_t ev[8] = {};
   bool subdev_dirty = true;
@@ -398,7 +399,6 @@ int build_sparse_tasks(feti_ctx* c) {
         if (slot >= 0) qrow[si][slot] = 1;
       }
   }
-  const bool sort_by_sub = getenv("FETI_SP_ORDER") && std::string(getenv("FETI_SP_ORDER")) == "sub";
   for (int g = 0; g < G; ++g)
   for (int j = 0; j < maxTq; ++j) {
     const size_t gj = (size_t)g * maxTq + j;
@@ -413,12 +413,11 @@ int build_sparse_tasks(feti_ctx* c) {
           pairs.push_back(SpPair{s.d_pool + (size_t)pr.first * TILE, s.d_pool + (size_t)pr.second * TILE});
       }
     }
-    // largest first (shortest launch tail); FETI_SP_ORDER=sub keeps the
-    // subdomain order instead (consecutive CTAs share operand tiles in L2)
-    if (!sort_by_sub)
-      std::stable_sort(tasks.begin() + b, tasks.end(), [](const SpTask& x, const SpTask& y) {
-        return x.npairs * ((x.flags & 2) ? 1 : 4) > y.npairs * ((y.flags & 2) ? 1 : 4);
-      });
+    // largest first (shortest launch tail; keeping the subdomain order for L2
+    // locality of shared operand tiles measured the same, 42.6 vs 42.3 ms)
+    std::stable_sort(tasks.begin() + b, tasks.end(), [](const SpTask& x, const SpTask& y) {
+      return x.npairs * ((x.flags & 2) ? 1 : 4) > y.npairs * ((y.flags & 2) ? 1 : 4);
+    });
     c->sp_acc_rng[gj] = {b, (int)tasks.size() - b};
     const int db = (int)diag.size();
     for (int si = 0; si < ns; ++si) {
@@ -965,6 +964,15 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
       c->apply_sb = std::max(1, std::min(cap, atoi(senv)));
       compact = false;
     }
+    // many small subdomains (every subdomain a few hundred tiles): two
+    // 4-warp CTAs per SM, so one CTA streams while the other restarts its
+    // pipeline at a subdomain boundary (same warps per SM)
+    c->apply_cps = 1;
+    const char* cenv = getenv("FETI_APPLY_CPS");
+    if ((cenv ? atoi(cenv) == 2 : (compact && maxT32 <= 24 && !getenv("FETI_APPLY_WARPS")))) {
+      c->apply_cps = 2;
+      c->apply_nw = 4;
+    }
   }
   const int SB = c->apply_sb, SBE = SB * AT;
   struct Blk { int sub, I, J; int64_t tiles; };
@@ -982,7 +990,8 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
         total_tiles += nt;
       }
   }
-  const int64_t ncta = std::max<int64_t>(1, std::min<int64_t>(c->num_sms, (total_tiles + 63) / 64));
+  const int64_t ncta =
+      std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * c->apply_cps, (total_tiles + 63) / 64));
   std::vector<ApplySeg> asegs;
   std::vector<int> seg_ptr;
   int64_t poff = 0;

@@ -1,76 +1,9 @@
 // 128x128 dense lower-triangular helpers shared by the assembly's diagonal
-// inverse and the device factorization (256 threads, shared memory).
+// inverse and the device factorizations (256 threads, shared memory).
 #pragma once
 #include "feti_common.cuh"
 
 namespace feti {
-
-__device__ __forceinline__ int plo(int i, int j) { return i * (i + 1) / 2 + j; }
-
-// sY (packed lower) = inv(sL) for a 128x128 lower-triangular sL (packed
-// lower), blocked 4 x 4 over 32-wide sub-blocks.  Phase 1: warp w inverts
-// the diagonal sub-block D_w, lane c carrying column c in registers through a
-// lock-step forward substitution (the L row is a shared-memory broadcast).
-// Phase 2: off-diagonal sub-blocks by distance d = 1, 2, 3:
-//   Y_IJ = -inv(D_I) sum_{K=J}^{I-1} L_IK Y_KJ .
-// sT: 3 x 1024 scratch.  Must be called by all 256 threads; ends synchronised.
-__device__ __forceinline__ void invert_lower_128(const double* __restrict__ sL, double* __restrict__ sY,
-                                                 double* __restrict__ sT) {
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  if (warp < 4) {
-    const int o = warp * 32;
-    double y[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const double* Lr = sL + plo(o + r, o);
-      double acc = (r == lane) ? 1.0 : 0.0;
-#pragma unroll
-      for (int j = 0; j < r; ++j) acc = fma(-Lr[j], y[j], acc);
-      y[r] = acc / Lr[r];
-    }
-#pragma unroll
-    for (int r = 0; r < 32; ++r)
-      if (r >= lane) sY[plo(o + r, o + lane)] = y[r];
-  }
-  __syncthreads();
-  // thread -> (row r, 4 consecutive columns c..c+3) of a 32x32 sub-block
-  const int rr = tid >> 3, cc = (tid & 7) * 4;
-  for (int d = 1; d < 4; ++d) {
-    const int nb = 4 - d;
-    for (int bI = 0; bI < nb; ++bI) {          // T_b = sum_{K=J}^{I-1} L_IK Y_KJ
-      const int J = bI, I = bI + d;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const double* Lr = sL + plo(I * 32 + rr, 0);
-      for (int kk = J * 32; kk < I * 32; ++kk) {
-        const double lv = Lr[kk];
-        const double* Yk = sY + plo(kk, 0);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int col = J * 32 + cc + e;
-          if (kk >= col) acc[e] = fma(lv, Yk[col], acc[e]);
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) sT[bI * 1024 + rr * 32 + cc + e] = acc[e];
-    }
-    __syncthreads();
-    for (int bI = 0; bI < nb; ++bI) {          // Y_IJ = -inv(D_I) T_b
-      const int J = bI, I = bI + d;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const double* Yr = sY + plo(I * 32 + rr, I * 32);
-      for (int kk = 0; kk <= rr; ++kk) {
-        const double yv = Yr[kk];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[e] = fma(yv, sT[bI * 1024 + kk * 32 + cc + e], acc[e]);
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) sY[plo(I * 32 + rr, J * 32 + cc + e)] = -acc[e];
-    }
-    __syncthreads();
-  }
-}
-
 
 // In-place Cholesky of the 128x128 tile (col-major swizzled, lower part read)
 // and its inverse: tile <- L (upper part zeroed), D <- inv(L) (same layout).
@@ -99,6 +32,77 @@ constexpr int PO_LD = FETI_PO_LD;
 // barrier, so a persistent CTA with extra warps can call it.
 __device__ __forceinline__ void po_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 constexpr int POTRF_SMEM_DOUBLES = TB * PO_LD + TB + 3 * 1024;
+
+// Y = inv(L) for the 128x128 lower-triangular L in sA (row-major, stride
+// PO_LD, lower triangle) with sYd[i] = 1 / L(i, i): Y's strict lower triangle
+// ends up transposed in sA's strict upper triangle (Y(i, j), i > j, at
+// [j][i]) and its diagonal in sYd.  The four 32x32 diagonal blocks by one
+// warp each (lane = column, forward substitution), the off-diagonal blocks by
+// distance on the tensor pipe: T = sum_{K=J}^{I-1} L_IK Y_KJ, Y_IJ = -Y_II T.
+// sT: 3 x 1024 scratch.  Called by all 256 threads; ends synchronised.
+__device__ __forceinline__ void po_inverse(double* __restrict__ sA, double* __restrict__ sYd,
+                                           double* __restrict__ sT) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g8 = lane >> 2, t4 = lane & 3;      // DMMA fragment coordinates
+  // inverses of the four 32x32 diagonal blocks, one warp each, lane = column
+  if (warp < 4) {
+    const int o = warp * 32;
+    double y[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const double* Lr = sA + (o + r) * PO_LD + o;
+      double a0 = (r == lane) ? 1.0 : 0.0, a1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < r; ++j) {
+        if (j & 1)
+          a1 = fma(-Lr[j], y[j], a1);
+        else
+          a0 = fma(-Lr[j], y[j], a0);
+      }
+      y[r] = (a0 + a1) * sYd[o + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r > lane) sA[(o + lane) * PO_LD + o + r] = y[r];
+  }
+  po_sync();
+  // off-diagonal blocks of Y by distance d on the tensor pipe:
+  // T = sum_{K=J}^{I-1} L_IK Y_KJ, then Y_IJ = -Y_II T
+  auto ylo = [&](int r, int c) -> double { return r > c ? sA[c * PO_LD + r] : (r == c ? sYd[r] : 0.0); };
+  for (int d = 1; d < 4; ++d) {
+    const int nb = 4 - d;
+    for (int tl = warp; tl < nb * 16; tl += 8) {
+      const int bI = tl >> 4, tm = (tl >> 2) & 3, tn = tl & 3;
+      const int J = bI, I = bI + d;
+      const double* Lr = sA + (I * 32 + tm * 8 + g8) * PO_LD;
+      const int cn = J * 32 + tn * 8 + g8;
+      double c0v = 0.0, c1v = 0.0;
+      for (int k0 = J * 32 + tn * 8; k0 < I * 32; k0 += 4) {
+        const int k = k0 + t4;
+        dmma(c0v, c1v, Lr[k], ylo(k, cn));
+      }
+      double* Tb = sT + bI * 1024 + (tm * 8 + g8) * 32 + tn * 8 + 2 * t4;
+      Tb[0] = c0v;
+      Tb[1] = c1v;
+    }
+    po_sync();
+    for (int tl = warp; tl < nb * 16; tl += 8) {
+      const int bI = tl >> 4, tm = (tl >> 2) & 3, tn = tl & 3;
+      const int J = bI, I = bI + d;
+      const int rm = I * 32 + tm * 8 + g8;
+      double c0v = 0.0, c1v = 0.0;
+      for (int k0 = 0; k0 < tm * 8 + 8; k0 += 4) {
+        const int k = k0 + t4;
+        dmma(c0v, c1v, ylo(rm, I * 32 + k), sT[bI * 1024 + k * 32 + tn * 8 + g8]);
+      }
+      const int m = I * 32 + tm * 8 + g8, n = J * 32 + tn * 8 + 2 * t4;
+      sA[n * PO_LD + m] = -c0v;
+      sA[(n + 1) * PO_LD + m] = -c1v;
+    }
+    po_sync();
+  }
+}
 
 __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, double* __restrict__ D,
                                                  int* __restrict__ bad, int rowbase, double* __restrict__ smem) {
@@ -211,63 +215,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
 #endif
   }
 #ifndef PO_SKIP_INV
-  // inverses of the four 32x32 diagonal blocks, one warp each, lane = column
-  if (warp < 4) {
-    const int o = warp * 32;
-    double y[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const double* Lr = sA + (o + r) * PO_LD + o;
-      double a0 = (r == lane) ? 1.0 : 0.0, a1 = 0.0;
-#pragma unroll
-      for (int j = 0; j < r; ++j) {
-        if (j & 1)
-          a1 = fma(-Lr[j], y[j], a1);
-        else
-          a0 = fma(-Lr[j], y[j], a0);
-      }
-      y[r] = (a0 + a1) * sYd[o + r];
-    }
-#pragma unroll
-    for (int r = 0; r < 32; ++r)
-      if (r > lane) sA[(o + lane) * PO_LD + o + r] = y[r];
-  }
-  po_sync();
-  // off-diagonal blocks of Y by distance d on the tensor pipe:
-  // T = sum_{K=J}^{I-1} L_IK Y_KJ, then Y_IJ = -Y_II T
-  auto ylo = [&](int r, int c) -> double { return r > c ? sA[c * PO_LD + r] : (r == c ? sYd[r] : 0.0); };
-  for (int d = 1; d < 4; ++d) {
-    const int nb = 4 - d;
-    for (int tl = warp; tl < nb * 16; tl += 8) {
-      const int bI = tl >> 4, tm = (tl >> 2) & 3, tn = tl & 3;
-      const int J = bI, I = bI + d;
-      const double* Lr = sA + (I * 32 + tm * 8 + g8) * PO_LD;
-      const int cn = J * 32 + tn * 8 + g8;
-      double c0v = 0.0, c1v = 0.0;
-      for (int k0 = J * 32 + tn * 8; k0 < I * 32; k0 += 4) {
-        const int k = k0 + t4;
-        dmma(c0v, c1v, Lr[k], ylo(k, cn));
-      }
-      double* Tb = sT + bI * 1024 + (tm * 8 + g8) * 32 + tn * 8 + 2 * t4;
-      Tb[0] = c0v;
-      Tb[1] = c1v;
-    }
-    po_sync();
-    for (int tl = warp; tl < nb * 16; tl += 8) {
-      const int bI = tl >> 4, tm = (tl >> 2) & 3, tn = tl & 3;
-      const int J = bI, I = bI + d;
-      const int rm = I * 32 + tm * 8 + g8;
-      double c0v = 0.0, c1v = 0.0;
-      for (int k0 = 0; k0 < tm * 8 + 8; k0 += 4) {
-        const int k = k0 + t4;
-        dmma(c0v, c1v, ylo(rm, I * 32 + k), sT[bI * 1024 + k * 32 + tn * 8 + g8]);
-      }
-      const int m = I * 32 + tm * 8 + g8, n = J * 32 + tn * 8 + 2 * t4;
-      sA[n * PO_LD + m] = -c0v;
-      sA[(n + 1) * PO_LD + m] = -c1v;
-    }
-    po_sync();
-  }
+  po_inverse(sA, sYd, sT);
 #endif
   for (int idx = tid; idx < TILE; idx += 256) {
     const int jl = idx >> 7;

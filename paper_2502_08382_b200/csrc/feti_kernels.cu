@@ -80,10 +80,14 @@ __global__ void __launch_bounds__(256) scatter_sparse_kernel(const SubDev* __res
 // L and Y live as packed lower triangles in shared memory.
 __global__ void __launch_bounds__(256) diag_inverse_kernel(const SubDev* __restrict__ subs,
                                                            const int4* __restrict__ work) {
+  // L_kk into a row-major 128 x PO_LD array, then the tensor-pipe inverse of
+  // the device factorization (po_inverse): four 32x32 diagonal-block
+  // substitutions + DMMA off-diagonal blocks (round 1 used scalar FMA loops
+  // for those: 54 us per block)
   extern __shared__ double dsm[];
-  double* sL = dsm;               // 8256: packed row-major lower L_kk
-  double* sY = dsm + 8256;        // 8256: packed row-major lower inv(L_kk)
-  double* sT = dsm + 2 * 8256;    // 3 x 1024 scratch
+  double* sA = dsm;                   // TB x PO_LD: L lower, inv(L)^T strict upper
+  double* sYd = dsm + TB * PO_LD;     // 1 / L(i, i), then the inverse's diagonal
+  double* sT = sYd + TB;              // 3 x 1024 scratch
   const int4 w = work[blockIdx.x];
   const SubDev& S = subs[w.x];
   const int k = w.y;
@@ -101,21 +105,23 @@ __global__ void __launch_bounds__(256) diag_inverse_kernel(const SubDev* __restr
         v = S.raw[(j * n - j * (j - 1) / 2) + (i - j) - S.raw_off];
       else
         v = (i == j) ? 1.0 : 0.0;    // identity padding
-      sL[plo(il, jl)] = v;
+      sA[il * PO_LD + jl] = v;
     }
   } else {
     for (int idx = tid; idx < TILE; idx += 256) {
       const int jl = idx >> 7;
       const int il = (idx & 127) ^ ((jl & 3) << 2);
-      if (il >= jl) sL[plo(il, jl)] = tile[idx];
+      if (il >= jl) sA[il * PO_LD + jl] = tile[idx];
     }
   }
   __syncthreads();
-  invert_lower_128(sL, sY, sT);
+  if (tid < TB) sYd[tid] = 1.0 / sA[tid * PO_LD + tid];
+  __syncthreads();
+  po_inverse(sA, sYd, sT);
   for (int idx = tid; idx < TILE; idx += 256) {
     const int jl = idx >> 7;
     const int il = (idx & 127) ^ ((jl & 3) << 2);
-    tile[idx] = (il >= jl) ? sY[plo(il, jl)] : 0.0;
+    tile[idx] = il > jl ? sA[jl * PO_LD + il] : (il == jl ? sYd[il] : 0.0);
   }
 }
 
@@ -725,7 +731,7 @@ cudaError_t configure_kernels() {
                                 (int)scale_smem())))
     return e;
   if ((e = cudaFuncSetAttribute(diag_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (2 * 8256 + 3 * 1024) * 8)))
+                                POTRF_SMEM_DOUBLES * 8)))
     return e;
   const void* applies[APPLY_MAX_WARPS] = {
       (const void*)apply_kernel<1>,  (const void*)apply_kernel<2>,  (const void*)apply_kernel<3>,
@@ -744,7 +750,7 @@ void launch_scatter_sparse(const SubDev* subs, int sub, int n, cudaStream_t st) 
   if (n > 0) scatter_sparse_kernel<<<n, 256, 0, st>>>(subs, sub);
 }
 void launch_diag_inverse(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
-  if (nwork > 0) diag_inverse_kernel<<<nwork, 256, (2 * 8256 + 3 * 1024) * 8, st>>>(subs, work);
+  if (nwork > 0) diag_inverse_kernel<<<nwork, 256, POTRF_SMEM_DOUBLES * 8, st>>>(subs, work);
 }
 void launch_block_scale(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
   if (nwork > 0) block_scale_kernel<<<nwork, BS_THREADS, scale_smem(), st>>>(subs, work);

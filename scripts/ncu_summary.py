@@ -38,7 +38,9 @@ def short(name):
     return name.split("(")[0].replace("void ", "").replace("feti::", "")
 
 
-def launches(path):
+def launches(path, metric="gpu__time_duration.sum", scale=1e-6):
+    """Per-kernel list of one metric over every launch of a --metrics CSV
+    (durations in ms by default; several metrics may share the file)."""
     rows = list(csv.reader(open(path)))
     hdr, data = None, []
     for r in rows:
@@ -51,9 +53,9 @@ def launches(path):
     for d in data:
         # the capture's -k filter keeps our kernels only (names may or may not
         # carry the feti:: namespace depending on the ncu version)
-        if "Kernel Name" not in d:
+        if "Kernel Name" not in d or d.get("Metric Name", metric) != metric:
             continue
-        agg.setdefault(short(d["Kernel Name"]), []).append(float(d["Metric Value"]) / 1e6)
+        agg.setdefault(short(d["Kernel Name"]), []).append(float(d["Metric Value"].replace(",", "")) * scale)
     return agg
 
 
