@@ -42,6 +42,37 @@ __host__ __device__ __forceinline__ int64_t tri_index(int64_t K, int64_t Lc) {
   return K * (K + 1) / 2 + Lc;   // lower block-triangle tile (K >= Lc)
 }
 
+// C -= acc for a warp's MI x 4 DMMA fragments (8 rows x 8 columns each) of a
+// 128x128 swizzled tile in global memory.  A plain `*cp -= acc` per element
+// serialises 8 MI load-use-store round trips to L2 (the stores may alias the
+// next loads); here fragment row mi+1 is loaded before row mi is stored, so
+// one round trip per fragment row overlaps the previous row's stores.
+template <int MI>
+__device__ __forceinline__ void tile_sub_acc(double* __restrict__ Ct, const double (&acc)[MI][4][2], int wm, int wn,
+                                             int gq, int t) {
+  double cur[8], nxt[8];
+  auto load_row = [&](int mi, double (&v)[8]) {
+    const int m = wm * 64 + mi * 8 + gq;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) v[ni * 2 + e] = __ldcg(Ct + swz(wn * 32 + ni * 8 + 2 * t + e, m));
+  };
+  load_row(0, cur);
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    if (mi + 1 < MI) load_row(mi + 1, nxt);
+    const int m = wm * 64 + mi * 8 + gq;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) Ct[swz(wn * 32 + ni * 8 + 2 * t + e, m)] = cur[ni * 2 + e] - acc[mi][ni][e];
+    if (mi + 1 < MI)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cur[k] = nxt[k];
+  }
+}
+
 // upper triangle of apply tiles, row-major over tile rows
 __host__ __device__ __forceinline__ int64_t apply_tile_index(int64_t ti, int64_t tj, int64_t T32) {
   return ti * T32 - ti * (ti - 1) / 2 + (tj - ti);

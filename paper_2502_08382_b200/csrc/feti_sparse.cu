@@ -210,31 +210,7 @@ __device__ __forceinline__ int sg_gemm(const SpPair* __restrict__ pairs, const S
     }
     return issued;
   }
-  // C -= acc.  A plain `*cp -= acc` per element serialises 64 load-use-store
-  // round trips to L2 (the stores may alias the next loads); instead the 8
-  // values of fragment row mi+1 are loaded before row mi is stored, so one
-  // L2 round trip per fragment row overlaps the previous row's stores.
-  double cur[8], nxt[8];
-  auto load_row = [&](int mi, double (&v)[8]) {
-    const int m = wm * 64 + mi * 8 + gq;
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) v[ni * 2 + e] = __ldcg(Ct + swz(wn * 32 + ni * 8 + 2 * t + e, m));
-  };
-  load_row(0, cur);
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi) {
-    if (mi + 1 < MI) load_row(mi + 1, nxt);
-    const int m = wm * 64 + mi * 8 + gq;
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) Ct[swz(wn * 32 + ni * 8 + 2 * t + e, m)] = cur[ni * 2 + e] - acc[mi][ni][e];
-    if (mi + 1 < MI)
-#pragma unroll
-      for (int k = 0; k < 8; ++k) cur[k] = nxt[k];
-  }
+  tile_sub_acc<MI>(Ct, acc, wm, wn, gq, t);   // C -= acc, loads one fragment row ahead
   return issued;
 }
 
