@@ -379,12 +379,17 @@ def lumped_operator(stiffness, cons):
     return apply
 
 
-def pcpg(gmat, e, d, coarse, fapply, tol=1e-9, maxit=None, mfun=None):
+def pcpg(gmat, e, d, coarse, fapply, tol=1e-9, maxit=None, mfun=None, wnorms=None, coarse_inverse=None):
     """Projected CG on the dual problem (solver.py:195-272); ``mfun`` the
-    preconditioner (identity by default, solver.py:157-158)."""
+    preconditioner (identity by default, solver.py:157-158).  ``wnorms``
+    (a list) receives ||w_k|| for k = 0, 1, ...; ``coarse_inverse`` replaces
+    the Cholesky solves of G^T G by a product with its explicit inverse (the
+    device loop's arithmetic) for rounding-sensitivity studies."""
     from scipy.linalg.lapack import dpotrs
 
     def csolve(b):
+        if coarse_inverse is not None:
+            return coarse_inverse @ b
         x, info = dpotrs(coarse, b, lower=0)
         return x
 
@@ -401,6 +406,8 @@ def pcpg(gmat, e, d, coarse, fapply, tol=1e-9, maxit=None, mfun=None):
     p = y.copy()
     w0 = float(np.linalg.norm(w))
     wy = float(w @ y)
+    if wnorms is not None:
+        wnorms.append(w0)
     if w0 <= 1e-14 * max(1.0, float(np.linalg.norm(d))):
         return lam, 0
     k = 0
@@ -416,7 +423,10 @@ def pcpg(gmat, e, d, coarse, fapply, tol=1e-9, maxit=None, mfun=None):
         y = project(mfun(w))
         k += 1
         wy_next = float(w @ y)
-        if float(np.linalg.norm(w)) <= tol * w0:
+        wn = float(np.linalg.norm(w))
+        if wnorms is not None:
+            wnorms.append(wn)
+        if wn <= tol * w0:
             return lam, k
         if k >= maxit:
             raise RuntimeError("PCPG did not converge")
