@@ -301,20 +301,6 @@ __device__ __forceinline__ void coarse_pieces(const PcpgDev& P, double* z) {
   }
 }
 
-// the same product by one CTA (rows over its warps)
-__device__ __forceinline__ void coarse_pieces_cta(const PcpgDev& P, double* z) {
-  __threadfence();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int row = warp; row < P.nk; row += PT / 32) {
-    const double* crow = P.cinv + (int64_t)row * P.nk;
-    double acc = 0.0;
-    for (int pc = lane; pc < P.npieces; pc += 32) acc = fma(crow[P.pieces[pc].x], __ldcg(P.ppart + pc), acc);
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) z[row] = acc;
-  }
-}
-
 __global__ void __launch_bounds__(PT) pcpg_iter_coop(PcpgDev P) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -352,17 +338,12 @@ __global__ void __launch_bounds__(PT) pcpg_iter_coop(PcpgDev P) {
     return;                                   // every CTA saw the same pq
   }
   const double delta = sc->wy / pq;
-  // kz = (G^T G)^-1 G^T (r - delta q): piece sums, then the coarse rows --
-  // by the last CTA to finish its pieces when the coarse product is small
-  // (one grid barrier fewer), else spread over the grid
-  const bool small_coarse = (int64_t)P.nk * P.npieces <= 65536;
+  // kz = (G^T G)^-1 G^T (r - delta q): piece sums, then the coarse rows
+  // spread over the grid (the last CTA doing all rows measured slower:
+  // 236 vs 220 us per iteration at c3)
   gtx_pieces(P, P.r, P.q, delta);
-  if (small_coarse) {
-    if (last_block(&sc->cnt[1])) coarse_pieces_cta(P, P.kz);
-  } else {
-    grid.sync();
-    coarse_pieces(P, P.kz);
-  }
+  grid.sync();
+  coarse_pieces(P, P.kz);
   grid.sync();
   // r <- r - delta q, lam <- lam + delta p, w = P r (materialised)
   for (int g = gt; g < P.n_mult; g += nthr) {
@@ -374,12 +355,8 @@ __global__ void __launch_bounds__(PT) pcpg_iter_coop(PcpgDev P) {
   grid.sync();
   // kz2 = (G^T G)^-1 G^T w
   gtx_pieces(P, P.w, nullptr, 0.0);
-  if (small_coarse) {
-    if (last_block(&sc->cnt[2])) coarse_pieces_cta(P, P.kz2);
-  } else {
-    grid.sync();
-    coarse_pieces(P, P.kz2);
-  }
+  grid.sync();
+  coarse_pieces(P, P.kz2);
   grid.sync();
   // y = P w; w.y, w.w
   double wy = 0.0, ww = 0.0;
