@@ -399,8 +399,6 @@ int build_sparse_tasks(feti_ctx* c) {
         if (slot >= 0) qrow[si][slot] = 1;
       }
   }
-  // FETI_SP_NOMASK=1: every tile product in full (A/B for the masks)
-  const bool fullmask = getenv("FETI_SP_NOMASK") && atoi(getenv("FETI_SP_NOMASK")) == 1;
   for (int g = 0; g < G; ++g)
   for (int j = 0; j < maxTq; ++j) {
     const size_t gj = (size_t)g * maxTq + j;
@@ -412,9 +410,7 @@ int build_sparse_tasks(feti_ctx* c) {
         tasks.push_back(SpTask{s.d_pool + (size_t)t.first * TILE, (int64_t)pairs.size(), (int)t.second.size(),
                                qrow[si][t.first] ? 2 : 0});
         for (const auto& pr : t.second)
-          pairs.push_back(SpPair{s.d_pool + (size_t)pr.first * TILE, s.d_pool + (size_t)pr.second * TILE,
-                                 fullmask ? 0xFFFFu : s.sp.rowmask[pr.first],
-                                 fullmask ? 0xFFFFu : s.sp.rowmask[pr.second]});
+          pairs.push_back(SpPair{s.d_pool + (size_t)pr.first * TILE, s.d_pool + (size_t)pr.second * TILE});
       }
     }
     // largest first (shortest launch tail; keeping the subdomain order for L2
@@ -438,7 +434,7 @@ int build_sparse_tasks(feti_ctx* c) {
       for (int slot : s.sp.panel[j]) {
         double* C = s.d_pool + (size_t)slot * TILE;
         tasks.push_back(SpTask{C, (int64_t)pairs.size(), 1, qrow[si][slot] ? 3 : 1});
-        pairs.push_back(SpPair{C, c->d_dinv + (size_t)si * TILE, fullmask ? 0xFFFFu : s.sp.rowmask[slot], 0xFFFFu});
+        pairs.push_back(SpPair{C, c->d_dinv + (size_t)si * TILE});
       }
     }
     c->sp_panel_rng[gj] = {b, (int)tasks.size() - b};

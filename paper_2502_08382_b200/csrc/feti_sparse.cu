@@ -108,12 +108,9 @@ constexpr int SG_STAGES = 3;
 
 // MI = 8: full 128-row tile; MI = 1: "thin" tile of the (P Q)^T block row,
 // whose rows >= r <= 8 are zero (only warp row-group 0, first 8 rows)
-// the warp's output fragments whose A rows (mask bit wm*8+mi) or B rows
-// (bit wn*4+ni) are structurally zero are skipped
 template <int MI>
-__device__ __forceinline__ void sg_mma_slice_masked(const double* __restrict__ a_s, const double* __restrict__ b_s,
-                                                    double (&acc)[MI][4][2], int wm, int wn, int g, int t,
-                                                    uint32_t am, uint32_t bm) {
+__device__ __forceinline__ void sg_mma_slice(const double* __restrict__ a_s, const double* __restrict__ b_s,
+                                             double (&acc)[MI][4][2], int wm, int wn, int g, int t) {
 #pragma unroll
   for (int kb = 0; kb < KS / 4; ++kb) {
     const int kr = kb * 4 + t;
@@ -122,11 +119,9 @@ __device__ __forceinline__ void sg_mma_slice_masked(const double* __restrict__ a
     for (int ni = 0; ni < 4; ++ni) bf[ni] = b_s[swz(kr, wn * 32 + ni * 8 + g)];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
-      if (!((am >> mi) & 1u)) continue;
       const double af = a_s[swz(kr, wm * 64 + mi * 8 + g)];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-        if ((bm >> ni) & 1u) dmma(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
+      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
     }
   }
 }
@@ -185,12 +180,7 @@ __device__ __forceinline__ int sg_gemm(const SpPair* __restrict__ pairs, const S
       sg_issue(pairs, tk.pair0, sl + SG_PREF, pos + SG_PREF, sA, sB, full, empty);
     const int st = (int)(pos % SG_STAGES);
     mbar_wait(&full[st], (pos / SG_STAGES) & 1);
-    if (active) {
-      // this warp's mask bits for the slice's pair (warp-uniform)
-      const SpPair& pr = pairs[tk.pair0 + sl / (TB / KS)];
-      const uint32_t am = (pr.amask >> (wm * 8)) & 0xFFu, bm = (pr.bmask >> (wn * 4)) & 0xFu;
-      if (am && bm) sg_mma_slice_masked<MI>(sA + st * SLICE, sB + st * SLICE, acc, wm, wn, gq, t, am, bm);
-    }
+    if (active) sg_mma_slice<MI>(sA + st * SLICE, sB + st * SLICE, acc, wm, wn, gq, t);
     fence_proxy_async_shared();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -424,7 +414,6 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
     for (int I = par + 1; I < Tq; ++I)
       if (cs[k][I]) cs[par][I] = 1;
   }
-  std::vector<uint16_t> fm;   // (I, J) -> row-fragment mask of the scalar structure
   // scalar work of the same ordering (the algorithmic figure): elimination
   // tree (Liu, path compression) and column counts by row-subtree walks,
   // O(nnz(L)); flops = sum_j c_j (c_j + 3), c_j = nonzeros below the diagonal
@@ -448,17 +437,13 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
         }
       }
     }
-    fm.assign((size_t)Tq * Tq, 0);
-    auto setfm = [&](int64_t i, int64_t j) { fm[(size_t)(i / TB) * Tq + j / TB] |= (uint16_t)(1u << ((i % TB) / 8)); };
     for (int64_t i = 0; i < npos; ++i) {
-      setfm(i, i);                           // diagonal (identity at padding positions)
       const int64_t a = pos_dof[i];
       if (a < 0) continue;
       mark[i] = i;
       for (int64_t p = indptr[a]; p < indptr[a + 1]; ++p) {
         for (int64_t j = iperm[indices[p]]; j >= 0 && j < i && mark[j] != i; j = parent[j]) {
           ++cnt[j];                          // L(i, j) != 0
-          setfm(i, j);
           mark[j] = i;
         }
       }
@@ -486,18 +471,6 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
     for (int J = smin; J <= I; ++J) P.tmap[(size_t)I * Tq + J] = (int)(ns + tri_index(I - smin, J - smin));
   ns += (int64_t)(T - smin) * (T - smin + 1) / 2;
   P.ntiles = ns;
-  // per-slot row-fragment masks: the scalar structure; the dense interface
-  // triangle in full; the (P Q)^T row's tiles hold rows 0..7 only
-  P.rowmask.assign((size_t)std::max<int64_t>(ns, 1), 0);
-  for (int I = 0; I < Tq; ++I)
-    for (int J = 0; J <= I; ++J) {
-      const int slot = P.tmap[(size_t)I * Tq + J];
-      if (slot < 0) continue;
-      uint16_t mk = fm[(size_t)I * Tq + J];
-      if (I >= T) mk = 1;
-      else if (J >= smin) mk = 0xFFFF;
-      P.rowmask[slot] = mk;
-    }
   // row structures (ascending)
   std::vector<std::vector<int>> rows(Tq);
   for (int J = 0; J < T; ++J)

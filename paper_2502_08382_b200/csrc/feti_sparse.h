@@ -44,10 +44,6 @@ struct SpSub {
 struct SpPair {
   const double* A;
   const double* B;
-  // structural row-fragment masks (bit f: rows 8f..8f+7 of the tile hold a
-  // nonzero of the scalar factor): output fragments whose A rows or B rows
-  // are structurally zero are skipped (exact zeros)
-  uint32_t amask, bmask;
 };
 struct SpTask {
   double* C;
@@ -74,7 +70,6 @@ struct SpPlan {
   int64_t trail_base = 0;             // slot of tile (smin, smin); the
                                       // trailing triangle follows in tri_index order
   std::vector<int> tmap;              // Tq x Tq -> slot or -1
-  std::vector<uint16_t> rowmask;      // per slot: 8-row fragments holding a scalar nonzero
   // per block column j in [0, Tq): accumulation targets (C slot, (A, B) slot pairs)
   std::vector<std::vector<std::pair<int, std::vector<std::pair<int, int>>>>> acc;
   std::vector<std::vector<int>> panel;  // per column j < T: slots of L_ij, i in struct(j)
