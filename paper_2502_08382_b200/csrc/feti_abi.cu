@@ -2073,11 +2073,21 @@ int feti_pcpg_solve(feti_ctx* c, const double* d, const double* e, double tol, i
   // FETI_PCPG_COOP=0: the five-launch iteration (B, D, F, G separately)
   const int coop = (getenv("FETI_PCPG_COOP") && atoi(getenv("FETI_PCPG_COOP")) == 0)
                        ? 0 : std::min(pcpg_coop_grid(c->num_sms), 1024);
+  // FETI_PCPG_FUSED=0: the apply and the vector work as two launches
+  const size_t asmem = apply_smem(c->apply_nw, c->apply_sb);
+  const int fused = (coop > 0 && c->apply_nw == 8 && c->apply_cps == 1 &&
+                     !(getenv("FETI_PCPG_FUSED") && atoi(getenv("FETI_PCPG_FUSED")) == 0))
+                        ? pcpg_fused_grid(c->n_apply, asmem) : 0;
+  const ApplyArgs aargs{c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->d_part, c->apply_sb, 0};
   if (!ge) {
     CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     const int* done = &c->pc_sc->done;
     const double* beta = &c->pc_sc->beta;
     for (int it = 0; it < feti_ctx::kPcpgGraphIters; ++it) {
+      if (precond == 0 && fused > 0) {
+        CUDA_TRY(launch_pcpg_iter_fused(P, aargs, fused, asmem, st));
+        continue;
+      }
       launch_apply(c->apply_nw, c->apply_sb, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, P.p, st,
                    P.y, beta, done);
       if (precond == 0 && coop > 0) {

@@ -129,6 +129,33 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
   po_sync();
   // Y(r, c) for r >= c (lower triangle of inv(L))
   auto yat = [&](int r, int c) -> double { return r == c ? sYd[r] : sA[c * PO_LD + r]; };
+  // trailing update A_ij -= L_ib L_jb^T of source block ob over the lower 8x8
+  // tiles of rows/cols >= ob + 32 (DMMA), tiles pidx in [p0, p1) (row-major
+  // over tile rows), spread over `nw` warps starting at warp `w0`
+  auto trail = [&](int ob, int p0, int p1, int w0, int nw) {
+    const int nb = (TB - ob - 32) / 8;
+    p1 = min(p1, nb * (nb + 1) / 2);
+    for (int pidx = p0 + (warp - w0); pidx < p1; pidx += nw) {
+      int I = (int)((sqrt(8.0 * pidx + 1.0) - 1.0) * 0.5);
+      while ((I + 1) * (I + 2) / 2 <= pidx) ++I;
+      while (I * (I + 1) / 2 > pidx) --I;
+      const int J = pidx - I * (I + 1) / 2;
+      const int i0 = ob + 32 + 8 * I, j0 = ob + 32 + 8 * J;
+      const double* Ar = sA + (i0 + g8) * PO_LD + ob;
+      const double* Br = sA + (j0 + g8) * PO_LD + ob;
+      double c0v = 0.0, c1v = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < 32; k0 += 4) dmma(c0v, c1v, Ar[k0 + t4], Br[k0 + t4]);
+      const int row = i0 + g8, col = j0 + 2 * t4;
+      if (I > J || row >= col) sA[row * PO_LD + col] -= c0v;
+      if (I > J || row >= col + 1) sA[row * PO_LD + col + 1] -= c1v;
+    }
+  };
+  // Look-ahead: block bb's trailing update is split into the next diagonal
+  // block ([o+32, o+64)^2: its first 10 tiles, applied right after the
+  // panel) and the rest, which warps 1-7 apply while warp 0 factors that
+  // next diagonal block.
+  constexpr int kNextDiagTiles = 10;   // 4 x 5 / 2 tiles of 8x8
   for (int bb = 0; bb < 4; ++bb) {
     const int o = bb * 32;
 #ifndef PO_SKIP_DIAG
@@ -146,8 +173,10 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
           if (tid == 0) atomicMin(bad, rowbase + o + k);    // first non-positive pivot (permuted row)
           d = 1.0;
         }
-        const double pv = sqrt(d);
-        const double rp = 1.0 / pv;
+        // one rsqrt + multiply instead of sqrt + divide on the serial chain
+        // (both are multi-instruction FP64 sequences): 1/L_kk and L_kk
+        const double rp = rsqrt(d);
+        const double pv = d * rp;
         if (lane == k) rdiag = rp;
         const double lik = (lane == k) ? pv : (lane > k ? row[k] * rp : 0.0);
         row[k] = lik;
@@ -162,6 +191,9 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
         if (j <= lane) sA[(o + lane) * PO_LD + o + j] = row[j];
       if (tid < 32) sYd[o + lane] = rdiag;     // 1 / L_kk (the inverse's diagonal, used by the panel)
     }
+#endif
+#ifndef PO_SKIP_TRAIL
+    if (warp != 0 && bb > 0) trail(o - 32, kNextDiagTiles, 1 << 20, 1, 7);
 #endif
     po_sync();
     const int R = TB - o - 32;                 // rows below the block
@@ -191,27 +223,8 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
     po_sync();
 #endif
 #ifndef PO_SKIP_TRAIL
-    // trailing update A_ij -= L_ib L_jb^T over the lower 8x8 tiles (DMMA)
-    {
-      const int nb = R / 8;
-      const int ntl = nb * (nb + 1) / 2;
-      for (int pidx = warp; pidx < ntl; pidx += 8) {
-        int I = (int)((sqrt(8.0 * pidx + 1.0) - 1.0) * 0.5);
-        while ((I + 1) * (I + 2) / 2 <= pidx) ++I;
-        while (I * (I + 1) / 2 > pidx) --I;
-        const int J = pidx - I * (I + 1) / 2;
-        const int i0 = o + 32 + 8 * I, j0 = o + 32 + 8 * J;
-        const double* Ar = sA + (i0 + g8) * PO_LD + o;
-        const double* Br = sA + (j0 + g8) * PO_LD + o;
-        double c0v = 0.0, c1v = 0.0;
-#pragma unroll
-        for (int k0 = 0; k0 < 32; k0 += 4) dmma(c0v, c1v, Ar[k0 + t4], Br[k0 + t4]);
-        const int row = i0 + g8, col = j0 + 2 * t4;
-        if (I > J || row >= col) sA[row * PO_LD + col] -= c0v;
-        if (I > J || row >= col + 1) sA[row * PO_LD + col + 1] -= c1v;
-      }
-      po_sync();
-    }
+    trail(o, 0, kNextDiagTiles, 0, 8);
+    po_sync();
 #endif
   }
 #ifndef PO_SKIP_INV

@@ -27,6 +27,7 @@
 
 #include "feti_coarse.h"
 #include "feti_common.cuh"
+#include "feti_apply.cuh"
 #include "feti_kernels.h"
 #include "feti_pcpg.h"
 
@@ -301,12 +302,10 @@ __device__ __forceinline__ void coarse_pieces(const PcpgDev& P, double* z) {
   }
 }
 
-__global__ void __launch_bounds__(PT) pcpg_iter_coop(PcpgDev P) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
+// the iteration's vector work after the apply's partials are complete
+__device__ __forceinline__ void pcpg_vector_phases(const PcpgDev& P, cooperative_groups::grid_group& grid) {
   __shared__ double red[PT / 32];
   PcpgScal* sc = P.sc;
-  if (sc->done) return;                       // uniform: written by the previous launch only
   const int G = gridDim.x, b = blockIdx.x;
   const int nthr = G * PT, gt = b * PT + threadIdx.x;
   // q = reduce(partials), p <- y + beta p, p.q
@@ -382,6 +381,43 @@ __global__ void __launch_bounds__(PT) pcpg_iter_coop(PcpgDev P) {
     sc->delta = delta;
     finalize(P, s_wy, s_ww);
   }
+}
+
+__global__ void __launch_bounds__(PT) pcpg_iter_coop(PcpgDev P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  if (P.sc->done) return;                     // uniform: written by the previous launch only
+  pcpg_vector_phases(P, grid);
+}
+
+// the whole iteration in one cooperative launch: the apply's SYMV on the
+// persistent CTAs (gathering p_new = y + beta p), a grid barrier, the vector
+// phases -- no launch gap between the apply and the vector work
+__global__ void __launch_bounds__(PT, 1) pcpg_iter_fused(PcpgDev P, ApplyArgs A) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  if (P.sc->done) return;
+  apply_body<PT / 32>(A.subs, A.segs, A.seg_ptr, A.part, P.p, P.y, &P.sc->beta, nullptr, A.sb);
+  grid.sync();
+  pcpg_vector_phases(P, grid);
+}
+
+int pcpg_fused_grid(int nctas, size_t smem) {
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaFuncSetAttribute(pcpg_iter_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+    return 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))
+    return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcpg_iter_fused, PT, smem) != cudaSuccess)
+    return 0;
+  return (per_sm * sms >= nctas) ? nctas : 0;   // every apply CTA co-resident
+}
+
+cudaError_t launch_pcpg_iter_fused(const PcpgDev& P, const ApplyArgs& A, int grid, size_t smem, cudaStream_t st) {
+  PcpgDev p = P;
+  ApplyArgs a = A;
+  void* args[] = {&p, &a};
+  return cudaLaunchCooperativeKernel((const void*)pcpg_iter_fused, dim3(grid), dim3(PT), args, smem, st);
 }
 
 int pcpg_coop_grid(int num_sms) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include "feti_coarse.h"
+#include "feti_common.cuh"
 
 namespace feti {
 
@@ -53,6 +54,18 @@ void launch_pcpg_gtx_w(const PcpgDev& P, cudaStream_t st);
 void launch_pcpg_gtx_x(const PcpgDev& P, const double* x, cudaStream_t st);
 void launch_pcpg_update(const PcpgDev& P, int mode, cudaStream_t st);
 size_t pcpg_bpart_doubles(int n_mult, int ncols);
+// the apply's work description (apply_kernel's arguments)
+struct ApplyArgs {
+  const SubDev* subs;
+  const ApplySeg* segs;
+  const int* seg_ptr;
+  double* part;
+  int sb, pad_;
+};
+// the whole iteration (apply + vector work) in one cooperative launch of the
+// apply's CTAs (8 warps each); returns 0 when they cannot all be co-resident
+int pcpg_fused_grid(int nctas, size_t smem);
+cudaError_t launch_pcpg_iter_fused(const PcpgDev& P, const ApplyArgs& A, int grid, size_t smem, cudaStream_t st);
 // one cooperative launch for B + D + F + G (grid-wide barriers); grid <= 0: unavailable
 int pcpg_coop_grid(int num_sms);
 cudaError_t launch_pcpg_iter_coop(const PcpgDev& P, int grid, cudaStream_t st);
