@@ -34,25 +34,24 @@ import test_gpu_parity as t  # noqa: E402
 
 t.test_sparse_pattern_factor_through_cabi()
 print("sparse pattern ok")
-# sparse-factor route: block-sparse device factorization (column launches and
-# the persistent dependency-driven kernel), assembly, rank-2r correction
-for dag in ("0", "1"):
-    os.environ["FETI_SP_DAG"] = dag
-    prob = inputs.Problem("elasticity", 2, 8, 2)
-    ks, qs, fs = [], [], []
-    for s in range(prob.n_sub):
-        k, f, qk = prob.subdomain_system(s)
-        ks.append(k)
-        qs.append(qk)
-        fs.append(f)
-    mats = [inputs.ShapeOnly((prob.n_dofs, prob.n_dofs)) for _ in range(prob.n_sub)]
-    with dualop.prepare(mats, prob.constraints(), prob.layout, CFG, device=0, factorization="sparse",
-                        stiffness=ks, kernels=qs) as op:
-        op.preprocess()
-        q = op.apply(np.random.default_rng(0).normal(size=prob.n_multipliers))
-        print("sparse route dag", dag, "apply norm", np.linalg.norm(q))
+# sparse-factor route: block-sparse device factorization, assembly, rank-2r
+# correction, the device dual right-hand side and the device PCPG
+prob = inputs.Problem("elasticity", 2, 8, 2)
+ks, qs, fs = [], [], []
+for s in range(prob.n_sub):
+    k, f, qk = prob.subdomain_system(s)
+    ks.append(k)
+    qs.append(qk)
+    fs.append(f)
+mats = [inputs.ShapeOnly((prob.n_dofs, prob.n_dofs)) for _ in range(prob.n_sub)]
+with dualop.prepare(mats, prob.constraints(), prob.layout, CFG, device=0, factorization="sparse",
+                    stiffness=ks, kernels=qs, forces=fs) as op:
+    op.preprocess()
+    op.preprocess()
+    q = op.apply(np.random.default_rng(0).normal(size=prob.n_multipliers))
+    lam, it, _ = DevicePCPG(op, qs, fs, prob.c).solve(tol=1e-9)
+    print("sparse route apply norm", np.linalg.norm(q), "device pcpg it", it)
 # tile-aligned dissection (padded positions) and the lumped preconditioner
-os.environ.pop("FETI_SP_DAG", None)
 prob = inputs.Problem("heat", 3, 6, 2)
 ks, qs, fs = [], [], []
 for s in range(prob.n_sub):

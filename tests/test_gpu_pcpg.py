@@ -88,3 +88,20 @@ def test_lumped_preconditioner_matches_reference(case):
     assert it in expected_iterations(case, gl)
     for got in (lam_h, lam):
         assert np.linalg.norm(got - gl["pcpg_lambda"]) <= 1e-9 * np.linalg.norm(gl["pcpg_lambda"])
+
+
+@pytest.mark.parametrize("variant", [{}, {"FETI_APPLY_CPS": "1"}, {"FETI_PCPG_FUSED": "0", "FETI_APPLY_CPS": "1"},
+                                     {"FETI_PCPG_COOP": "0"}])
+def test_device_pcpg_iteration_variants(variant, monkeypatch):
+    """Every device-loop schedule gives the reference's count and multipliers:
+    the fused single-launch iteration (apply + vector phases, 8-warp apply:
+    FETI_APPLY_CPS=1 on these small subdomains), the apply + cooperative
+    vector kernel, and the five-launch iteration (FETI_PCPG_COOP=0)."""
+    for k, v in variant.items():
+        monkeypatch.setenv(k, v)
+    case = "heat3d_4x2"
+    g = load_golden(case)
+    prob = inputs.Problem(str(g["physics"]), int(g["dim"]), int(g["cells"]), int(g["subs"]))
+    lam, it, _ = _solve(prob)
+    assert it in expected_iterations(case, g)
+    assert np.linalg.norm(lam - g["pcpg_lambda"]) <= 1e-9 * np.linalg.norm(g["pcpg_lambda"])
