@@ -716,7 +716,11 @@ def run_sparse(args, rank, world, local_rank):
                   "roofline": {"bound": "hbm", "kernel": "apply_kernel + reduce_kernel",
                                "achieved": app_bytes / (apply_kernel_ms / 1e3) / 1e9, "peak": hbm_peak,
                                "unit": "GB/s", "frac": app_bytes / (apply_kernel_ms / 1e3) / 1e9 / hbm_peak,
-                               "peak_source": hbm_src, "algorithmic_bytes": app_bytes}},
+                               "peak_source": hbm_src, "algorithmic_bytes": app_bytes,
+                               "traffic": (lambda t: (t.get("apply_kernel<8>", 0) + t.get("reduce_kernel", 0)) or None)(
+                                   load_traffic(args.config, "sparse")),
+                               "traffic_note": "DRAM read+write per apply (apply_kernel + reduce_kernel, ncu "
+                                               "dram__bytes_*.sum, profiles/ncu_traffic.json, r02_apply_traffic.md)"}},
         "e2e": {"value": pre_wall + apply_e2e_ms / 1e3, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": int(8 * prob.n_multipliers),
                 "what": "preprocess through the drop-in (sparse K values + kernel basis H2D from page-locked host "

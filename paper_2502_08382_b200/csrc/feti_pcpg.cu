@@ -404,12 +404,21 @@ __global__ void __launch_bounds__(PT, 1) pcpg_iter_fused(PcpgDev P, ApplyArgs A)
 
 int pcpg_fused_grid(int nctas, size_t smem) {
   int per_sm = 0, dev = 0, sms = 0;
-  if (cudaFuncSetAttribute(pcpg_iter_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+  cudaFuncAttributes fa;
+  // the dynamic limit excludes the kernel's static shared memory (227 KB per
+  // block in total); any failure leaves the two-launch iteration in place and
+  // no pending error behind
+  bool ok = cudaFuncGetAttributes(&fa, pcpg_iter_fused) == cudaSuccess &&
+            smem + fa.sharedSizeBytes <= 227 * 1024 &&
+            cudaFuncSetAttribute(pcpg_iter_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(227 * 1024 - fa.sharedSizeBytes)) == cudaSuccess &&
+            cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcpg_iter_fused, PT, smem) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
     return 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))
-    return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcpg_iter_fused, PT, smem) != cudaSuccess)
-    return 0;
+  }
   return (per_sm * sms >= nctas) ? nctas : 0;   // every apply CTA co-resident
 }
 

@@ -506,10 +506,18 @@ class DualOperator:
         Cached per subdomain while the caller hands over an unchanged basis
         (the kernel depends on the mesh only; run_steps rebuilds equal arrays);
         ``changed`` (a list) receives whether the basis differs from the cache."""
-        kern = np.asarray(self.kernels[index], dtype=np.float64).reshape(n, -1)
+        src = self.kernels[index]
         sub = self._subs.get(index)
+        if sub is not None and sub.kcache is not None and sub.kcache[2] is src:
+            # the very object handed over last time: not re-compared (O(n r)
+            # per subdomain and step; a changed basis comes as a new array)
+            if changed is not None:
+                changed.append(False)
+            return sub.kcache[1]
+        kern = np.asarray(src, dtype=np.float64).reshape(n, -1)
         if sub is not None and sub.kcache is not None and sub.kcache[0].shape == kern.shape \
-                and (sub.kcache[0] is kern or np.array_equal(sub.kcache[0], kern)):
+                and np.array_equal(sub.kcache[0], kern):
+            sub.kcache = (sub.kcache[0], sub.kcache[1], src)
             if changed is not None:
                 changed.append(False)
             return sub.kcache[1]
@@ -518,7 +526,7 @@ class DualOperator:
         else:
             q = np.ascontiguousarray(np.linalg.qr(kern)[0])
         if sub is not None:
-            sub.kcache = (kern.copy(), q)
+            sub.kcache = (kern.copy(), q, src)
         if changed is not None:
             changed.append(True)
         return q
