@@ -706,6 +706,8 @@ def run_sparse(args, rank, world, local_rank):
                      "note": "128-row tiles execute executed/algorithmic = "
                              f"{st['flops_factor_exec'] / max(st['flops_factor_alg'], 1.0):.2f}x the scalar flops; "
                              "frac_executed is the DMMA pipe's utilisation"},
+        "assembly_flops": {k: st[k] for k in ("flops_trsm_alg", "flops_trsm_exec", "flops_syrk_alg",
+                                              "flops_syrk_exec", "flops_scale_exec")},
         "phases_ms": {"ms_factorize": statistics.mean(fac_ms), "ms_preprocess": statistics.mean(pre_ms),
                       "ms_assembly_tail": statistics.mean(asm_ms),
                       "note": "each group's interface assembly + correction runs on its stream right behind its "
