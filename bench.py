@@ -720,7 +720,7 @@ def run_sparse(args, rank, world, local_rank):
                                "unit": "GB/s", "frac": app_bytes / (apply_kernel_ms / 1e3) / 1e9 / hbm_peak,
                                "peak_source": hbm_src, "algorithmic_bytes": app_bytes,
                                "traffic": (lambda t: (t.get("apply_kernel<8>", 0) + t.get("reduce_kernel", 0)) or None)(
-                                   load_traffic(args.config, "sparse")),
+                                   load_traffic(args.config, "sparse")) if world == 1 else None,
                                "traffic_note": "DRAM read+write per apply (apply_kernel + reduce_kernel, ncu "
                                                "dram__bytes_*.sum, profiles/ncu_traffic.json, r02_apply_traffic.md)"}},
         "e2e": {"value": pre_wall + apply_e2e_ms / 1e3, "unit": UNIT, "h2d_bytes_per_step": h2d,
