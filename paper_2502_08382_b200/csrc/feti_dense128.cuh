@@ -33,39 +33,42 @@ constexpr int PO_LD = FETI_PO_LD;
 __device__ __forceinline__ void po_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 constexpr int POTRF_SMEM_DOUBLES = TB * PO_LD + TB + 3 * 1024;
 
-// inverse of the 32x32 diagonal block b by one warp (lane = column, forward
-// substitution in registers): Y_bb's strict lower triangle transposed into
-// sA's upper part of the block, its diagonal is sYd
-__device__ __forceinline__ void po_inverse_diag(double* __restrict__ sA, const double* __restrict__ sYd, int b,
-                                                int lane) {
-  const int o = b * 32;
-  double y[32];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const double* Lr = sA + (o + r) * PO_LD + o;
-    double a0 = (r == lane) ? 1.0 : 0.0, a1 = 0.0;
-#pragma unroll
-    for (int j = 0; j < r; ++j) {
-      if (j & 1)
-        a1 = fma(-Lr[j], y[j], a1);
-      else
-        a0 = fma(-Lr[j], y[j], a0);
-    }
-    y[r] = (a0 + a1) * sYd[o + r];
-  }
-#pragma unroll
-  for (int r = 0; r < 32; ++r)
-    if (r > lane) sA[(o + lane) * PO_LD + o + r] = y[r];
-}
-
-// off-diagonal blocks of Y by distance d on the tensor pipe (needs all four
-// diagonal inverses): T = sum_{K=J}^{I-1} L_IK Y_KJ, then Y_IJ = -Y_II T.
-// All 256 threads; ends synchronised.
-__device__ __forceinline__ void po_inverse_offdiag(double* __restrict__ sA, const double* __restrict__ sYd,
-                                                   double* __restrict__ sT) {
+// Y = inv(L) for the 128x128 lower-triangular L in sA (row-major, stride
+// PO_LD, lower triangle) with sYd[i] = 1 / L(i, i): Y's strict lower triangle
+// ends up transposed in sA's strict upper triangle (Y(i, j), i > j, at
+// [j][i]) and its diagonal in sYd.  The four 32x32 diagonal blocks by one
+// warp each (lane = column, forward substitution), the off-diagonal blocks by
+// distance on the tensor pipe: T = sum_{K=J}^{I-1} L_IK Y_KJ, Y_IJ = -Y_II T.
+// sT: 3 x 1024 scratch.  Called by all 256 threads; ends synchronised.
+__device__ __forceinline__ void po_inverse(double* __restrict__ sA, double* __restrict__ sYd,
+                                           double* __restrict__ sT) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, t4 = lane & 3;      // DMMA fragment coordinates
+  // inverses of the four 32x32 diagonal blocks, one warp each, lane = column
+  if (warp < 4) {
+    const int o = warp * 32;
+    double y[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const double* Lr = sA + (o + r) * PO_LD + o;
+      double a0 = (r == lane) ? 1.0 : 0.0, a1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < r; ++j) {
+        if (j & 1)
+          a1 = fma(-Lr[j], y[j], a1);
+        else
+          a0 = fma(-Lr[j], y[j], a0);
+      }
+      y[r] = (a0 + a1) * sYd[o + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r > lane) sA[(o + lane) * PO_LD + o + r] = y[r];
+  }
+  po_sync();
+  // off-diagonal blocks of Y by distance d on the tensor pipe:
+  // T = sum_{K=J}^{I-1} L_IK Y_KJ, then Y_IJ = -Y_II T
   auto ylo = [&](int r, int c) -> double { return r > c ? sA[c * PO_LD + r] : (r == c ? sYd[r] : 0.0); };
   for (int d = 1; d < 4; ++d) {
     const int nb = 4 - d;
@@ -74,24 +77,14 @@ __device__ __forceinline__ void po_inverse_offdiag(double* __restrict__ sA, cons
       const int J = bI, I = bI + d;
       const double* Lr = sA + (I * 32 + tm * 8 + g8) * PO_LD;
       const int cn = J * 32 + tn * 8 + g8;
-      double c0v = 0.0, c1v = 0.0, c2v = 0.0, c3v = 0.0;
-      // K = J (the triangular diagonal block of Y), then K > J, where
-      // Y(k, cn) is always the transposed strict lower part: no branches,
-      // two accumulator chains
-      for (int k0 = J * 32 + tn * 8; k0 < J * 32 + 32; k0 += 4) {
+      double c0v = 0.0, c1v = 0.0;
+      for (int k0 = J * 32 + tn * 8; k0 < I * 32; k0 += 4) {
         const int k = k0 + t4;
         dmma(c0v, c1v, Lr[k], ylo(k, cn));
       }
-      const double* Yc = sA + cn * PO_LD;
-      int k0 = J * 32 + 32;
-      for (; k0 + 4 < I * 32; k0 += 8) {
-        dmma(c0v, c1v, Lr[k0 + t4], Yc[k0 + t4]);
-        dmma(c2v, c3v, Lr[k0 + 4 + t4], Yc[k0 + 4 + t4]);
-      }
-      for (; k0 < I * 32; k0 += 4) dmma(c0v, c1v, Lr[k0 + t4], Yc[k0 + t4]);
       double* Tb = sT + bI * 1024 + (tm * 8 + g8) * 32 + tn * 8 + 2 * t4;
-      Tb[0] = c0v + c2v;
-      Tb[1] = c1v + c3v;
+      Tb[0] = c0v;
+      Tb[1] = c1v;
     }
     po_sync();
     for (int tl = warp; tl < nb * 16; tl += 8) {
@@ -109,20 +102,6 @@ __device__ __forceinline__ void po_inverse_offdiag(double* __restrict__ sA, cons
     }
     po_sync();
   }
-}
-
-// Y = inv(L) for the 128x128 lower-triangular L in sA (row-major, stride
-// PO_LD, lower triangle) with sYd[i] = 1 / L(i, i): Y's strict lower triangle
-// ends up transposed in sA's strict upper triangle (Y(i, j), i > j, at
-// [j][i]) and its diagonal in sYd.  The four diagonal blocks by one warp
-// each, then the off-diagonal blocks on the tensor pipe.  sT: 3 x 1024
-// scratch.  Called by all 256 threads; ends synchronised.
-__device__ __forceinline__ void po_inverse(double* __restrict__ sA, double* __restrict__ sYd,
-                                           double* __restrict__ sT) {
-  const int warp = threadIdx.x >> 5;
-  if (warp < 4) po_inverse_diag(sA, sYd, warp, threadIdx.x & 31);
-  po_sync();
-  po_inverse_offdiag(sA, sYd, sT);
 }
 
 __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, double* __restrict__ D,
@@ -214,11 +193,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
     }
 #endif
 #ifndef PO_SKIP_TRAIL
-    if (warp != 0 && warp != 7 && bb > 0) trail(o - 32, kNextDiagTiles, 1 << 20, 1, 6);
-#endif
-#ifndef PO_SKIP_INV
-    // the previous diagonal block is final: its 32x32 inverse by warp 7
-    if (warp == 7 && bb > 0) po_inverse_diag(sA, sYd, bb - 1, lane);
+    if (warp != 0 && bb > 0) trail(o - 32, kNextDiagTiles, 1 << 20, 1, 7);
 #endif
     po_sync();
     const int R = TB - o - 32;                 // rows below the block
@@ -253,11 +228,7 @@ __device__ __forceinline__ void potrf_invert_128(double* __restrict__ tile, doub
 #endif
   }
 #ifndef PO_SKIP_INV
-  // blocks 0-2 were inverted inside the loop; block 3 now, then the
-  // off-diagonal blocks on the tensor pipe
-  if (warp == 0) po_inverse_diag(sA, sYd, 3, lane);
-  po_sync();
-  po_inverse_offdiag(sA, sYd, sT);
+  po_inverse(sA, sYd, sT);
 #endif
   for (int idx = tid; idx < TILE; idx += 256) {
     const int jl = idx >> 7;
