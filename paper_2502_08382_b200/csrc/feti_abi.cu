@@ -1374,12 +1374,8 @@ static int implicit_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStr
 // apply reads only finalize-time fields of it (F~ tiles, index maps).
 static int apply_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st, bool time_it) {
   if (time_it) CUDA_TRY(cudaEventRecord(c->ev[0], st));
-  if (!launch_apply_reduce(c->apply_nw, c->apply_sb, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply,
-                           c->d_part, d_p, (int)c->n_mult, c->d_cptr, c->d_cent, c->d_ridx, d_q, st)) {
-    launch_apply(c->apply_nw, c->apply_sb, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part,
-                 d_p, st);
-    launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_ridx, c->d_part, d_q, st);
-  }
+  launch_apply(c->apply_nw, c->apply_sb, c->d_subdev, c->d_apply_segs, c->d_apply_seg_ptr, c->n_apply, c->d_part, d_p, st);
+  launch_reduce((int)c->n_mult, c->d_cptr, c->d_cent, c->d_ridx, c->d_part, d_q, st);
   CUDA_TRY(cudaGetLastError());
   if (time_it) CUDA_TRY(cudaEventRecord(c->ev[1], st));
   return mark_apply(c, st);

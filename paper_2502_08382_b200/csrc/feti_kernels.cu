@@ -24,8 +24,6 @@
 #include <cstdlib>
 
 #include "feti_common.cuh"
-#include <cooperative_groups.h>
-
 #include "feti_apply.cuh"
 #include "feti_dense128.cuh"
 #include "feti_kernels.h"
@@ -624,73 +622,6 @@ void launch_apply(int nw, int sb, const SubDev* subs, const ApplySeg* segs, cons
 void launch_reduce(int n_mult, const int* cptr, const int4* cent, const int64_t* ridx, const double* part,
                    double* q, cudaStream_t st) {
   if (n_mult > 0) reduce_kernel<<<(n_mult + 255) / 256, 256, 0, st>>>(n_mult, cptr, cent, ridx, part, q);
-}
-
-// apply + ordered reduction in one cooperative launch of the persistent apply
-// CTAs: the segments' SYMV, a grid barrier, then q over a grid-stride loop (no
-// second launch and its drain between the two)
-template <int NW>
-__global__ void __launch_bounds__(NW * 32) apply_reduce_kernel(const SubDev* __restrict__ subs,
-                                                               const ApplySeg* __restrict__ segs,
-                                                               const int* __restrict__ seg_ptr,
-                                                               double* __restrict__ part,
-                                                               const double* __restrict__ p, int sb, int n_mult,
-                                                               const int* __restrict__ cptr,
-                                                               const int4* __restrict__ cent,
-                                                               const int64_t* __restrict__ ridx,
-                                                               double* __restrict__ q) {
-  apply_body<NW>(subs, segs, seg_ptr, part, p, nullptr, nullptr, nullptr, sb);
-  cooperative_groups::this_grid().sync();
-  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n_mult; g += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int e = cptr[g]; e < cptr[g + 1]; ++e) {
-      const int4 c = cent[e];
-      double v = 0.0;
-      for (int k = c.y; k < c.z; ++k) v += __ldcg(part + ridx[k]);
-      acc += v;
-    }
-    q[g] = acc;
-  }
-}
-
-template <int NW>
-static bool coop_apply_ok(int nctas, size_t smem) {
-  // every apply CTA must be co-resident; the dynamic limit excludes static smem
-  static int cached_nctas = -1;
-  static size_t cached_smem = 0;
-  static bool cached_ok = false;
-  if (nctas == cached_nctas && smem == cached_smem) return cached_ok;
-  cudaFuncAttributes fa;
-  int per_sm = 0, dev = 0, sms = 0;
-  bool ok = cudaFuncGetAttributes(&fa, apply_reduce_kernel<NW>) == cudaSuccess &&
-            smem + fa.sharedSizeBytes <= 227 * 1024 &&
-            cudaFuncSetAttribute(apply_reduce_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(227 * 1024 - fa.sharedSizeBytes)) == cudaSuccess &&
-            cudaGetDevice(&dev) == cudaSuccess &&
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, apply_reduce_kernel<NW>, NW * 32, smem) ==
-                cudaSuccess &&
-            per_sm * sms >= nctas;
-  if (!ok) cudaGetLastError();
-  cached_nctas = nctas;
-  cached_smem = smem;
-  cached_ok = ok;
-  return ok;
-}
-
-bool launch_apply_reduce(int nw, int sb, const SubDev* subs, const ApplySeg* segs, const int* seg_ptr, int nctas,
-                         double* part, const double* p, int n_mult, const int* cptr, const int4* cent,
-                         const int64_t* ridx, double* q, cudaStream_t st) {
-  if (nctas <= 0 || getenv("FETI_APPLY_NOFUSE")) return false;
-  const size_t smem = apply_smem(nw, sb);
-  void* args[] = {&subs, &segs, &seg_ptr, &part, &p, &sb, &n_mult, &cptr, &cent, &ridx, &q};
-  if (nw == 8 && coop_apply_ok<8>(nctas, smem))
-    return cudaLaunchCooperativeKernel((const void*)apply_reduce_kernel<8>, dim3(nctas), dim3(256), args, smem, st) ==
-           cudaSuccess;
-  if (nw == 4 && coop_apply_ok<4>(nctas, smem))
-    return cudaLaunchCooperativeKernel((const void*)apply_reduce_kernel<4>, dim3(nctas), dim3(128), args, smem, st) ==
-           cudaSuccess;
-  return false;
 }
 
 }  // namespace feti

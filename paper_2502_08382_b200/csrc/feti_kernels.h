@@ -27,10 +27,5 @@ void launch_apply(int nw, int sb, const SubDev* subs, const ApplySeg* segs, cons
                   const double* pbeta = nullptr, const int* done = nullptr);
 void launch_reduce(int n_mult, const int* cptr, const int4* cent, const int64_t* ridx, const double* part,
                    double* q, cudaStream_t st);
-// apply + reduction as one cooperative launch (8- or 4-warp CTAs, all
-// co-resident); false: not launched, use launch_apply + launch_reduce
-bool launch_apply_reduce(int nw, int sb, const SubDev* subs, const ApplySeg* segs, const int* seg_ptr, int nctas,
-                         double* part, const double* p, int n_mult, const int* cptr, const int4* cent,
-                         const int64_t* ridx, double* q, cudaStream_t st);
 
 }  // namespace feti
