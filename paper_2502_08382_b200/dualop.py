@@ -204,7 +204,11 @@ class DualOperator:
             kernels = [x.kernel for x in matrices] if kernels is None else kernels
             if forces is None and all(hasattr(x, "force") for x in matrices):
                 forces = [x.force for x in matrices]
-            factorization = factorization or "sparse"
+            # the sparse route assembles F~; the implicit strategy (the
+            # reference's default) runs on the dense-tile host route
+            factorization = factorization or ("host" if config.strategy == "implicit" else "sparse")
+            if factorization != "sparse":
+                forces = None
             matrices = ([x.stiffness_reg for x in matrices] if factorization == "host"
                         else [_Shape(x.stiffness.shape) for x in matrices])
         factorization = factorization or "host"

@@ -100,6 +100,9 @@ def test_problem_like_inputs_select_the_sparse_route():
     assert op.matrices[0].shape == mats[0].shape
     op2 = dualop.DualOperator(subs, cons, lay, dualop.DualOpConfig(strategy="explicit"), factorization="host")
     assert op2.matrices[0] is mats[0]
+    # the reference's default strategy (implicit) takes the dense-tile host route
+    op3 = dualop.DualOperator(subs, cons, lay, dualop.DualOpConfig())
+    assert op3.factorization == "host" and op3.matrices[0] is mats[0]
 
 
 @pytest.mark.parametrize("n", [7, 40])
