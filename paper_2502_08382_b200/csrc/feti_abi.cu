@@ -210,6 +210,7 @@ struct feti_ctx {
   SpDiag* d_sp_diag = nullptr;
   int2* d_sp_panels = nullptr;
   int n_sp_init = 0, n_sp_panels = 0, sp_max_T32 = 0, sp_max_n = 0;
+  int sp_u2_cols = 0;                // implicit sparse route: columns of the U2 sweep (max r, +1 for f')
   // subdomains are split into sp_groups groups, each factored on its own
   // stream: one group's latency-bound diagonal factorizations overlap the
   // DMMA tile work of the others.  Ranges are indexed [g * sp_maxTq + j].
@@ -353,6 +354,7 @@ int build_sparse_tasks(feti_ctx* c) {
     maxTq = std::max(maxTq, P.Tq);
     c->sp_max_T32 = std::max(c->sp_max_T32, s.T32);
     c->sp_max_n = std::max<int>(c->sp_max_n, (int)s.sp_n);
+    c->sp_u2_cols = std::max(c->sp_u2_cols, s.sp_r + (c->dual_rhs ? 1 : 0));
     for (int K = 0; K < P.Tq; ++K)
       for (int L = 0; L <= K; ++L) {
         const int slot = P.tmap[(size_t)K * P.Tq + L];
@@ -751,8 +753,9 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
   if (c->finalized) return fail(FETI_ERR_LIFECYCLE, "prepare was already called on this operator");
   if (n_multipliers < 0 || n_multipliers >= (int64_t)1 << 31) return fail(FETI_ERR_ARG, "bad n_multipliers");
-  if (c->implicit && c->sparse_factor)
-    return fail(FETI_ERR_ARG, "the implicit strategy is not available with the sparse-factor route");
+  if (c->sparse_factor && c->dual_rhs)
+    for (auto& s : c->subs)
+      if (s.sp_r >= 8) return fail(FETI_ERR_ARG, "the device dual rhs needs a kernel dimension < 8");
   CUDA_TRY(cudaSetDevice(c->device));
   c->n_mult = n_multipliers;
   for (auto& s : c->subs)
@@ -1090,6 +1093,8 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
       c->impl_max_blocks = -1;   // implicit apply unavailable for this size
     else
       CUDA_TRY(configure_implicit(c->impl_max_blocks));
+    if (c->implicit && c->sparse_factor && c->impl_max_blocks < 0)
+      return fail(FETI_ERR_CAPACITY, "implicit strategy: subdomain too large for the cluster sweep's shared memory");
   }
   if ((rc = dev_alloc(c, (void**)&c->d_p, (size_t)std::max<int64_t>(c->n_mult, 1) * 8, true))) return rc;
   if ((rc = dev_alloc(c, (void**)&c->d_q, (size_t)std::max<int64_t>(c->n_mult, 1) * 8, true))) return rc;
@@ -1241,9 +1246,17 @@ int feti_assemble(feti_ctx* c) {
                                 c->d_wv[3] + r[3][g].first, r[3][g].second, c->d_wv[4] + r[4][g].first,
                                 r[4][g].second, none, nullptr, &launches)))
         return rc;
-      launch_sp_correct(c->d_subdev, c->d_spsub, c->d_sp_panels + c->sp_corr_rng[g].first, c->sp_corr_rng[g].second,
-                        c->sp_sub_rng[g].first, c->sp_sub_rng[g].second, c->sp_max_T32, gs);
-      launches += 2;
+      if (c->implicit) {
+        // no F~: U2 (and U2f) by the backward sweep; the apply adds the correction
+        launch_implicit_u2(c->d_subdev, c->d_spsub, c->sp_sub_rng[g].first, c->sp_sub_rng[g].second,
+                           c->sp_u2_cols, c->impl_max_blocks, gs);
+        launches += c->sp_u2_cols > 0;
+      } else {
+        launch_sp_correct(c->d_subdev, c->d_spsub, c->d_sp_panels + c->sp_corr_rng[g].first,
+                          c->sp_corr_rng[g].second, c->sp_sub_rng[g].first, c->sp_sub_rng[g].second, c->sp_max_T32,
+                          gs);
+        launches += 2;
+      }
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaEventRecord(c->sp_join[g], gs));
       CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
@@ -1835,12 +1848,10 @@ int feti_solve_many(feti_ctx* c, int64_t nslots, const int64_t* slots, const dou
 }
 
 static int implicit_enqueue(feti_ctx* c, const double* d_p, double* d_q, cudaStream_t st, bool time_it) {
-  if (c->sparse_factor)
-    return fail(FETI_ERR_ARG, "implicit apply is not available with the sparse-factor route");
   if (c->impl_max_blocks < 0)
     return fail(FETI_ERR_CAPACITY, "implicit apply: subdomain too large for the single-CTA sweep");
   if (time_it) CUDA_TRY(cudaEventRecord(c->ev[0], st));
-  launch_implicit_apply(c->d_subdev, (int)c->subs.size(), c->impl_max_blocks, c->d_impl_off, d_p, c->d_impl_part,
+  launch_implicit_apply(c->d_subdev, c->sparse_factor ? c->d_spsub : nullptr, (int)c->subs.size(), c->impl_max_blocks, c->d_impl_off, d_p, c->d_impl_part,
                         (int)c->n_mult, c->d_cptr, c->d_cent, d_q, st);
   CUDA_TRY(cudaGetLastError());
   if (time_it) CUDA_TRY(cudaEventRecord(c->ev[1], st));

@@ -10,10 +10,19 @@
 // smallest first row on, and q needs y only at the constrained rows, so both
 // sweeps run over block rows [smin, T) only -- the tiles the assembly keeps.
 // A 2-CTA cluster per subdomain streams its trailing tiles twice (HBM-bound).
+//
+// Sparse-factor route (K_s = K + rho E E^T factored on the device, see
+// feti_sparse.cu): the same sweeps give F_s p; the rank-2r correction
+//   F~ p = F_s p + U1 (W^T p) - U2 (U1^T p),  W = U1 C - U2 (C = y^T y + I/rho)
+// is added to each subdomain's partial from two r-vectors of dots (W^T p =
+// C U1^T p - U2^T p).  U2 = B~ K_s^-1 Q is solved once per assembly by the
+// backward sweep alone, started from y = L^-1 P Q (the appended block row),
+// one column per launch row (MODE_U2; the device dual rhs's f' column too).
 #include <cooperative_groups.h>
 
 #include "feti_common.cuh"
 #include "feti_implicit.h"
+#include "feti_sparse.h"
 
 namespace feti {
 
@@ -25,14 +34,20 @@ constexpr int IM_CLUSTER = 2;                // CTAs per subdomain (DSMEM exchan
 // are dealt round-robin over the CTA-groups (rank, group); each step's
 // partial sums are exchanged through distributed shared memory so that every
 // CTA holds the full x/u/y vectors.
+enum { MODE_APPLY = 0, MODE_U2 = 1 };
+constexpr int IM_MAXR = 8;
+
+template <int MODE>
 __global__ void __cluster_dims__(IM_CLUSTER, 1, 1) __launch_bounds__(IM_THREADS, 1)
-    implicit_apply_kernel(const SubDev* __restrict__ subs, const int64_t* __restrict__ out_off,
-                          const double* __restrict__ p, double* __restrict__ out) {
+    implicit_apply_kernel(const SubDev* __restrict__ subs, const SpSub* __restrict__ ss, int sub0,
+                          const int64_t* __restrict__ out_off, const double* __restrict__ p,
+                          double* __restrict__ out) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ double ism[];
   const int rank = (int)cluster.block_rank();
-  const SubDev S = subs[blockIdx.x / IM_CLUSTER];
+  const int sub = sub0 + blockIdx.x / IM_CLUSTER;
+  const SubDev S = subs[sub];
   const int nb = S.T - S.smin;             // block rows touched
   double* xs = ism;                        // nb*128: b, then x, then u
   double* ys = ism + nb * TB;              // nb*128: y
@@ -42,8 +57,21 @@ __global__ void __cluster_dims__(IM_CLUSTER, 1, 1) __launch_bounds__(IM_THREADS,
   const int i = tid & (TB - 1), grp = tid >> 7;
   const int lane_id = rank * IM_GROUPS + grp, nlanes = IM_CLUSTER * IM_GROUPS;
   const int r0 = S.smin * TB;
-  const bool active = S.m > 0 && nb > 0;   // uniform over the cluster
-  if (active) {
+  // MODE_U2: launch row q solves column q of y (Q columns, then the f' row)
+  const int qcol = blockIdx.y;
+  int nr = 0;
+  if (MODE == MODE_U2) nr = ss[sub].frow >= 0 ? ss[sub].frow + 1 : ss[sub].r;
+  const bool active = S.m > 0 && nb > 0 && (MODE == MODE_APPLY || qcol < nr);   // uniform over the cluster
+  if (active && MODE == MODE_U2) {
+    // x = y[:, q] over block rows [smin, T): row q of the (P Q)^T block-row tiles
+    const SpSub& Q = ss[sub];
+    for (int a = tid; a < nb * TB; a += IM_THREADS) {
+      const int kb = S.smin + a / TB, il = a % TB;
+      const int slot = Q.tmap[(size_t)Q.T * Q.Tq + kb];
+      xs[a] = slot >= 0 ? Q.pool[(size_t)slot * TILE + swz(il, qcol)] : 0.0;
+    }
+  }
+  if (active && MODE == MODE_APPLY) {
     for (int a = tid; a < nb * TB; a += IM_THREADS) xs[a] = 0.0;
     __syncthreads();
     // b = P B~^T p: columns are sorted by first row, runs of equal rows summed
@@ -72,7 +100,7 @@ __global__ void __cluster_dims__(IM_CLUSTER, 1, 1) __launch_bounds__(IM_THREADS,
   };
   if (active) {
     // ---- forward sweep: x_k = inv(L_kk) b_k - sum_{l<k} Lhat_kl x_l
-    for (int k = S.smin; k < S.T; ++k) {
+    for (int k = S.smin; k < S.T && MODE == MODE_APPLY; ++k) {
       double* bk = xs + (k - S.smin) * TB;
       double acc = 0.0;
       // work items: the k - smin off-diagonal tiles plus the diagonal (inverse) tile
@@ -117,10 +145,73 @@ __global__ void __cluster_dims__(IM_CLUSTER, 1, 1) __launch_bounds__(IM_THREADS,
       if (grp == 0) ys[(k - S.smin) * TB + i] = yk;
     }
     __syncthreads();
+    if (MODE == MODE_U2) {
+      // U2[a][q] = B~_a (K_s^-1 Q)[:, q] (or U2f[a] for the f' column)
+      const SpSub& Q = ss[sub];
+      if (rank == 0)
+        for (int a = tid; a < S.m; a += IM_THREADS) {
+          const double v = S.s_sorted[a] * ys[S.r_sorted[a] - r0];
+          if (qcol < Q.r) Q.U2W[(size_t)a * 2 * Q.r + qcol] = v;
+          else Q.U2f[a] = v;
+        }
+      return;
+    }
     // q_loc[a] = B~_a y[r_a] (sorted local order), written by cluster rank 0
     if (rank == 0) {
-      double* o = out + out_off[blockIdx.x / IM_CLUSTER];
-      for (int a = tid; a < S.m; a += IM_THREADS) o[a] = S.s_sorted[a] * ys[S.r_sorted[a] - r0];
+      double* o = out + out_off[sub];
+      const int r = ss ? ss[sub].r : 0;
+      if (r == 0) {
+        for (int a = tid; a < S.m; a += IM_THREADS) o[a] = S.s_sorted[a] * ys[S.r_sorted[a] - r0];
+      } else {
+        // sparse route: + U1 (C al - be) - U2 al with al = U1^T p, be = U2^T p
+        // (fixed-order reductions: per-thread strided sums, warp tree, warps in order)
+        const SpSub& Q = ss[sub];
+        double d[2 * IM_MAXR];
+#pragma unroll
+        for (int q = 0; q < 2 * IM_MAXR; ++q) d[q] = 0.0;
+        for (int a = tid; a < S.m; a += IM_THREADS) {
+          const double pa = __ldg(p + S.gids_sorted[a]);
+#pragma unroll
+          for (int q = 0; q < IM_MAXR; ++q)
+            if (q < r) {
+              d[q] = fma(Q.U1[(size_t)a * r + q], pa, d[q]);
+              d[IM_MAXR + q] = fma(Q.U2W[(size_t)a * 2 * r + q], pa, d[IM_MAXR + q]);
+            }
+        }
+        const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+        for (int q = 0; q < 2 * IM_MAXR; ++q) {
+          double v = d[q];
+#pragma unroll
+          for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
+          if (lane == 0) red[warp * 2 * IM_MAXR + q] = v;
+        }
+        __syncthreads();
+        double* g = red + (IM_THREADS / 32) * 2 * IM_MAXR;   // al[0..r), ga[0..r)
+        if (tid < 2 * IM_MAXR) {
+          double v = 0.0;
+          for (int w = 0; w < IM_THREADS / 32; ++w) v += red[w * 2 * IM_MAXR + tid];
+          g[tid] = v;
+        }
+        __syncthreads();
+        if (tid < r) {
+          // ga = C al - be,  C[q][q2] = -tile(T,T)[q][q2] + [q == q2] / rho
+          const double* cq = Q.pool + (size_t)Q.tmap[(size_t)Q.T * Q.Tq + Q.T] * TILE;
+          double v = -g[IM_MAXR + tid];
+          for (int q2 = 0; q2 < r; ++q2)
+            v = fma(-cq[swz(q2, tid)] + (tid == q2 ? 1.0 / *Q.rho : 0.0), g[q2], v);
+          g[2 * IM_MAXR + tid] = v;
+        }
+        __syncthreads();
+        for (int a = tid; a < S.m; a += IM_THREADS) {
+          double v = S.s_sorted[a] * ys[S.r_sorted[a] - r0];
+          for (int q = 0; q < r; ++q) {
+            v = fma(Q.U1[(size_t)a * r + q], g[2 * IM_MAXR + q], v);
+            v = fma(-Q.U2W[(size_t)a * 2 * r + q], g[q], v);
+          }
+          o[a] = v;
+        }
+      }
     }
   }
 }
@@ -142,17 +233,30 @@ __global__ void __launch_bounds__(256) implicit_reduce_kernel(int n_mult, const 
 }
 
 size_t implicit_smem(int max_blocks) { return ((size_t)2 * max_blocks * TB + IM_GROUPS * TB) * sizeof(double); }
+static_assert((IM_THREADS / 32 + 2) * 2 * IM_MAXR <= IM_GROUPS * TB, "correction scratch fits the partials buffer");
 
 cudaError_t configure_implicit(int max_blocks) {
-  return cudaFuncSetAttribute(implicit_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(implicit_apply_kernel<MODE_APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)implicit_smem(max_blocks));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(implicit_apply_kernel<MODE_U2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)implicit_smem(max_blocks));
 }
 
-void launch_implicit_apply(const SubDev* subs, int nsub, int max_blocks, const int64_t* out_off, const double* p,
-                           double* part, int n_mult, const int* cptr, const int4* cent, double* q, cudaStream_t st) {
+void launch_implicit_apply(const SubDev* subs, const SpSub* ss, int nsub, int max_blocks, const int64_t* out_off,
+                           const double* p, double* part, int n_mult, const int* cptr, const int4* cent, double* q,
+                           cudaStream_t st) {
   if (nsub > 0)
-    implicit_apply_kernel<<<nsub * IM_CLUSTER, IM_THREADS, implicit_smem(max_blocks), st>>>(subs, out_off, p, part);
+    implicit_apply_kernel<MODE_APPLY>
+        <<<nsub * IM_CLUSTER, IM_THREADS, implicit_smem(max_blocks), st>>>(subs, ss, 0, out_off, p, part);
   if (n_mult > 0) implicit_reduce_kernel<<<(n_mult + 255) / 256, 256, 0, st>>>(n_mult, cptr, cent, out_off, part, q);
+}
+
+void launch_implicit_u2(const SubDev* subs, const SpSub* ss, int sub0, int nsub, int max_cols, int max_blocks,
+                        cudaStream_t st) {
+  if (nsub > 0 && max_cols > 0)
+    implicit_apply_kernel<MODE_U2><<<dim3(nsub * IM_CLUSTER, max_cols), IM_THREADS, implicit_smem(max_blocks), st>>>(
+        subs, ss, sub0, nullptr, nullptr, nullptr);
 }
 
 }  // namespace feti

@@ -204,17 +204,12 @@ class DualOperator:
             kernels = [x.kernel for x in matrices] if kernels is None else kernels
             if forces is None and all(hasattr(x, "force") for x in matrices):
                 forces = [x.force for x in matrices]
-            # the sparse route assembles F~; the implicit strategy (the
-            # reference's default) runs on the dense-tile host route
-            factorization = factorization or ("host" if config.strategy == "implicit" else "sparse")
+            factorization = factorization or "sparse"
             if factorization != "sparse":
                 forces = None
             matrices = ([x.stiffness_reg for x in matrices] if factorization == "host"
                         else [_Shape(x.stiffness.shape) for x in matrices])
         factorization = factorization or "host"
-        if config.strategy == "implicit" and factorization == "sparse":
-            raise ValueError("strategy='implicit' runs on the dense-tile factor routes (factorization='host' or "
-                             "'device'); the sparse-factor route assembles F~ explicitly")
         if ordering not in ORDERINGS:
             raise ValueError(f"ordering must be one of {ORDERINGS}")
         self.matrices = list(matrices)

@@ -276,3 +276,64 @@ def test_prepare_from_problems_runs_the_sparse_route():
     assert np.array_equal(q1, q2)
     assert np.linalg.norm(q1 - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
     assert it in expected_iterations("heat3d_4x2", g)
+
+
+def _implicit_op(prob, subs=None, forces=True):
+    ks, qs, fs = _systems(prob, subs)
+    full = list(range(prob.n_sub))
+    mats = [inputs.ShapeOnly((prob.n_dofs, prob.n_dofs)) for _ in full]
+    op = dualop.prepare(mats, prob.constraints(), prob.layout, dualop.DualOpConfig(strategy="implicit"), device=0,
+                        factorization="sparse", stiffness=[ks.get(s) for s in full],
+                        kernels=[qs.get(s) for s in full], subdomains=subs,
+                        forces=[fs.get(s) for s in full] if forces else None)
+    return op, ks, qs, fs
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+def test_sparse_route_implicit_strategy(case):
+    """strategy='implicit' (the reference's default, dualop.py:59) on the
+    sparse route: no F~ is assembled; each apply runs the two block sweeps over
+    K_s's trailing factor tiles plus the rank-2r correction U1 (W^T p) -
+    U2 (U1^T p) (U2 solved once per assembly by the backward sweep from the
+    factored (P Q)^T row).  q against the reference's implicit q (north-star
+    bar 1e-10), bit-stable, the device dual rhs from the same U2 sweep, and
+    the reference's PCPG iteration count driving it."""
+    g = load_golden(case)
+    prob = inputs.Problem(str(g["physics"]), int(g["dim"]), int(g["cells"]), int(g["subs"]))
+    op, ks, qs, fs = _implicit_op(prob)
+    with op:
+        op.preprocess()
+        st = op.stats()
+        assert st["flops_trsm_exec"] == 0.0 and st["flops_syrk_exec"] == 0.0
+        assert op.local_operator(0) is None
+        q = op.apply(g["p"])
+        assert np.array_equal(q, op.apply(g["p"]))
+        assert np.linalg.norm(q - g["q_implicit"]) <= 1e-10 * np.linalg.norm(g["q_implicit"])
+        qk, fk = [qs[s] for s in range(prob.n_sub)], [fs[s] for s in range(prob.n_sub)]
+        cons = [(prob.gids[s], prob.bcol[s], prob.bval[s]) for s in range(prob.n_sub)]
+        gm, e, d, coarse = ora.assemble_dual_system(qk, fk, cons, prob.n_multipliers, prob.c, op.solve_local)
+        dd = op.dual_rhs(fk) - prob.c
+        assert np.linalg.norm(dd - d) <= 1e-10 * np.linalg.norm(d), case
+        lam, it = ora.pcpg(gm, e, d, coarse, op.apply, tol=1e-9)
+    assert it in expected_iterations(case, g)
+    assert np.linalg.norm(lam - g["pcpg_lambda"]) <= 1e-9 * np.linalg.norm(g["pcpg_lambda"])
+
+
+def test_sparse_route_implicit_matches_explicit_c4_subdomains():
+    """Config 4 (3D elasticity, r = 6): the implicit sparse apply of three
+    subdomains against the explicit sparse route's F~ apply (same K_s
+    factor, 1e-10), and repeated preprocess/apply bit-identical."""
+    prob = inputs.Problem(*inputs.CONFIGS["c4"])
+    subs = [0, 13, 31]
+    p = np.random.default_rng(7).normal(size=prob.n_multipliers)
+    op, _, _, _ = _implicit_op(prob, subs, forces=False)
+    with op:
+        op.preprocess()
+        qi = op.apply(p)
+        op.preprocess()
+        assert np.array_equal(qi, op.apply(p))
+    ope, _, _, _ = _sparse_op(prob, subs)
+    with ope:
+        ope.preprocess()
+        qe = ope.apply(p)
+    assert np.linalg.norm(qi - qe) <= 1e-10 * np.linalg.norm(qe)

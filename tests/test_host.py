@@ -65,17 +65,6 @@ def test_config_mirrors_reference():
     assert cfg2.path == "syrk" and cfg2.strategy == "implicit"
 
 
-def test_implicit_strategy_needs_a_dense_tile_route():
-    """strategy='implicit' runs on the host/device-factor routes; the
-    sparse-factor route only assembles F~ explicitly (rejected up front)."""
-    prob = inputs.Problem("heat", 2, 3, 2)
-    mats, cons, lay = inputs.reference_inputs(prob)
-    shapes = [inputs.ShapeOnly(m.shape) for m in mats]
-    with pytest.raises(ValueError, match="implicit"):
-        dualop.DualOperator(shapes, cons, lay, dualop.DualOpConfig(strategy="implicit"), factorization="sparse",
-                            stiffness=[None] * len(mats), kernels=[None] * len(mats))
-
-
 class _SubProblem:
     """Duck type of the reference's SubdomainProblem (solver.py:100-106)."""
 
@@ -100,9 +89,9 @@ def test_problem_like_inputs_select_the_sparse_route():
     assert op.matrices[0].shape == mats[0].shape
     op2 = dualop.DualOperator(subs, cons, lay, dualop.DualOpConfig(strategy="explicit"), factorization="host")
     assert op2.matrices[0] is mats[0]
-    # the reference's default strategy (implicit) takes the dense-tile host route
+    # the reference's default strategy (implicit) takes the sparse route too
     op3 = dualop.DualOperator(subs, cons, lay, dualop.DualOpConfig())
-    assert op3.factorization == "host" and op3.matrices[0] is mats[0]
+    assert op3.factorization == "sparse" and op3.forces[0] is subs[0].force
 
 
 @pytest.mark.parametrize("n", [7, 40])
