@@ -636,6 +636,45 @@ def run_sparse(args, rank, world, local_rank):
     op.close()
     del op, dco, p_dev, q_dev
     torch.cuda.empty_cache()
+    implicit = None
+    if world == 1:
+        # the reference's default strategy on the same route: no F~, each apply
+        # = two block sweeps over K_s's trailing tiles + the rank-2r correction;
+        # the amortization point vs the explicit strategy (the paper's metric)
+        iop = dualop.DualOperator(mats, cons, prob.layout, dualop.DualOpConfig(strategy="implicit"),
+                                  device=local_rank, subdomains=owned, factorization="sparse", stiffness=stiff,
+                                  kernels=kern)
+        iop.prepare()
+        iop.preprocess()
+        ipre = []
+        for i in range(args.warmup + args.steps):
+            barrier()
+            iop.preprocess_resident()
+            barrier()
+            if i >= args.warmup:
+                ipre.append(iop.stats()["ms_preprocess"])
+        p_dev = torch.from_numpy(np.random.default_rng(0).normal(size=prob.n_multipliers)).to(dev)
+        q_dev = torch.empty_like(p_dev)
+        for _ in range(5):
+            iop.apply_implicit_device(p_dev, q_dev, stream)
+        n_impl = max(10, args.applies // 10)
+        e0.record()
+        for _ in range(n_impl):
+            iop.apply_implicit_device(p_dev, q_dev, stream)
+        e1.record()
+        e1.synchronize()
+        imp_ms = e0.elapsed_time(e1) / n_impl
+        ipre_ms = statistics.mean(ipre)
+        implicit = {"preprocess_ms": ipre_ms, "apply_ms_per_iter": imp_ms,
+                    "amortization_explicit_vs_implicit": amortization_point(
+                        (ipre_ms / 1e3, imp_ms / 1e3), (step_ms / 1e3, apply_kernel_ms / 1e3)),
+                    "what": "strategy='implicit' on the sparse route (device, K resident): preprocess = K_s "
+                            "factorization + diagonal inverses + block scaling + U2 backward sweep; apply = "
+                            "forward/backward block sweeps (2-CTA cluster per subdomain) + correction + reduction"}
+        log(f"[rank {rank}] implicit strategy: preprocess {ipre_ms:.1f} ms, apply {imp_ms:.3f} ms")
+        iop.close()
+        del iop, p_dev, q_dev
+        torch.cuda.empty_cache()
     solve = None
     if world == 1 and args.solve:
         # the device-native PCPG on this route: the loads
@@ -728,6 +767,7 @@ def run_sparse(args, rank, world, local_rank):
                 "what": "preprocess through the drop-in (sparse K values + kernel basis H2D from page-locked host "
                         "buffers, device factorization, assembly, correction) + one apply with host p/q"},
         "prepare_s": t_prepare,
+        "implicit_strategy": implicit,
         "solve": solve,
         "host_side_ms": {"stiffness_upload_per_step": statistics.mean(host_up) * 1e3,
                          "preprocess_wall_per_step": statistics.mean(walls) * 1e3},
