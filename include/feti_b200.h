@@ -250,7 +250,10 @@ int feti_set_forces(feti_ctx* ctx, int64_t nslots, const int64_t* slots, const d
                     const double* const* qtf);
 int feti_dual_rhs(feti_ctx* ctx, const double* c, double* d);
 /* x = K_reg^-1 b for the listed slots (host vectors concatenated in list
- * order), through the device factor (CholFactor.solve, sparse.py:324-337). */
+ * order), through the device factor (CholFactor.solve, sparse.py:324-337):
+ * the dense device factor, or the sparse route's block-sparse factor of
+ * K_s = K + rho E E^T (K_reg^-1 = Pi K_s^-1 Pi + rho^-1 Q Q^T, one CTA per
+ * right-hand side; needs an assembled context, repeated slots allowed). */
 int feti_solve_many(feti_ctx* ctx, int64_t nslots, const int64_t* slots, const double* b, double* x);
 
 /* Lumped preconditioner (make_preconditioner("lumped"), solver.py:155-175):

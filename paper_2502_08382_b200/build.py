@@ -15,7 +15,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libfeti_b200.so")
-SOURCES = ("feti_kernels.cu", "feti_coarse.cu", "feti_implicit.cu", "feti_factor.cu", "feti_sparse.cu", "feti_exchange.cu", "feti_pcpg.cu", "feti_abi.cu")
+SOURCES = ("feti_kernels.cu", "feti_coarse.cu", "feti_implicit.cu", "feti_factor.cu", "feti_sparse.cu", "feti_spsolve.cu", "feti_exchange.cu", "feti_pcpg.cu", "feti_abi.cu")
 HEADERS = ("feti_common.cuh", "feti_dense128.cuh", "feti_kernels.h", "feti_coarse.h", "feti_implicit.h",
            "feti_factor.h", "feti_sparse.h", "feti_exchange.h", "feti_pcpg.h", "feti_apply.cuh")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -171,6 +171,11 @@ struct feti_ctx {
   int* d_bad = nullptr;
   int64_t* d_vec_off = nullptr;
   double *d_sb = nullptr, *d_sx = nullptr;
+  // sparse-route solve: growing per-call buffers (b, x, scratch; items)
+  double* d_sps = nullptr;
+  size_t sps_cap = 0;
+  SpSolveItem* d_sps_items = nullptr;
+  size_t sps_items_cap = 0;
   int* d_slots = nullptr;
   // implicit apply: per-slot offsets into a partial buffer of sum(m) values
   int64_t* d_impl_off = nullptr;
@@ -453,6 +458,7 @@ int build_sparse_tasks(feti_ctx* c) {
     decltype(s.sp.panel)().swap(s.sp.panel);
   }
   CUDA_TRY(configure_sparse());
+  CUDA_TRY(configure_sp_solve());
   return FETI_OK;
 }
 
@@ -1781,6 +1787,7 @@ int feti_factorize(feti_ctx* c) {
     if (!c->subs[i].stiff_set) return fail(FETI_ERR_LIFECYCLE, "subdomain slot %zu has no stiffness", i);
   CUDA_TRY(cudaSetDevice(c->device));
   if (int rc0 = wait_applies(c)) return rc0;
+  c->assembled = false;   // apply / solve need the assembly of the new factor
   if (c->sparse_factor) return factorize_sparse(c);
   cudaStream_t st = c->stream;
   const int ns = (int)c->subs.size();
@@ -1821,8 +1828,57 @@ int feti_factorize(feti_ctx* c) {
   return FETI_OK;
 }
 
+// replace a per-call device buffer by a larger one (frees the old one)
+static int grow(feti_ctx* c, void** p, size_t* cap, size_t bytes) {
+  if (bytes <= *cap) return FETI_OK;
+  if (*p) {
+    c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), *p));
+    c->bytes_temporary -= (int64_t)*cap;
+    CUDA_TRY(cudaFree(*p));
+    *p = nullptr;
+    *cap = 0;
+  }
+  int rc = dev_alloc(c, p, bytes, false);
+  if (rc) return rc;
+  *cap = bytes;
+  return FETI_OK;
+}
+
+// sparse route: one CTA per right-hand side through the block-sparse factor
+static int solve_many_sparse(feti_ctx* c, int64_t nslots, const int64_t* slots, const double* b, double* x) {
+  cudaStream_t st = c->stream;
+  std::vector<SpSolveItem> items((size_t)nslots);
+  int64_t nb = 0, nscr = 0;
+  for (int64_t q = 0; q < nslots; ++q) {
+    if (slots[q] < 0 || slots[q] >= (int64_t)c->subs.size()) return fail(FETI_ERR_ARG, "slot out of range");
+    const SubHost& s = c->subs[slots[q]];
+    items[q] = SpSolveItem{(int)slots[q], 0, nb, nscr};
+    nb += s.sp_n;
+    nscr += 3 * (int64_t)s.sp.T * TB;
+  }
+  int rc;
+  const size_t bytes = (size_t)(2 * nb + nscr) * 8;
+  if ((rc = grow(c, (void**)&c->d_sps, &c->sps_cap, bytes))) return rc;
+  if ((rc = grow(c, (void**)&c->d_sps_items, &c->sps_items_cap, items.size() * sizeof(SpSolveItem)))) return rc;
+  double* db = c->d_sps;
+  double* dx = db + nb;
+  CUDA_TRY(cudaMemcpyAsync(c->d_sps_items, items.data(), items.size() * sizeof(SpSolveItem), cudaMemcpyHostToDevice,
+                           st));
+  CUDA_TRY(cudaMemcpyAsync(db, b, (size_t)nb * 8, cudaMemcpyHostToDevice, st));
+  launch_sp_solve(c->d_subdev, c->d_spsub, c->d_sps_items, (int)nslots, db, dx, dx + nb, st);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(x, dx, (size_t)nb * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return FETI_OK;
+}
+
 int feti_solve_many(feti_ctx* c, int64_t nslots, const int64_t* slots, const double* b, double* x) {
   if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (c->sparse_factor && c->assembled) {
+    if (nslots <= 0 || !slots || !b || !x) return fail(FETI_ERR_ARG, "bad solve arguments");
+    CUDA_TRY(cudaSetDevice(c->device));
+    return solve_many_sparse(c, nslots, slots, b, x);
+  }
   if (!c->device_factor || !c->assembled)
     return fail(FETI_ERR_LIFECYCLE, "solve needs an assembled context with dense device factorization");
   if (nslots <= 0 || nslots > (int64_t)c->subs.size() || !slots || !b || !x) return fail(FETI_ERR_ARG, "bad solve arguments");

@@ -103,4 +103,15 @@ void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, 
                        int max_T32,
                        cudaStream_t st);
 
+// device solve_local (feti_spsolve.cu): one right-hand side per item, b/x at
+// `off` (n values), scratch at `scr` (3 x T*128 values)
+struct SpSolveItem {
+  int sub, pad_;
+  int64_t off, scr;
+};
+size_t sp_solve_smem();
+cudaError_t configure_sp_solve();
+void launch_sp_solve(const SubDev* subs, const SpSub* ss, const SpSolveItem* items, int nitems, const double* b,
+                     double* x, double* scratch, cudaStream_t st);
+
 }  // namespace feti

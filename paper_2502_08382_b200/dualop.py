@@ -155,7 +155,7 @@ def _constraint_rows(sc, n):
 
 class _Sub:
     __slots__ = ("index", "n", "m", "gids", "bcol", "bval", "perm", "iperm", "slot", "values", "pinned",
-                 "cluster", "fix", "solver", "diagpos", "kcache", "npos")
+                 "cluster", "fix", "diagpos", "kcache", "npos")
 
 
 class DualOperator:
@@ -365,7 +365,6 @@ class DualOperator:
                 sub.npos = sub.n
             sub.values = None
             sub.pinned = None
-            sub.solver = None
             sub.fix = None
             sub.diagpos = None
             sub.kcache = None
@@ -541,7 +540,6 @@ class DualOperator:
             if n != sub.n:
                 raise ValueError("stiffness size does not match the subdomain")
             q = self._kernel_basis(sub.index, n)
-            sub.solver = None
             # diagonal positions: the pattern is frozen after the first step
             # (symbolic once, dualop.py:212-269); equality checks are O(nnz)
             # (the reference refills values into a frozen pattern without
@@ -579,7 +577,6 @@ class DualOperator:
                 data[k] = dt.ctypes.data
                 nnz[k] = dt.shape[0]
                 qptr[k] = q.ctypes.data if (changed[0] and q.shape[1] > 0) else None
-                sub.solver = None
             _call(self._lib.feti_set_stiffness_values(self._ctx, ns, _lib.i64ptr(slots), data,
                                                       _lib.i64ptr(nnz), qptr))
         elif self._handed_over and len(subs) > 1:
@@ -804,13 +801,7 @@ class DualOperator:
         if not self.step_ready:
             raise LifecycleError("solve_local before preprocess")
         sub = self._subs[int(index)]
-        if self.factorization == "sparse":
-            x = self._sparse_solver(sub).solve(rhs)
-            if out is not None:
-                out[:] = x
-                return out
-            return x
-        if self.factorization == "device":
+        if self.factorization in ("device", "sparse"):
             x = self.solve_local_many([index], [rhs])[0]
             if out is not None:
                 out[:] = x
@@ -823,9 +814,7 @@ class DualOperator:
         if not self.step_ready:
             raise LifecycleError("solve_local before preprocess")
         subs = [self._subs[int(i)] for i in indices]
-        if self.factorization == "sparse":
-            return [self._sparse_solver(s).solve(r) for s, r in zip(subs, rhs_list)]
-        if self.factorization != "device":
+        if self.factorization not in ("device", "sparse"):
             return [fct.solve_packed(s.values, s.perm, r) for s, r in zip(subs, rhs_list)]
         slots = np.array([s.slot for s in subs], dtype=np.int64)
         b = np.ascontiguousarray(np.concatenate([np.asarray(r, dtype=np.float64) for r in rhs_list]))
@@ -857,14 +846,6 @@ class DualOperator:
         for s, kf in zip(subs, kfs):
             d[s.gids] += s.bval * kf[s.bcol]
         return d
-
-    def _sparse_solver(self, sub):
-        """Host K_reg^-1 through a sparse LU of K_s (solve_local is off the
-        explicit hot path; assemble_dual_system/recover_solution call it)."""
-        if sub.solver is None:
-            sub.solver = spr.HostSparseSolver(self.stiffness[sub.index], self._kernel_basis(sub.index, sub.n),
-                                              sub.fix)
-        return sub.solver
 
     def local_operator(self, index: int):
         """Host copy of F~_i: m x m, upper triangle, strictly lower = 0 (None

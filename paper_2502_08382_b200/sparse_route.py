@@ -79,34 +79,6 @@ def regularization_shift(indptr, indices, data, n: int) -> float:
     return float(np.asarray(data, np.float64)[rows == ix].sum()) / n
 
 
-class HostSparseSolver:
-    """x = K_reg^-1 b = Pi K_s^-1 Pi b + rho^-1 Q Q^T b on the host (solve_local,
-    sparse.py:324-337, for the sparse-factor route; not on the explicit hot
-    path).  K_s is factored once with SuperLU."""
-
-    def __init__(self, stiffness, q: np.ndarray, fix: np.ndarray):
-        from scipy.sparse.linalg import splu
-
-        from .factor import csr_arrays
-
-        n, ip, ix, dt = csr_arrays(stiffness)
-        self.n = n
-        self.q = np.asarray(q, dtype=np.float64).reshape(n, -1)
-        self.rho = regularization_shift(ip, ix, dt, n)
-        fix = np.asarray(fix, np.int64)
-        shift = csr_matrix((np.full(fix.shape[0], self.rho), (fix, fix)), shape=(n, n))
-        k = csr_matrix((dt, ix, ip), shape=(n, n)) + shift
-        self.lu = splu(k.tocsc(), permc_spec="MMD_AT_PLUS_A")
-
-    def _proj(self, v):
-        return v - self.q @ (self.q.T @ v)
-
-    def solve(self, b) -> np.ndarray:
-        b = np.asarray(b, dtype=np.float64)
-        x = self._proj(self.lu.solve(self._proj(b)))
-        return x + self.q @ (self.q.T @ b) / self.rho
-
-
 # ---------------------------------------------------------------------------
 # tile-aligned dissection ordering (padded positions)
 # ---------------------------------------------------------------------------

@@ -337,3 +337,49 @@ def test_sparse_route_implicit_matches_explicit_c4_subdomains():
         ope.preprocess()
         qe = ope.apply(p)
     assert np.linalg.norm(qi - qe) <= 1e-10 * np.linalg.norm(qe)
+
+
+def _woodbury(prob, k, q):
+    return ora.WoodburyKregSolver(prob.n_dofs, k.indptr, k.indices, k.data, q)
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+@pytest.mark.parametrize("strategy", ["explicit", "implicit"])
+def test_sparse_route_device_solve_local(case, strategy):
+    """solve_local / solve_local_many on the sparse route run on the device
+    (feti_solve_many: forward/backward sweeps over the block-sparse factor of
+    K_s, K_reg^-1 = Pi K_s^-1 Pi + rho^-1 Q Q^T; CholFactor.solve,
+    sparse.py:324-337): every subdomain against the oracle's independent
+    Woodbury K_reg^-1 (1e-10), repeated slots allowed, bit-stable."""
+    g = load_golden(case)
+    prob = inputs.Problem(str(g["physics"]), int(g["dim"]), int(g["cells"]), int(g["subs"]))
+    op, ks, qs, fs = (_sparse_op(prob) if strategy == "explicit" else _implicit_op(prob, forces=False))
+    rng = np.random.default_rng(11)
+    idx = list(range(prob.n_sub)) + [0]
+    rhs = [rng.normal(size=prob.n_dofs) for _ in idx]
+    with op:
+        op.preprocess()
+        xs = op.solve_local_many(idx, rhs)
+        x0 = op.solve_local(idx[-1], rhs[-1])
+        assert np.array_equal(op.solve_local_many(idx, rhs)[1], xs[1])
+    assert np.array_equal(x0, xs[-1])
+    for s, b, x in zip(idx, rhs, xs):
+        ref = _woodbury(prob, ks[s], qs[s]).solve(b)
+        assert np.linalg.norm(x - ref) <= 1e-10 * np.linalg.norm(ref), (case, s)
+
+
+@pytest.mark.parametrize("config,subs", [("c4", [0, 21]), ("c5", [0, 17])])
+def test_sparse_route_device_solve_local_large(config, subs):
+    """The device solve at config 4 (3D elasticity, 79 block rows) and config
+    5 (2D elasticity, 33,282 DOFs, 261 block rows: vectors larger than shared
+    memory) against the Woodbury oracle."""
+    prob = inputs.Problem(*inputs.CONFIGS[config])
+    op, ks, qs, fs = _sparse_op(prob, subs)
+    rng = np.random.default_rng(5)
+    rhs = [rng.normal(size=prob.n_dofs) for _ in subs]
+    with op:
+        op.preprocess()
+        xs = op.solve_local_many(subs, rhs)
+    for s, b, x in zip(subs, rhs, xs):
+        ref = _woodbury(prob, ks[s], qs[s]).solve(b)
+        assert np.linalg.norm(x - ref) <= 1e-10 * np.linalg.norm(ref), (config, s)

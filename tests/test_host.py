@@ -13,8 +13,32 @@ from conftest import ROOT
 from paper_2502_08382_b200 import _lib, dualop
 from harness import inputs
 from paper_2502_08382_b200 import factor as fct
+from paper_2502_08382_b200 import sparse_route as spr
 
 HEADER = os.path.join(ROOT, "include", "feti_b200.h")
+
+
+class _HostKsSolver:
+    """x = K_reg^-1 b = Pi K_s^-1 Pi b + rho^-1 Q Q^T b with SuperLU of
+    K_s = K + rho E E^T: the identity the sparse route's correction and its
+    device solve rest on, checked here on the host."""
+
+    def __init__(self, stiffness, q, fix):
+        from scipy.sparse.linalg import splu
+
+        n, ip, ix, dt = fct.csr_arrays(stiffness)
+        self.q = np.asarray(q, dtype=np.float64).reshape(n, -1)
+        self.rho = spr.regularization_shift(ip, ix, dt, n)
+        fix = np.asarray(fix, np.int64)
+        shift = csr_matrix((np.full(fix.shape[0], self.rho), (fix, fix)), shape=(n, n))
+        self.lu = splu((csr_matrix((dt, ix, ip), shape=(n, n)) + shift).tocsc(), permc_spec="MMD_AT_PLUS_A")
+
+    def _proj(self, v):
+        return v - self.q @ (self.q.T @ v)
+
+    def solve(self, b):
+        b = np.asarray(b, dtype=np.float64)
+        return self._proj(self.lu.solve(self._proj(b))) + self.q @ (self.q.T @ b) / self.rho
 
 
 def _declared():
@@ -147,7 +171,6 @@ def test_sparse_route_host_pieces(case):
     from conftest import load_golden
     from oracle import feti_oracle as ora
     from harness import inputs
-    from paper_2502_08382_b200 import sparse_route as spr
 
     g = load_golden(case)
     for s in range(int(g["n_sub"])):
@@ -166,7 +189,7 @@ def test_sparse_route_host_pieces(case):
         dense = k.to_dense()
         dense[fix, fix] += spr.regularization_shift(ip, ix, dt, n)
         assert np.linalg.eigvalsh(dense).min() > 0.0
-        f = ora.fmatrix_via_solver(spr.HostSparseSolver(k, q, fix), n, bcol, bval)
+        f = ora.fmatrix_via_solver(_HostKsSolver(k, q, fix), n, bcol, bval)
         m = f.shape[0]
         ref = np.zeros((m, m))
         ref[np.triu_indices(m)] = g[f"s{s}_F_upper"]
@@ -179,7 +202,6 @@ def test_sparse_route_tile_aligned_dissection():
     recipe for config 3 is a dissection with fewer estimated tile flops
     than the onion ordering."""
     from harness import inputs
-    from paper_2502_08382_b200 import sparse_route as spr
 
     prob = inputs.Problem("heat", 3, 12, 2)
     k, _, q = prob.subdomain_system(3)
