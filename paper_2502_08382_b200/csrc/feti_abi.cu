@@ -768,6 +768,18 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     for (int a = 0; a < s.m; ++a)
       if (s.gids_sorted[a] >= n_multipliers) return fail(FETI_ERR_ARG, "multiplier id out of range");
 
+  if (c->device_factor) {
+    // the factorization and full solves need every tile (tbase = 0) and run
+    // one batched launch per block step: every slot is given the largest
+    // block count, rows >= n being identity (kreg_fill_kernel) -- decoupled,
+    // so L, X and F~ of the real rows are unchanged
+    for (auto& s : c->subs) c->uniform_T = std::max(c->uniform_T, s.T);
+    for (auto& s : c->subs) {
+      s.tbase = 0;
+      if (s.P == 0) s.smin = c->uniform_T;
+      s.T = c->uniform_T;
+    }
+  }
   // capacity check before allocating anything large
   size_t need = 0;
   if (c->sparse_factor)
@@ -794,19 +806,8 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
                 fr, need);
 
   int rc;
-  if (c->device_factor) {
-    // the factorization and full solves need every tile; every slot must
-    // share the block count (one batched launch per factorization step)
-    for (auto& s : c->subs) {
-      s.tbase = 0;
-      if (c->uniform_T == 0) c->uniform_T = s.T;
-      if (s.T != c->uniform_T)
-        return fail(FETI_ERR_ARG, "device factorization needs equally sized subdomains (%d vs %d blocks)", s.T,
-                    c->uniform_T);
-    }
-  } else {
+  if (!c->device_factor)
     for (auto& s : c->subs) s.tbase = s.smin;
-  }
   for (auto& s : c->subs) {
     if (c->sparse_factor) {
       if ((rc = dev_alloc(c, (void**)&s.d_pool, (size_t)std::max<int64_t>(s.sp.ntiles, 1) * TILE * 8, false)))
@@ -1805,7 +1806,9 @@ int feti_factorize(feti_ctx* c) {
   CUDA_TRY(cudaMemcpyAsync(c->d_bad, big.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaEventRecord(c->ev[0], st));
   const int T = c->uniform_T;
-  launch_kreg_build(c->d_subdev, c->d_fsub, ns, T, (int)c->subs[0].n, st);
+  int max_n = 0;
+  for (auto& s : c->subs) max_n = std::max(max_n, (int)s.n);
+  launch_kreg_build(c->d_subdev, c->d_fsub, ns, T, max_n, st);
   CUDA_TRY(cudaGetLastError());
   FETI_DEBUG_SYNC(st);
   for (int k = 0; k < T;) {

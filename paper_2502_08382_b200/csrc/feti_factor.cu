@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(128) kreg_scatter_kernel(const SubDev* __restr
   const int a = blockIdx.x % n;
   const SubDev& S = subs[sub];
   const FactorSub& F = fs[sub];
+  if (a >= S.n) return;   // max_n grid: smaller subdomains skip the tail rows
   const int pa = F.iperm[a];
   for (int64_t p = F.indptr[a] + threadIdx.x; p < F.indptr[a + 1]; p += blockDim.x) {
     const int pb = F.iperm[F.indices[p]];

@@ -100,3 +100,56 @@ def test_device_factor_c3_subdomain_checksums():
     for name, got in (("Fv", full @ g["v"]), ("F_diag", np.diag(full)), ("F_row0", full[0])):
         ref = g[name]
         assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref), name
+
+
+def _with_decoupled_dofs(k, q, extra):
+    """K_ext = blockdiag(K, d I) (d = mean diagonal of K), kernel [Q; 0]."""
+    n = k.shape[0]
+    ip = np.asarray(k.indptr, np.int64)
+    d = float(np.mean(k.to_dense().diagonal()))
+    ip2 = np.concatenate([ip, ip[-1] + 1 + np.arange(extra, dtype=np.int64)])
+    ix2 = np.concatenate([np.asarray(k.indices, np.int64), n + np.arange(extra, dtype=np.int64)])
+    dt2 = np.concatenate([np.asarray(k.data, np.float64), np.full(extra, d)])
+    return (inputs.Csr((n + extra, n + extra), ip2, ix2, dt2),
+            np.vstack([q, np.zeros((extra, q.shape[1]))]))
+
+
+@pytest.mark.parametrize("route", ["device", "sparse"])
+@pytest.mark.parametrize("physics,dim,cells", [("elasticity", 2, 8), ("heat", 3, 5)])
+def test_device_factor_non_uniform_subdomains(physics, dim, cells, route):
+    """Subdomains of different sizes on the device-factor routes (the
+    reference's symbolic/numeric stages are per subdomain, sparse.py:340-424):
+    subdomain 0 carries 300 extra decoupled DOFs, so it spans more 128-row
+    blocks than the others.  Every F~_i, q = F p and solve_local equal the
+    host-factor route's on the same K_reg (1e-10)."""
+    prob = inputs.Problem(physics, dim, cells, 2)
+    ks, qs = [], []
+    for s in range(prob.n_sub):
+        k, _, q = prob.subdomain_system(s)
+        ks.append(k)
+        qs.append(q)
+    ks[0], qs[0] = _with_decoupled_dofs(ks[0], qs[0], 300)
+    assert -(-ks[0].shape[0] // 128) > -(-ks[1].shape[0] // 128)
+    cons, lay = prob.constraints(), prob.layout
+    c0 = cons.per_subdomain[0]
+    mat = c0.matrix
+    cons.per_subdomain[0] = inputs.SubdomainConstraints(
+        c0.multiplier_ids, inputs.Csr((mat.shape[0], ks[0].shape[0]), mat.indptr, mat.indices, mat.data))
+    p = np.random.default_rng(2).normal(size=prob.n_multipliers)
+    b0 = np.random.default_rng(3).normal(size=ks[0].shape[0])
+    host = [inputs.regularized_csr(k, q) for k, q in zip(ks, qs)]
+    with dualop.prepare(host, cons, lay, CFG) as oph:
+        oph.preprocess()
+        fh = [oph.local_operator(s) for s in range(prob.n_sub)]
+        qh = oph.apply(p)
+        xh = oph.solve_local(0, b0)
+    with dualop.prepare([inputs.ShapeOnly(k.shape) for k in ks], cons, lay, CFG, device=0, factorization=route,
+                        stiffness=ks, kernels=qs) as opd:
+        opd.preprocess()
+        fd = [opd.local_operator(s) for s in range(prob.n_sub)]
+        qd = opd.apply(p)
+        xd = opd.solve_local(0, b0)
+    for a, b in zip(fd, fh):
+        assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
+    assert np.linalg.norm(qd - qh) <= 1e-10 * np.linalg.norm(qh)
+    assert np.linalg.norm(xd - xh) <= 1e-10 * np.linalg.norm(xh)
