@@ -58,6 +58,7 @@ enum { FETI_FACTOR_HOST = 0, FETI_FACTOR_DEVICE = 1 };
  * implicit strategy -- no F~, each apply runs two block triangular sweeps
  * over the factor (apply_implicit_local, dualop.py:504-521). */
 enum { FETI_STRATEGY_EXPLICIT = 0, FETI_STRATEGY_IMPLICIT = 1 };
+enum { FETI_PATH_SYRK = 0, FETI_PATH_TRSM = 1 };
 
 typedef struct feti_ctx feti_ctx;
 
@@ -127,9 +128,17 @@ int feti_add_subdomain(feti_ctx* ctx, int64_t n, int64_t m, const int64_t* first
  * 382-388).  Implicit: feti_assemble only prepares the block-scaled factor
  * (no TRSM/SYRK, no F~ memory) and feti_apply/feti_apply_device run the
  * implicit sweeps; feti_local_operator is unavailable (the reference's
- * local_operator returns None, dualop.py:399-401).  Not available with the
- * sparse-factor route. */
+ * local_operator returns None, dualop.py:399-401).  On the sparse-factor
+ * route the apply adds the rank-2r correction (U2 solved once per assembly). */
 int feti_set_strategy(feti_ctx* ctx, int strategy);
+
+/* Choose the explicit assembly's path before feti_finalize (config.path,
+ * assemble_explicit_local, dualop.py:470-479): FETI_PATH_SYRK (default)
+ * F = X^T X; FETI_PATH_TRSM the second triangular solve Y = L^-T X and the
+ * row gather F = B~ Y (spmm_rows), as the reference's "trsm" path -- the
+ * same F~ to roundoff, about twice the flops, extra U/Y panels and a
+ * transposed copy of the trailing factor tiles. */
+int feti_set_path(feti_ctx* ctx, int path);
 
 /* Allocate persistent and temporary device memory; n_multipliers is the
  * global dual-vector length. */

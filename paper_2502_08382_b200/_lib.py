@@ -28,6 +28,8 @@ FETI_FACTOR_HOST = 0
 FETI_FACTOR_DEVICE = 1
 FETI_STRATEGY_EXPLICIT = 0
 FETI_STRATEGY_IMPLICIT = 1
+FETI_PATH_SYRK = 0
+FETI_PATH_TRSM = 1
 
 EXPORTED = (
     "feti_abi_version", "feti_last_error", "feti_create", "feti_destroy", "feti_add_subdomain",
@@ -39,7 +41,7 @@ EXPORTED = (
     "feti_set_preconditioner", "feti_precond_apply", "feti_precond_apply_device",
     "feti_exchange_setup", "feti_exchange_connect", "feti_apply_exchange_device", "feti_exchange_status",
     "feti_set_strategy", "feti_set_stiffness_values", "feti_pcpg_solve", "feti_enable_dual_rhs",
-    "feti_set_forces", "feti_dual_rhs",
+    "feti_set_forces", "feti_dual_rhs", "feti_set_path",
 )
 FETI_IPC_HANDLE_BYTES = 64
 
@@ -102,6 +104,7 @@ def load() -> C.CDLL:
         "feti_coarse_apply_device": ([P, P, P, P], C.c_int),
         "feti_apply_implicit": ([P, f64p, f64p], C.c_int),
         "feti_set_strategy": ([P, C.c_int], C.c_int),
+        "feti_set_path": ([P, C.c_int], C.c_int),
         "feti_set_stiffness_values": ([P, C.c_int64, P, P, P, P], C.c_int),
         "feti_pcpg_solve": ([P, f64p, f64p, C.c_double, C.c_int64, C.c_int, f64p, P, P], C.c_int),
         "feti_enable_dual_rhs": ([P], C.c_int),

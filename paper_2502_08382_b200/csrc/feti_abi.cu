@@ -87,6 +87,7 @@ struct SubHost {
   double* d_tiles = nullptr;
   double* d_X = nullptr;
   double* d_F = nullptr;
+  double *d_U = nullptr, *d_Y = nullptr, *d_Lt = nullptr;   // path "trsm" only
   double* d_Fp = nullptr;            // lumped preconditioner B~ K B~^T, same tile layout as d_F
   int* d_r = nullptr;
   double* d_s = nullptr;
@@ -142,6 +143,7 @@ struct feti_ctx {
   int64_t n_mult = 0;
   bool finalized = false, assembled = false;
   bool implicit = false;             // FETI_STRATEGY_IMPLICIT: no F~, sweeps per apply
+  bool path_trsm = false;            // FETI_PATH_TRSM: F = B~ (L^-T X) instead of X^T X
   std::vector<void*> allocs;
   int64_t bytes_persistent = 0, bytes_temporary = 0;
   // device tables
@@ -324,6 +326,9 @@ void fill_subdev(const feti_ctx* c, std::vector<SubDev>& h) {
     d.tiles = s.d_tiles;
     d.X = s.d_X;
     d.F = s.d_F;
+    d.U = s.d_U;
+    d.Y = s.d_Y;
+    d.Lt = s.d_Lt;
     d.r_sorted = s.d_r;
     d.s_sorted = s.d_s;
     d.gids_sorted = s.d_g;
@@ -755,6 +760,14 @@ int feti_set_strategy(feti_ctx* c, int strategy) {
   return FETI_OK;
 }
 
+int feti_set_path(feti_ctx* c, int path) {
+  if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
+  if (c->finalized) return fail(FETI_ERR_LIFECYCLE, "the path must be chosen before finalize");
+  if (path != FETI_PATH_SYRK && path != FETI_PATH_TRSM) return fail(FETI_ERR_ARG, "unknown path %d", path);
+  c->path_trsm = path == FETI_PATH_TRSM;
+  return FETI_OK;
+}
+
 int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
   if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
   if (c->finalized) return fail(FETI_ERR_LIFECYCLE, "prepare was already called on this operator");
@@ -796,6 +809,8 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
     if (!c->implicit) {
       need += (size_t)s.P * (s.T - s.smin) * TILE * 8;   // X panels
       need += (size_t)s.f_tiles() * ATILE * 8;          // F~
+      if (c->path_trsm)                                  // U, Y panels + transposed trailing tiles
+        need += (size_t)(2 * s.P + (s.T - s.smin + 1) / 2) * (s.T - s.smin) * TILE * 8;
     }
   }
   size_t fr = 0, tot = 0;
@@ -831,6 +846,14 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
         return rc;
       if ((rc = dev_alloc(c, (void**)&s.d_F, (size_t)std::max<int64_t>(s.f_tiles(), 1) * ATILE * 8, true)))
         return rc;
+      if (c->path_trsm) {
+        const size_t pb = (size_t)std::max(s.P, 1) * std::max(s.T - s.smin, 1) * TILE * 8;
+        const int64_t tt = s.T - s.smin;
+        if ((rc = dev_alloc(c, (void**)&s.d_U, pb, false))) return rc;
+        if ((rc = dev_alloc(c, (void**)&s.d_Y, pb, false))) return rc;
+        if ((rc = dev_alloc(c, (void**)&s.d_Lt, (size_t)std::max<int64_t>(tt * (tt + 1) / 2, 1) * TILE * 8, false)))
+          return rc;
+      }
     }
     if ((rc = upload(c, &s.d_r, s.r_sorted))) return rc;
     if ((rc = upload(c, &s.d_s, s.s_sorted))) return rc;
@@ -866,9 +889,13 @@ int feti_finalize(feti_ctx* c, int64_t n_multipliers) {
       wc.push_back(make_int4(si, p, 0, 0));
       const double s0 = s.panel_minrow[p] / TB;
       trsm_exec += tb3 * (s.T - 1 - s0) * (s.T - s0) / 2.0;
+      if (c->path_trsm) {   // backward chain over [smin, T) + inv(L_kk)^T per block row
+        const double tt = s.T - s.smin;
+        trsm_exec += tb3 * (tt * (tt - 1) / 2.0 + tt);
+      }
     }
     const int rend = (int)((s.n + KS - 1) / KS * KS);
-    for (int I = 0; I < s.P && !c->implicit; ++I)
+    for (int I = 0; I < s.P && !c->implicit && !c->path_trsm; ++I)
       for (int J = I; J < s.P; ++J) {
         wy.push_back(make_int4(si, I, J, 0));
         const int rs = std::max(s.panel_minrow[I], s.panel_minrow[J]) & ~(KS - 1);
@@ -1206,6 +1233,11 @@ static int launch_assembly(feti_ctx* c, cudaStream_t st, const int4* wu, int nu,
   CUDA_TRY(cudaGetLastError());
   FETI_DEBUG_SYNC(st);
   if (marks) CUDA_TRY(cudaEventRecord(marks[4], st));
+  if (c->path_trsm) {
+    // second solve + row gather (dualop.py:472-479) in the SYRK's place
+    launch_trsm_path(c->d_subdev, wd, nd, wc, nc, st);
+    *launches += (nd > 0) + 2 * (nc > 0);
+  }
   launch_syrk(c->d_subdev, wy, ny, st);
   *launches += ny > 0;
   CUDA_TRY(cudaGetLastError());

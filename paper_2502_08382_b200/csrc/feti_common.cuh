@@ -86,6 +86,9 @@ struct SubDev {
   double* tiles;            // T(T+1)/2 tiles, col-major swizzled
   double* X;                // P panels x (T*128 rows) x 128, row-major swizzled
   double* F;                // apply tiles (upper triangle of 32x32 tiles)
+  double* U;                // path "trsm": u = L_ll^T Y panels (X layout), or nullptr
+  double* Y;                // path "trsm": Y = L^-T X panels (X layout)
+  double* Lt;               // path "trsm": transposed trailing tiles (slot of (l, k) holds Lhat_lk^T, inv(L_kk)^T)
   const int* r_sorted;      // P*128 first rows, sorted ascending, BIG_ROW pads
   const double* s_sorted;   // P*128 signs (0 for pads)
   const int* gids_sorted;   // T32*32 global multiplier ids (-1 pads)
@@ -114,6 +117,10 @@ __device__ __forceinline__ double* tile_ptr(const SubDev& S, int K, int Lc) {
 // X panel c, global row `row` (>= smin*128), row-major swizzled, 128 wide
 __device__ __forceinline__ double* xrow_ptr(const SubDev& S, int c, int row) {
   return S.X + (size_t)c * (S.T - S.smin) * TILE + (size_t)(row - S.smin * TB) * TB;
+}
+// the same layout in another panel buffer (U, Y of the TRSM path)
+__device__ __forceinline__ double* panel_row_ptr(const SubDev& S, double* base, int c, int row) {
+  return base + (size_t)c * (S.T - S.smin) * TILE + (size_t)(row - S.smin * TB) * TB;
 }
 
 // ---- PTX wrappers ------------------------------------------------------------

@@ -421,6 +421,174 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) trsm_chain_kernel(const SubDe
 }
 
 // ---------------------------------------------------------------------------
+// 4b. path "trsm" (assemble_explicit_local with config.path == "trsm",
+// dualop.py:472-479): the second triangular solve Y = L^-T X and the row
+// gather F = B~ Y (spmm_rows) instead of the SYRK.
+//   transpose_trail_kernel  Lt(l, k) = Lhat_lk^T, Lt(k, k) = inv(L_kk)^T (smin <= k <= l)
+//   backward_chain_kernel   per (subdomain, panel), k = T-1 .. smin:
+//                             u_k = X_k - sum_{l>k} Lhat_lk^T u_l   (u_l = L_ll^T Y_l)
+//                             Y_k = inv(L_kk)^T u_k
+//   trsm_gather_kernel      F[a][b] = s_a Y[r_a][b] (upper), diagonal tiles mirrored
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) transpose_trail_kernel(const SubDev* __restrict__ subs,
+                                                              const int4* __restrict__ work) {
+  __shared__ double blk[32][33];
+  const int4 w = work[blockIdx.x];
+  const SubDev& S = subs[w.x];
+  const int l = w.y;
+  if (l < S.smin) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int k = S.smin; k <= l; ++k) {
+    const double* src = tile_ptr(S, l, k);
+    double* dst = S.Lt + tile_offset(S.smin, l, k);
+    // 32x32 blocks: dst[swz(a, b)] = src[swz(b, a)]
+    for (int bb = 0; bb < 16; ++bb) {
+      const int a0 = (bb >> 2) * 32, b0 = (bb & 3) * 32;
+      for (int y = ty; y < 32; y += 8) blk[y][tx] = src[swz(b0 + y, a0 + tx)];
+      __syncthreads();
+      for (int y = ty; y < 32; y += 8) dst[swz(a0 + y, b0 + tx)] = blk[tx][y];
+      __syncthreads();
+    }
+  }
+}
+
+// consumer side of the bulk-copy ring: acc = sum of nsl (A, B) slices
+__device__ __forceinline__ void pipe_consume(int nsl, double (&acc)[8][4][2], const double* sA, const double* sB,
+                                             uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase, int wm,
+                                             int wn, int g, int t, int lane) {
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int sl = 0; sl < nsl; ++sl) {
+    mbar_wait(&full[stage], phase);
+    mma_slice_128x128(sA + stage * SLICE, sB + stage * SLICE, acc, wm, wn, g, t);
+    fence_proxy_async_shared();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == PIPE_STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(PIPE_THREADS, 1) backward_chain_kernel(const SubDev* __restrict__ subs,
+                                                                         const int4* __restrict__ work) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sA = reinterpret_cast<double*>(smem_raw);
+  double* sB = sA + PIPE_STAGES * SLICE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + PIPE_STAGES * SLICE);
+  uint64_t* empty = full + PIPE_STAGES;
+  uint64_t* uready = empty + PIPE_STAGES;
+
+  const int4 w = work[blockIdx.x];
+  const SubDev& S = subs[w.x];
+  const int c = w.y;
+  const int T = S.T, s0 = S.smin;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PIPE_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 8);
+    }
+    mbar_init(uready, 8);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == 8) {  // ---- producer: (Lhat_lk^T, u_l) slices, then (inv(L_kk)^T, u_k)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      auto issue = [&](const double* At, const double* Bt) {
+        for (int sl = 0; sl < TB / KS; ++sl) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], 2 * SLICE * 8);
+          bulk_g2s(sA + stage * SLICE, At + sl * SLICE, SLICE * 8, &full[stage]);
+          bulk_g2s(sB + stage * SLICE, Bt + sl * SLICE, SLICE * 8, &full[stage]);
+          if (++stage == PIPE_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      };
+      for (int k = T - 1; k >= s0; --k) {
+        for (int l = T - 1; l > k; --l)
+          issue(S.Lt + tile_offset(s0, l, k), panel_row_ptr(S, S.U, c, l * TB));
+        mbar_wait(uready, (uint32_t)((T - 1 - k) & 1));   // u_k written by the consumers
+        issue(S.Lt + tile_offset(s0, k, k), panel_row_ptr(S, S.U, c, k * TB));
+      }
+    }
+    return;
+  }
+
+  const int wm = warp >> 2, wn = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+  double acc[8][4][2];
+  for (int k = T - 1; k >= s0; --k) {
+    pipe_consume((T - 1 - k) * (TB / KS), acc, sA, sB, full, empty, stage, phase, wm, wn, g, t, lane);
+    // u_k = X_k - acc (X_k is zero above the panel's first block row and
+    // was never written there by the forward chain)
+    const double* Xk = xrow_ptr(S, c, k * TB);
+    double* Uk = panel_row_ptr(S, S.U, c, k * TB);
+    const bool xnz = k >= S.panel_minrow[c] / TB;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int i = wm * 64 + mi * 8 + g;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int j0 = wn * 32 + ni * 8 + 2 * t;
+        const double2 x = xnz ? *reinterpret_cast<const double2*>(Xk + swz(i, j0)) : make_double2(0.0, 0.0);
+        *reinterpret_cast<double2*>(Uk + swz(i, j0)) = make_double2(x.x - acc[mi][ni][0], x.y - acc[mi][ni][1]);
+      }
+    }
+    fence_proxy_async_global();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(uready);
+    // Y_k = inv(L_kk)^T u_k
+    pipe_consume(TB / KS, acc, sA, sB, full, empty, stage, phase, wm, wn, g, t, lane);
+    double* Yk = panel_row_ptr(S, S.Y, c, k * TB);
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int i = wm * 64 + mi * 8 + g;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int j0 = wn * 32 + ni * 8 + 2 * t;
+        *reinterpret_cast<double2*>(Yk + swz(i, j0)) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      }
+    }
+  }
+}
+
+// one CTA per (subdomain, panel c): the 4 tile columns of F that panel c's
+// 128 columns make up, rows a <= b
+__global__ void __launch_bounds__(256) trsm_gather_kernel(const SubDev* __restrict__ subs,
+                                                          const int4* __restrict__ work) {
+  const int4 w = work[blockIdx.x];
+  const SubDev& S = subs[w.x];
+  const int c = w.y, T32 = S.T32;
+  auto yval = [&](int a, int b) -> double {   // s_a Y[r_a][b] (0 for padding rows/columns)
+    if (a >= S.m || b >= S.m) return 0.0;
+    const int ra = S.r_sorted[a];
+    const double* yr = panel_row_ptr(S, S.Y, b / TB, ra);
+    return S.s_sorted[a] * yr[(b % TB) ^ ((ra & 3) << 2)];
+  };
+  for (int tj = c * (TB / AT); tj < min((c + 1) * (TB / AT), T32); ++tj)
+    for (int ti = 0; ti <= tj; ++ti) {
+      double* F = S.F + apply_tile_index(ti, tj, T32) * ATILE;
+      for (int e = threadIdx.x; e < ATILE; e += 256) {
+        const int al = e / AT, bl = e % AT;
+        const int a = ti * AT + al, b = tj * AT + bl;
+        F[e] = (ti == tj && al > bl) ? yval(b, a) : yval(a, b);
+      }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // 5. SYRK  F_IJ = X_I^T X_J  (I <= J), pruned to rows >= max first row
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(PIPE_THREADS, 1) syrk_kernel(const SubDev* __restrict__ subs,
@@ -556,6 +724,9 @@ cudaError_t configure_kernels() {
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(trsm_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem())))
     return e;
+  if ((e = cudaFuncSetAttribute(backward_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pipe_smem())))
+    return e;
   if ((e = cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem())))
     return e;
   if ((e = cudaFuncSetAttribute(block_scale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -589,6 +760,14 @@ void launch_block_scale(const SubDev* subs, const int4* work, int nwork, cudaStr
 void launch_trsm_chain(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
   if (nwork > 0) trsm_chain_kernel<<<nwork, PIPE_THREADS, pipe_smem(), st>>>(subs, work);
 }
+void launch_trsm_path(const SubDev* subs, const int4* wd, int nd, const int4* wc, int nc, cudaStream_t st) {
+  if (nd > 0) transpose_trail_kernel<<<nd, 256, 0, st>>>(subs, wd);
+  if (nc > 0) {
+    backward_chain_kernel<<<nc, PIPE_THREADS, pipe_smem(), st>>>(subs, wc);
+    trsm_gather_kernel<<<nc, 256, 0, st>>>(subs, wc);
+  }
+}
+
 void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t st) {
   if (nwork > 0) syrk_kernel<<<nwork, PIPE_THREADS, pipe_smem(), st>>>(subs, work);
 }

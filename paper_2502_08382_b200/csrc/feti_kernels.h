@@ -15,6 +15,9 @@ void launch_diag_inverse(const SubDev* subs, const int4* work, int nwork, cudaSt
 void launch_block_scale(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
 void launch_trsm_chain(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
 void launch_syrk(const SubDev* subs, const int4* work, int nwork, cudaStream_t st);
+// path "trsm": transpose of the trailing tiles (wd: (sub, block row)), the
+// backward chains and the row gather into F (wc: (sub, panel))
+void launch_trsm_path(const SubDev* subs, const int4* wd, int nd, const int4* wc, int nc, cudaStream_t st);
 constexpr int APPLY_MAX_WARPS = 8;   // 3 tile buffers x 32 doubles: > 8 warps spill
 size_t apply_smem(int nw, int sb);
 int apply_max_sb(int nw);   // largest super-block edge (tiles) whose accumulators fit 227 KB

@@ -83,9 +83,11 @@ class DualOpConfig:
     the reference's dense test oracle for F~ (dualop.py:524-549) -- it keeps
     the oracle's size cap and is served by the explicit device assembly (the
     same F~ to rounding, strategy invariance test_dualop.py:297-308).
-    ``path``: the TRSM and
-    SYRK paths produce the same F~_i to roundoff (test_dualop.py:143-149), so
-    both are served by the device SYRK path.  The storage/order knobs select
+    ``path``: "syrk" forms F~ = X^T X; "trsm" (the reference's default) runs
+    the second triangular solve Y = L^-T X and the row gather B~ Y on the
+    device like the reference (dualop.py:472-479) -- the same F~_i to
+    roundoff (test_dualop.py:143-149) at about twice the flops; bench.py uses
+    "syrk".  The storage/order knobs select
     CPU kernel variants in the reference; the device has one tiled layout, so
     they are accepted and have no effect on the result (all variants agree to
     <=1e-12, test_dualop.py:160-176).
@@ -400,6 +402,9 @@ class DualOperator:
                     f"pool of {self.pool.capacity} bytes cannot hold the {need}-byte device operator")
         if self.config.strategy == "implicit":
             _call(self._lib.feti_set_strategy(ctx, _lib.FETI_STRATEGY_IMPLICIT))
+        elif self.config.path == "trsm":
+            # the reference's second solve + row gather (dualop.py:472-479)
+            _call(self._lib.feti_set_path(ctx, _lib.FETI_PATH_TRSM))
         if self.factorization == "device":
             _call(self._lib.feti_enable_device_factorization(ctx))
         if self.factorization == "sparse":

@@ -18,7 +18,8 @@ for s in range(prob.n_sub):
     qs.append(q)
     fs.append(f)
 mats = [inputs.ShapeOnly((prob.n_dofs, prob.n_dofs))] * prob.n_sub
-op = dualop.prepare(mats, prob.constraints(), prob.layout, dualop.DualOpConfig(strategy="explicit"), device=0,
+cfg_op = dualop.DualOpConfig(strategy="explicit", path="syrk")
+op = dualop.prepare(mats, prob.constraints(), prob.layout, cfg_op, device=0,
                     factorization="sparse", stiffness=ks, kernels=qs, forces=fs)
 op.preprocess()
 sol = DevicePCPG(op, qs, fs, prob.c)

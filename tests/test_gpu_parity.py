@@ -442,3 +442,41 @@ def test_apply_without_multiplier_limit():
         assert np.linalg.norm(q - qr) <= 1e-12 * np.linalg.norm(qr)
     finally:
         lib.feti_destroy(ctx)
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+@pytest.mark.parametrize("factorization", ["host", "device", "sparse"])
+def test_trsm_path_matches_reference(case, factorization):
+    """config.path="trsm" (the reference's default path, dualop.py:472-479):
+    the second triangular solve Y = L^-T X on the device (transposed trailing
+    tiles, backward DMMA chains) and the row gather F = B~ Y instead of the
+    SYRK.  Every F~_i and q against the reference (north-star bar 1e-10) on
+    the three factor routes; F~ agrees with the SYRK path to rounding."""
+    g = load_golden(case)
+    prob, mats, cons, lay = _golden_problem(g)
+    kw = {}
+    if factorization != "host":
+        ks, qs = [], []
+        for s in range(prob.n_sub):
+            k, _, q = prob.subdomain_system(s)
+            ks.append(k)
+            qs.append(q)
+        kw = dict(factorization=factorization, stiffness=ks, kernels=qs, device=0)
+        mats = [inputs.ShapeOnly(m.shape) for m in mats]
+    fs = {}
+    for path in ("trsm", "syrk"):
+        with dualop.prepare(mats, cons, lay, dualop.DualOpConfig(strategy="explicit", path=path), **kw) as op:
+            op.preprocess()
+            fs[path] = [op.local_operator(s) for s in range(prob.n_sub)]
+            q = op.apply(g["p"])
+            if path == "trsm":
+                assert op.stats()["flops_syrk_exec"] == 0.0
+                assert np.linalg.norm(q - g["q_explicit"]) <= 1e-10 * np.linalg.norm(g["q_explicit"])
+    for s in range(prob.n_sub):
+        m = prob.gids[s].shape[0]
+        ref = np.zeros((m, m))
+        ref[np.triu_indices(m)] = g[f"s{s}_F_upper"]
+        f = fs["trsm"][s]
+        assert np.all(np.tril(f, -1) == 0.0)
+        assert np.linalg.norm(f - ref) <= 1e-10 * np.linalg.norm(ref), (case, s)
+        assert np.linalg.norm(f - fs["syrk"][s]) <= 1e-12 * np.linalg.norm(ref)
