@@ -109,8 +109,13 @@ __global__ void __cluster_dims__(IM_CLUSTER, 1, 1) __launch_bounds__(IM_THREADS,
         if (l < k) {
           const double* t = tile_ptr(S, k, l);
           const double* xl = xs + (l - S.smin) * TB;
-#pragma unroll 8
-          for (int j = 0; j < TB; ++j) acc = fma(-__ldcs(t + swz(j, i)), xl[j], acc);
+          double a2 = 0.0;
+#pragma unroll 16
+          for (int j = 0; j < TB; j += 2) {
+            acc = fma(-__ldcs(t + swz(j, i)), xl[j], acc);
+            a2 = fma(-__ldcs(t + swz(j + 1, i)), xl[j + 1], a2);
+          }
+          acc += a2;
         } else {
           const double* inv = tile_ptr(S, k, k);
 #pragma unroll 8
@@ -128,8 +133,13 @@ __global__ void __cluster_dims__(IM_CLUSTER, 1, 1) __launch_bounds__(IM_THREADS,
         const int l = k + 1 + w;
         const double* col = tile_ptr(S, l, k) + i * TB;     // column i of Lhat_lk
         const double* ul = xs + (l - S.smin) * TB;
-#pragma unroll 8
-        for (int r = 0; r < TB; ++r) acc = fma(__ldcs(col + (r ^ ((i & 3) << 2))), ul[r], acc);
+        double a2 = 0.0;
+#pragma unroll 16
+        for (int r = 0; r < TB; r += 2) {
+          acc = fma(__ldcs(col + (r ^ ((i & 3) << 2))), ul[r], acc);
+          a2 = fma(__ldcs(col + ((r + 1) ^ ((i & 3) << 2))), ul[r + 1], a2);
+        }
+        acc += a2;
       }
       double* uk = xs + (k - S.smin) * TB;
       const double uk_i = uk[i] - combine(acc);
