@@ -747,6 +747,16 @@ def run_sparse(args, rank, world, local_rank):
                              "frac_executed is the DMMA pipe's utilisation"},
         "assembly_flops": {k: st[k] for k in ("flops_trsm_alg", "flops_trsm_exec", "flops_syrk_alg",
                                               "flops_syrk_exec", "flops_scale_exec")},
+        "roofline_step": (lambda alg, ex: {
+            "bound": "tensor", "unit": "TFLOP/s", "peak": peak_f64,
+            "algorithmic_flops": alg, "achieved": alg / (step_ms / 1e3) / 1e12,
+            "frac": alg / (step_ms / 1e3) / 1e12 / peak_f64,
+            "executed_flops": ex, "frac_executed": ex / (step_ms / 1e3) / 1e12 / peak_f64,
+            "what": "the whole step (factorization + interface TRSM/SYRK + correction) against DGEMM: scalar "
+                    "Cholesky flops of K_s plus the pruned TRSM/SYRK counts of the interface block, over "
+                    "ms_per_step (supplementary to `roofline`, which is the factorization alone)"})(
+            st["flops_factor_alg"] + st["flops_trsm_alg"] + st["flops_syrk_alg"],
+            st["flops_factor_exec"] + st["flops_trsm_exec"] + st["flops_syrk_exec"] + st["flops_scale_exec"]),
         "phases_ms": {"ms_factorize": statistics.mean(fac_ms), "ms_preprocess": statistics.mean(pre_ms),
                       "ms_assembly_tail": statistics.mean(asm_ms),
                       "note": "each group's interface assembly + correction runs on its stream right behind its "
