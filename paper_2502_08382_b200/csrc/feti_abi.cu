@@ -329,6 +329,11 @@ void fill_subdev(const feti_ctx* c, std::vector<SubDev>& h) {
     d.U = s.d_U;
     d.Y = s.d_Y;
     d.Lt = s.d_Lt;
+    // sparse route, SYRK path: the rank-2r correction rides in the SYRK epilogue
+    const bool fused = c->sparse_factor && !c->implicit && !c->path_trsm && s.sp_r > 0 && s.d_U1;
+    d.U1 = fused ? s.d_U1 : nullptr;
+    d.U2W = fused ? s.d_U2W : nullptr;
+    d.kr = fused ? s.sp_r : 0;
     d.r_sorted = s.d_r;
     d.s_sorted = s.d_s;
     d.gids_sorted = s.d_g;
@@ -1280,16 +1285,24 @@ int feti_assemble(feti_ctx* c) {
       // the captured graph ran on the context stream
       if (c->sp_graph_used) CUDA_TRY(cudaStreamWaitEvent(gs, c->ev[2], 0));
       std::vector<int> none;
+      const bool fused = !c->implicit && !c->path_trsm;   // the SYRK follows sp_u2 below
       if ((rc = launch_assembly(c, gs, c->d_wv[0] + r[0][g].first, r[0][g].second, c->d_wv[1] + r[1][g].first,
                                 r[1][g].second, c->d_wv[2] + r[2][g].first, r[2][g].second,
                                 c->d_wv[3] + r[3][g].first, r[3][g].second, c->d_wv[4] + r[4][g].first,
-                                r[4][g].second, none, nullptr, &launches)))
+                                fused ? 0 : r[4][g].second, none, nullptr, &launches)))
         return rc;
       if (c->implicit) {
         // no F~: U2 (and U2f) by the backward sweep; the apply adds the correction
         launch_implicit_u2(c->d_subdev, c->d_spsub, c->sp_sub_rng[g].first, c->sp_sub_rng[g].second,
                            c->sp_u2_cols, c->impl_max_blocks, gs);
         launches += c->sp_u2_cols > 0;
+      } else if (!c->path_trsm) {
+        // U2/W from X, then the SYRK with the correction in its epilogue
+        // (launch_assembly above ran without the SYRK: ny = 0)
+        launch_sp_u2(c->d_subdev, c->d_spsub, c->d_sp_panels + c->sp_corr_rng[g].first, c->sp_corr_rng[g].second,
+                     gs);
+        launch_syrk(c->d_subdev, c->d_wv[4] + r[4][g].first, r[4][g].second, gs);
+        launches += (c->sp_corr_rng[g].second > 0) + (r[4][g].second > 0);
       } else {
         launch_sp_correct(c->d_subdev, c->d_spsub, c->d_sp_panels + c->sp_corr_rng[g].first,
                           c->sp_corr_rng[g].second, c->sp_sub_rng[g].first, c->sp_sub_rng[g].second, c->sp_max_T32,

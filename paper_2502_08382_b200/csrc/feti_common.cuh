@@ -89,6 +89,8 @@ struct SubDev {
   double* U;                // path "trsm": u = L_ll^T Y panels (X layout), or nullptr
   double* Y;                // path "trsm": Y = L^-T X panels (X layout)
   double* Lt;               // path "trsm": transposed trailing tiles (slot of (l, k) holds Lhat_lk^T, inv(L_kk)^T)
+  const double* U1;         // sparse route, fused correction in the SYRK epilogue (kr > 0):
+  const double* U2W;        //   F[a][b] += U1[a] . W[b] - U2[a] . U1[b]  (feti_sparse.h SpSub)
   const int* r_sorted;      // P*128 first rows, sorted ascending, BIG_ROW pads
   const double* s_sorted;   // P*128 signs (0 for pads)
   const int* gids_sorted;   // T32*32 global multiplier ids (-1 pads)
@@ -99,6 +101,7 @@ struct SubDev {
   int smin;                 // first block row any X column reaches (pruning)
   int tbase;                // first block row/column stored in `tiles`
   int src;                  // factor source: SRC_RAW_DENSE / SRC_RAW_SPARSE / SRC_TILES
+  int kr;                   // kernel dimension of the fused correction (0: none)
 };
 
 enum { SRC_RAW_DENSE = 0, SRC_RAW_SPARSE = 1, SRC_TILES = 2 };

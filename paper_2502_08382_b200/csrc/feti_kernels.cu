@@ -660,6 +660,30 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) syrk_kernel(const SubDev* __r
     }
   }
   const int T32 = S.T32;
+  if (S.kr > 0) {
+    // sparse route: + U1[a] . W[b] - U2[a] . U1[b]  (W = C U1 - U2; U2W rows hold [U2 | W])
+    const int r = S.kr;
+    for (int q = 0; q < r; ++q) {
+      double u1b[4][2], wb[4][2];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int b = J * TB + wn * 32 + ni * 8 + 2 * t + e;
+          u1b[ni][e] = S.U1[(size_t)b * r + q];
+          wb[ni][e] = S.U2W[(size_t)b * 2 * r + r + q];
+        }
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) {
+        const int a = I * TB + wm * 64 + mi * 8 + g;
+        const double u1a = S.U1[(size_t)a * r + q], u2a = S.U2W[(size_t)a * 2 * r + q];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) acc[mi][ni][e] += u1a * wb[ni][e] - u2a * u1b[ni][e];
+      }
+    }
+  }
 #pragma unroll
   for (int mi = 0; mi < 8; ++mi) {
     const int a = I * TB + wm * 64 + mi * 8 + g;

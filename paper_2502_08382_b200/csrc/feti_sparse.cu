@@ -560,6 +560,10 @@ void launch_sp_dual_rhs(const SpSub* ss, int n_mult, const int* cptr, const int4
   if (n_mult > 0) sp_dual_rhs_kernel<<<(n_mult + 255) / 256, 256, 0, st>>>(ss, n_mult, cptr, cent, c, d);
 }
 
+void launch_sp_u2(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, cudaStream_t st) {
+  if (npanels > 0) sp_u2_kernel<<<npanels, U2_GROUPS * TB, 0, st>>>(subs, ss, panels);
+}
+
 void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int sub0, int nsub,
                        int max_T32, cudaStream_t st) {
   if (npanels > 0) sp_u2_kernel<<<npanels, U2_GROUPS * TB, 0, st>>>(subs, ss, panels);

@@ -98,6 +98,8 @@ void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st);
 // (assemble_dual_system, solver.py:141-143), from U2f, U1, y^T y_f, rho, Q^T f
 void launch_sp_dual_rhs(const SpSub* ss, int n_mult, const int* cptr, const int4* cent, const double* c, double* d,
                         cudaStream_t st);
+// U2/W (and U2f) per (sub, panel) from the X panels
+void launch_sp_u2(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, cudaStream_t st);
 // after the assembly: U2/W per (sub, panel), then the rank-2r update of F~
 void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int sub0, int nsub,
                        int max_T32,
