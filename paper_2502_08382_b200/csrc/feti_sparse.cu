@@ -311,12 +311,14 @@ __global__ void __launch_bounds__(U2_GROUPS * TB) sp_u2_kernel(const SubDev* __r
   if (r == 0) return;
   double* out = Q.U2W + (size_t)a * 2 * r;
   const double* u1 = Q.U1 + (size_t)a * r;
-  for (int q = 0; q < r; ++q) {
-    double w = -acc[q];
-    for (int q2 = 0; q2 < r; ++q2) w = fma(Cm[q * r + q2], u1[q2], w);
-    out[q] = acc[q];
-    out[r + q] = (a < S.m) ? w : 0.0;
-  }
+#pragma unroll
+  for (int q = 0; q < MAXR; ++q)
+    if (q < r) {
+      double w = -acc[q];
+      for (int q2 = 0; q2 < r; ++q2) w = fma(Cm[q * r + q2], u1[q2], w);
+      out[q] = acc[q];
+      out[r + q] = (a < S.m) ? w : 0.0;
+    }
 }
 
 // F[a][b] += U1[a] . W[b] - U2[a] . U1[b] over every stored apply tile
