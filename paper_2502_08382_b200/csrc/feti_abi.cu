@@ -436,12 +436,19 @@ int build_sparse_tasks(feti_ctx* c) {
       return x.npairs * ((x.flags & 2) ? 1 : 4) > y.npairs * ((y.flags & 2) ? 1 : 4);
     });
     c->sp_acc_rng[gj] = {b, (int)tasks.size() - b};
+    // inv(L_jj): the subdomain's scratch, or -- in the trailing triangle,
+    // where the assembly wants inv(L_jj) in the diagonal tile anyway -- the
+    // diagonal tile itself (potrf_invert_128 stores L, then the inverse over it)
+    auto dinv_of = [&](int si) -> double* {
+      const SubHost& s = c->subs[si];
+      return j >= s.smin ? s.d_pool + (size_t)s.sp.tmap[(size_t)j * s.sp.Tq + j] * TILE
+                         : c->d_dinv + (size_t)si * TILE;
+    };
     const int db = (int)diag.size();
     for (int si = 0; si < ns; ++si) {
       const SubHost& s = c->subs[si];
       if (j >= s.sp.T || group_of(si) != g) continue;
-      diag.push_back(SpDiag{s.d_pool + (size_t)s.sp.tmap[(size_t)j * s.sp.Tq + j] * TILE,
-                            c->d_dinv + (size_t)si * TILE, si, j * TB});
+      diag.push_back(SpDiag{s.d_pool + (size_t)s.sp.tmap[(size_t)j * s.sp.Tq + j] * TILE, dinv_of(si), si, j * TB});
     }
     c->sp_diag_rng[gj] = {db, (int)diag.size() - db};
     b = (int)tasks.size();
@@ -451,7 +458,7 @@ int build_sparse_tasks(feti_ctx* c) {
       for (int slot : s.sp.panel[j]) {
         double* C = s.d_pool + (size_t)slot * TILE;
         tasks.push_back(SpTask{C, (int64_t)pairs.size(), 1, qrow[si][slot] ? 3 : 1});
-        pairs.push_back(SpPair{C, c->d_dinv + (size_t)si * TILE});
+        pairs.push_back(SpPair{C, dinv_of(si)});
       }
     }
     c->sp_panel_rng[gj] = {b, (int)tasks.size() - b};
@@ -1213,6 +1220,8 @@ int feti_set_factor(feti_ctx* c, int64_t slot, const double* values, int64_t nnz
 static int launch_assembly(feti_ctx* c, cudaStream_t st, const int4* wu, int nu, const int4* wd, int nd,
                            const int4* ws, int ns, const int4* wc, int nc, const int4* wy, int ny,
                            const std::vector<int>& sparse_slots, cudaEvent_t* marks, int* launches) {
+  // the sparse factorization already left inv(L_kk) in the trailing diagonal tiles
+  const bool inv_ready = c->sparse_factor;
   if (marks) CUDA_TRY(cudaEventRecord(marks[0], st));
   launch_unpack(c->d_subdev, wu, nu, st);
   *launches += nu > 0;
@@ -1223,8 +1232,10 @@ static int launch_assembly(feti_ctx* c, cudaStream_t st, const int4* wu, int nu,
   CUDA_TRY(cudaGetLastError());
   FETI_DEBUG_SYNC(st);
   if (marks) CUDA_TRY(cudaEventRecord(marks[1], st));
-  launch_diag_inverse(c->d_subdev, wd, nd, st);
-  *launches += nd > 0;
+  if (!inv_ready) {
+    launch_diag_inverse(c->d_subdev, wd, nd, st);
+    *launches += nd > 0;
+  }
   CUDA_TRY(cudaGetLastError());
   FETI_DEBUG_SYNC(st);
   if (marks) CUDA_TRY(cudaEventRecord(marks[2], st));
