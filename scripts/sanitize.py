@@ -68,3 +68,21 @@ with dualop.prepare(mats, prob.constraints(), prob.layout, CFG, device=0, factor
     op.set_lumped_preconditioner(ks)
     mq = op.precond_apply(q)
     print("dissection route apply norm", np.linalg.norm(q), "lumped", np.linalg.norm(mq))
+    xs = op.solve_local_many(list(range(prob.n_sub)), [np.ones(prob.n_dofs)] * prob.n_sub)
+    print("sparse device solve_local norm", np.linalg.norm(xs[0]))
+# path "trsm" (transposed trailing tiles, backward chains, row gather) on the
+# sparse route, and the implicit strategy on the sparse route (U2 sweep +
+# corrected sweeps)
+prob = inputs.Problem("elasticity", 2, 8, 2)
+ks, qs = [], []
+for s in range(prob.n_sub):
+    k, _, qk = prob.subdomain_system(s)
+    ks.append(k)
+    qs.append(qk)
+mats = [inputs.ShapeOnly((prob.n_dofs, prob.n_dofs)) for _ in range(prob.n_sub)]
+p = np.random.default_rng(0).normal(size=prob.n_multipliers)
+for cfg in (dualop.DualOpConfig(strategy="explicit", path="trsm"), dualop.DualOpConfig(strategy="implicit")):
+    with dualop.prepare(mats, prob.constraints(), prob.layout, cfg, device=0, factorization="sparse",
+                        stiffness=ks, kernels=qs) as op:
+        op.preprocess()
+        print(cfg.strategy, cfg.path, "sparse route apply norm", np.linalg.norm(op.apply(p)))
