@@ -1311,13 +1311,13 @@ int feti_assemble(feti_ctx* c) {
         // U2/W from X, then the SYRK with the correction in its epilogue
         // (launch_assembly above ran without the SYRK: ny = 0)
         launch_sp_u2(c->d_subdev, c->d_spsub, c->d_sp_panels + c->sp_corr_rng[g].first, c->sp_corr_rng[g].second,
-                     gs);
+                     c->sp_u2_cols, gs);
         launch_syrk(c->d_subdev, c->d_wv[4] + r[4][g].first, r[4][g].second, gs);
         launches += (c->sp_corr_rng[g].second > 0) + (r[4][g].second > 0);
       } else {
         launch_sp_correct(c->d_subdev, c->d_spsub, c->d_sp_panels + c->sp_corr_rng[g].first,
                           c->sp_corr_rng[g].second, c->sp_sub_rng[g].first, c->sp_sub_rng[g].second, c->sp_max_T32,
-                          gs);
+                          c->sp_u2_cols, gs);
         launches += 2;
       }
       CUDA_TRY(cudaGetLastError());

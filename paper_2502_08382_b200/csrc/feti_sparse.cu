@@ -254,6 +254,10 @@ constexpr int MAXR = 8;
 // W[a] = C U1[a] - U2[a] with C = y^T y + I/rho = -tile(T,T) + I/rho
 constexpr int U2_GROUPS = 4;   // row groups per CTA (U2_GROUPS x 128 threads)
 
+// NR: accumulator columns (>= every launched subdomain's nr), CH independent
+// row chains per thread (loads in flight: the kernel is latency-bound at one
+// row per chain step)
+template <int NR, int CH>
 __global__ void __launch_bounds__(U2_GROUPS * TB) sp_u2_kernel(const SubDev* __restrict__ subs,
                                                               const SpSub* __restrict__ ss,
                                                               const int2* __restrict__ panels) {
@@ -272,51 +276,61 @@ __global__ void __launch_bounds__(U2_GROUPS * TB) sp_u2_kernel(const SubDev* __r
     Cm[threadIdx.x] = -cq[swz(q2, q)] + (q == q2 ? 1.0 / *Q.rho : 0.0);
   }
   // rows split over the row groups (row = kb*128 + il, il = rg mod U2_GROUPS),
-  // two independent accumulator chains per group
-  double acc[MAXR], acc2[MAXR];
+  // CH independent accumulator chains per group
+  double acc[CH][NR];
 #pragma unroll
-  for (int q = 0; q < MAXR; ++q) acc[q] = acc2[q] = 0.0;
+  for (int h = 0; h < CH; ++h)
+#pragma unroll
+    for (int q = 0; q < NR; ++q) acc[h][q] = 0.0;
   const int r0 = (S.panel_minrow[c] / TB) * TB;
   for (int kb = r0 / TB; kb < T; ++kb) {
     const double* yt = Q.pool + (size_t)Q.tmap[T * Q.Tq + kb] * TILE;
-    for (int il = rg; il < TB; il += 2 * U2_GROUPS) {
-      const int row = kb * TB + il, row2 = row + U2_GROUPS;
-      const double x = xrow_ptr(S, c, row)[col ^ ((row & 3) << 2)];
-      const double x2 = xrow_ptr(S, c, row2)[col ^ ((row2 & 3) << 2)];
+    for (int il = rg; il < TB; il += CH * U2_GROUPS) {
+      double x[CH];
 #pragma unroll
-      for (int q = 0; q < MAXR; ++q)
-        if (q < nr) {
-          acc[q] = fma(x, yt[swz(il, q)], acc[q]);
-          acc2[q] = fma(x2, yt[swz(il + U2_GROUPS, q)], acc2[q]);
-        }
+      for (int h = 0; h < CH; ++h) {
+        const int row = kb * TB + il + h * U2_GROUPS;
+        x[h] = xrow_ptr(S, c, row)[col ^ ((row & 3) << 2)];
+      }
+#pragma unroll
+      for (int h = 0; h < CH; ++h)
+#pragma unroll
+        for (int q = 0; q < NR; ++q)
+          if (q < nr) acc[h][q] = fma(x[h], yt[swz(il + h * U2_GROUPS, q)], acc[h][q]);
     }
   }
 #pragma unroll
-  for (int q = 0; q < MAXR; ++q)
-    if (q < nr) red[rg][q][col] = acc[q] + acc2[q];
+  for (int q = 0; q < NR; ++q)
+    if (q < nr) {
+      double v = 0.0;
+#pragma unroll
+      for (int h = 0; h < CH; ++h) v += acc[h][q];
+      red[rg][q][col] = v;
+    }
   __syncthreads();
   if (rg != 0) return;
+  double tot[NR];
 #pragma unroll
-  for (int q = 0; q < MAXR; ++q) {
+  for (int q = 0; q < NR; ++q) {
     double v = 0.0;
     if (q < nr)
       for (int g2 = 0; g2 < U2_GROUPS; ++g2) v += red[g2][q][col];
-    acc[q] = (a < S.m) ? v : 0.0;
+    tot[q] = (a < S.m) ? v : 0.0;
   }
   if (Q.frow >= 0) {
 #pragma unroll
-    for (int q = 0; q < MAXR; ++q)
-      if (q == Q.frow) Q.U2f[a] = acc[q];   // X^T y_f = B~ K_s^-1 f'
+    for (int q = 0; q < NR; ++q)
+      if (q == Q.frow) Q.U2f[a] = tot[q];   // X^T y_f = B~ K_s^-1 f'
   }
   if (r == 0) return;
   double* out = Q.U2W + (size_t)a * 2 * r;
   const double* u1 = Q.U1 + (size_t)a * r;
 #pragma unroll
-  for (int q = 0; q < MAXR; ++q)
+  for (int q = 0; q < NR; ++q)
     if (q < r) {
-      double w = -acc[q];
+      double w = -tot[q];
       for (int q2 = 0; q2 < r; ++q2) w = fma(Cm[q * r + q2], u1[q2], w);
-      out[q] = acc[q];
+      out[q] = tot[q];
       out[r + q] = (a < S.m) ? w : 0.0;
     }
 }
@@ -562,13 +576,23 @@ void launch_sp_dual_rhs(const SpSub* ss, int n_mult, const int* cptr, const int4
   if (n_mult > 0) sp_dual_rhs_kernel<<<(n_mult + 255) / 256, 256, 0, st>>>(ss, n_mult, cptr, cent, c, d);
 }
 
-void launch_sp_u2(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, cudaStream_t st) {
-  if (npanels > 0) sp_u2_kernel<<<npanels, U2_GROUPS * TB, 0, st>>>(subs, ss, panels);
+void launch_sp_u2(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int max_cols,
+                  cudaStream_t st) {
+  if (npanels <= 0) return;
+  // more row chains for narrow y (heat: one kernel column)
+  if (max_cols <= 1)
+    sp_u2_kernel<1, 8><<<npanels, U2_GROUPS * TB, 0, st>>>(subs, ss, panels);
+  else if (max_cols <= 2)
+    sp_u2_kernel<2, 8><<<npanels, U2_GROUPS * TB, 0, st>>>(subs, ss, panels);
+  else if (max_cols <= 4)
+    sp_u2_kernel<4, 4><<<npanels, U2_GROUPS * TB, 0, st>>>(subs, ss, panels);
+  else
+    sp_u2_kernel<MAXR, 2><<<npanels, U2_GROUPS * TB, 0, st>>>(subs, ss, panels);
 }
 
 void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int sub0, int nsub,
-                       int max_T32, cudaStream_t st) {
-  if (npanels > 0) sp_u2_kernel<<<npanels, U2_GROUPS * TB, 0, st>>>(subs, ss, panels);
+                       int max_T32, int max_cols, cudaStream_t st) {
+  launch_sp_u2(subs, ss, panels, npanels, max_cols, st);
   if (nsub > 0 && max_T32 > 0) sp_correct_kernel<<<dim3(max_T32, nsub), 256, 0, st>>>(subs, ss, sub0);
 }
 

@@ -99,11 +99,12 @@ void launch_sp_potrf(const SpDiag* d, int nd, int* bad, cudaStream_t st);
 void launch_sp_dual_rhs(const SpSub* ss, int n_mult, const int* cptr, const int4* cent, const double* c, double* d,
                         cudaStream_t st);
 // U2/W (and U2f) per (sub, panel) from the X panels
-void launch_sp_u2(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, cudaStream_t st);
+// max_cols >= every panel's subdomain's r (+ 1 with the device dual rhs)
+void launch_sp_u2(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int max_cols,
+                  cudaStream_t st);
 // after the assembly: U2/W per (sub, panel), then the rank-2r update of F~
 void launch_sp_correct(const SubDev* subs, const SpSub* ss, const int2* panels, int npanels, int sub0, int nsub,
-                       int max_T32,
-                       cudaStream_t st);
+                       int max_T32, int max_cols, cudaStream_t st);
 
 // device solve_local (feti_spsolve.cu): one right-hand side per item, b/x at
 // `off` (n values), scratch at `scr` (3 x T*128 values)
