@@ -67,6 +67,20 @@ class _Shape:
         self.shape = tuple(int(v) for v in shape)
 
 
+def _multiplier_owners(constraints):
+    """(first, second) owning subdomain of every multiplier (-1: a Dirichlet
+    row has one owner)."""
+    nm = int(constraints.n_multipliers)
+    first = np.full(nm, -1, np.int64)
+    second = np.full(nm, -1, np.int64)
+    for s, sc in enumerate(constraints.per_subdomain):
+        g = np.asarray(sc.multiplier_ids, np.int64)
+        taken = first[g] >= 0
+        second[g[taken]] = s
+        first[g[~taken]] = s
+    return first, second
+
+
 def _problem_like(x) -> bool:
     """A ``SubdomainProblem`` (solver.py:100-106) or anything carrying the
     unregularized ``stiffness`` and its ``kernel`` basis."""
@@ -240,8 +254,8 @@ class DualOperator:
         self._forces_dev = None
         self.owned = (list(range(self.n_subdomains)) if subdomains is None
                       else sorted(int(s) for s in subdomains))
-        if not (sparse_ordering in ("auto", "onion") or sparse_ordering.startswith("dissection:")):
-            raise ValueError("sparse_ordering must be 'auto', 'onion' or 'dissection:<depth>'")
+        if not (sparse_ordering in ("auto", "onion") or sparse_ordering.startswith(("dissection:", "faces:"))):
+            raise ValueError("sparse_ordering must be 'auto', 'onion', 'dissection:<depth>' or 'faces:<depth>'")
         self.sparse_ordering = sparse_ordering
         self.sparse_recipe = None
 
@@ -348,7 +362,8 @@ class DualOperator:
                 n, ip, ix, _ = fct.csr_arrays(self.stiffness[i])
                 if n != sub.n:
                     raise ValueError("stiffness size does not match the subdomain")
-                sub.perm, sub.iperm = spr.sparse_route_ordering(n, ip, ix, sub.bcol, self.sparse_recipe)
+                pieces = self._interface_pieces(i, sub.bcol) if self.sparse_recipe[0] == "faces" else None
+                sub.perm, sub.iperm = spr.sparse_route_ordering(n, ip, ix, sub.bcol, self.sparse_recipe, pieces)
                 sub.npos = int(sub.perm.shape[0])
             elif self.factorization == "device":
                 base = np.arange(sub.n - 1, -1, -1, dtype=np.int64)   # RCM of the dense K_reg
@@ -375,14 +390,17 @@ class DualOperator:
             return sub
 
         if self.factorization == "sparse":
-            # one ordering recipe for the operator, chosen on its first subdomain
-            # by the tile flops it leaves (subdomains of one problem are alike)
-            i0 = order[0]
+            # one ordering recipe for the operator, chosen on its subdomain with
+            # the most multipliers by the tile flops it leaves (subdomains of one
+            # problem are alike)
+            self._owners = _multiplier_owners(self.constraints)
+            i0 = max(order, key=lambda i: self.constraints.per_subdomain[i].multiplier_ids.shape[0])
             n0, ip0, ix0, _ = fct.csr_arrays(self.stiffness[i0])
             sc0 = self.constraints.per_subdomain[i0]
             bcol0, _ = _constraint_rows(sc0, n0)
             r0 = self._kernel_basis(i0, n0).shape[1]
-            self.sparse_recipe = spr.choose_ordering(n0, ip0, ix0, bcol0, r0, self.sparse_ordering)
+            self.sparse_recipe = spr.choose_ordering(n0, ip0, ix0, bcol0, r0, self.sparse_ordering,
+                                                     pieces=self._interface_pieces(i0, bcol0))
         subs = self._map(symbolic, order)
         ctx = C.c_void_p()
         _call(self._lib.feti_create(self._resolve_device(), C.byref(ctx)))
@@ -430,6 +448,14 @@ class DualOperator:
         self.symbolic_count = len(self._subs)
         self.prepared = True
         return self
+
+    def _interface_pieces(self, i, bcol):
+        """Subdomain i's interface faces/edges/corners: constrained DOFs grouped
+        by the subdomains their multipliers glue them to."""
+        gids = np.asarray(self.constraints.per_subdomain[i].multiplier_ids, np.int64)
+        first, second = self._owners
+        nb = np.where(first[gids] == i, second[gids], first[gids])
+        return spr.interface_pieces(bcol, nb)
 
     def device_bytes_estimate(self) -> int:
         """Dense-tile routes: factor tile triangle + X panels + packed F~ (the

@@ -19,7 +19,8 @@ for s in range(prob.n_sub):
 mats = [inputs.ShapeOnly((prob.n_dofs, prob.n_dofs))] * prob.n_sub
 cfg_op = dualop.DualOpConfig(strategy="explicit", path=os.environ.get("FETI_PATH", "syrk"))
 op = dualop.prepare(mats, prob.constraints(), prob.layout, cfg_op, device=0,
-                    factorization="sparse", stiffness=ks, kernels=qs)
+                    factorization="sparse", stiffness=ks, kernels=qs,
+                    sparse_ordering=os.environ.get("FETI_SPARSE_ORDERING", "auto"))
 for _ in range(3):
     op.preprocess()
 fac, pre = [], []
@@ -28,7 +29,7 @@ for _ in range(steps):
     st = op.stats()
     fac.append(st["ms_factorize"])
     pre.append(st["ms_preprocess"])
-print(f"{cfg} groups={os.environ.get('FETI_SP_GROUPS', 8)} flags={os.environ.get('FETI_NVCC_FLAGS', '')!r}: "
+print(f"{cfg} recipe={op.sparse_recipe} groups={os.environ.get('FETI_SP_GROUPS', 8)} flags={os.environ.get('FETI_NVCC_FLAGS', '')!r}: "
       f"factorize {statistics.median(fac):.2f} ms, preprocess {statistics.median(pre):.2f} ms, "
       f"tail {statistics.median(pre) - statistics.median(fac):.2f} ms")
 op.close()

@@ -226,3 +226,48 @@ def test_sparse_route_tile_aligned_dissection():
     kb, _, qb = big.subdomain_system(21)
     rec = spr.choose_ordering(kb.shape[0], kb.indptr, kb.indices, big.bcol[21], qb.shape[1])
     assert rec[0] == "dissection"
+
+
+def test_sparse_route_face_dissection():
+    """Interface pieces (constrained DOFs grouped by the subdomains their
+    multipliers glue them to) and the face-grown dissection: a partition of
+    the DOFs on tile-aligned segments with the interface last; on config 3's
+    interior subdomain it cuts the axis planes (separators 361 / 171 / 81
+    DOFs, leaves of 9x9x9) and leaves fewer estimated tile flops than the
+    breadth-first dissection, so the chooser takes it."""
+    from harness import inputs
+    from paper_2502_08382_b200 import dualop
+
+    prob = inputs.Problem(*inputs.CONFIGS["c3"])
+    cons = prob.constraints()
+    first, second = dualop._multiplier_owners(cons)
+    s = 21                                   # an interior subdomain: six glued faces
+    g = prob.gids[s]
+    nb = np.where(first[g] == s, second[g], first[g])
+    assert (nb >= 0).all()
+    pieces = spr.interface_pieces(prob.bcol[s], nb)
+    sizes = sorted((p.size for p in pieces), reverse=True)
+    # chained gluing (one multiplier per adjacent owner pair): six face-sized
+    # pieces (edges/corners join the face of their chain neighbour), then edges
+    assert len(pieces) == 14 and all(361 <= x <= 400 for x in sizes[:6]) and max(sizes[6:]) <= 21
+    assert np.array_equal(np.sort(np.concatenate(pieces)), np.unique(prob.bcol[s]))
+    k, _, q = prob.subdomain_system(s)
+    n = k.shape[0]
+    segs = spr.face_dissection_segments(n, k.indptr, k.indices, prob.bcol[s], pieces, depth=3)
+    assert [x.size for x in segs[:3]] == [729, 729, 81]
+    assert sorted(x.size for x in segs[:-1] if x.size < 729) == [81] * 4 + [171] * 2 + [361]
+    perm, iperm = spr.padded_positions(segs)
+    assert np.array_equal(np.sort(perm[perm >= 0]), np.arange(n))
+    assert np.array_equal(perm[iperm], np.arange(n))
+    iface = np.unique(prob.bcol[s])
+    e_face = spr.tile_flops_estimate(n, k.indptr, k.indices, iperm, perm.shape[0], 1, iface.size)
+    p2, i2 = spr.sparse_route_ordering(n, k.indptr, k.indices, prob.bcol[s], ("dissection", 2))
+    e_bfs = spr.tile_flops_estimate(n, k.indptr, k.indices, i2, p2.shape[0], 1, iface.size)
+    assert e_face < 0.85 * e_bfs
+    rec = spr.choose_ordering(n, k.indptr, k.indices, prob.bcol[s], q.shape[1], pieces=pieces)
+    assert rec[0] == "faces"
+    # a Dirichlet row has one owner: its neighbour is -1
+    s0 = 0
+    g0 = prob.gids[s0]
+    nb0 = np.where(first[g0] == s0, second[g0], first[g0])
+    assert (nb0 == -1).any()
