@@ -229,6 +229,11 @@ struct feti_ctx {
   static constexpr int kSpStreams = 16;   // upper bound on factorization groups (FETI_SP_GROUPS, default 8)
   std::vector<std::pair<int, int>> sp_corr_rng, sp_sub_rng;   // per group: panels, subdomains
   cudaEvent_t sp_ev[3] = {};   // factorize start, factorize end, assemble end
+  // fused graph: each group's interface assembly + correction captured right
+  // behind its column sequence on its stream (FETI_SP_FUSE=0: separate);
+  // sp_fend[g] marks group g's factorization end (external event records)
+  bool sp_graph_fused = false, sp_assembled_in_graph = false;
+  cudaEvent_t sp_fend[kSpStreams] = {};
   // sparse-route stiffness hand-over: values are copied on copy_stream while
   // the pool is zeroed; k_ready = copies issued so far landed, k_free = the
   // last scatter finished reading the previous values
@@ -272,6 +277,10 @@ struct feti_ctx {
   double sp_flops = 0.0;
   double sp_flops_scalar = 0.0;
 };
+
+extern "C" {
+static int sparse_group_assembly(feti_ctx* c, int g, cudaStream_t gs, int* launches);
+}
 
 namespace {
 
@@ -403,6 +412,7 @@ int build_sparse_tasks(feti_ctx* c) {
     CUDA_TRY(cudaEventCreateWithFlags(&c->sp_join[g], cudaEventDisableTiming));
   }
   for (auto& e : c->sp_ev) CUDA_TRY(cudaEventCreate(&e));
+  for (int g = 0; g < G; ++g) CUDA_TRY(cudaEventCreate(&c->sp_fend[g]));
   // contiguous groups of subdomains
   auto group_of = [&](int si) { return (int)((int64_t)si * G / std::max(ns, 1)); };
   // slots of the (P Q)^T block row: their tasks run "thin" (rows < 8 only)
@@ -526,6 +536,10 @@ int factorize_sparse(feti_ctx* c) {
     CUDA_TRY(cudaGraphLaunch(c->sp_graph_exec, st));
     launches = 2 + c->sp_graph_launches;
   } else {
+    // each group's assembly is captured behind its own column sequence: it
+    // overlaps the other groups' factorization (the end of every column
+    // sequence is the latency-bound dense interface chain)
+    c->sp_graph_fused = use_graph && !(getenv("FETI_SP_FUSE") && atoi(getenv("FETI_SP_FUSE")) == 0);
     if (use_graph) CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     CUDA_TRY(cudaEventRecord(c->ev[2], st));
     for (int g = 0; g < G; ++g) CUDA_TRY(cudaStreamWaitEvent(c->sp_streams[g], c->ev[2], 0));
@@ -545,6 +559,16 @@ int factorize_sparse(feti_ctx* c) {
         }
       }
     for (int g = 0; g < G; ++g) {
+      if (c->sp_graph_fused) {
+        CUDA_TRY(cudaEventRecordWithFlags(c->sp_fend[g], c->sp_streams[g], cudaEventRecordExternal));
+        int rc2 = sparse_group_assembly(c, g, c->sp_streams[g], &nl);
+        if (rc2) {
+          cudaGraph_t junk = nullptr;
+          cudaStreamEndCapture(st, &junk);
+          if (junk) cudaGraphDestroy(junk);
+          return rc2;
+        }
+      }
       CUDA_TRY(cudaEventRecord(c->sp_join[g], c->sp_streams[g]));
       CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
     }
@@ -559,6 +583,7 @@ int factorize_sparse(feti_ctx* c) {
     }
   }
   c->sp_graph_used = use_graph;
+  c->sp_assembled_in_graph = use_graph && c->sp_graph_fused;
   // the factorization end on the context stream (timing only); no host sync:
   // feti_assemble runs each group's assembly right behind its factorization
   // on the group's stream and checks the pivots once everything finished
@@ -683,6 +708,7 @@ int feti_destroy(feti_ctx* c) {
   if (c->sp_graph_exec) cudaGraphExecDestroy(c->sp_graph_exec);
   for (int g = 0; g < feti_ctx::kSpStreams; ++g) {
     if (c->sp_join[g]) cudaEventDestroy(c->sp_join[g]);
+    if (c->sp_fend[g]) cudaEventDestroy(c->sp_fend[g]);
     if (c->sp_streams[g]) cudaStreamDestroy(c->sp_streams[g]);
   }
   for (double* pp : c->x_open) cudaIpcCloseMemHandle(pp);
@@ -1262,6 +1288,41 @@ static int launch_assembly(feti_ctx* c, cudaStream_t st, const int4* wu, int nu,
   return FETI_OK;
 }
 
+// One factorization group's interface assembly + correction on its stream
+// (sparse route): TRSM chain, then U2/W and the SYRK with the correction in
+// its epilogue (explicit "syrk"), the U2 sweep (implicit), or the second
+// solve + gather and the correction pass (path "trsm").
+static int sparse_group_assembly(feti_ctx* c, int g, cudaStream_t gs, int* launches) {
+  const auto& r = c->wv_range;
+  std::vector<int> none;
+  const bool fused = !c->implicit && !c->path_trsm;   // the SYRK follows sp_u2 below
+  int rc;
+  if ((rc = launch_assembly(c, gs, c->d_wv[0] + r[0][g].first, r[0][g].second, c->d_wv[1] + r[1][g].first,
+                            r[1][g].second, c->d_wv[2] + r[2][g].first, r[2][g].second, c->d_wv[3] + r[3][g].first,
+                            r[3][g].second, c->d_wv[4] + r[4][g].first, fused ? 0 : r[4][g].second, none, nullptr,
+                            launches)))
+    return rc;
+  if (c->implicit) {
+    // no F~: U2 (and U2f) by the backward sweep; the apply adds the correction
+    launch_implicit_u2(c->d_subdev, c->d_spsub, c->sp_sub_rng[g].first, c->sp_sub_rng[g].second, c->sp_u2_cols,
+                       c->impl_max_blocks, gs);
+    *launches += c->sp_u2_cols > 0;
+  } else if (!c->path_trsm) {
+    // U2/W from X, then the SYRK with the correction in its epilogue
+    // (launch_assembly above ran without the SYRK: ny = 0)
+    launch_sp_u2(c->d_subdev, c->d_spsub, c->d_sp_panels + c->sp_corr_rng[g].first, c->sp_corr_rng[g].second,
+                 c->sp_u2_cols, gs);
+    launch_syrk(c->d_subdev, c->d_wv[4] + r[4][g].first, r[4][g].second, gs);
+    *launches += (c->sp_corr_rng[g].second > 0) + (r[4][g].second > 0);
+  } else {
+    launch_sp_correct(c->d_subdev, c->d_spsub, c->d_sp_panels + c->sp_corr_rng[g].first, c->sp_corr_rng[g].second,
+                      c->sp_sub_rng[g].first, c->sp_sub_rng[g].second, c->sp_max_T32, c->sp_u2_cols, gs);
+    *launches += 2;
+  }
+  CUDA_TRY(cudaGetLastError());
+  return FETI_OK;
+}
+
 int feti_assemble(feti_ctx* c) {
   if (!c) return fail(FETI_ERR_ARG, "ctx is NULL");
   if (!c->finalized) return fail(FETI_ERR_LIFECYCLE, "preprocess before prepare");
@@ -1289,40 +1350,22 @@ int feti_assemble(feti_ctx* c) {
     // right behind its factorization (the persistent scheduler ran on the
     // context stream: the groups wait for it)
     const int G = c->sp_groups;
-    CUDA_TRY(cudaEventRecord(c->ev[2], st));
-    const auto& r = c->wv_range;
-    for (int g = 0; g < G; ++g) {
-      cudaStream_t gs = c->sp_streams[g];
-      // the captured graph ran on the context stream
-      if (c->sp_graph_used) CUDA_TRY(cudaStreamWaitEvent(gs, c->ev[2], 0));
-      std::vector<int> none;
-      const bool fused = !c->implicit && !c->path_trsm;   // the SYRK follows sp_u2 below
-      if ((rc = launch_assembly(c, gs, c->d_wv[0] + r[0][g].first, r[0][g].second, c->d_wv[1] + r[1][g].first,
-                                r[1][g].second, c->d_wv[2] + r[2][g].first, r[2][g].second,
-                                c->d_wv[3] + r[3][g].first, r[3][g].second, c->d_wv[4] + r[4][g].first,
-                                fused ? 0 : r[4][g].second, none, nullptr, &launches)))
-        return rc;
-      if (c->implicit) {
-        // no F~: U2 (and U2f) by the backward sweep; the apply adds the correction
-        launch_implicit_u2(c->d_subdev, c->d_spsub, c->sp_sub_rng[g].first, c->sp_sub_rng[g].second,
-                           c->sp_u2_cols, c->impl_max_blocks, gs);
-        launches += c->sp_u2_cols > 0;
-      } else if (!c->path_trsm) {
-        // U2/W from X, then the SYRK with the correction in its epilogue
-        // (launch_assembly above ran without the SYRK: ny = 0)
-        launch_sp_u2(c->d_subdev, c->d_spsub, c->d_sp_panels + c->sp_corr_rng[g].first, c->sp_corr_rng[g].second,
-                     c->sp_u2_cols, gs);
-        launch_syrk(c->d_subdev, c->d_wv[4] + r[4][g].first, r[4][g].second, gs);
-        launches += (c->sp_corr_rng[g].second > 0) + (r[4][g].second > 0);
-      } else {
-        launch_sp_correct(c->d_subdev, c->d_spsub, c->d_sp_panels + c->sp_corr_rng[g].first,
-                          c->sp_corr_rng[g].second, c->sp_sub_rng[g].first, c->sp_sub_rng[g].second, c->sp_max_T32,
-                          c->sp_u2_cols, gs);
-        launches += 2;
+    const bool in_graph = c->sp_assembled_in_graph;
+    c->sp_assembled_in_graph = false;
+    if (in_graph) {
+      // the factorization graph already ran every group's assembly behind its
+      // column sequence
+      launches = 0;
+    } else {
+      CUDA_TRY(cudaEventRecord(c->ev[2], st));
+      for (int g = 0; g < G; ++g) {
+        cudaStream_t gs = c->sp_streams[g];
+        // the captured graph ran on the context stream
+        if (c->sp_graph_used) CUDA_TRY(cudaStreamWaitEvent(gs, c->ev[2], 0));
+        if ((rc = sparse_group_assembly(c, g, gs, &launches))) return rc;
+        CUDA_TRY(cudaEventRecord(c->sp_join[g], gs));
+        CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
       }
-      CUDA_TRY(cudaGetLastError());
-      CUDA_TRY(cudaEventRecord(c->sp_join[g], gs));
-      CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
     }
     CUDA_TRY(cudaEventRecord(c->sp_ev[2], st));
     std::vector<int> bad(c->subs.size(), 1 << 30);
@@ -1330,8 +1373,17 @@ int feti_assemble(feti_ctx* c) {
       CUDA_TRY(cudaMemcpyAsync(bad.data(), c->d_bad, bad.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     float mf = 0, mp = 0;
-    CUDA_TRY(cudaEventElapsedTime(&mf, c->sp_ev[0], c->sp_ev[1]));
     CUDA_TRY(cudaEventElapsedTime(&mp, c->sp_ev[0], c->sp_ev[2]));
+    if (in_graph) {
+      // the last group's factorization end
+      for (int g = 0; g < G; ++g) {
+        float t = 0;
+        CUDA_TRY(cudaEventElapsedTime(&t, c->sp_ev[0], c->sp_fend[g]));
+        mf = std::max(mf, t);
+      }
+    } else {
+      CUDA_TRY(cudaEventElapsedTime(&mf, c->sp_ev[0], c->sp_ev[1]));
+    }
     S.ms_factorize = mf;
     S.ms_preprocess = mp;
     S.ms_wait_upload = 0.0;
