@@ -725,42 +725,44 @@ def run_sparse(args, rank, world, local_rank):
                    "l2": f"inputs larger than L2 (block-sparse factor tiles {st['bytes_temporary'] / 1e9:.0f} GB, "
                          f"packed F~ {8 * sum(m * (m + 1) / 2 for m in prob.m_per_subdomain()) / 1e9:.2f} GB "
                          f"per apply)"},
-        "roofline": {"bound": "tensor",
-                     "kernel": "feti_factorize: sp_gemm8_kernel (FP64 DMMA tile tasks) + sp_potrf_kernel, per step",
-                     "achieved": st["flops_factor_alg"] / fac_s / 1e12, "peak": peak_f64, "unit": "TFLOP/s",
-                     "frac": st["flops_factor_alg"] / fac_s / 1e12 / peak_f64,
-                     "peak_source": "measured in-run: cuBLAS DGEMM 8192^3 f64 (torch.matmul), best of 5",
-                     "traffic": load_traffic(args.config, "sparse").get(
-                         "feti_factorize (sp_gemm8 + sp_potrf, per factorization)"),
-                     "traffic_note": "DRAM read+write of every sp_gemm8/sp_potrf launch of one factorization "
-                                     "(ncu dram__bytes_*.sum over all launches, profiles/ncu_traffic.json); far "
-                                     "above the pool's size (tiles re-read per tile product) but ~1 TB/s: not the "
-                                     "bound",
-                     "algorithmic": "scalar Cholesky flops of K_s in the chosen ordering, sum_j c_j (c_j + 3) from "
-                                    "the exact column counts (+ the y = L^-1 P Q solve), per factorization",
-                     "algorithmic_flops": st["flops_factor_alg"],
-                     "executed_tile_flops": st["flops_factor_exec"],
-                     "achieved_executed": st["flops_factor_exec"] / fac_s / 1e12,
-                     "frac_executed": st["flops_factor_exec"] / fac_s / 1e12 / peak_f64,
-                     "note": "128-row tiles execute executed/algorithmic = "
-                             f"{st['flops_factor_exec'] / max(st['flops_factor_alg'], 1.0):.2f}x the scalar flops; "
-                             "frac_executed is the DMMA pipe's utilisation"},
-        "assembly_flops": {k: st[k] for k in ("flops_trsm_alg", "flops_trsm_exec", "flops_syrk_alg",
-                                              "flops_syrk_exec", "flops_scale_exec")},
-        "roofline_step": (lambda alg, ex: {
-            "bound": "tensor", "unit": "TFLOP/s", "peak": peak_f64,
-            "algorithmic_flops": alg, "achieved": alg / (step_ms / 1e3) / 1e12,
+        # the step is ONE captured CUDA graph: every group's factorization
+        # (sp_gemm8 tile tasks + sp_potrf) with its interface assembly (TRSM
+        # chain, U2, SYRK + correction) behind it on the group's stream
+        "roofline": (lambda alg, ex: {
+            "bound": "tensor",
+            "kernel": "the step's CUDA graph: sp_gemm8_kernel + sp_potrf_kernel (factorization) and trsm_chain / "
+                      "sp_u2 / syrk (interface assembly), FP64 DMMA tile work",
+            "achieved": alg / (step_ms / 1e3) / 1e12, "peak": peak_f64, "unit": "TFLOP/s",
             "frac": alg / (step_ms / 1e3) / 1e12 / peak_f64,
-            "executed_flops": ex, "frac_executed": ex / (step_ms / 1e3) / 1e12 / peak_f64,
-            "what": "the whole step (factorization + interface TRSM/SYRK + correction) against DGEMM: scalar "
-                    "Cholesky flops of K_s plus the pruned TRSM/SYRK counts of the interface block, over "
-                    "ms_per_step (supplementary to `roofline`, which is the factorization alone)"})(
+            "peak_source": "measured in-run: cuBLAS DGEMM 8192^3 f64 (torch.matmul), best of 5",
+            "traffic": load_traffic(args.config, "sparse").get("step (fused graph, per step)"),
+            "traffic_note": "DRAM read+write of every launch of one step (ncu dram__bytes_*.sum summed over the "
+                            "launch list, profiles/ncu_traffic.json); tiles are re-read per tile product, but at "
+                            "~1 TB/s the step is not HBM-bound",
+            "algorithmic": "scalar Cholesky flops of K_s in the chosen ordering, sum_j c_j (c_j + 3) from the exact "
+                           "column counts (+ the y = L^-1 P Q solve), plus the pruned interface TRSM "
+                           "sum_j (n_I - r_j)^2 and SYRK sum_(a<=b) 2 (n_I - max(r_a, r_b)) flops, per step",
+            "algorithmic_flops": alg, "executed_tile_flops": ex,
+            "achieved_executed": ex / (step_ms / 1e3) / 1e12,
+            "frac_executed": ex / (step_ms / 1e3) / 1e12 / peak_f64,
+            "note": f"128-row tiles execute executed/algorithmic = {ex / max(alg, 1.0):.2f}x; frac_executed is "
+                    "the DMMA pipe's utilisation over the step"})(
             st["flops_factor_alg"] + st["flops_trsm_alg"] + st["flops_syrk_alg"],
             st["flops_factor_exec"] + st["flops_trsm_exec"] + st["flops_syrk_exec"] + st["flops_scale_exec"]),
+        "roofline_factorization": {
+            "bound": "tensor", "kernel": "sp_gemm8_kernel + sp_potrf_kernel", "unit": "TFLOP/s", "peak": peak_f64,
+            "algorithmic_flops": st["flops_factor_alg"], "executed_tile_flops": st["flops_factor_exec"],
+            "achieved": st["flops_factor_alg"] / fac_s / 1e12, "frac": st["flops_factor_alg"] / fac_s / 1e12 / peak_f64,
+            "frac_executed": st["flops_factor_exec"] / fac_s / 1e12 / peak_f64,
+            "what": "supplementary: factorization flops over ms_factorize (the last group's factorization end; "
+                    "in the fused graph that span also carries the earlier groups' interface assembly)"},
+        "assembly_flops": {k: st[k] for k in ("flops_trsm_alg", "flops_trsm_exec", "flops_syrk_alg",
+                                              "flops_syrk_exec", "flops_scale_exec")},
         "phases_ms": {"ms_factorize": statistics.mean(fac_ms), "ms_preprocess": statistics.mean(pre_ms),
                       "ms_assembly_tail": statistics.mean(asm_ms),
-                      "note": "each group's interface assembly + correction runs on its stream right behind its "
-                              "factorization; ms_assembly_tail = past the last group's factorization"},
+                      "note": "each group's interface assembly + correction is captured right behind its "
+                              "factorization on its stream (one graph per step); ms_assembly_tail = past the last "
+                              "group's factorization"},
         "apply": {"ms_per_iter": apply_ms, "kernel_ms_per_iter": apply_kernel_ms, "e2e_ms_per_iter": apply_e2e_ms,
                   "what": "ms_per_iter: local kernels + fused exchange (N > 1), max over ranks; kernel_ms_per_iter: "
                           "this rank's apply kernels alone; e2e: host p -> q through the public API",
