@@ -29,7 +29,7 @@ for _ in range(steps):
     st = op.stats()
     fac.append(st["ms_factorize"])
     pre.append(st["ms_preprocess"])
-print(f"{cfg} recipe={op.sparse_recipe} groups={os.environ.get('FETI_SP_GROUPS', 8)} flags={os.environ.get('FETI_NVCC_FLAGS', '')!r}: "
+print(f"{cfg} recipe={op.sparse_recipe} groups={os.environ.get('FETI_SP_GROUPS', 8)}: "
       f"factorize {statistics.median(fac):.2f} ms, preprocess {statistics.median(pre):.2f} ms, "
       f"tail {statistics.median(pre) - statistics.median(fac):.2f} ms")
 op.close()
