@@ -353,10 +353,41 @@ def tile_flops_estimate(n, indptr, indices, iperm, npos, kernel_dim, n_iface):
     return ops * 2.0 * TB ** 3
 
 
+_ORDERING_CACHE = {}
+_ORDERING_CACHE_MAX = 256
+
+
+def _ordering_key(n, indptr, indices, interface, recipe, pieces):
+    import hashlib
+
+    h = hashlib.blake2b(digest_size=16)
+    h.update(repr((int(n), tuple(recipe) if recipe else None)).encode())
+    for a in (indptr, indices, np.unique(np.asarray(interface, np.int64))):
+        h.update(np.ascontiguousarray(a, np.int64).tobytes())
+        h.update(b"|")
+    for piece in sorted((np.asarray(x, np.int64).tobytes() for x in (pieces or [])), key=lambda b: (len(b), b)):
+        h.update(piece)
+        h.update(b";")
+    return h.hexdigest()
+
+
 def sparse_route_ordering(n, indptr, indices, interface, recipe, pieces=None):
     """(perm_pos, iperm) for a recipe ("onion",), ("dissection", depth),
     ("dissection", depth, sep_rule) or ("faces", depth) (needs the
-    subdomain's `interface_pieces`)."""
+    subdomain's `interface_pieces`).  Subdomains with the same pattern,
+    interface and pieces (most of a structured decomposition) share one
+    computation."""
+    key = _ordering_key(n, indptr, indices, interface, recipe, pieces)
+    hit = _ORDERING_CACHE.get(key)
+    if hit is None:
+        hit = _sparse_route_ordering(n, indptr, indices, interface, recipe, pieces)
+        if len(_ORDERING_CACHE) >= _ORDERING_CACHE_MAX:
+            _ORDERING_CACHE.clear()
+        _ORDERING_CACHE[key] = hit
+    return hit[0].copy(), hit[1].copy()
+
+
+def _sparse_route_ordering(n, indptr, indices, interface, recipe, pieces=None):
     if recipe is None or recipe[0] == "onion":
         perm = onion_interface_last(n, indptr, indices, interface)
         iperm = np.empty(n, np.int64)

@@ -271,3 +271,23 @@ def test_sparse_route_face_dissection():
     g0 = prob.gids[s0]
     nb0 = np.where(first[g0] == s0, second[g0], first[g0])
     assert (nb0 == -1).any()
+
+
+def test_sparse_route_ordering_cache():
+    """Structurally identical subdomains (same pattern, interface and pieces)
+    share one ordering computation; callers get private copies."""
+    from harness import inputs
+
+    prob = inputs.Problem("heat", 3, 8, 3)
+    k, _, _ = prob.subdomain_system(13)
+    bcol = prob.bcol[13]
+    spr._ORDERING_CACHE.clear()
+    p1, i1 = spr.sparse_route_ordering(k.shape[0], k.indptr, k.indices, bcol, ("dissection", 2))
+    assert len(spr._ORDERING_CACHE) == 1
+    p1[:] = -7
+    p2, i2 = spr.sparse_route_ordering(k.shape[0], k.indptr, k.indices, bcol, ("dissection", 2))
+    assert len(spr._ORDERING_CACHE) == 1 and not (p2 == -7).any()
+    p3, _ = spr._sparse_route_ordering(k.shape[0], k.indptr, k.indices, bcol, ("dissection", 2))
+    assert np.array_equal(p2, p3) and np.array_equal(p2[i2], np.arange(k.shape[0]))
+    spr.sparse_route_ordering(k.shape[0], k.indptr, k.indices, bcol[: bcol.size // 2], ("dissection", 2))
+    assert len(spr._ORDERING_CACHE) == 2
