@@ -86,3 +86,18 @@ for cfg in (dualop.DualOpConfig(strategy="explicit", path="trsm"), dualop.DualOp
                         stiffness=ks, kernels=qs) as op:
         op.preprocess()
         print(cfg.strategy, cfg.path, "sparse route apply norm", np.linalg.norm(op.apply(p)))
+# face-grown dissection (interface pieces) through the fused step graph
+# (factorization + each group's assembly captured together), two steps
+prob = inputs.Problem("heat", 3, 12, 2)
+ks, qs = [], []
+for s in range(prob.n_sub):
+    k, _, qk = prob.subdomain_system(s)
+    ks.append(k)
+    qs.append(qk)
+mats = [inputs.ShapeOnly((prob.n_dofs, prob.n_dofs)) for _ in range(prob.n_sub)]
+with dualop.prepare(mats, prob.constraints(), prob.layout, CFG, device=0, factorization="sparse",
+                    stiffness=ks, kernels=qs, sparse_ordering="faces:2") as op:
+    op.preprocess()
+    op.preprocess()
+    print("faces route", op.sparse_recipe, "apply norm",
+          np.linalg.norm(op.apply(np.random.default_rng(0).normal(size=prob.n_multipliers))))
