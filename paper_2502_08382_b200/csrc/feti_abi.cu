@@ -223,8 +223,6 @@ struct feti_ctx {
   // DMMA tile work of the others.  Ranges are indexed [g * sp_maxTq + j].
   std::vector<std::pair<int, int>> sp_acc_rng, sp_panel_rng, sp_diag_rng;
   int sp_groups = 1, sp_maxTq = 0;
-  cudaGraphExec_t sp_graph_exec = nullptr;   // captured column-launch sequence
-  int sp_graph_launches = 0;
   bool sp_graph_used = false;
   static constexpr int kSpStreams = 16;   // upper bound on factorization groups (FETI_SP_GROUPS, default 8)
   std::vector<std::pair<int, int>> sp_corr_rng, sp_sub_rng;   // per group: panels, subdomains
@@ -232,7 +230,12 @@ struct feti_ctx {
   // fused graph: each group's interface assembly + correction captured right
   // behind its column sequence on its stream (FETI_SP_FUSE=0: separate);
   // sp_fend[g] marks group g's factorization end (external event records)
-  bool sp_graph_fused = false, sp_assembled_in_graph = false;
+  bool sp_graph_fused = false, sp_assembled_in_graph = false, sp_graph_built = false;
+  cudaGraphExec_t sp_gexec[kSpStreams] = {};   // per-group step graphs
+  int sp_glaunches[kSpStreams] = {};
+  cudaEvent_t k_ready_grp[kSpStreams] = {};    // a group's K values (and Q / forces) landed
+  std::vector<int> sp_group_of;                // slot -> factorization group
+  std::vector<std::pair<int, int>> sp_init_rng;  // per group: range of d_sp_init
   cudaEvent_t sp_fend[kSpStreams] = {};
   // sparse-route stiffness hand-over: values are copied on copy_stream while
   // the pool is zeroed; k_ready = copies issued so far landed, k_free = the
@@ -412,9 +415,14 @@ int build_sparse_tasks(feti_ctx* c) {
     CUDA_TRY(cudaEventCreateWithFlags(&c->sp_join[g], cudaEventDisableTiming));
   }
   for (auto& e : c->sp_ev) CUDA_TRY(cudaEventCreate(&e));
-  for (int g = 0; g < G; ++g) CUDA_TRY(cudaEventCreate(&c->sp_fend[g]));
+  for (int g = 0; g < G; ++g) {
+    CUDA_TRY(cudaEventCreate(&c->sp_fend[g]));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->k_ready_grp[g], cudaEventDisableTiming));
+  }
   // contiguous groups of subdomains
   auto group_of = [&](int si) { return (int)((int64_t)si * G / std::max(ns, 1)); };
+  c->sp_group_of.assign(ns, 0);
+  for (int si = 0; si < ns; ++si) c->sp_group_of[si] = group_of(si);
   // slots of the (P Q)^T block row: their tasks run "thin" (rows < 8 only)
   std::vector<std::vector<char>> qrow(ns);
   for (int si = 0; si < ns; ++si) {
@@ -473,6 +481,17 @@ int build_sparse_tasks(feti_ctx* c) {
     }
     c->sp_panel_rng[gj] = {b, (int)tasks.size() - b};
   }
+  // per group: its subdomains' init entries (the list is in subdomain order)
+  c->sp_init_rng.assign(G, {0, 0});
+  {
+    size_t a = 0;
+    for (int g = 0; g < G; ++g) {
+      size_t b = a;
+      while (b < init.size() && group_of(init[b].sub) == g) ++b;
+      c->sp_init_rng[g] = {(int)a, (int)(b - a)};
+      a = b;
+    }
+  }
   if ((rc = upload(c, &c->d_sp_init, init))) return rc;
   if ((rc = upload(c, &c->d_sp_tasks, tasks))) return rc;
   if ((rc = upload(c, &c->d_sp_pairs, pairs))) return rc;
@@ -507,79 +526,108 @@ int factorize_sparse(feti_ctx* c) {
   c->sp_bad_init.assign(ns, 1 << 30);
   CUDA_TRY(cudaMemcpyAsync(c->d_bad, c->sp_bad_init.data(), ns * sizeof(int), cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaEventRecord(c->sp_ev[0], st));
-  // the step's K values were copied on copy_stream while the pool was being
-  // zeroed; a changed kernel basis or force (read by the pool init itself)
-  // has to land before it
-  if (c->k_pending && c->k_early) {
-    CUDA_TRY(cudaStreamWaitEvent(st, c->k_ready, 0));
-    c->k_pending = c->k_early = false;
-  }
-  launch_sp_init(c->d_sp_init, c->n_sp_init, c->d_spsub, st);
-  if (c->k_pending) {
-    CUDA_TRY(cudaStreamWaitEvent(st, c->k_ready, 0));
-    c->k_pending = false;
-  }
-  launch_sp_trace(c->d_spsub, ns, st);
-  launch_sp_scatter(c->d_spsub, 0, ns, c->sp_max_n, st);
-  CUDA_TRY(cudaEventRecord(c->k_free, st));
-  CUDA_TRY(cudaGetLastError());
-  FETI_DEBUG_SYNC(st);
-  int launches = 2;
-  // the groups' column sequences are independent: issue them round-robin on
-  // their own streams so the GPU interleaves one group's diagonal blocks with
-  // another's tile GEMMs.  The ~900 launches are captured once into a CUDA
-  // graph (fork/join over the group streams) and replayed per factorization
-  // (FETI_SP_GRAPH=0 or FETI_DEBUG_SYNC: issued directly).
   const int G = c->sp_groups;
   const bool use_graph = !g_debug_sync && !(getenv("FETI_SP_GRAPH") && atoi(getenv("FETI_SP_GRAPH")) == 0);
-  if (use_graph && c->sp_graph_exec) {
-    CUDA_TRY(cudaGraphLaunch(c->sp_graph_exec, st));
-    launches = 2 + c->sp_graph_launches;
+  int launches = 0;
+  if (use_graph) {
+    // one CUDA graph per group, replayed on the group's stream: [rho, K scatter,
+    // the group's column sequence, its interface assembly + correction].  The
+    // group's pool is zeroed on its stream first, and its graph waits only for
+    // its own subdomains' K values (k_ready_grp), so with host K values the
+    // H2D copy of later groups overlaps the factorization of earlier ones.
+    // Each group's assembly overlaps the other groups' factorization.
+    if (!c->sp_graph_built)
+      c->sp_graph_fused = !(getenv("FETI_SP_FUSE") && atoi(getenv("FETI_SP_FUSE")) == 0);
+    CUDA_TRY(cudaEventRecord(c->ev[2], st));
+    int nl = 0;
+    for (int g = 0; g < G; ++g) {
+      cudaStream_t gs = c->sp_streams[g];
+      const auto ir = c->sp_init_rng[g], sr = c->sp_sub_rng[g];
+      CUDA_TRY(cudaStreamWaitEvent(gs, c->ev[2], 0));
+      // a changed kernel basis / force is read by the pool init itself
+      if (c->k_pending && c->k_early) CUDA_TRY(cudaStreamWaitEvent(gs, c->k_ready_grp[g], 0));
+      launch_sp_init(c->d_sp_init + ir.first, ir.second, c->d_spsub, gs);
+      if (c->k_pending) CUDA_TRY(cudaStreamWaitEvent(gs, c->k_ready_grp[g], 0));
+      launches += ir.second > 0;
+      if (!c->sp_gexec[g]) {
+        int gl = 0;
+        CUDA_TRY(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+        launch_sp_trace(c->d_spsub + sr.first, sr.second, gs);
+        launch_sp_scatter(c->d_spsub, sr.first, sr.second, c->sp_max_n, gs);
+        gl += 2 * (sr.second > 0);
+        for (int j = 0; j < c->sp_maxTq; ++j) {
+          const size_t gj = (size_t)g * c->sp_maxTq + j;
+          const auto a = c->sp_acc_rng[gj], d = c->sp_diag_rng[gj], pp = c->sp_panel_rng[gj];
+          launch_sp_gemm(c->d_sp_tasks + a.first, a.second, c->d_sp_pairs, gs);
+          launch_sp_potrf(c->d_sp_diag + d.first, d.second, c->d_bad, gs);
+          launch_sp_gemm(c->d_sp_tasks + pp.first, pp.second, c->d_sp_pairs, gs);
+          gl += (a.second > 0) + (d.second > 0) + (pp.second > 0);
+        }
+        int rc2 = FETI_OK;
+        if (c->sp_graph_fused) {
+          cudaError_t e = cudaEventRecordWithFlags(c->sp_fend[g], gs, cudaEventRecordExternal);
+          rc2 = e != cudaSuccess ? fail(FETI_ERR_CUDA, "%s", cudaGetErrorString(e))
+                                 : sparse_group_assembly(c, g, gs, &gl);
+        }
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(gs, &graph);
+        if (rc2) {
+          if (graph) cudaGraphDestroy(graph);
+          return rc2;
+        }
+        CUDA_TRY(e);
+        e = cudaGraphInstantiate(&c->sp_gexec[g], graph, 0);
+        cudaGraphDestroy(graph);
+        CUDA_TRY(e);
+        c->sp_glaunches[g] = gl;
+      }
+      CUDA_TRY(cudaGraphLaunch(c->sp_gexec[g], gs));
+      nl += c->sp_glaunches[g];
+      CUDA_TRY(cudaEventRecord(c->sp_join[g], gs));
+      CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
+    }
+    c->sp_graph_built = true;
+    c->k_pending = c->k_early = false;
+    // the last scatter that read the step's K values ran inside the graphs
+    CUDA_TRY(cudaEventRecord(c->k_free, st));
+    launches += nl;
   } else {
-    // each group's assembly is captured behind its own column sequence: it
-    // overlaps the other groups' factorization (the end of every column
-    // sequence is the latency-bound dense interface chain)
-    c->sp_graph_fused = use_graph && !(getenv("FETI_SP_FUSE") && atoi(getenv("FETI_SP_FUSE")) == 0);
-    if (use_graph) CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    // direct launches (FETI_SP_GRAPH=0 or FETI_DEBUG_SYNC): one init + scatter
+    // over every subdomain, then the groups' column sequences round-robin on
+    // their own streams; feti_assemble runs each group's assembly
+    c->sp_graph_fused = false;
+    if (c->k_pending && c->k_early) {
+      CUDA_TRY(cudaStreamWaitEvent(st, c->k_ready, 0));
+      c->k_pending = c->k_early = false;
+    }
+    launch_sp_init(c->d_sp_init, c->n_sp_init, c->d_spsub, st);
+    if (c->k_pending) {
+      CUDA_TRY(cudaStreamWaitEvent(st, c->k_ready, 0));
+      c->k_pending = false;
+    }
+    launch_sp_trace(c->d_spsub, ns, st);
+    launch_sp_scatter(c->d_spsub, 0, ns, c->sp_max_n, st);
+    CUDA_TRY(cudaEventRecord(c->k_free, st));
+    CUDA_TRY(cudaGetLastError());
+    FETI_DEBUG_SYNC(st);
+    launches = 3;
     CUDA_TRY(cudaEventRecord(c->ev[2], st));
     for (int g = 0; g < G; ++g) CUDA_TRY(cudaStreamWaitEvent(c->sp_streams[g], c->ev[2], 0));
-    int nl = 0;
     for (int j = 0; j < c->sp_maxTq; ++j)
       for (int g = 0; g < G; ++g) {
         const size_t gj = (size_t)g * c->sp_maxTq + j;
         cudaStream_t gs = c->sp_streams[g];
-        const auto a = c->sp_acc_rng[gj], d = c->sp_diag_rng[gj], p = c->sp_panel_rng[gj];
+        const auto a = c->sp_acc_rng[gj], d = c->sp_diag_rng[gj], pp = c->sp_panel_rng[gj];
         launch_sp_gemm(c->d_sp_tasks + a.first, a.second, c->d_sp_pairs, gs);
         launch_sp_potrf(c->d_sp_diag + d.first, d.second, c->d_bad, gs);
-        launch_sp_gemm(c->d_sp_tasks + p.first, p.second, c->d_sp_pairs, gs);
-        nl += (a.second > 0) + (d.second > 0) + (p.second > 0);
-        if (!use_graph) {
-          CUDA_TRY(cudaGetLastError());
-          FETI_DEBUG_SYNC(gs);
-        }
+        launch_sp_gemm(c->d_sp_tasks + pp.first, pp.second, c->d_sp_pairs, gs);
+        launches += (a.second > 0) + (d.second > 0) + (pp.second > 0);
+        CUDA_TRY(cudaGetLastError());
+        FETI_DEBUG_SYNC(gs);
       }
     for (int g = 0; g < G; ++g) {
-      if (c->sp_graph_fused) {
-        CUDA_TRY(cudaEventRecordWithFlags(c->sp_fend[g], c->sp_streams[g], cudaEventRecordExternal));
-        int rc2 = sparse_group_assembly(c, g, c->sp_streams[g], &nl);
-        if (rc2) {
-          cudaGraph_t junk = nullptr;
-          cudaStreamEndCapture(st, &junk);
-          if (junk) cudaGraphDestroy(junk);
-          return rc2;
-        }
-      }
       CUDA_TRY(cudaEventRecord(c->sp_join[g], c->sp_streams[g]));
       CUDA_TRY(cudaStreamWaitEvent(st, c->sp_join[g], 0));
-    }
-    launches += nl;
-    if (use_graph) {
-      cudaGraph_t graph = nullptr;
-      CUDA_TRY(cudaStreamEndCapture(st, &graph));
-      CUDA_TRY(cudaGraphInstantiate(&c->sp_graph_exec, graph, 0));
-      CUDA_TRY(cudaGraphDestroy(graph));
-      c->sp_graph_launches = nl;
-      CUDA_TRY(cudaGraphLaunch(c->sp_graph_exec, st));
     }
   }
   c->sp_graph_used = use_graph;
@@ -619,6 +667,14 @@ int wait_applies(feti_ctx* c) {
 // after zeroing the pool.  The caller keeps `data` alive and unchanged
 // until feti_assemble returns; Q and U1 are staged in the slot's own host
 // buffers.
+// the slot's factorization group may start once its copies landed (the
+// group's step graph waits for k_ready_grp, recorded after each of its slots)
+int mark_group_ready(feti_ctx* c, int slot) {
+  if (slot >= 0 && slot < (int)c->sp_group_of.size())
+    CUDA_TRY(cudaEventRecord(c->k_ready_grp[c->sp_group_of[slot]], c->copy_stream));
+  return FETI_OK;
+}
+
 int stiffness_values_async(feti_ctx* c, SubHost& s, const double* data, const double* Q) {
   if (!c->k_pending) {
     CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->k_free, 0));   // the last scatter read the old values
@@ -647,6 +703,7 @@ int stiffness_values_async(feti_ctx* c, SubHost& s, const double* data, const do
     return fail(FETI_ERR_ARG, "the first hand-over of a slot needs its kernel basis");
   }
   CUDA_TRY(cudaEventRecord(c->k_ready, c->copy_stream));
+  mark_group_ready(c, (int)(&s - c->subs.data()));
   return FETI_OK;
 }
 
@@ -705,10 +762,11 @@ int feti_destroy(feti_ctx* c) {
   }
   for (auto& e : c->sp_ev)
     if (e) cudaEventDestroy(e);
-  if (c->sp_graph_exec) cudaGraphExecDestroy(c->sp_graph_exec);
   for (int g = 0; g < feti_ctx::kSpStreams; ++g) {
     if (c->sp_join[g]) cudaEventDestroy(c->sp_join[g]);
     if (c->sp_fend[g]) cudaEventDestroy(c->sp_fend[g]);
+    if (c->k_ready_grp[g]) cudaEventDestroy(c->k_ready_grp[g]);
+    if (c->sp_gexec[g]) cudaGraphExecDestroy(c->sp_gexec[g]);
     if (c->sp_streams[g]) cudaStreamDestroy(c->sp_streams[g]);
   }
   for (double* pp : c->x_open) cudaIpcCloseMemHandle(pp);
@@ -1866,6 +1924,7 @@ int feti_set_forces(feti_ctx* c, int64_t nslots, const int64_t* slots, const dou
       s.h_qtf.assign(qtf[i], qtf[i] + s.sp_r);
       CUDA_TRY(cudaMemcpyAsync(s.d_qtf, s.h_qtf.data(), (size_t)s.sp_r * 8, cudaMemcpyHostToDevice, c->copy_stream));
     }
+    mark_group_ready(c, (int)slots[i]);
   }
   CUDA_TRY(cudaEventRecord(c->k_ready, c->copy_stream));
   return FETI_OK;
