@@ -442,10 +442,18 @@ int build_sparse_tasks(feti_ctx* c) {
       const SubHost& s = c->subs[si];
       if (j >= s.sp.Tq || group_of(si) != g) continue;
       for (const auto& t : s.sp.acc[j]) {
-        tasks.push_back(SpTask{s.d_pool + (size_t)t.first * TILE, (int64_t)pairs.size(), (int)t.second.size(),
+        // one entry per needed k-slice of every product (structurally zero
+        // slices of either operand skipped: they add exact zeros)
+        const int64_t p0 = (int64_t)pairs.size();
+        for (const auto& pr : t.second) {
+          const unsigned mk = s.sp.slot_mask[pr.first] & s.sp.slot_mask[pr.second];
+          for (int q = 0; q < TB / KS; ++q)
+            if (mk >> q & 1)
+              pairs.push_back(SpPair{s.d_pool + (size_t)pr.first * TILE + (size_t)q * SLICE,
+                                     s.d_pool + (size_t)pr.second * TILE + (size_t)q * SLICE});
+        }
+        tasks.push_back(SpTask{s.d_pool + (size_t)t.first * TILE, p0, (int)((int64_t)pairs.size() - p0),
                                qrow[si][t.first] ? 2 : 0});
-        for (const auto& pr : t.second)
-          pairs.push_back(SpPair{s.d_pool + (size_t)pr.first * TILE, s.d_pool + (size_t)pr.second * TILE});
       }
     }
     // largest first (shortest launch tail; keeping the subdomain order for L2
@@ -474,9 +482,13 @@ int build_sparse_tasks(feti_ctx* c) {
       const SubHost& s = c->subs[si];
       if (j >= s.sp.T || group_of(si) != g) continue;
       for (int slot : s.sp.panel[j]) {
+        // L_ij = A_ij inv(L_jj)^T over the k-slices (columns of block j) where A_ij has nonzeros
         double* C = s.d_pool + (size_t)slot * TILE;
-        tasks.push_back(SpTask{C, (int64_t)pairs.size(), 1, qrow[si][slot] ? 3 : 1});
-        pairs.push_back(SpPair{C, dinv_of(si)});
+        const int64_t p0 = (int64_t)pairs.size();
+        const unsigned mk = s.sp.slot_mask[slot];
+        for (int q = 0; q < TB / KS; ++q)
+          if (mk >> q & 1) pairs.push_back(SpPair{C + (size_t)q * SLICE, dinv_of(si) + (size_t)q * SLICE});
+        tasks.push_back(SpTask{C, p0, (int)((int64_t)pairs.size() - p0), qrow[si][slot] ? 3 : 1});
       }
     }
     c->sp_panel_rng[gj] = {b, (int)tasks.size() - b};
@@ -502,6 +514,7 @@ int build_sparse_tasks(feti_ctx* c) {
   for (auto& s : c->subs) {   // the plan's task lists live on the device now
     decltype(s.sp.acc)().swap(s.sp.acc);
     decltype(s.sp.panel)().swap(s.sp.panel);
+    decltype(s.sp.slot_mask)().swap(s.sp.slot_mask);
   }
   CUDA_TRY(configure_sparse());
   CUDA_TRY(configure_sp_solve());

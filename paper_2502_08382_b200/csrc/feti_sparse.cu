@@ -142,12 +142,11 @@ __device__ __forceinline__ void sg_issue(const SpPair* __restrict__ pairs, int64
                                           double* sA, double* sB, uint64_t* full, uint64_t* empty) {
   const int st = (int)(pos % SG_STAGES);
   const uint32_t ph = (pos / SG_STAGES) & 1;
-  const SpPair pr = pairs[pair0 + sl / (TB / KS)];
-  const int so = (sl % (TB / KS)) * SLICE;
+  const SpPair pr = pairs[pair0 + sl];
   mbar_wait(&empty[st], ph ^ 1);
   mbar_arrive_expect_tx(&full[st], 2 * SLICE * 8);
-  bulk_g2s(sA + st * SLICE, pr.A + so, SLICE * 8, &full[st]);
-  bulk_g2s(sB + st * SLICE, pr.B + so, SLICE * 8, &full[st]);
+  bulk_g2s(sA + st * SLICE, pr.A, SLICE * 8, &full[st]);
+  bulk_g2s(sB + st * SLICE, pr.B, SLICE * 8, &full[st]);
 }
 
 // One tile task on the ring (positions pos0 ...).  `pre` slices of it were
@@ -158,7 +157,7 @@ template <int MI>
 __device__ __forceinline__ int sg_gemm(const SpPair* __restrict__ pairs, const SpTask& tk, double* sA, double* sB,
                                        uint64_t* full, uint64_t* empty, uint32_t pos0, int warp, int lane, int pre,
                                        const SpTask* next) {
-  const int nsl = tk.npairs * (TB / KS);
+  const int nsl = tk.npairs;
   const int wm = warp >> 2, wn = warp & 3;
   const int gq = lane >> 2, t = lane & 3;
   const bool issuer = (threadIdx.x == 0);
@@ -187,7 +186,7 @@ __device__ __forceinline__ int sg_gemm(const SpPair* __restrict__ pairs, const S
   }
   int issued = 0;
   if (next) {
-    const int nsl2 = next->npairs * (TB / KS);
+    const int nsl2 = next->npairs;
     issued = min(SG_PREF, nsl2);
     if (issuer) {
       if (!(next->flags & 1)) bulk_prefetch_l2(next->C, TILE * 8);
@@ -241,7 +240,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) sp_gemm8_kernel(const SpTask* _
       pre = sg_gemm<8>(pairs, tk, sA, sB, full, empty, pos, warp, lane, pre, nx);
     else
       pre = sg_gemm<1>(pairs, tk, sA, sB, full, empty, pos, warp, lane, pre, nx);
-    pos += (uint32_t)(tk.npairs * (TB / KS));
+    pos += (uint32_t)tk.npairs;
   }
 }
 
@@ -430,6 +429,8 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
     for (int I = par + 1; I < Tq; ++I)
       if (cs[k][I]) cs[par][I] = 1;
   }
+  // k-slice masks of the scalar factor per (block row, block column)
+  std::vector<uint8_t> smask;
   // scalar work of the same ordering (the algorithmic figure): elimination
   // tree (Liu, path compression) and column counts by row-subtree walks,
   // O(nnz(L)); flops = sum_j c_j (c_j + 3), c_j = nonzeros below the diagonal
@@ -453,7 +454,9 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
         }
       }
     }
+    smask.assign((size_t)Tq * Tq, 0);
     for (int64_t i = 0; i < npos; ++i) {
+      smask[(size_t)(i / TB) * Tq + i / TB] |= (uint8_t)(1u << ((i % TB) / KS));   // L(i, i) (identity at padding)
       const int64_t a = pos_dof[i];
       if (a < 0) continue;
       mark[i] = i;
@@ -461,6 +464,7 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
         for (int64_t j = iperm[indices[p]]; j >= 0 && j < i && mark[j] != i; j = parent[j]) {
           ++cnt[j];                          // L(i, j) != 0
           mark[j] = i;
+          smask[(size_t)(i / TB) * Tq + j / TB] |= (uint8_t)(1u << ((j % TB) / KS));
         }
       }
     }
@@ -487,6 +491,15 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
     for (int J = smin; J <= I; ++J) P.tmap[(size_t)I * Tq + J] = (int)(ns + tri_index(I - smin, J - smin));
   ns += (int64_t)(T - smin) * (T - smin + 1) / 2;
   P.ntiles = ns;
+  const bool kmask = !(getenv("FETI_SP_KMASK") && atoi(getenv("FETI_SP_KMASK")) == 0);
+  P.slot_mask.assign((size_t)ns, 0xF);
+  if (kmask)
+    for (int I = 0; I < T; ++I)
+      for (int J = 0; J <= I; ++J) {
+        const int sl = P.tmap[(size_t)I * Tq + J];
+        if (sl >= 0) P.slot_mask[sl] = smask[(size_t)I * Tq + J];
+      }
+  auto popc = [](unsigned v) { return (double)__builtin_popcount(v); };
   // row structures (ascending)
   std::vector<std::vector<int>> rows(Tq);
   for (int J = 0; J < T; ++J)
@@ -519,13 +532,24 @@ void sp_symbolic(int64_t n, const int64_t* indptr, const int64_t* indices, const
         }
       }
       const double tfi = (i == T && Tq > T) ? tf / 16.0 : tf;   // thin (P Q)^T row tiles
-      if (!pr.empty()) {
-        P.flops_exec += tfi * pr.size();
-        P.acc[j].emplace_back(P.tmap[(size_t)i * Tq + j], std::move(pr));
+      // drop products whose operands share no nonzero k-slice (exact zeros)
+      std::vector<std::pair<int, int>> live;
+      double sl_count = 0;
+      for (const auto& ab : pr) {
+        const unsigned mk = P.slot_mask[ab.first] & P.slot_mask[ab.second];
+        if (mk) {
+          live.push_back(ab);
+          sl_count += popc(mk);
+        }
+      }
+      if (!live.empty()) {
+        P.flops_exec += tfi * sl_count / (TB / KS);
+        P.acc[j].emplace_back(P.tmap[(size_t)i * Tq + j], std::move(live));
       }
       if (i != j) {
-        P.panel[j].push_back(P.tmap[(size_t)i * Tq + j]);
-        P.flops_exec += tfi;
+        const int cs_slot = P.tmap[(size_t)i * Tq + j];
+        P.panel[j].push_back(cs_slot);
+        P.flops_exec += tfi * popc(P.slot_mask[cs_slot]) / (TB / KS);
       }
     }
     if (j < T) P.flops_exec += (double)TB * TB * TB / 3.0 + (double)TB * TB * TB / 3.0;  // potrf + inverse

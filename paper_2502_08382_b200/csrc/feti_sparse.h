@@ -41,6 +41,9 @@ struct SpSub {
 //   accumulate (flags 0):  C -= sum_p A_p B_p^T
 //   panel      (flags 1):  C  = C B^T  (B = inv(L_jj), one pair (C, B))
 //   flags & 2: C is a tile of the (P Q)^T block row (rows >= 8 are zero)
+// one 32-deep k-slice of a tile product: A and B point at the slice (tiles
+// are stored k-slice major, SLICE doubles per slice); k-slices where either
+// operand is structurally zero in the scalar factor are not listed
 struct SpPair {
   const double* A;
   const double* B;
@@ -48,7 +51,7 @@ struct SpPair {
 struct SpTask {
   double* C;
   int64_t pair0;
-  int npairs;
+  int npairs;     // k-slices (SpPair entries) of this task
   int flags;
 };
 struct SpDiag {
@@ -73,6 +76,11 @@ struct SpPlan {
   // per block column j in [0, Tq): accumulation targets (C slot, (A, B) slot pairs)
   std::vector<std::vector<std::pair<int, std::vector<std::pair<int, int>>>>> acc;
   std::vector<std::vector<int>> panel;  // per column j < T: slots of L_ij, i in struct(j)
+  // per slot: bit s set when the tile's k-slice s (columns [32 s, 32 s + 32)
+  // of its block column) holds a nonzero of the scalar factor in the tile's
+  // rows (the (P Q)^T row: all slices).  A product's slice s is needed only
+  // when both operands have bit s: the others add exact zeros.
+  std::vector<uint8_t> slot_mask;
   double flops_exec = 0.0;            // tile flops the factorization executes
   double flops_scalar = 0.0;          // scalar Cholesky flops of K_s in this ordering (+ the y = L^-1 P Q solve)
   int64_t nnz_l = 0;                  // nonzeros of the scalar factor

@@ -410,3 +410,25 @@ def test_sparse_route_graph_matches_direct_launches(monkeypatch):
     # the third step (K back to 1x) reproduces the first
     assert np.array_equal(res["graph"][0][1], res["graph"][2][1])
     assert np.linalg.norm(3.0 * res["graph"][1][1] - res["graph"][0][1]) <= 1e-12 * np.linalg.norm(res["graph"][0][1])
+
+
+@pytest.mark.parametrize("config,subs", [("c3", [0, 21]), ("c4", [21])])
+def test_sparse_route_kslice_skipping_exact(config, subs, monkeypatch):
+    """Tile products skip the k-slices where either operand is structurally
+    zero in the scalar factor (FETI_SP_KMASK, default on): the skipped slices
+    only ever add exact zeros, so F~, q and the factor are the same values as
+    with every slice computed (array_equal: +0.0 == -0.0)."""
+    prob = inputs.Problem(*inputs.CONFIGS[config])
+    p = np.random.default_rng(11).normal(size=prob.n_multipliers)
+    res = {}
+    for tag, env in (("mask", "1"), ("full", "0")):
+        monkeypatch.setenv("FETI_SP_KMASK", env)
+        op, _, _, _ = _sparse_op(prob, subs=subs)
+        with op:
+            op.preprocess()
+            st = op.stats()
+            res[tag] = ([op.local_operator(s) for s in subs], op.apply(p), st["flops_factor_exec"])
+    assert res["mask"][2] < res["full"][2]
+    assert np.array_equal(res["mask"][1], res["full"][1])
+    for a, b in zip(res["mask"][0], res["full"][0]):
+        assert np.array_equal(a, b)
