@@ -725,12 +725,12 @@ def run_sparse(args, rank, world, local_rank):
                    "l2": f"inputs larger than L2 (block-sparse factor tiles {st['bytes_temporary'] / 1e9:.0f} GB, "
                          f"packed F~ {8 * sum(m * (m + 1) / 2 for m in prob.m_per_subdomain()) / 1e9:.2f} GB "
                          f"per apply)"},
-        # the step is ONE captured CUDA graph: every group's factorization
+        # the step is one captured CUDA graph per subdomain group: the group's factorization
         # (sp_gemm8 tile tasks + sp_potrf) with its interface assembly (TRSM
         # chain, U2, SYRK + correction) behind it on the group's stream
         "roofline": (lambda alg, ex: {
             "bound": "tensor",
-            "kernel": "the step's CUDA graph: sp_gemm8_kernel + sp_potrf_kernel (factorization) and trsm_chain / "
+            "kernel": "the step's CUDA graphs (one per subdomain group): sp_gemm8_kernel + sp_potrf_kernel (factorization) and trsm_chain / "
                       "sp_u2 / syrk (interface assembly), FP64 DMMA tile work",
             "achieved": alg / (step_ms / 1e3) / 1e12, "peak": peak_f64, "unit": "TFLOP/s",
             "frac": alg / (step_ms / 1e3) / 1e12 / peak_f64,
@@ -761,7 +761,7 @@ def run_sparse(args, rank, world, local_rank):
         "phases_ms": {"ms_factorize": statistics.mean(fac_ms), "ms_preprocess": statistics.mean(pre_ms),
                       "ms_assembly_tail": statistics.mean(asm_ms),
                       "note": "each group's interface assembly + correction is captured right behind its "
-                              "factorization on its stream (one graph per step); ms_assembly_tail = past the last "
+                              "factorization in the group's step graph; ms_assembly_tail = past the last "
                               "group's factorization"},
         "apply": {"ms_per_iter": apply_ms, "kernel_ms_per_iter": apply_kernel_ms, "e2e_ms_per_iter": apply_e2e_ms,
                   "what": "ms_per_iter: local kernels + fused exchange (N > 1), max over ranks; kernel_ms_per_iter: "
